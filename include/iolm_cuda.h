@@ -1,0 +1,139 @@
+/*
+ * iolm_cuda.h - C ABI of the B200-native prompt() hot path.
+ *
+ * This is the drop-in boundary for the reference's model runtime, iolm::ModelRuntime
+ * (/root/reference/proj/include/iolm/runtime.hpp:37-95, proj/src/runtime.cpp:60-345). The
+ * reference has no plugin registry; every caller (PromptResolver::flush, proj/src/exec.cpp:133;
+ * semantic join, exec.cpp:320-322; validate, proj/src/optimize.cpp:335-336) holds a
+ * `const ModelRuntime&`. The C++ shim in include/iolm_cuda_runtime.hpp rebuilds that exact class
+ * surface on top of these entry points; INTEGRATION.md shows the swap.
+ *
+ * Plain pointers and sizes only: no C++ or torch types cross this boundary.
+ *
+ * Status codes (return value of every int-returning entry point) mirror the reference's
+ * exception classes (proj/include/iolm/common.hpp:16-89):
+ */
+#ifndef IOLM_CUDA_H_
+#define IOLM_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IOLM_OK 0
+#define IOLM_E_CONTRACT 1          /* iolm::ContractViolation */
+#define IOLM_E_SEQ_TOO_LONG 2      /* iolm::SequenceTooLong (bad_row set) */
+#define IOLM_E_UNSUPPORTED 3       /* encoding/shape this GPU build does not run */
+#define IOLM_E_CUDA 4              /* CUDA runtime / launch failure */
+#define IOLM_E_OOM 5               /* device memory exhausted */
+#define IOLM_E_CORRUPT_HEADER 6    /* iolm::CorruptHeader */
+#define IOLM_E_TRUNCATED_BLOB 7    /* iolm::TruncatedBlob */
+#define IOLM_E_UNKNOWN_ENCODING 8  /* iolm::UnknownEncoding */
+
+/* Tokenizer constants (proj/include/iolm/tokenizer.hpp:17-20). */
+#define IOLM_VOCAB 131
+#define IOLM_PAD 128
+#define IOLM_BOS 129
+#define IOLM_EOS 130
+
+typedef struct iolm_cuda_ctx iolm_cuda_ctx;
+
+/* Engine options. Zero means "default" for every field. */
+typedef struct iolm_cuda_opts {
+  int32_t max_tokens_per_step; /* continuous-batching token budget per engine step (default 16384) */
+  int32_t max_slots;           /* sequences resident in the paged KV pool (default: derived) */
+  int32_t page_size;           /* KV page size in tokens (default 16) */
+  int32_t act_quant;           /* 1: W8A8 int8 activations for q8 / sparse24 weights (default 0) */
+  int32_t prefix_sharing;      /* -1: off; 0/1: share the common prompt prefix KV (default on) */
+  int32_t use_cuda_graph;      /* reserved */
+  int32_t reserved[10];
+} iolm_cuda_opts;
+
+/* ModelConfig (proj/include/iolm/model.hpp:20-41); per-layer lists are queried separately. */
+typedef struct iolm_cuda_model_config {
+  int32_t vocab_size, d_model, n_layers, n_heads, d_ff, max_seq_len, head_dim;
+} iolm_cuda_model_config;
+
+/* Counters of the most recent decode/forward call. */
+typedef struct iolm_cuda_stats {
+  int64_t steps;          /* engine steps (one batched forward each) */
+  int64_t tokens;         /* token rows pushed through the layers */
+  int64_t prefill_tokens; /* of which prompt tokens */
+  int64_t decode_tokens;  /* of which generated-token advances */
+  int64_t prefix_tokens;  /* shared-prefix tokens computed once */
+  int64_t kernel_launches;
+  double device_ms;       /* device time of the call measured with CUDA events */
+} iolm_cuda_stats;
+
+/*
+ * Replaces ModelRuntime::ModelRuntime(const ModelBundle&) (runtime.cpp:60-89).
+ * bundle_bytes: the canonical serialize_bundle() byte stream (proj/src/model.cpp:311-346,
+ * proj/docs/format.md). The weights are decoded/repacked onto `device`; the bytes may be freed
+ * after the call returns.
+ */
+int iolm_cuda_create(const uint8_t* bundle_bytes, size_t len, int device,
+                     const iolm_cuda_opts* opts, iolm_cuda_ctx** out);
+void iolm_cuda_destroy(iolm_cuda_ctx* ctx);
+
+/* ModelRuntime::bundle_hash() (runtime.hpp:42; FNV-1a over the serialized bundle, model.cpp:408). */
+int iolm_cuda_bundle_hash(const iolm_cuda_ctx* ctx, uint64_t* out);
+/* ModelRuntime::config() (runtime.hpp:41). */
+int iolm_cuda_config(const iolm_cuda_ctx* ctx, iolm_cuda_model_config* out);
+/* Per-layer pruning info: active head count and FFN width of layer l (model.hpp:30-31). */
+int iolm_cuda_layer_shape(const iolm_cuda_ctx* ctx, int32_t layer, int32_t* heads, int32_t* ffn);
+
+/*
+ * Replaces ModelRuntime::batch_decode(prompts, max_new_tokens, counter) (runtime.cpp:241-309).
+ * ids/row_offsets: CSR token rows, row i = ids[row_offsets[i] .. row_offsets[i+1]) and already
+ * tokenized exactly as the reference does it: [BOS] + one id per ASCII byte (runtime.cpp:262-263).
+ * Host buffers. Outputs (host): out_ids[i*max_new_tokens + t] for t < out_len[i] are the emitted
+ * ids (PAD/BOS included; they render nothing), out_len[i] the count. madds (optional) receives the
+ * multiply-adds the reference FlopCounter would have added for the same call (runtime.cpp:311-345).
+ * On IOLM_E_SEQ_TOO_LONG, *bad_row is the first offending row (runtime.cpp:264-267).
+ */
+int iolm_cuda_decode(iolm_cuda_ctx* ctx, const int32_t* ids, const int64_t* row_offsets,
+                     int64_t n_rows, int32_t max_new_tokens, int32_t* out_ids, int32_t* out_len,
+                     uint64_t* madds, int64_t* bad_row);
+
+/* Same as iolm_cuda_decode but `d_ids` is already resident in device memory (row_offsets stay on
+ * the host). Used to time the device path with inputs already in HBM. */
+int iolm_cuda_decode_device_ids(iolm_cuda_ctx* ctx, const int32_t* d_ids,
+                                const int64_t* row_offsets, int64_t n_rows,
+                                int32_t max_new_tokens, int32_t* out_ids, int32_t* out_len,
+                                uint64_t* madds, int64_t* bad_row);
+
+/*
+ * Replaces ModelRuntime::forward(ids, mask, counter) (runtime.cpp:217-232): logits for every
+ * position, logits[n x 131] row-major f32. mask may be NULL (all valid); masked positions are
+ * excluded as attention keys and their logits rows are unspecified (the reference says "callers
+ * must not read", runtime.hpp:44-47).
+ */
+int iolm_cuda_forward_logits(iolm_cuda_ctx* ctx, const int32_t* ids, const uint8_t* mask,
+                             int32_t n, float* logits, uint64_t* madds);
+
+/* Counters of the last decode/forward call on this context. */
+int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* out);
+
+/* Thread-local message for the last non-OK status. */
+const char* iolm_cuda_last_error(void);
+
+/* ---- kernel-level entry points used by the parity tests (device work, host buffers) ---- */
+
+/* C[M x N] = A[M x K] * W[N x K]^T with bf16 operands (raw uint16 bit patterns), f32 result,
+ * through the production tcgen05 GEMM. epi: 0 f32 store, 2 GELU (result returned as f32 after a
+ * bf16 round trip). bn: 128 or 256. */
+int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, float* C, int32_t M, int32_t N,
+                              int32_t K, int32_t bn, int32_t epi);
+
+/* W8A8 integer GEMM: C_i32[M x N] = A_s8[M x K] * W_s8[N x K]^T through tcgen05 kind::i8.
+ * Bit-exact integer accumulators. */
+int iolm_cuda_debug_gemm_s8(const int8_t* A, const int8_t* W, int32_t* C, int32_t M, int32_t N,
+                            int32_t K);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IOLM_CUDA_H_ */

@@ -1,0 +1,282 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a:  C[M x N] = A[M x K] * W[N x K]^T
+//
+//   A  : activations, K-major (row-major [M x K]), bf16 (or int8 for the W8A8 variant)
+//   W  : weights as stored in the bundle, [out x in] = [N x K] row-major, i.e. also K-major
+//        (the reference applies x * W^T via transposed copies, runtime.cpp:80-85; on the GPU the
+//        bundle layout is already the K-major B operand, so no transpose is materialised)
+//
+// Roles (192 threads, one CTA per SM, persistent over output tiles):
+//   warp 0      : TMA producer (one elected lane) - A and W tiles into a STAGES-deep smem ring
+//   warp 1      : TMEM allocator + MMA issuer (one elected lane), tcgen05.mma into a
+//                 double-buffered fp32 accumulator in TMEM (2 x BN columns)
+//   warps 2..5  : epilogue - tcgen05.ld 32 lanes x 32 columns per step, fused op, global store
+//
+// Reduction order per output element is fixed by K alone (BK-blocks ascending, UMMA_K steps
+// ascending inside a block) and never depends on M, the tile a row lands in, or the batch, which is
+// what keeps batch_decode(P)[i] == batch_decode({P[i]}) bitwise on the GPU (the invariant the
+// reference proves for its CPU matmul, test_model.cpp:240-267).
+#pragma once
+#include "ptx.cuh"
+
+namespace iolmk {
+
+enum EpiMode : int {
+  EPI_F32 = 0,        // out f32 [M x ldo]
+  EPI_BF16 = 1,       // out bf16 [M x ldo]
+  EPI_GELU_BF16 = 2,  // out bf16 gelu(acc)
+  EPI_RESID_F32 = 3,  // resid f32 [M x ldo] += acc   (x += z*Wo^T, x += g*Wout^T)
+  EPI_QKV = 4,        // cols [0,kh) -> q bf16; [kh,2kh) -> K pages; [2kh,3kh) -> V pages
+};
+
+struct GemmEpi {
+  int M = 0, N = 0;
+  void* out = nullptr;
+  int ldo = 0;
+  // QKV scatter into the paged KV pool of one layer. Page layout: [page][K|V][head][PAGE][hd].
+  __nv_bfloat16* kv_layer = nullptr;
+  const int* tok_slot = nullptr;
+  const int* tok_pos = nullptr;
+  const int* page_table = nullptr;
+  int max_pages = 0;
+  int kh = 0, hd = 0, heads = 0, page_size = 16;
+  // W8A8 dequant epilogue: acc_i32 * a_scale[row] * w_scale[col]
+  const float* a_scale = nullptr;
+  const float* w_scale = nullptr;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int BM = 128;
+  static constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per operand row
+  static constexpr int STAGES = BN >= 256 ? 4 : 6;
+  static constexpr uint32_t A_BYTES = BM * BK_BYTES;
+  static constexpr uint32_t B_BYTES = BN * BK_BYTES;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+template <int EPI>
+__device__ __forceinline__ void epi_apply(const GemmEpi& ep, int m, int n0, float (&v)[32]) {
+  const int N = ep.N;
+  if constexpr (EPI == EPI_GELU_BF16) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+  }
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
+    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n0;
+    if (n0 + 32 <= N && (ep.ldo & 7) == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint4 w;
+        w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+        w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+        w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+        w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+        reinterpret_cast<uint4*>(o)[j] = w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) o[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else if constexpr (EPI == EPI_F32) {
+    float* o = static_cast<float*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n0;
+    if (n0 + 32 <= N && (ep.ldo & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        reinterpret_cast<float4*>(o)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) o[j] = v[j];
+    }
+  } else if constexpr (EPI == EPI_RESID_F32) {
+    float* o = static_cast<float*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n0;
+    if (n0 + 32 <= N && (ep.ldo & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 x = reinterpret_cast<float4*>(o)[j];
+        x.x += v[4 * j];
+        x.y += v[4 * j + 1];
+        x.z += v[4 * j + 2];
+        x.w += v[4 * j + 3];
+        reinterpret_cast<float4*>(o)[j] = x;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) o[j] += v[j];
+    }
+  } else if constexpr (EPI == EPI_QKV) {
+    const int kh = ep.kh;
+    const int slot = ep.tok_slot[m];
+    const int pos = ep.tok_pos[m];
+    const int page = ep.page_table[static_cast<size_t>(slot) * ep.max_pages + pos / ep.page_size];
+    const int in_page = pos % ep.page_size;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + 8 * j;
+      if (n >= N) break;
+      uint4 w;
+      w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+      w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+      w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+      w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+      __nv_bfloat16* dst;
+      if (n < kh) {
+        dst = static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n;
+      } else {
+        const int c = n - kh;
+        const int which = c >= kh ? 1 : 0;
+        const int cc = c - which * kh;
+        const int head = cc / ep.hd;
+        const int dim = cc - head * ep.hd;
+        dst = ep.kv_layer +
+              ((static_cast<size_t>(page) * 2 + which) * ep.heads + head) * ep.page_size * ep.hd +
+              static_cast<size_t>(in_page) * ep.hd + dim;
+      }
+      *reinterpret_cast<uint4*>(dst) = w;
+    }
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        int M, int N, int K, GemmEpi ep) {
+  using C = GemmCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t sA = base;
+  const uint32_t sB = base + STAGES * C::A_BYTES;
+  const uint32_t bars = sB + STAGES * C::B_BYTES;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * STAGES + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * STAGES + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * STAGES + 4);
+  const uint32_t* tmem_slot_ptr =
+      reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - raw));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 4);
+    }
+    mbar_fence_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+
+  const int m_tiles = (M + C::BM - 1) / C::BM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int kbs = (K * 2 + C::BK_BYTES - 1) / C::BK_BYTES;  // 64 bf16 elements per block
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mt = tile / n_tiles;
+        const int nt = tile - mt * n_tiles;
+        for (int kb = 0; kb < kbs; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);
+          mbar_expect_tx(full_bar(stage), C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, full_bar(stage), kb * 64, mt * C::BM);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, full_bar(stage), kb * 64, nt * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16(128, BN, 1);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < kbs; ++kb) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint64_t ad = smem_desc_k_sw128(sA + stage * C::A_BYTES);
+          const uint64_t bd = smem_desc_k_sw128(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_f16(d, ad + 2u * kk, bd + 2u * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+          umma_commit(empty_bar(stage));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        umma_commit(tfull_bar(acc));
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1u;
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mt = tile / n_tiles;
+      const int nt = tile - mt * n_tiles;
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      const int m = mt * C::BM + q * 32 + lane;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                             static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int n0 = nt * BN + c * 32;
+        if (n0 >= N) break;  // warp-uniform
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tbase + c * 32, r);
+        tmem_ld_wait();
+        if (m < M) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          epi_apply<EPI>(ep, m, n0, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar(acc));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1u;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+}  // namespace iolmk

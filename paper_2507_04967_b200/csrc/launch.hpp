@@ -1,0 +1,59 @@
+// Host-side declarations shared by the engine translation units: error types (mapped 1:1 onto the
+// C-ABI status codes in include/iolm_cuda.h) and kernel launchers.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "gemm_sm100.cuh"
+#include "../../include/iolm_cuda.h"
+
+namespace iolmh {
+
+// One exception per C-ABI status; the C entry points catch these and return the code.
+struct EngineError : std::runtime_error {
+  int code;
+  EngineError(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+struct ContractViolation : EngineError {
+  explicit ContractViolation(const std::string& w) : EngineError(IOLM_E_CONTRACT, w) {}
+};
+struct SequenceTooLong : EngineError {
+  explicit SequenceTooLong(const std::string& w) : EngineError(IOLM_E_SEQ_TOO_LONG, w) {}
+};
+struct Unsupported : EngineError {
+  explicit Unsupported(const std::string& w) : EngineError(IOLM_E_UNSUPPORTED, w) {}
+};
+struct CudaError : EngineError {
+  explicit CudaError(const std::string& w) : EngineError(IOLM_E_CUDA, w) {}
+};
+struct OutOfMemory : EngineError {
+  explicit OutOfMemory(const std::string& w) : EngineError(IOLM_E_OOM, w) {}
+};
+struct CorruptHeader : EngineError {
+  explicit CorruptHeader(const std::string& w) : EngineError(IOLM_E_CORRUPT_HEADER, w) {}
+};
+struct TruncatedBlob : EngineError {
+  explicit TruncatedBlob(const std::string& w) : EngineError(IOLM_E_TRUNCATED_BLOB, w) {}
+};
+struct UnknownEncoding : EngineError {
+  explicit UnknownEncoding(const std::string& w) : EngineError(IOLM_E_UNKNOWN_ENCODING, w) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  std::string msg = std::string(what) + " failed at " + file + ":" + std::to_string(line) + ": " +
+                    cudaGetErrorString(e);
+  if (e == cudaErrorMemoryAllocation) throw OutOfMemory(msg);
+  throw CudaError(msg);
+}
+#define CUDA_OK(x) ::iolmh::cuda_check((x), #x, __FILE__, __LINE__)
+
+// ---- launchers (gemm_launch.cu, kernels.cu)
+void launch_gemm_bf16(int bn, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N,
+                      int K, const iolmk::GemmEpi& ep, cudaStream_t st, int grid_cap);
+
+}  // namespace iolmh

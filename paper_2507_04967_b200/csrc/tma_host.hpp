@@ -1,0 +1,51 @@
+// Host-side TMA descriptor construction (cuTensorMapEncodeTiled through the runtime's driver
+// entry point, so the library does not link libcuda directly).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace iolmh {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled entry point unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2D K-major operand [rows x inner] with a row stride in bytes; box = 128 bytes of inner x box_rows,
+// SWIZZLE_128B (matches smem_desc_k_sw128 on the device). Out-of-bounds elements read as zero.
+inline CUtensorMap make_kmajor_map(const void* ptr, CUtensorMapDataType dt, int elem_bytes,
+                                   uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
+                                   uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / elem_bytes), box_rows};
+  cuuint32_t es[2] = {1, 1};
+  if ((row_stride_bytes % 16) != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
+    throw std::runtime_error("TMA operand must be 16-byte aligned with a 16-byte row stride");
+  CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed with code " + std::to_string(r));
+  return m;
+}
+
+}  // namespace iolmh

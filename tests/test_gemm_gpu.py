@@ -1,0 +1,59 @@
+"""Parity of the production tcgen05 GEMM (bf16 operands, fp32 accumulate) against an fp32
+reference of the same op on the same bf16-rounded inputs (the reference's `matmul`,
+proj/src/numerics.cpp:56-76, is the f32 sum of the same products)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def bf16_bits(x: np.ndarray) -> np.ndarray:
+    u = x.astype(np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    return r
+
+
+def bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+def run_gemm(lib, A, W, bn=256, epi=0, C0=None):
+    M, K = A.shape
+    N = W.shape[0]
+    a = np.ascontiguousarray(bf16_bits(A))
+    w = np.ascontiguousarray(bf16_bits(W))
+    out = np.zeros((M, N), np.float32) if C0 is None else C0.copy()
+    st = lib.iolm_cuda_debug_gemm_bf16(a.ctypes.data, w.ctypes.data, out.ctypes.data, M, N, K, bn, epi)
+    assert st == 0, lib.iolm_cuda_last_error()
+    return out, bits_to_f32(a).reshape(M, K), bits_to_f32(w).reshape(N, K)
+
+
+@pytest.mark.parametrize("M,N,K,bn", [
+    (128, 256, 64, 256), (300, 3840, 1280, 256), (1000, 1280, 5120, 256), (77, 131, 1280, 128),
+    (4096, 5120, 1280, 256), (33, 96, 32, 128), (129, 2500, 2512, 256),
+])
+def test_gemm_f32(engine_lib, M, N, K, bn):
+    rng = np.random.default_rng(M * 7 + N)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (0.02 * rng.standard_normal((N, K))).astype(np.float32)
+    out, a, w = run_gemm(engine_lib, A, W, bn, 0)
+    ref = a.astype(np.float64) @ w.astype(np.float64).T
+    err = np.abs(out - ref).max() / (np.abs(ref).max() + 1e-30)
+    assert err < 1e-5, err
+
+
+def test_gemm_gelu_resid(engine_lib):
+    rng = np.random.default_rng(3)
+    M, N, K = 500, 1024, 640
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (0.05 * rng.standard_normal((N, K))).astype(np.float32)
+    out, a, w = run_gemm(engine_lib, A, W, 256, 2)
+    x = a.astype(np.float64) @ w.astype(np.float64).T
+    ref = 0.5 * x * (1 + np.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+    assert np.abs(out - ref).max() < 2e-2 * np.abs(ref).max()
+    base = rng.standard_normal((M, N)).astype(np.float32)
+    out, a, w = run_gemm(engine_lib, A, W, 128, 3, base)
+    ref = base + a.astype(np.float64) @ w.astype(np.float64).T
+    assert np.abs(out - ref).max() < 1e-4
