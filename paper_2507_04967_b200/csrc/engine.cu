@@ -1,0 +1,727 @@
+// The B200 model runtime behind the C ABI (include/iolm_cuda.h).
+//
+// Replaces iolm::ModelRuntime (proj/src/runtime.cpp:60-345):
+//   * construction: the bundle is parsed/validated like the reference (bundle.cu), every linear
+//     weight is decoded ONCE on the device into the GEMM operand layout (bf16, K-major = the
+//     bundle's own [out x in] layout, so no transpose), norms/embeddings stay fp32;
+//   * batch_decode: a continuous-batching scheduler. Each engine step is ONE batched forward over
+//     a token list mixing (a) one generated token for every live sequence and (b) the prompt tokens
+//     of newly admitted rows, so every GEMM runs at M = thousands of rows. The common prompt prefix
+//     of the call is prefilled once into shared KV pages that every row's page table references.
+//   * K/V live in a paged bf16 pool (16-token pages); attention reads through per-slot page tables.
+// Output semantics follow batch_decode exactly (runtime.cpp:280-307): argmax (ties -> lowest id),
+// stop on EOS / budget before emitting, stop on a full context after emitting; the FlopCounter
+// contribution is the reference's closed form (runtime.cpp:311-345).
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "bundle.hpp"
+#include "capi_util.hpp"
+#include "kernels.cuh"
+#include "launch.hpp"
+#include "tma_host.hpp"
+
+namespace iolmh {
+
+using iolmk::AttnGroup;
+using iolmk::AttnParams;
+using iolmk::GemmEpi;
+
+void launch_ln(const float* x, int M, int d, const float* g, const float* b, __nv_bfloat16* h, int ldh,
+               cudaStream_t st);
+void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_slot, const int* tok_pos,
+                     const int32_t* last_tok, int M, int d, const float* tok_embed, const float* pos_embed, float* x,
+                     const float* g, const float* b, __nv_bfloat16* h, int ldh, cudaStream_t st);
+void launch_attention(const AttnParams& prefill, const AttnParams& decode, int hd, cudaStream_t st);
+void launch_head(const float* x, int d, const int* rows, int n_rows, const float* g, const float* b,
+                 const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
+                 float* logits_out, cudaStream_t st);
+void launch_lcp(const int32_t* ids, const int64_t* offsets, int64_t n_rows, int limit, int* out, cudaStream_t st);
+void launch_check_ids(const int32_t* ids, int64_t n, int V, int* bad, cudaStream_t st);
+void launch_decode_weight(const void* payload, int enc, int rows, int cols, __nv_bfloat16* dst, int ld,
+                          cudaStream_t st);
+void launch_transpose(const float* src, int rows, int cols, float* dst, cudaStream_t st);
+
+namespace {
+
+constexpr int PAGE = 16;
+constexpr int QCHUNK = 64;
+
+template <typename T>
+struct DevArray {
+  T* p = nullptr;
+  size_t n = 0;
+  DevArray() = default;
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+  ~DevArray() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+};
+
+template <typename T>
+struct PinnedArray {
+  T* p = nullptr;
+  size_t n = 0;
+  PinnedArray() = default;
+  PinnedArray(const PinnedArray&) = delete;
+  ~PinnedArray() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    CUDA_OK(cudaMallocHost(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    n = count;
+  }
+};
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+struct Layer {
+  int heads = 0, kh = 0, f = 0;
+  DevArray<float> ln1_g, ln1_b, ln2_g, ln2_b;
+  DevArray<__nv_bfloat16> w_qkv, w_o, w_in, w_out;
+  int bn_qkv = 256, bn_o = 256, bn_in = 256, bn_out = 256;
+  CUtensorMap tm_qkv, tm_o, tm_in, tm_out;  // B operands (weights)
+  CUtensorMap tm_z, tm_g;                   // A operands with this layer's K extent
+  DevArray<__nv_bfloat16> kv;               // paged pool [pages][K|V][heads][PAGE][hd]
+};
+
+int pick_bn(int N) { return N >= 384 ? 256 : 128; }
+
+}  // namespace
+
+class Engine {
+ public:
+  Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opts* opts);
+  ~Engine() {
+    if (stream_) cudaStreamDestroy(stream_);
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+  }
+
+  const ModelConfig& config() const { return cfg_; }
+  uint64_t bundle_hash() const { return hash_; }
+  const iolm_cuda_stats& stats() const { return stats_; }
+
+  void decode(const int32_t* ids, bool ids_on_device, const int64_t* offsets, int64_t n_rows, int max_new,
+              int32_t* out_ids, int32_t* out_len, uint64_t* madds, int64_t* bad_row);
+  void forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds);
+
+  std::mutex mu;
+
+ private:
+  struct Step {
+    std::vector<int64_t> tok_src;
+    std::vector<int> tok_slot, tok_pos;
+    std::vector<AttnGroup> pre, dec;
+    std::vector<int> head_rows, head_slot;
+    void clear() {
+      tok_src.clear();
+      tok_slot.clear();
+      tok_pos.clear();
+      pre.clear();
+      dec.clear();
+      head_rows.clear();
+      head_slot.clear();
+    }
+    int T() const { return static_cast<int>(tok_src.size()); }
+  };
+
+  void upload_weights(const BundleView& b);
+  void alloc_runtime();
+  void set_prefix_pages(int prefix_pages);
+  void add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head);
+  void run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits);
+  void gemm(int bn, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
+  uint64_t ref_madds_row(int s0, int advances) const;
+
+  ModelConfig cfg_;
+  uint64_t hash_ = 0;
+  int device_ = 0, sms_ = 148;
+  int d_ = 0, L_ = 0, V_ = 0, S_ = 0, hd_ = 0, kh_max_ = 0, f_ld_max_ = 0;
+  int T_max_ = 16384, max_slots_ = 0, pps_ = 0, prefix_slot_ = 0;
+  int cur_prefix_pages_ = -1;
+  bool prefix_sharing_ = true;
+  uint64_t madds_A_ = 0, madds_B_ = 0;  // sum_l (4*d*kh + 2*d*f), sum_l kh
+  cudaStream_t stream_ = nullptr;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  iolm_cuda_stats stats_{};
+
+  std::vector<std::unique_ptr<Layer>> layers_;
+  DevArray<float> tok_embed_, tok_embed_t_, pos_embed_, lnf_g_, lnf_b_;
+  DevArray<float> x_;
+  DevArray<__nv_bfloat16> h_, q_, z_, g_;
+  CUtensorMap tm_h_;
+  DevArray<int> page_table_;
+  DevArray<int64_t> d_tok_src_;
+  DevArray<int> d_tok_slot_, d_tok_pos_, d_head_rows_, d_head_slot_;
+  DevArray<AttnGroup> d_pre_, d_dec_;
+  DevArray<int32_t> d_next_, d_last_tok_, d_ids_;
+  DevArray<int64_t> d_offsets_;
+  DevArray<int> d_scalar_;
+  DevArray<float> d_logits_;
+  DevArray<uint8_t> d_mask_;
+  PinnedArray<int32_t> h_next_;
+  PinnedArray<int32_t> h_ids_stage_;
+};
+
+Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opts* opts) {
+  if (!bytes || len == 0) throw ContractViolation("iolm_cuda_create: empty bundle");
+  BundleView b = parse_bundle(bytes, len);
+  cfg_ = b.config;
+  hash_ = b.hash = fnv1a64(bytes, len);
+  d_ = cfg_.d_model;
+  L_ = cfg_.n_layers;
+  V_ = cfg_.vocab_size;
+  S_ = cfg_.max_seq_len;
+  hd_ = cfg_.head_dim();
+  if (V_ != IOLM_VOCAB) throw Unsupported("vocab_size must be 131 (tokenizer.hpp:17)");
+  if (d_ % 8 != 0) throw Unsupported("d_model must be a multiple of 8 for the GPU layout");
+  if (hd_ != 16 && hd_ != 32 && hd_ != 64 && hd_ != 128)
+    throw Unsupported("head_dim must be 16, 32, 64 or 128 on the GPU path");
+  if (d_ > 4096) throw Unsupported("d_model > 4096");
+  device_ = device;
+  CUDA_OK(cudaSetDevice(device_));
+  CUDA_OK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device_));
+  CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  CUDA_OK(cudaEventCreate(&ev0_));
+  CUDA_OK(cudaEventCreate(&ev1_));
+  if (opts) {
+    if (opts->max_tokens_per_step > 0) T_max_ = opts->max_tokens_per_step;
+    if (opts->max_slots > 0) max_slots_ = opts->max_slots;
+    if (opts->page_size != 0 && opts->page_size != PAGE) throw Unsupported("page_size must be 16");
+    if (opts->act_quant != 0) throw Unsupported("act_quant (W8A8) is not available in this build");
+    if (opts->prefix_sharing < 0) prefix_sharing_ = false;
+  }
+  T_max_ = std::max(round_up(T_max_, 128), round_up(S_, 128));
+  for (int l = 0; l < L_; ++l) {
+    const uint64_t kh = static_cast<uint64_t>(cfg_.layer_heads(l)) * hd_;
+    madds_A_ += 4ull * d_ * kh + 2ull * d_ * cfg_.layer_ffn(l);
+    madds_B_ += kh;
+  }
+  upload_weights(b);
+  alloc_runtime();
+}
+
+void Engine::upload_weights(const BundleView& b) {
+  // Stage every payload through one device scratch buffer; decode kernels write the final layout.
+  size_t max_payload = 0;
+  for (const auto& t : b.tensors) max_payload = std::max<size_t>(max_payload, t.length);
+  DevArray<uint8_t> scratch;
+  scratch.alloc(max_payload + 16);
+  auto upload_f32 = [&](const std::string& name, DevArray<float>& dst) {
+    const auto& t = b.tensor(name);
+    dst.alloc(static_cast<size_t>(t.rows) * t.cols);
+    CUDA_OK(cudaMemcpy(dst.p, b.payload(t), t.length, cudaMemcpyHostToDevice));
+  };
+  upload_f32("tok_embed", tok_embed_);
+  upload_f32("pos_embed", pos_embed_);
+  upload_f32("final_norm.gain", lnf_g_);
+  upload_f32("final_norm.bias", lnf_b_);
+  tok_embed_t_.alloc(static_cast<size_t>(V_) * d_);
+  launch_transpose(tok_embed_.p, V_, d_, tok_embed_t_.p, stream_);
+
+  auto decode_into = [&](const std::string& name, __nv_bfloat16* dst, int ld) {
+    const auto& t = b.tensor(name);
+    CUDA_OK(cudaMemcpyAsync(scratch.p, b.payload(t), t.length, cudaMemcpyHostToDevice, stream_));
+    launch_decode_weight(scratch.p, t.encoding, t.rows, t.cols, dst, ld, stream_);
+    CUDA_OK(cudaStreamSynchronize(stream_));  // scratch is reused by the next tensor
+  };
+  for (int l = 0; l < L_; ++l) {
+    auto ly = std::make_unique<Layer>();
+    const std::string p = "layers." + std::to_string(l) + ".";
+    ly->heads = cfg_.layer_heads(l);
+    ly->kh = ly->heads * hd_;
+    ly->f = cfg_.layer_ffn(l);
+    upload_f32(p + "attn_norm.gain", ly->ln1_g);
+    upload_f32(p + "attn_norm.bias", ly->ln1_b);
+    upload_f32(p + "ffn_norm.gain", ly->ln2_g);
+    upload_f32(p + "ffn_norm.bias", ly->ln2_b);
+    const int kh = ly->kh, f = ly->f, f_ld = round_up(f, 8);
+    ly->w_qkv.alloc(static_cast<size_t>(3) * kh * d_);
+    decode_into(p + "attn.wq", ly->w_qkv.p, d_);
+    decode_into(p + "attn.wk", ly->w_qkv.p + static_cast<size_t>(kh) * d_, d_);
+    decode_into(p + "attn.wv", ly->w_qkv.p + static_cast<size_t>(2) * kh * d_, d_);
+    ly->w_o.alloc(static_cast<size_t>(d_) * kh);
+    decode_into(p + "attn.wo", ly->w_o.p, kh);
+    ly->w_in.alloc(static_cast<size_t>(f) * d_);
+    decode_into(p + "ffn.w_in", ly->w_in.p, d_);
+    ly->w_out.alloc(static_cast<size_t>(d_) * f_ld);
+    decode_into(p + "ffn.w_out", ly->w_out.p, f_ld);
+    ly->bn_qkv = pick_bn(3 * kh);
+    ly->bn_o = pick_bn(d_);
+    ly->bn_in = pick_bn(f);
+    ly->bn_out = pick_bn(d_);
+    const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    ly->tm_qkv = make_kmajor_map(ly->w_qkv.p, BF, 2, d_, 3ull * kh, 2ull * d_, ly->bn_qkv);
+    ly->tm_o = make_kmajor_map(ly->w_o.p, BF, 2, kh, d_, 2ull * kh, ly->bn_o);
+    ly->tm_in = make_kmajor_map(ly->w_in.p, BF, 2, d_, f, 2ull * d_, ly->bn_in);
+    ly->tm_out = make_kmajor_map(ly->w_out.p, BF, 2, f, d_, 2ull * f_ld, ly->bn_out);
+    kh_max_ = std::max(kh_max_, kh);
+    f_ld_max_ = std::max(f_ld_max_, f_ld);
+    layers_.push_back(std::move(ly));
+  }
+  CUDA_OK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::alloc_runtime() {
+  const size_t T = T_max_;
+  x_.alloc(T * d_);
+  h_.alloc(T * d_);
+  q_.alloc(T * kh_max_);
+  z_.alloc(T * kh_max_);
+  g_.alloc(T * f_ld_max_);
+  CUDA_OK(cudaMemset(z_.p, 0, T * kh_max_ * sizeof(__nv_bfloat16)));
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  tm_h_ = make_kmajor_map(h_.p, BF, 2, d_, T, 2ull * d_, 128);
+  for (auto& ly : layers_) {
+    ly->tm_z = make_kmajor_map(z_.p, BF, 2, ly->kh, T, 2ull * kh_max_, 128);
+    ly->tm_g = make_kmajor_map(g_.p, BF, 2, ly->f, T, 2ull * f_ld_max_, 128);
+  }
+  d_tok_src_.alloc(T);
+  d_tok_slot_.alloc(T);
+  d_tok_pos_.alloc(T);
+  d_head_rows_.alloc(T);
+  d_head_slot_.alloc(T);
+  d_pre_.alloc(T);
+  d_dec_.alloc(T);
+  d_next_.alloc(T);
+  h_next_.ensure(T);
+  d_logits_.alloc(T * V_);
+  d_mask_.alloc(S_);
+  d_scalar_.alloc(4);
+
+  // Paged KV pool: one fixed run of pps_ pages per slot plus one prefix slot.
+  pps_ = (S_ + PAGE - 1) / PAGE;
+  size_t bytes_per_slot = 0;
+  for (auto& ly : layers_) bytes_per_slot += static_cast<size_t>(pps_) * 2 * ly->heads * PAGE * hd_ * 2;
+  size_t free_b = 0, total_b = 0;
+  CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+  const size_t cap = static_cast<size_t>(0.7 * static_cast<double>(free_b)) / std::max<size_t>(bytes_per_slot, 1);
+  if (max_slots_ <= 0) max_slots_ = 2048;
+  max_slots_ = static_cast<int>(std::min<size_t>(max_slots_, cap > 1 ? cap - 1 : 0));
+  if (max_slots_ < 1) throw OutOfMemory("KV pool: not enough device memory for one sequence");
+  prefix_slot_ = max_slots_;
+  const size_t pages = static_cast<size_t>(max_slots_ + 1) * pps_;
+  for (auto& ly : layers_) {
+    const size_t elems = pages * 2 * ly->heads * PAGE * hd_;
+    ly->kv.alloc(elems);
+    CUDA_OK(cudaMemset(ly->kv.p, 0, elems * sizeof(__nv_bfloat16)));
+  }
+  page_table_.alloc(static_cast<size_t>(max_slots_ + 1) * pps_);
+  d_last_tok_.alloc(max_slots_ + 1);
+  CUDA_OK(cudaMemset(d_last_tok_.p, 0, (max_slots_ + 1) * sizeof(int32_t)));
+}
+
+// Page table: slot s owns pages [s*pps, (s+1)*pps); positions below the shared prefix map to the
+// prefix slot's pages instead.
+void Engine::set_prefix_pages(int prefix_pages) {
+  if (prefix_pages == cur_prefix_pages_) return;
+  std::vector<int> pt(static_cast<size_t>(max_slots_ + 1) * pps_);
+  for (int s = 0; s <= max_slots_; ++s)
+    for (int i = 0; i < pps_; ++i)
+      pt[static_cast<size_t>(s) * pps_ + i] =
+          (s != prefix_slot_ && i < prefix_pages) ? prefix_slot_ * pps_ + i : s * pps_ + i;
+  CUDA_OK(cudaMemcpyAsync(page_table_.p, pt.data(), pt.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+  CUDA_OK(cudaStreamSynchronize(stream_));
+  cur_prefix_pages_ = prefix_pages;
+}
+
+void Engine::add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head) {
+  const int m0 = s.T();
+  for (int p = p_begin; p < p_end; ++p) {
+    s.tok_src.push_back(src_base + p);
+    s.tok_slot.push_back(slot);
+    s.tok_pos.push_back(p);
+  }
+  for (int c = p_begin; c < p_end; c += QCHUNK)
+    s.pre.push_back(AttnGroup{slot, m0 + (c - p_begin), std::min(QCHUNK, p_end - c), c});
+  if (want_head) {
+    s.head_rows.push_back(m0 + (p_end - p_begin) - 1);
+    s.head_slot.push_back(slot);
+  }
+}
+
+void Engine::gemm(int bn, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
+                  const GemmEpi& ep) {
+  launch_gemm_bf16(bn, epi, A, B, M, N, K, ep, stream_, sms_);
+  ++stats_.kernel_launches;
+}
+
+void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits) {
+  const int T = s.T();
+  auto h2d = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes) CUDA_OK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_));
+  };
+  h2d(d_tok_src_.p, s.tok_src.data(), T * sizeof(int64_t));
+  h2d(d_tok_slot_.p, s.tok_slot.data(), T * sizeof(int));
+  h2d(d_tok_pos_.p, s.tok_pos.data(), T * sizeof(int));
+  h2d(d_pre_.p, s.pre.data(), s.pre.size() * sizeof(AttnGroup));
+  h2d(d_dec_.p, s.dec.data(), s.dec.size() * sizeof(AttnGroup));
+  h2d(d_head_rows_.p, s.head_rows.data(), s.head_rows.size() * sizeof(int));
+  h2d(d_head_slot_.p, s.head_slot.data(), s.head_slot.size() * sizeof(int));
+
+  launch_embed_ln(d_ids, d_tok_src_.p, d_tok_slot_.p, d_tok_pos_.p, d_last_tok_.p, T, d_, tok_embed_.p,
+                  pos_embed_.p, x_.p, layers_[0]->ln1_g.p, layers_[0]->ln1_b.p, h_.p, d_, stream_);
+  ++stats_.kernel_launches;
+  const float scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(hd_));
+  for (int l = 0; l < L_; ++l) {
+    Layer& ly = *layers_[l];
+    GemmEpi ep;
+    ep.M = T;
+    // QKV projection; K/V scattered into the paged pool by the epilogue.
+    ep.N = 3 * ly.kh;
+    ep.out = q_.p;
+    ep.ldo = kh_max_;
+    ep.kv_layer = ly.kv.p;
+    ep.tok_slot = d_tok_slot_.p;
+    ep.tok_pos = d_tok_pos_.p;
+    ep.page_table = page_table_.p;
+    ep.max_pages = pps_;
+    ep.kh = ly.kh;
+    ep.hd = hd_;
+    ep.heads = ly.heads;
+    ep.page_size = PAGE;
+    gemm(ly.bn_qkv, iolmk::EPI_QKV, tm_h_, ly.tm_qkv, T, 3 * ly.kh, d_, ep);
+    // attention
+    AttnParams ap{};
+    ap.q = q_.p;
+    ap.ldq = kh_max_;
+    ap.z = z_.p;
+    ap.ldz = kh_max_;
+    ap.kv = ly.kv.p;
+    ap.page_table = page_table_.p;
+    ap.max_pages = pps_;
+    ap.heads = ly.heads;
+    ap.key_mask = d_key_mask;
+    ap.scale_log2 = scale_log2;
+    AttnParams pre = ap, dec = ap;
+    pre.groups = d_pre_.p;
+    pre.n_groups = static_cast<int>(s.pre.size());
+    dec.groups = d_dec_.p;
+    dec.n_groups = static_cast<int>(s.dec.size());
+    launch_attention(pre, dec, hd_, stream_);
+    stats_.kernel_launches += (pre.n_groups > 0) + (dec.n_groups > 0);
+    // x += z * Wo^T
+    GemmEpi eo;
+    eo.M = T;
+    eo.N = d_;
+    eo.out = x_.p;
+    eo.ldo = d_;
+    gemm(ly.bn_o, iolmk::EPI_RESID_F32, ly.tm_z, ly.tm_o, T, d_, ly.kh, eo);
+    // h = LN2(x)
+    launch_ln(x_.p, T, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_);
+    ++stats_.kernel_launches;
+    // g = gelu(h * Win^T)
+    GemmEpi ei;
+    ei.M = T;
+    ei.N = ly.f;
+    ei.out = g_.p;
+    ei.ldo = f_ld_max_;
+    gemm(ly.bn_in, iolmk::EPI_GELU_BF16, tm_h_, ly.tm_in, T, ly.f, d_, ei);
+    // x += g * Wout^T
+    gemm(ly.bn_out, iolmk::EPI_RESID_F32, ly.tm_g, ly.tm_out, T, d_, ly.f, eo);
+    if (l + 1 < L_) {
+      launch_ln(x_.p, T, d_, layers_[l + 1]->ln1_g.p, layers_[l + 1]->ln1_b.p, h_.p, d_, stream_);
+      ++stats_.kernel_launches;
+    }
+  }
+  const int R = static_cast<int>(s.head_rows.size());
+  if (R > 0) {
+    launch_head(x_.p, d_, d_head_rows_.p, R, lnf_g_.p, lnf_b_.p, tok_embed_t_.p, V_, d_head_slot_.p, d_next_.p,
+                d_last_tok_.p, d_logits, stream_);
+    ++stats_.kernel_launches;
+    CUDA_OK(cudaMemcpyAsync(h_next_.p, d_next_.p, R * sizeof(int32_t), cudaMemcpyDeviceToHost, stream_));
+  }
+  ++stats_.steps;
+  stats_.tokens += T;
+}
+
+uint64_t Engine::ref_madds_row(int s0, int advances) const {
+  const uint64_t dv = static_cast<uint64_t>(d_) * V_;
+  const uint64_t S0 = static_cast<uint64_t>(s0);
+  uint64_t t = S0 * madds_A_ + madds_B_ * S0 * (S0 + 1) + dv;
+  for (int i = 1; i <= advances; ++i) t += madds_A_ + 2 * madds_B_ * (S0 + static_cast<uint64_t>(i)) + dv;
+  return t;
+}
+
+void Engine::decode(const int32_t* ids, bool ids_on_device, const int64_t* offsets, int64_t n_rows, int max_new,
+                    int32_t* out_ids, int32_t* out_len, uint64_t* madds, int64_t* bad_row) {
+  CUDA_OK(cudaSetDevice(device_));
+  stats_ = iolm_cuda_stats{};
+  if (bad_row) *bad_row = -1;
+  if (n_rows <= 0) throw ContractViolation("batch_decode: batch size must be >= 1");
+  if (max_new < 0) throw ContractViolation("batch_decode: max_new_tokens must be >= 0");
+  if (!offsets || !out_len || (max_new > 0 && !out_ids)) throw ContractViolation("batch_decode: null buffer");
+  for (int64_t i = 0; i < n_rows; ++i) out_len[i] = 0;
+  if (madds) *madds = 0;
+  if (max_new == 0) return;  // runtime.cpp:249 - no encode, no compute
+  int min_len = INT32_MAX;
+  for (int64_t i = 0; i < n_rows; ++i) {
+    const int64_t len = offsets[i + 1] - offsets[i];
+    if (len <= 0) throw ContractViolation("batch_decode: empty token row " + std::to_string(i));
+    if (len > S_) {
+      if (bad_row) *bad_row = i;
+      throw SequenceTooLong("batch_decode: prompt " + std::to_string(i) + " needs " + std::to_string(len) +
+                            " tokens, max_seq_len is " + std::to_string(S_));
+    }
+    min_len = std::min<int>(min_len, static_cast<int>(len));
+  }
+  CUDA_OK(cudaEventRecord(ev0_, stream_));
+  const int64_t total = offsets[n_rows] - offsets[0];
+  const int32_t* d_ids;
+  const int64_t base = offsets[0];
+  if (ids_on_device) {
+    d_ids = ids;
+  } else {
+    d_ids_.ensure(total + 1);
+    CUDA_OK(cudaMemcpyAsync(d_ids_.p, ids + base, total * sizeof(int32_t), cudaMemcpyHostToDevice, stream_));
+    d_ids = d_ids_.p - base;  // keep absolute offsets valid
+  }
+  // id range check + longest common prefix, on the device
+  d_offsets_.ensure(n_rows + 1);
+  CUDA_OK(cudaMemcpyAsync(d_offsets_.p, offsets, (n_rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+  int init[2] = {1, min_len - 1};
+  CUDA_OK(cudaMemcpyAsync(d_scalar_.p, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
+  launch_check_ids(d_ids + base, total, V_, d_scalar_.p, stream_);
+  if (prefix_sharing_) launch_lcp(d_ids, d_offsets_.p, n_rows, min_len - 1, d_scalar_.p + 1, stream_);
+  int res[2];
+  CUDA_OK(cudaMemcpyAsync(res, d_scalar_.p, sizeof(res), cudaMemcpyDeviceToHost, stream_));
+  CUDA_OK(cudaStreamSynchronize(stream_));
+  if (res[0] == 0) throw ContractViolation("forward: token id out of range");
+  const int prefix_pages = prefix_sharing_ ? std::max(0, res[1]) / PAGE : 0;
+  const int P = prefix_pages * PAGE;
+  set_prefix_pages(prefix_pages);
+
+  Step s;
+  if (P > 0) {  // shared prefix: K/V only, computed once per call
+    s.clear();
+    add_prefill(s, prefix_slot_, offsets[0], 0, P, false);
+    run_step(s, d_ids, nullptr, nullptr);
+    stats_.prefix_tokens += P;
+  }
+
+  struct RowState {
+    int slot = -1, s0 = 0, cur = 0, emitted = 0;
+  };
+  std::vector<RowState> rows(n_rows);
+  std::vector<int> slot_row(max_slots_, -1);
+  std::vector<int> free_slots;
+  for (int sl = max_slots_ - 1; sl >= 0; --sl) free_slots.push_back(sl);
+  std::vector<int> decode_slots, next_decode;
+  int64_t next_row = 0;
+  uint64_t madd_total = 0;
+  while (next_row < n_rows || !decode_slots.empty()) {
+    s.clear();
+    for (int sl : decode_slots) {
+      RowState& r = rows[slot_row[sl]];
+      const int m = s.T();
+      s.tok_src.push_back(-1);  // token comes from the slot's last argmax (device register)
+      s.tok_slot.push_back(sl);
+      s.tok_pos.push_back(r.cur);
+      s.dec.push_back(AttnGroup{sl, m, 1, r.cur});
+      s.head_rows.push_back(m);
+      s.head_slot.push_back(sl);
+      ++r.cur;  // sequence length after this step's advance
+    }
+    stats_.decode_tokens += s.T();
+    while (next_row < n_rows && !free_slots.empty()) {
+      const int len = static_cast<int>(offsets[next_row + 1] - offsets[next_row]);
+      if (s.T() + (len - P) > T_max_) break;
+      const int sl = free_slots.back();
+      free_slots.pop_back();
+      slot_row[sl] = static_cast<int>(next_row);
+      rows[next_row].slot = sl;
+      rows[next_row].s0 = len;
+      rows[next_row].cur = len;
+      add_prefill(s, sl, offsets[next_row], P, len, true);
+      stats_.prefill_tokens += len - P;
+      ++next_row;
+    }
+    if (s.T() == 0) throw CudaError("scheduler stalled (no slot or token budget)");
+    run_step(s, d_ids, nullptr, nullptr);
+    CUDA_OK(cudaStreamSynchronize(stream_));
+    next_decode.clear();
+    for (size_t i = 0; i < s.head_slot.size(); ++i) {
+      const int sl = s.head_slot[i];
+      const int ri = slot_row[sl];
+      RowState& r = rows[ri];
+      const int nxt = h_next_.p[i];
+      int advances = -1;  // >= 0 once the row is finished: advances the reference performs
+      if (nxt == IOLM_EOS || r.emitted == max_new) {
+        advances = r.emitted;  // stop before emitting (runtime.cpp:287-290)
+      } else {
+        out_ids[static_cast<size_t>(ri) * max_new + r.emitted] = nxt;
+        ++r.emitted;
+        if (r.cur == S_) {
+          advances = r.emitted - 1;  // context full: stop without advancing (runtime.cpp:293-296)
+        } else if (r.emitted == max_new) {
+          advances = r.emitted;  // the reference advances once more and discards the logits
+        } else {
+          next_decode.push_back(sl);
+        }
+      }
+      if (advances >= 0) {
+        out_len[ri] = r.emitted;
+        madd_total += ref_madds_row(r.s0, advances);
+        slot_row[sl] = -1;
+        free_slots.push_back(sl);
+      }
+    }
+    decode_slots.swap(next_decode);
+  }
+  if (madds) *madds = madd_total;
+  CUDA_OK(cudaEventRecord(ev1_, stream_));
+  CUDA_OK(cudaEventSynchronize(ev1_));
+  float ms = 0.f;
+  CUDA_OK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  stats_.device_ms = ms;
+}
+
+void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds) {
+  CUDA_OK(cudaSetDevice(device_));
+  stats_ = iolm_cuda_stats{};
+  if (n <= 0 || !ids) throw ContractViolation("forward: empty sequence");
+  if (n > S_)
+    throw SequenceTooLong("forward: sequence length " + std::to_string(n) + " exceeds max_seq_len " +
+                          std::to_string(S_));
+  for (int i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= V_) throw ContractViolation("forward: token id out of range");
+  CUDA_OK(cudaEventRecord(ev0_, stream_));
+  d_ids_.ensure(n);
+  CUDA_OK(cudaMemcpyAsync(d_ids_.p, ids, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream_));
+  const uint8_t* dmask = nullptr;
+  if (mask) {
+    CUDA_OK(cudaMemcpyAsync(d_mask_.p, mask, n, cudaMemcpyHostToDevice, stream_));
+    dmask = d_mask_.p;
+  }
+  set_prefix_pages(0);
+  Step s;
+  add_prefill(s, 0, 0, 0, n, false);
+  for (int i = 0; i < n; ++i) {
+    s.head_rows.push_back(i);
+    s.head_slot.push_back(0);
+  }
+  run_step(s, d_ids_.p, dmask, d_logits_.p);
+  CUDA_OK(cudaMemcpyAsync(logits, d_logits_.p, sizeof(float) * n * V_, cudaMemcpyDeviceToHost, stream_));
+  CUDA_OK(cudaEventRecord(ev1_, stream_));
+  CUDA_OK(cudaEventSynchronize(ev1_));
+  float ms = 0.f;
+  CUDA_OK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  stats_.device_ms = ms;
+  stats_.prefill_tokens = n;
+  if (madds) {
+    // full_forward_flops with the reference's attention count for a masked sequence
+    uint64_t t = 0;
+    const uint64_t dv = static_cast<uint64_t>(d_) * V_;
+    for (int i = 0; i < n; ++i) {
+      t += madds_A_ + dv;
+      if (!mask || mask[i]) t += 2 * madds_B_ * static_cast<uint64_t>(i + 1);
+    }
+    *madds = t;
+  }
+}
+
+}  // namespace iolmh
+
+// ====================================================================== C ABI
+using iolmh::Engine;
+using iolmh::guarded;
+
+struct iolm_cuda_ctx {
+  std::unique_ptr<Engine> eng;
+};
+
+extern "C" int iolm_cuda_create(const uint8_t* bundle_bytes, size_t len, int device, const iolm_cuda_opts* opts,
+                                iolm_cuda_ctx** out) {
+  return guarded([&] {
+    if (!out) throw iolmh::ContractViolation("iolm_cuda_create: null out");
+    *out = nullptr;
+    auto ctx = std::make_unique<iolm_cuda_ctx>();
+    ctx->eng = std::make_unique<Engine>(bundle_bytes, len, device, opts);
+    *out = ctx.release();
+  });
+}
+
+extern "C" void iolm_cuda_destroy(iolm_cuda_ctx* ctx) { delete ctx; }
+
+extern "C" int iolm_cuda_bundle_hash(const iolm_cuda_ctx* ctx, uint64_t* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw iolmh::ContractViolation("null argument");
+    *out = ctx->eng->bundle_hash();
+  });
+}
+
+extern "C" int iolm_cuda_config(const iolm_cuda_ctx* ctx, iolm_cuda_model_config* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw iolmh::ContractViolation("null argument");
+    const auto& c = ctx->eng->config();
+    *out = iolm_cuda_model_config{c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.d_ff, c.max_seq_len,
+                                  c.head_dim()};
+  });
+}
+
+extern "C" int iolm_cuda_layer_shape(const iolm_cuda_ctx* ctx, int32_t layer, int32_t* heads, int32_t* ffn) {
+  return guarded([&] {
+    if (!ctx || !heads || !ffn) throw iolmh::ContractViolation("null argument");
+    const auto& c = ctx->eng->config();
+    if (layer < 0 || layer >= c.n_layers) throw iolmh::ContractViolation("layer index out of range");
+    *heads = c.layer_heads(layer);
+    *ffn = c.layer_ffn(layer);
+  });
+}
+
+extern "C" int iolm_cuda_decode(iolm_cuda_ctx* ctx, const int32_t* ids, const int64_t* row_offsets, int64_t n_rows,
+                                int32_t max_new_tokens, int32_t* out_ids, int32_t* out_len, uint64_t* madds,
+                                int64_t* bad_row) {
+  return guarded([&] {
+    if (!ctx) throw iolmh::ContractViolation("null context");
+    std::lock_guard<std::mutex> lock(ctx->eng->mu);
+    ctx->eng->decode(ids, false, row_offsets, n_rows, max_new_tokens, out_ids, out_len, madds, bad_row);
+  });
+}
+
+extern "C" int iolm_cuda_decode_device_ids(iolm_cuda_ctx* ctx, const int32_t* d_ids, const int64_t* row_offsets,
+                                           int64_t n_rows, int32_t max_new_tokens, int32_t* out_ids,
+                                           int32_t* out_len, uint64_t* madds, int64_t* bad_row) {
+  return guarded([&] {
+    if (!ctx) throw iolmh::ContractViolation("null context");
+    std::lock_guard<std::mutex> lock(ctx->eng->mu);
+    ctx->eng->decode(d_ids, true, row_offsets, n_rows, max_new_tokens, out_ids, out_len, madds, bad_row);
+  });
+}
+
+extern "C" int iolm_cuda_forward_logits(iolm_cuda_ctx* ctx, const int32_t* ids, const uint8_t* mask, int32_t n,
+                                        float* logits, uint64_t* madds) {
+  return guarded([&] {
+    if (!ctx || !logits) throw iolmh::ContractViolation("null argument");
+    std::lock_guard<std::mutex> lock(ctx->eng->mu);
+    ctx->eng->forward(ids, mask, n, logits, madds);
+  });
+}
+
+extern "C" int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw iolmh::ContractViolation("null argument");
+    *out = ctx->eng->stats();
+  });
+}

@@ -1,0 +1,611 @@
+// Non-GEMM kernels of the prompt() hot path on sm_100a:
+//   embed_ln_kernel   x = tok_embed[id] + pos_embed[pos]; h = LN1(x)       (runtime.cpp:122-141)
+//   ln_kernel         h = LN(x) -> bf16 GEMM operand                        (numerics.cpp:158-177)
+//   attn_prefill      causal flash attention over paged KV, mma.sync tiles  (runtime.cpp:152-174)
+//   attn_decode       one query per sequence, split by absolute 32-key chunks
+//   head_argmax       final LN + tied head (fp32) + greedy argmax           (runtime.cpp:202-215,
+//                                                                            numerics.cpp:190-197)
+//   lcp / decode helpers
+#include <cfloat>
+#include <cmath>
+
+#include "kernels.cuh"
+#include "launch.hpp"
+#include "ptx.cuh"
+
+namespace iolmk {
+
+constexpr int PAGE = 16;
+
+// ------------------------------------------------------------------ LayerNorm
+// One warp per row. Two-pass mean / variance in fp32 over the row held in registers.
+template <int MAXV>  // max float4 per lane
+__device__ __forceinline__ void ln_row_warp(const float* __restrict__ xr, int d, const float* __restrict__ g,
+                                            const float* __restrict__ b, __nv_bfloat16* __restrict__ hr,
+                                            int lane) {
+  float4 v[MAXV];
+  const int nv = d >> 2;
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int idx = lane + 32 * i;
+    if (idx < nv) {
+      v[i] = reinterpret_cast<const float4*>(xr)[idx];
+      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / static_cast<float>(d);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int idx = lane + 32 * i;
+    if (idx < nv) {
+      const float a = v[i].x - mean, bb = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
+      q += (a * a + bb * bb) + (c * c + e * e);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float inv = 1.0f / sqrtf(q / static_cast<float>(d) + 1e-5f);
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int idx = lane + 32 * i;
+    if (idx < nv) {
+      const float4 gg = reinterpret_cast<const float4*>(g)[idx];
+      const float4 bb = reinterpret_cast<const float4*>(b)[idx];
+      uint2 w;
+      w.x = pack_bf16x2((v[i].x - mean) * inv * gg.x + bb.x, (v[i].y - mean) * inv * gg.y + bb.y);
+      w.y = pack_bf16x2((v[i].z - mean) * inv * gg.z + bb.z, (v[i].w - mean) * inv * gg.w + bb.w);
+      reinterpret_cast<uint2*>(hr)[idx] = w;
+    }
+  }
+}
+
+template <int MAXV>
+__global__ void __launch_bounds__(256) ln_kernel(const float* __restrict__ x, int M, int d,
+                                                 const float* __restrict__ g, const float* __restrict__ b,
+                                                 __nv_bfloat16* __restrict__ h, int ldh) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= M) return;
+  ln_row_warp<MAXV>(x + static_cast<size_t>(row) * d, d, g, b, h + static_cast<size_t>(row) * ldh,
+                    threadIdx.x & 31);
+}
+
+// token id of step row m: prompt tokens come from the id table, generated tokens from the
+// per-slot "last token" register written by head_argmax_kernel.
+template <int MAXV>
+__global__ void __launch_bounds__(256)
+    embed_ln_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ tok_src,
+                    const int* __restrict__ tok_slot, const int* __restrict__ tok_pos,
+                    const int32_t* __restrict__ last_tok, int M, int d, const float* __restrict__ tok_embed,
+                    const float* __restrict__ pos_embed, float* __restrict__ x, const float* __restrict__ g,
+                    const float* __restrict__ b, __nv_bfloat16* __restrict__ h, int ldh) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= M) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t src = tok_src[row];
+  const int id = src >= 0 ? ids[src] : last_tok[tok_slot[row]];
+  const float4* te = reinterpret_cast<const float4*>(tok_embed + static_cast<size_t>(id) * d);
+  const float4* pe = reinterpret_cast<const float4*>(pos_embed + static_cast<size_t>(tok_pos[row]) * d);
+  float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(row) * d);
+  for (int i = lane; i < (d >> 2); i += 32) {
+    const float4 a = te[i], c = pe[i];
+    xr[i] = make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
+  }
+  __syncwarp();
+  ln_row_warp<MAXV>(x + static_cast<size_t>(row) * d, d, g, b, h + static_cast<size_t>(row) * ldh, lane);
+}
+
+// ------------------------------------------------------------------ attention (prefill, mma.sync)
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// 64 queries of one group x one head per CTA (4 warps x 16 query rows). Key blocks of 64 positions
+// aligned to absolute position 0, so a query's arithmetic depends only on its own position and the
+// K/V values (never on how the step was composed): batch-invariant.
+template <int HD>
+__global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
+  constexpr int LD = HD + 8;
+  constexpr int KB = 64;
+  extern __shared__ __align__(16) uint8_t attn_smem[];
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(attn_smem);
+  __nv_bfloat16* sK = sQ + 64 * LD;
+  __nv_bfloat16* sV = sK + KB * LD;
+  const AttnGroup grp = p.groups[blockIdx.x];
+  const int head = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  for (int idx = tid; idx < 64 * (HD / 8); idx += 128) {
+    const int r = idx / (HD / 8), c = (idx % (HD / 8)) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < grp.nq)
+      v = *reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(grp.m0 + r) * p.ldq + head * HD + c);
+    *reinterpret_cast<uint4*>(sQ + r * LD + c) = v;
+  }
+  __syncthreads();
+  uint32_t qf[HD / 16][4];
+#pragma unroll
+  for (int kc = 0; kc < HD / 16; ++kc)
+    ldsm_x4(qf[kc], sQ + (warp * 16 + (lane & 15)) * LD + kc * 16 + (lane >> 4) * 8);
+
+  const int last_key = grp.pos0 + grp.nq - 1;
+  const int qpos0 = grp.pos0 + warp * 16 + gq;  // rows gq and gq+8 of this warp
+  const int qpos1 = qpos0 + 8;
+  const int warp_max_pos = grp.pos0 + min(grp.nq - 1, warp * 16 + 15);
+  float m_i[2] = {-INFINITY, -INFINITY};
+  float l_i[2] = {0.f, 0.f};
+  float o[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+
+  const size_t head_off = static_cast<size_t>(head) * PAGE * HD;
+  const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
+  const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
+  const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
+  const int nblocks = last_key / KB + 1;
+  for (int kb = 0; kb < nblocks; ++kb) {
+    __syncthreads();
+    for (int idx = tid; idx < KB * (HD / 8); idx += 128) {
+      const int r = idx / (HD / 8), c = (idx % (HD / 8)) * 8;
+      const int pos = kb * KB + r;
+      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+      if (pos <= last_key) {
+        const int pg = pt[pos / PAGE];
+        const __nv_bfloat16* base = p.kv + static_cast<size_t>(pg) * page_stride + head_off + (pos % PAGE) * HD + c;
+        kv = *reinterpret_cast<const uint4*>(base);
+        vv = *reinterpret_cast<const uint4*>(base + v_off);
+      }
+      *reinterpret_cast<uint4*>(sK + r * LD + c) = kv;
+      *reinterpret_cast<uint4*>(sV + r * LD + c) = vv;
+    }
+    __syncthreads();
+    if (kb * KB > warp_max_pos || warp * 16 >= grp.nq) continue;  // warp-uniform: nothing visible
+
+    float s[KB / 8][4];
+#pragma unroll
+    for (int i = 0; i < KB / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < HD / 16; ++kc) {
+#pragma unroll
+      for (int np = 0; np < KB / 16; ++np) {
+        uint32_t b[4];
+        ldsm_x4(b, sK + (np * 16 + (lane & 7) + (lane >> 4) * 8) * LD + kc * 16 + ((lane >> 3) & 1) * 8);
+        mma_bf16(s[2 * np], qf[kc], b[0], b[1]);
+        mma_bf16(s[2 * np + 1], qf[kc], b[2], b[3]);
+      }
+    }
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int nt = 0; nt < KB / 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = kb * KB + nt * 8 + 2 * tq + (e & 1);
+        const int qp = e < 2 ? qpos0 : qpos1;
+        bool ok = key <= qp;
+        if (p.key_mask) ok = ok && p.key_mask[key];
+        const float v = ok ? s[nt][e] * p.scale_log2 : -INFINITY;
+        s[nt][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+    }
+    float alpha[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      const float mnew = fmaxf(m_i[r], mx[r]);
+      alpha[r] = mnew == -INFINITY ? 1.f : exp2f(m_i[r] - mnew);
+      m_i[r] = mnew;
+      l_i[r] *= alpha[r];
+    }
+#pragma unroll
+    for (int nt = 0; nt < KB / 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float mm = m_i[e >> 1];
+        const float pv = mm == -INFINITY ? 0.f : exp2f(s[nt][e] - mm);
+        s[nt][e] = pv;
+        l_i[e >> 1] += pv;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      o[i][0] *= alpha[0];
+      o[i][1] *= alpha[0];
+      o[i][2] *= alpha[1];
+      o[i][3] *= alpha[1];
+    }
+#pragma unroll
+    for (int kc = 0; kc < KB / 16; ++kc) {
+      uint32_t a[4];
+      a[0] = pack_bf16x2(s[2 * kc][0], s[2 * kc][1]);
+      a[1] = pack_bf16x2(s[2 * kc][2], s[2 * kc][3]);
+      a[2] = pack_bf16x2(s[2 * kc + 1][0], s[2 * kc + 1][1]);
+      a[3] = pack_bf16x2(s[2 * kc + 1][2], s[2 * kc + 1][3]);
+#pragma unroll
+      for (int dn = 0; dn < HD / 16; ++dn) {
+        uint32_t b[4];
+        ldsm_x4_t(b, sV + (kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LD + dn * 16 + (lane >> 4) * 8);
+        mma_bf16(o[2 * dn], a, b[0], b[1]);
+        mma_bf16(o[2 * dn + 1], a, b[2], b[3]);
+      }
+    }
+  }
+  float inv[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    float l = l_i[r];
+    l += __shfl_xor_sync(0xffffffffu, l, 1);
+    l += __shfl_xor_sync(0xffffffffu, l, 2);
+    inv[r] = l > 0.f ? 1.f / l : 0.f;
+  }
+  const int r0 = warp * 16 + gq;
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) {
+    const int col = head * HD + i * 8 + 2 * tq;
+    if (r0 < grp.nq)
+      *reinterpret_cast<uint32_t*>(p.z + static_cast<size_t>(grp.m0 + r0) * p.ldz + col) =
+          pack_bf16x2(o[i][0] * inv[0], o[i][1] * inv[0]);
+    if (r0 + 8 < grp.nq)
+      *reinterpret_cast<uint32_t*>(p.z + static_cast<size_t>(grp.m0 + r0 + 8) * p.ldz + col) =
+          pack_bf16x2(o[i][2] * inv[1], o[i][3] * inv[1]);
+  }
+}
+
+// ------------------------------------------------------------------ attention (decode)
+// One warp per (sequence, head), single query at position pos0. Keys in absolute 32-position
+// chunks: lane j scores key chunk*32+j, then the warp accumulates p*V with lanes owning dims.
+template <int HD>
+__global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
+  constexpr int DPL = HD >= 32 ? HD / 32 : 1;  // dims per lane in the PV accumulation
+  __shared__ __align__(16) float sq[4][HD];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * 4 + warp;
+  if (item >= p.n_groups * p.heads) return;
+  const int gi = item / p.heads, head = item - gi * p.heads;
+  const AttnGroup grp = p.groups[gi];
+  const __nv_bfloat16* qr = p.q + static_cast<size_t>(grp.m0) * p.ldq + head * HD;
+  for (int i = lane; i < HD; i += 32) sq[warp][i] = __bfloat162float(qr[i]) * p.scale_log2;
+  __syncwarp();
+  const int last = grp.pos0;
+  const size_t head_off = static_cast<size_t>(head) * PAGE * HD;
+  const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
+  const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
+  const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
+  float m = -INFINITY, l = 0.f;
+  float acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+  for (int c0 = 0; c0 <= last; c0 += 32) {
+    const int key = c0 + lane;
+    float s = -INFINITY;
+    if (key <= last && (!p.key_mask || p.key_mask[key])) {
+      const __nv_bfloat16* kr =
+          p.kv + static_cast<size_t>(pt[key / PAGE]) * page_stride + head_off + (key % PAGE) * HD;
+      float dot = 0.f;
+#pragma unroll
+      for (int c = 0; c < HD; c += 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(kr + c);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(h2[j]);
+          dot = fmaf(f.x, sq[warp][c + 2 * j], dot);
+          dot = fmaf(f.y, sq[warp][c + 2 * j + 1], dot);
+        }
+      }
+      s = dot;
+    }
+    float cm = s;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    const float mnew = fmaxf(m, cm);
+    const float alpha = mnew == -INFINITY ? 1.f : exp2f(m - mnew);
+    const float pj = mnew == -INFINITY ? 0.f : exp2f(s - mnew);
+    float ps = pj;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    l = l * alpha + ps;
+    m = mnew;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) acc[i] *= alpha;
+    const int nk = min(32, last - c0 + 1);
+    for (int j = 0; j < nk; ++j) {
+      const float w = __shfl_sync(0xffffffffu, pj, j);
+      const int kk = c0 + j;
+      const __nv_bfloat16* vr =
+          p.kv + static_cast<size_t>(pt[kk / PAGE]) * page_stride + v_off + head_off + (kk % PAGE) * HD;
+      if (DPL == 2) {
+        const float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(vr)[lane]);
+        acc[0] = fmaf(w, f.x, acc[0]);
+        acc[DPL - 1] = fmaf(w, f.y, acc[DPL - 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < DPL; ++i)
+          if (lane * DPL + i < HD) acc[i] = fmaf(w, __bfloat162float(vr[lane * DPL + i]), acc[i]);
+      }
+    }
+  }
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  __nv_bfloat16* zr = p.z + static_cast<size_t>(grp.m0) * p.ldz + head * HD;
+#pragma unroll
+  for (int i = 0; i < DPL; ++i)
+    if (lane * DPL + i < HD) zr[lane * DPL + i] = __float2bfloat16_rn(acc[i] * inv);
+}
+
+// ------------------------------------------------------------------ head + argmax
+// 16 rows per CTA: final LN in fp32, logits = y * tok_embed^T with the fp32 embedding (transposed
+// copy, coalesced over the vocabulary), greedy argmax (strict >, ties to the lowest id).
+constexpr int HEAD_ROWS = 16;
+__global__ void __launch_bounds__(256)
+    head_argmax_kernel(const float* __restrict__ x, int d, const int* __restrict__ rows, int n_rows,
+                       const float* __restrict__ g, const float* __restrict__ b,
+                       const float* __restrict__ embed_t, int V, const int* __restrict__ row_slot,
+                       int32_t* __restrict__ next_tok, int32_t* __restrict__ last_tok,
+                       float* __restrict__ logits_out) {
+  extern __shared__ float sy[];  // [HEAD_ROWS][d] then [HEAD_ROWS][V]
+  float* slog = sy + HEAD_ROWS * d;
+  const int r0 = blockIdx.x * HEAD_ROWS;
+  const int nr = min(HEAD_ROWS, n_rows - r0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < nr; r += 8) {
+    const float* xr = x + static_cast<size_t>(rows[r0 + r]) * d;
+    float s = 0.f;
+    for (int i = lane; i < d; i += 32) s += xr[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s / static_cast<float>(d);
+    float q = 0.f;
+    for (int i = lane; i < d; i += 32) {
+      const float t = xr[i] - mean;
+      q += t * t;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float inv = 1.0f / sqrtf(q / static_cast<float>(d) + 1e-5f);
+    for (int i = lane; i < d; i += 32) sy[r * d + i] = (xr[i] - mean) * inv * g[i] + b[i];
+  }
+  for (int r = nr; r < HEAD_ROWS; ++r)
+    for (int i = threadIdx.x; i < d; i += blockDim.x) sy[r * d + i] = 0.f;
+  __syncthreads();
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    float acc[HEAD_ROWS];
+#pragma unroll
+    for (int r = 0; r < HEAD_ROWS; ++r) acc[r] = 0.f;
+    for (int k = 0; k < d; ++k) {
+      const float e = embed_t[static_cast<size_t>(k) * V + v];
+#pragma unroll
+      for (int r = 0; r < HEAD_ROWS; ++r) acc[r] = fmaf(sy[r * d + k], e, acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < HEAD_ROWS; ++r) slog[r * V + v] = acc[r];
+  }
+  __syncthreads();
+  for (int r = warp; r < nr; r += 8) {
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int v = lane; v < V; v += 32) {
+      const float val = slog[r * V + v];
+      if (val > best || (val == best && v < bi)) {
+        best = val;
+        bi = v;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (bi == 0x7fffffff) bi = 0;  // all-NaN row: argmax_row returns index 0
+    if (lane == 0) {
+      next_tok[r0 + r] = bi;
+      if (last_tok) last_tok[row_slot[r0 + r]] = bi;
+    }
+    if (logits_out)
+      for (int v = lane; v < V; v += 32) logits_out[static_cast<size_t>(r0 + r) * V + v] = slog[r * V + v];
+  }
+}
+
+// ------------------------------------------------------------------ misc
+// Longest common prefix (in tokens) of every row with row 0, bounded by `limit`.
+__global__ void lcp_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ offsets, int64_t n_rows,
+                           int limit, int* __restrict__ out) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n_rows || r == 0) return;
+  const int32_t* a = ids + offsets[0];
+  const int32_t* b = ids + offsets[r];
+  const int n = static_cast<int>(min(static_cast<int64_t>(limit), offsets[r + 1] - offsets[r]));
+  int i = 0;
+  while (i < n && a[i] == b[i]) ++i;
+  atomicMin(out, i);
+}
+
+__global__ void check_ids_kernel(const int32_t* __restrict__ ids, int64_t n, int V, int* __restrict__ bad) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n && (ids[i] < 0 || ids[i] >= V)) atomicMin(bad, 0);
+}
+
+// Weight decode: bundle payload -> device GEMM operand (row-major [rows x ld], zero padded).
+__global__ void decode_dense_bf16_kernel(const float* __restrict__ src, int rows, int cols, __nv_bfloat16* dst,
+                                         int ld) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(rows) * ld) return;
+  const int r = static_cast<int>(i / ld), c = static_cast<int>(i % ld);
+  dst[i] = c < cols ? __float2bfloat16_rn(src[static_cast<size_t>(r) * cols + c]) : __float2bfloat16_rn(0.f);
+}
+
+// q8 / q4 / sparse24 payload -> dequantized bf16 value code*scale (model.cpp:153-199).
+__global__ void decode_quant_bf16_kernel(const uint8_t* __restrict__ p, int enc, int rows, int cols,
+                                         __nv_bfloat16* dst, int ld) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(rows) * ld) return;
+  const int r = static_cast<int>(i / ld), c = static_cast<int>(i % ld);
+  float v = 0.f;
+  if (c < cols) {
+    if (enc == 1) {
+      const float s = reinterpret_cast<const float*>(p + static_cast<size_t>(rows) * cols)[r];
+      v = static_cast<float>(reinterpret_cast<const int8_t*>(p)[static_cast<size_t>(r) * cols + c]) * s;
+    } else if (enc == 2) {
+      const size_t rb = (static_cast<size_t>(cols) + 1) / 2;
+      float s;
+      memcpy(&s, p + rows * rb + 4ull * r, 4);
+      const uint8_t byte = p[r * rb + c / 2];
+      const int nib = (c & 1) ? (byte >> 4) : (byte & 0xF);
+      v = static_cast<float>(nib - 8) * s;
+    } else if (enc == 3) {
+      const size_t groups = cols / 4, irb = (groups + 1) / 2;
+      const int8_t* codes = reinterpret_cast<const int8_t*>(p);
+      const uint8_t* idx = p + static_cast<size_t>(rows) * groups * 2;
+      float s;
+      memcpy(&s, idx + rows * irb + 4ull * r, 4);
+      const size_t gidx = c / 4;
+      const uint8_t byte = idx[r * irb + gidx / 2];
+      const int nib = (gidx & 1) ? (byte >> 4) : (byte & 0xF);
+      const int p0 = nib & 3, p1 = (nib >> 2) & 3, j = c & 3;
+      if (j == p0) v = static_cast<float>(codes[(r * groups + gidx) * 2]) * s;
+      if (j == p1) v = static_cast<float>(codes[(r * groups + gidx) * 2 + 1]) * s;
+    }
+  }
+  dst[i] = __float2bfloat16_rn(v);
+}
+
+__global__ void transpose_f32_kernel(const float* __restrict__ src, int rows, int cols, float* __restrict__ dst) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(rows) * cols) return;
+  const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+  dst[static_cast<size_t>(c) * rows + r] = src[i];
+}
+
+}  // namespace iolmk
+
+// ====================================================================== host launchers
+namespace iolmh {
+using namespace iolmk;
+
+static inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+void launch_ln(const float* x, int M, int d, const float* g, const float* b, __nv_bfloat16* h, int ldh,
+               cudaStream_t st) {
+  if (M <= 0) return;
+  const unsigned grid = blocks_for(M, 8);
+  const int nv = (d / 4 + 31) / 32;
+  if (nv <= 4) ln_kernel<4><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh);
+  else if (nv <= 8) ln_kernel<8><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh);
+  else if (nv <= 16) ln_kernel<16><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh);
+  else if (nv <= 32) ln_kernel<32><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh);
+  else throw Unsupported("layernorm: d_model > 4096");
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_slot, const int* tok_pos,
+                     const int32_t* last_tok, int M, int d, const float* tok_embed, const float* pos_embed, float* x,
+                     const float* g, const float* b, __nv_bfloat16* h, int ldh, cudaStream_t st) {
+  if (M <= 0) return;
+  const unsigned grid = blocks_for(M, 8);
+  const int nv = (d / 4 + 31) / 32;
+#define EMB(V)                                                                                          \
+  embed_ln_kernel<V><<<grid, 256, 0, st>>>(ids, tok_src, tok_slot, tok_pos, last_tok, M, d, tok_embed, \
+                                           pos_embed, x, g, b, h, ldh)
+  if (nv <= 4) EMB(4);
+  else if (nv <= 8) EMB(8);
+  else if (nv <= 16) EMB(16);
+  else if (nv <= 32) EMB(32);
+  else throw Unsupported("embed: d_model > 4096");
+#undef EMB
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_attention(const AttnParams& prefill, const AttnParams& decode, int hd, cudaStream_t st) {
+#define ATT(HD)                                                                                     \
+  do {                                                                                              \
+    constexpr int smem = 3 * 64 * (HD + 8) * 2;                                                     \
+    static bool cfg = false;                                                                        \
+    if (!cfg) {                                                                                     \
+      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD>,                                         \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));             \
+      cfg = true;                                                                                   \
+    }                                                                                               \
+    if (prefill.n_groups > 0)                                                                       \
+      attn_prefill_kernel<HD><<<dim3(prefill.n_groups, prefill.heads), 128, smem, st>>>(prefill);   \
+    if (decode.n_groups > 0)                                                                        \
+      attn_decode_kernel<HD><<<blocks_for(static_cast<int64_t>(decode.n_groups) * decode.heads, 4), \
+                               128, 0, st>>>(decode);                                               \
+  } while (0)
+  switch (hd) {
+    case 16: ATT(16); break;
+    case 32: ATT(32); break;
+    case 64: ATT(64); break;
+    case 128: ATT(128); break;
+    default: throw Unsupported("attention: head_dim must be 16, 32, 64 or 128");
+  }
+#undef ATT
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_head(const float* x, int d, const int* rows, int n_rows, const float* g, const float* b,
+                 const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
+                 float* logits_out, cudaStream_t st) {
+  if (n_rows <= 0) return;
+  const size_t smem = sizeof(float) * HEAD_ROWS * (d + V);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    CUDA_OK(cudaFuncSetAttribute(head_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    configured = smem;
+  }
+  head_argmax_kernel<<<blocks_for(n_rows, HEAD_ROWS), 256, smem, st>>>(x, d, rows, n_rows, g, b, embed_t, V,
+                                                                       row_slot, next_tok, last_tok, logits_out);
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_lcp(const int32_t* ids, const int64_t* offsets, int64_t n_rows, int limit, int* out, cudaStream_t st) {
+  if (n_rows > 1) lcp_kernel<<<blocks_for(n_rows, 256), 256, 0, st>>>(ids, offsets, n_rows, limit, out);
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_check_ids(const int32_t* ids, int64_t n, int V, int* bad, cudaStream_t st) {
+  if (n > 0) check_ids_kernel<<<blocks_for(n, 256), 256, 0, st>>>(ids, n, V, bad);
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_decode_weight(const void* payload, int enc, int rows, int cols, __nv_bfloat16* dst, int ld,
+                          cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(rows) * ld;
+  if (enc == 0)
+    decode_dense_bf16_kernel<<<blocks_for(n, 256), 256, 0, st>>>(static_cast<const float*>(payload), rows, cols,
+                                                                 dst, ld);
+  else
+    decode_quant_bf16_kernel<<<blocks_for(n, 256), 256, 0, st>>>(static_cast<const uint8_t*>(payload), enc, rows,
+                                                                 cols, dst, ld);
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_transpose(const float* src, int rows, int cols, float* dst, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(rows) * cols;
+  transpose_f32_kernel<<<blocks_for(n, 256), 256, 0, st>>>(src, rows, cols, dst);
+  CUDA_OK(cudaGetLastError());
+}
+
+}  // namespace iolmh

@@ -1,0 +1,33 @@
+// Non-GEMM kernels of the prompt() hot path (declarations + parameter blocks).
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+
+namespace iolmk {
+
+// One attention work item: `nq` consecutive query tokens of one sequence slot, at positions
+// pos0 .. pos0+nq-1, whose q rows are m0 .. m0+nq-1 of the step's q buffer. Keys are positions
+// 0 .. pos0+nq-1 of the slot (causal), read through the slot's page table.
+struct AttnGroup {
+  int slot;
+  int m0;
+  int nq;
+  int pos0;
+};
+
+struct AttnParams {
+  const __nv_bfloat16* q;  // [T x ldq] (head h at columns h*hd ..)
+  int ldq;
+  __nv_bfloat16* z;  // [T x ldz] output
+  int ldz;
+  const __nv_bfloat16* kv;  // layer pool: [page][K|V][heads][PAGE][hd]
+  const int* page_table;    // [slots x max_pages]
+  int max_pages;
+  int heads;
+  const AttnGroup* groups;
+  int n_groups;
+  const uint8_t* key_mask;  // optional: per position validity for slot of forward(); NULL = all valid
+  float scale_log2;         // log2(e) / sqrt(hd)
+};
+
+}  // namespace iolmk
