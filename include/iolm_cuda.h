@@ -49,7 +49,8 @@ typedef struct iolm_cuda_opts {
   int32_t act_quant;           /* 1: W8A8 int8 activations for q8 / sparse24 weights (default 0) */
   int32_t prefix_sharing;      /* -1: off; 0/1: share the common prompt prefix KV (default on) */
   int32_t use_cuda_graph;      /* reserved */
-  int32_t reserved[10];
+  int32_t kernel_timing;       /* 1: time every kernel class with CUDA events (iolm_cuda_kernel_times) */
+  int32_t reserved[9];
 } iolm_cuda_opts;
 
 /* ModelConfig (proj/include/iolm/model.hpp:20-41); per-layer lists are queried separately. */
@@ -116,6 +117,14 @@ int iolm_cuda_forward_logits(iolm_cuda_ctx* ctx, const int32_t* ids, const uint8
 
 /* Counters of the last decode/forward call on this context. */
 int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* out);
+
+/* Per kernel-class device time of the last call, recorded with CUDA events on the engine stream
+ * when opts.kernel_timing = 1. Classes (index): 0 embed+LN1, 1 QKV GEMM, 2 prefill attention,
+ * 3 decode attention, 4 Wo GEMM, 5 LN, 6 W_in GEMM, 7 W_out GEMM, 8 head+argmax.
+ * ms[i]: summed launch durations; work[i]: algorithmic FLOPs (GEMMs, attention) or bytes (LN,
+ * head, embed) of those launches; launches[i]: launch count. n: capacity of the arrays (>= 9). */
+#define IOLM_KCLASSES 9
+int iolm_cuda_kernel_times(const iolm_cuda_ctx* ctx, double* ms, double* work, int64_t* launches, int32_t n);
 
 /* Thread-local message for the last non-OK status. */
 const char* iolm_cuda_last_error(void);

@@ -23,6 +23,8 @@ IOLM_E_TRUNCATED_BLOB = 7
 IOLM_E_UNKNOWN_ENCODING = 8
 
 VOCAB, PAD, BOS, EOS = 131, 128, 129, 130
+KCLASSES = ["embed_ln", "gemm_qkv", "attn_prefill", "attn_decode", "gemm_o", "ln", "gemm_in",
+            "gemm_out", "head"]
 
 
 class Opts(C.Structure):
@@ -33,7 +35,8 @@ class Opts(C.Structure):
         ("act_quant", C.c_int32),
         ("prefix_sharing", C.c_int32),
         ("use_cuda_graph", C.c_int32),
-        ("reserved", C.c_int32 * 10),
+        ("kernel_timing", C.c_int32),
+        ("reserved", C.c_int32 * 9),
     ]
 
 
@@ -70,6 +73,7 @@ SIGNATURES = {
                                            C.POINTER(C.c_uint64)]),
     "iolm_cuda_last_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
     "iolm_cuda_last_error": (C.c_char_p, []),
+    "iolm_cuda_kernel_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "iolm_cuda_debug_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                             C.c_int32, C.c_int32, C.c_int32]),
     "iolm_cuda_debug_gemm_s8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,

@@ -113,6 +113,7 @@ class Engine {
  public:
   Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opts* opts);
   ~Engine() {
+    for (auto e : kev_) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
@@ -146,6 +147,7 @@ class Engine {
     int T() const { return static_cast<int>(tok_src.size()); }
   };
 
+  void reset_counters();
   void upload_weights(const BundleView& b);
   void alloc_runtime();
   void set_prefix_pages(int prefix_pages);
@@ -153,6 +155,9 @@ class Engine {
   void run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits);
   void gemm(int bn, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
   uint64_t ref_madds_row(int s0, int advances) const;
+  template <typename F>
+  void timed(int cat, double work, F&& f);
+  void collect_times();
 
   ModelConfig cfg_;
   uint64_t hash_ = 0;
@@ -165,6 +170,20 @@ class Engine {
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   iolm_cuda_stats stats_{};
+  // kernel-class timing (opts.kernel_timing)
+  bool ktime_ = false;
+  std::vector<cudaEvent_t> kev_;
+  struct KPending {
+    int cat, ev;
+    double work;
+  };
+  std::vector<KPending> kpend_;
+
+ public:
+  double kms_[IOLM_KCLASSES] = {}, kwork_[IOLM_KCLASSES] = {};
+  int64_t kcount_[IOLM_KCLASSES] = {};
+
+ private:
 
   std::vector<std::unique_ptr<Layer>> layers_;
   DevArray<float> tok_embed_, tok_embed_t_, pos_embed_, lnf_g_, lnf_b_;
@@ -211,6 +230,7 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
     if (opts->page_size != 0 && opts->page_size != PAGE) throw Unsupported("page_size must be 16");
     if (opts->act_quant != 0) throw Unsupported("act_quant (W8A8) is not available in this build");
     if (opts->prefix_sharing < 0) prefix_sharing_ = false;
+    ktime_ = opts->kernel_timing != 0;
   }
   T_max_ = std::max(round_up(T_max_, 128), round_up(S_, 128));
   for (int l = 0; l < L_; ++l) {
@@ -367,6 +387,37 @@ void Engine::gemm(int bn, int epi, const CUtensorMap& A, const CUtensorMap& B, i
   ++stats_.kernel_launches;
 }
 
+template <typename F>
+void Engine::timed(int cat, double work, F&& f) {
+  if (!ktime_) {
+    f();
+    return;
+  }
+  const int i = static_cast<int>(kpend_.size()) * 2;
+  while (static_cast<int>(kev_.size()) < i + 2) {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreate(&e));
+    kev_.push_back(e);
+  }
+  CUDA_OK(cudaEventRecord(kev_[i], stream_));
+  f();
+  CUDA_OK(cudaEventRecord(kev_[i + 1], stream_));
+  kpend_.push_back({cat, i, work});
+}
+
+void Engine::collect_times() {
+  if (!ktime_ || kpend_.empty()) return;
+  CUDA_OK(cudaStreamSynchronize(stream_));
+  for (const auto& k : kpend_) {
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, kev_[k.ev], kev_[k.ev + 1]));
+    kms_[k.cat] += ms;
+    kwork_[k.cat] += k.work;
+    kcount_[k.cat] += 1;
+  }
+  kpend_.clear();
+}
+
 void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits) {
   const int T = s.T();
   auto h2d = [&](void* dst, const void* src, size_t bytes) {
@@ -380,9 +431,18 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
   h2d(d_head_rows_.p, s.head_rows.data(), s.head_rows.size() * sizeof(int));
   h2d(d_head_slot_.p, s.head_slot.data(), s.head_slot.size() * sizeof(int));
 
-  launch_embed_ln(d_ids, d_tok_src_.p, d_tok_slot_.p, d_tok_pos_.p, d_last_tok_.p, T, d_, tok_embed_.p,
-                  pos_embed_.p, x_.p, layers_[0]->ln1_g.p, layers_[0]->ln1_b.p, h_.p, d_, stream_);
+  const double dT = static_cast<double>(T);
+  timed(0, dT * d_ * 14.0, [&] {
+    launch_embed_ln(d_ids, d_tok_src_.p, d_tok_slot_.p, d_tok_pos_.p, d_last_tok_.p, T, d_, tok_embed_.p,
+                    pos_embed_.p, x_.p, layers_[0]->ln1_g.p, layers_[0]->ln1_b.p, h_.p, d_, stream_);
+  });
   ++stats_.kernel_launches;
+  // algorithmic attention work of this step (per head): prefill FLOPs 4*hd*sum(pos+1),
+  // decode K+V bytes 2*2*hd*(pos+1)
+  double pre_keys = 0, dec_keys = 0;
+  for (const auto& g : s.pre)
+    for (int i = 0; i < g.nq; ++i) pre_keys += g.pos0 + i + 1;
+  for (const auto& g : s.dec) dec_keys += g.pos0 + 1;
   const float scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(hd_));
   for (int l = 0; l < L_; ++l) {
     Layer& ly = *layers_[l];
@@ -401,7 +461,7 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     ep.hd = hd_;
     ep.heads = ly.heads;
     ep.page_size = PAGE;
-    gemm(ly.bn_qkv, iolmk::EPI_QKV, tm_h_, ly.tm_qkv, T, 3 * ly.kh, d_, ep);
+    timed(1, 2.0 * dT * 3 * ly.kh * d_, [&] { gemm(ly.bn_qkv, iolmk::EPI_QKV, tm_h_, ly.tm_qkv, T, 3 * ly.kh, d_, ep); });
     // attention
     AttnParams ap{};
     ap.q = q_.p;
@@ -419,7 +479,12 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     pre.n_groups = static_cast<int>(s.pre.size());
     dec.groups = d_dec_.p;
     dec.n_groups = static_cast<int>(s.dec.size());
-    launch_attention(pre, dec, hd_, stream_);
+    {
+      AttnParams none = pre;
+      none.n_groups = 0;
+      if (pre.n_groups) timed(2, 4.0 * hd_ * ly.heads * pre_keys, [&] { launch_attention(pre, none, hd_, stream_); });
+      if (dec.n_groups) timed(3, 4.0 * hd_ * ly.heads * dec_keys, [&] { launch_attention(none, dec, hd_, stream_); });
+    }
     stats_.kernel_launches += (pre.n_groups > 0) + (dec.n_groups > 0);
     // x += z * Wo^T
     GemmEpi eo;
@@ -427,9 +492,9 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     eo.N = d_;
     eo.out = x_.p;
     eo.ldo = d_;
-    gemm(ly.bn_o, iolmk::EPI_RESID_F32, ly.tm_z, ly.tm_o, T, d_, ly.kh, eo);
+    timed(4, 2.0 * dT * d_ * ly.kh, [&] { gemm(ly.bn_o, iolmk::EPI_RESID_F32, ly.tm_z, ly.tm_o, T, d_, ly.kh, eo); });
     // h = LN2(x)
-    launch_ln(x_.p, T, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_);
+    timed(5, dT * d_ * 6.0, [&] { launch_ln(x_.p, T, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_); });
     ++stats_.kernel_launches;
     // g = gelu(h * Win^T)
     GemmEpi ei;
@@ -437,23 +502,28 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     ei.N = ly.f;
     ei.out = g_.p;
     ei.ldo = f_ld_max_;
-    gemm(ly.bn_in, iolmk::EPI_GELU_BF16, tm_h_, ly.tm_in, T, ly.f, d_, ei);
+    timed(6, 2.0 * dT * ly.f * d_, [&] { gemm(ly.bn_in, iolmk::EPI_GELU_BF16, tm_h_, ly.tm_in, T, ly.f, d_, ei); });
     // x += g * Wout^T
-    gemm(ly.bn_out, iolmk::EPI_RESID_F32, ly.tm_g, ly.tm_out, T, d_, ly.f, eo);
+    timed(7, 2.0 * dT * d_ * ly.f, [&] { gemm(ly.bn_out, iolmk::EPI_RESID_F32, ly.tm_g, ly.tm_out, T, d_, ly.f, eo); });
     if (l + 1 < L_) {
-      launch_ln(x_.p, T, d_, layers_[l + 1]->ln1_g.p, layers_[l + 1]->ln1_b.p, h_.p, d_, stream_);
+      timed(5, dT * d_ * 6.0, [&] {
+        launch_ln(x_.p, T, d_, layers_[l + 1]->ln1_g.p, layers_[l + 1]->ln1_b.p, h_.p, d_, stream_);
+      });
       ++stats_.kernel_launches;
     }
   }
   const int R = static_cast<int>(s.head_rows.size());
   if (R > 0) {
-    launch_head(x_.p, d_, d_head_rows_.p, R, lnf_g_.p, lnf_b_.p, tok_embed_t_.p, V_, d_head_slot_.p, d_next_.p,
-                d_last_tok_.p, d_logits, stream_);
+    timed(8, static_cast<double>(R) * d_ * 4.0 + static_cast<double>(V_) * d_ * 4.0, [&] {
+      launch_head(x_.p, d_, d_head_rows_.p, R, lnf_g_.p, lnf_b_.p, tok_embed_t_.p, V_, d_head_slot_.p, d_next_.p,
+                  d_last_tok_.p, d_logits, stream_);
+    });
     ++stats_.kernel_launches;
     CUDA_OK(cudaMemcpyAsync(h_next_.p, d_next_.p, R * sizeof(int32_t), cudaMemcpyDeviceToHost, stream_));
   }
   ++stats_.steps;
   stats_.tokens += T;
+  collect_times();
 }
 
 uint64_t Engine::ref_madds_row(int s0, int advances) const {
@@ -464,10 +534,18 @@ uint64_t Engine::ref_madds_row(int s0, int advances) const {
   return t;
 }
 
+void Engine::reset_counters() {
+  stats_ = iolm_cuda_stats{};
+  for (int i = 0; i < IOLM_KCLASSES; ++i) {
+    kms_[i] = kwork_[i] = 0;
+    kcount_[i] = 0;
+  }
+}
+
 void Engine::decode(const int32_t* ids, bool ids_on_device, const int64_t* offsets, int64_t n_rows, int max_new,
                     int32_t* out_ids, int32_t* out_len, uint64_t* madds, int64_t* bad_row) {
   CUDA_OK(cudaSetDevice(device_));
-  stats_ = iolm_cuda_stats{};
+  reset_counters();
   if (bad_row) *bad_row = -1;
   if (n_rows <= 0) throw ContractViolation("batch_decode: batch size must be >= 1");
   if (max_new < 0) throw ContractViolation("batch_decode: max_new_tokens must be >= 0");
@@ -599,7 +677,7 @@ void Engine::decode(const int32_t* ids, bool ids_on_device, const int64_t* offse
 
 void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds) {
   CUDA_OK(cudaSetDevice(device_));
-  stats_ = iolm_cuda_stats{};
+  reset_counters();
   if (n <= 0 || !ids) throw ContractViolation("forward: empty sequence");
   if (n > S_)
     throw SequenceTooLong("forward: sequence length " + std::to_string(n) + " exceeds max_seq_len " +
@@ -723,5 +801,18 @@ extern "C" int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* o
   return guarded([&] {
     if (!ctx || !out) throw iolmh::ContractViolation("null argument");
     *out = ctx->eng->stats();
+  });
+}
+
+extern "C" int iolm_cuda_kernel_times(const iolm_cuda_ctx* ctx, double* ms, double* work, int64_t* launches,
+                                      int32_t n) {
+  return guarded([&] {
+    if (!ctx || !ms || !work || !launches) throw iolmh::ContractViolation("null argument");
+    if (n < IOLM_KCLASSES) throw iolmh::ContractViolation("kernel_times: array too small");
+    for (int i = 0; i < IOLM_KCLASSES; ++i) {
+      ms[i] = ctx->eng->kms_[i];
+      work[i] = ctx->eng->kwork_[i];
+      launches[i] = ctx->eng->kcount_[i];
+    }
   });
 }

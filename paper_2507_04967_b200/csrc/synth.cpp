@@ -10,7 +10,9 @@
 //   * RTN compression twins (quantize_rtn, proj/src/quant.cpp:23-38,79-92; magnitude 2:4,
 //     quant.cpp:181-200) for the compressed configs, encoded per proj/docs/format.md.
 // This is harness code: the engine never links it.
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -68,6 +70,66 @@ struct Rng {
     has_cached = true;
     return r * std::cos(theta);
   }
+};
+
+// Batched, multi-threaded view of Rng::next_normal() * stddev cast to float.
+class NormalStream {
+ public:
+  explicit NormalStream(uint64_t seed) : rng_(seed) {}
+  void fill(float* out, size_t n, double sd) {
+    size_t i = 0;
+    if (has_cached_ && n > 0) {
+      out[i++] = static_cast<float>(sd * cached_);
+      has_cached_ = false;
+    }
+    while (i < n) {
+      const size_t pairs = std::min<size_t>((n - i + 1) / 2, kChunkPairs);
+      draws_.resize(2 * pairs);
+      for (size_t j = 0; j < 2 * pairs; ++j) draws_[j] = rng_.next_u64();
+      normals_.resize(2 * pairs);
+      const size_t take = std::min(n - i, 2 * pairs);
+      transform(pairs, out + i, take, sd);
+      i += take;
+      if (take < 2 * pairs) {  // odd tail: keep the sin half for the next request
+        cached_ = normals_[take];
+        has_cached_ = true;
+      }
+    }
+  }
+
+ private:
+  static constexpr size_t kChunkPairs = 1u << 22;
+  void transform(size_t pairs, float* out, size_t take, double sd) {
+    auto work = [&](size_t lo, size_t hi) {
+      for (size_t j = lo; j < hi; ++j) {
+        const double u1 = (static_cast<double>(draws_[2 * j] >> 11) + 1.0) * 0x1.0p-53;
+        const double u2 = static_cast<double>(draws_[2 * j + 1] >> 11) * 0x1.0p-53;
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double theta = 2.0 * 3.141592653589793238462643 * u2;
+        normals_[2 * j] = r * std::cos(theta);
+        normals_[2 * j + 1] = r * std::sin(theta);
+        if (2 * j < take) out[2 * j] = static_cast<float>(sd * normals_[2 * j]);
+        if (2 * j + 1 < take) out[2 * j + 1] = static_cast<float>(sd * normals_[2 * j + 1]);
+      }
+    };
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (pairs < 65536 || hw == 1) {
+      work(0, pairs);
+      return;
+    }
+    std::vector<std::thread> pool;
+    const size_t chunk = (pairs + hw - 1) / hw;
+    for (unsigned t = 0; t < hw; ++t) {
+      const size_t lo = t * chunk, hi = std::min(pairs, lo + chunk);
+      if (lo < hi) pool.emplace_back(work, lo, hi);
+    }
+    for (auto& th : pool) th.join();
+  }
+  Rng rng_;
+  std::vector<uint64_t> draws_;
+  std::vector<double> normals_;
+  double cached_ = 0.0;
+  bool has_cached_ = false;
 };
 
 struct Tensor {
@@ -215,111 +277,129 @@ int synth_toy_bundle(int d, int L, int H, int F, int S, uint64_t seed, int quant
     for (int h = 0; h < nh; ++h) c.heads[l].push_back(h);
     c.ffn[l] = prune_ffn ? prune_ffn[l] : F;
   }
-  Rng rng(seed);
+  // The reference draws every normal from one Rng stream (train.cpp:21-25): pair j of the
+  // Box-Muller stream consumes u64 draws 2j and 2j+1 and yields normals 2j (cos) and 2j+1 (sin)
+  // (rng.cpp:60-73). Drawing the u64s is cheap and sequential; the transcendental transform is
+  // done in parallel over chunks, giving the identical float stream. Tensors are planned first so
+  // the serialized bundle is written once, in place.
+  NormalStream ns(seed);
   const double base_std = 0.02;
   const double resid_std = base_std / std::sqrt(2.0 * L);
-  std::vector<Tensor> ts;
-  std::vector<uint8_t> blob;
-  auto normal = [&](int rows, int cols, double sd) {
-    std::vector<float> m(static_cast<size_t>(rows) * cols);
-    for (auto& v : m) v = static_cast<float>(sd * rng.next_normal());
-    return m;
+  struct Plan {
+    std::string name;
+    int rows, cols;
+    double sd;     // > 0: normal(sd); else constant
+    float value;   // constant fill
   };
-  auto constant = [&](int cols, float v) { return std::vector<float>(cols, v); };
-  auto append = [&](const std::string& name, int rows, int cols, std::vector<float> w) {
-    Tensor t{name, rows, cols, 0, blob.size(), 0};
-    if (!is_weight(name) || quant == 0) {
-      const auto* b = reinterpret_cast<const uint8_t*>(w.data());
-      blob.insert(blob.end(), b, b + w.size() * 4);
-      t.enc = 0;
-    } else if (quant == 8 || quant == 4) {
-      std::vector<int8_t> codes;
-      std::vector<float> scales;
-      rtn(w.data(), rows, cols, quant == 8 ? 127 : 7, codes, scales);
-      if (quant == 8) {
-        t.enc = 1;
-        blob.insert(blob.end(), reinterpret_cast<uint8_t*>(codes.data()),
-                    reinterpret_cast<uint8_t*>(codes.data()) + codes.size());
-      } else {
-        t.enc = 2;
-        const size_t rb = (static_cast<size_t>(cols) + 1) / 2;
-        for (int r = 0; r < rows; ++r) {
-          std::vector<uint8_t> packed(rb, 0);
-          for (int j = 0; j < cols; ++j) {
-            const auto nib = static_cast<uint8_t>(codes[static_cast<size_t>(r) * cols + j] + 8);
-            packed[j / 2] |= (j % 2 == 0) ? nib : static_cast<uint8_t>(nib << 4);
-          }
-          blob.insert(blob.end(), packed.begin(), packed.end());
-        }
-      }
-      const auto* sb = reinterpret_cast<const uint8_t*>(scales.data());
-      blob.insert(blob.end(), sb, sb + scales.size() * 4);
-    } else if (quant == 24) {
-      if (cols % 4 != 0) return false;
-      std::vector<uint8_t> mask;
-      magnitude24(w, rows, cols, mask);
-      std::vector<int8_t> codes;
-      std::vector<float> scales;
-      rtn(w.data(), rows, cols, 127, codes, scales);
-      t.enc = 3;
-      const size_t groups = cols / 4;
-      std::vector<uint8_t> kept;
-      std::vector<uint8_t> pos;
-      for (int r = 0; r < rows; ++r)
-        for (size_t g = 0; g < groups; ++g) {
-          int found = 0;
-          for (int j = 0; j < 4 && found < 2; ++j)
-            if (mask[static_cast<size_t>(r) * cols + g * 4 + j]) {
-              kept.push_back(static_cast<uint8_t>(codes[static_cast<size_t>(r) * cols + g * 4 + j]));
-              pos.push_back(static_cast<uint8_t>(j));
-              ++found;
-            }
-        }
-      blob.insert(blob.end(), kept.begin(), kept.end());
-      const size_t irb = (groups + 1) / 2;
-      for (int r = 0; r < rows; ++r) {
-        std::vector<uint8_t> packed(irb, 0);
-        for (size_t g = 0; g < groups; ++g) {
-          const uint8_t p0 = pos[(static_cast<size_t>(r) * groups + g) * 2];
-          const uint8_t p1 = pos[(static_cast<size_t>(r) * groups + g) * 2 + 1];
-          const auto nib = static_cast<uint8_t>(p0 | (p1 << 2));
-          packed[g / 2] |= (g % 2 == 0) ? nib : static_cast<uint8_t>(nib << 4);
-        }
-        blob.insert(blob.end(), packed.begin(), packed.end());
-      }
-      const auto* sb = reinterpret_cast<const uint8_t*>(scales.data());
-      blob.insert(blob.end(), sb, sb + scales.size() * 4);
-    } else {
-      return false;
-    }
-    t.length = blob.size() - t.offset;
-    ts.push_back(t);
-    return true;
-  };
-  bool ok = true;
-  ok &= append("tok_embed", c.V, d, normal(c.V, d, base_std));
-  ok &= append("pos_embed", S, d, normal(S, d, base_std));
+  std::vector<Plan> plan;
+  plan.push_back({"tok_embed", c.V, d, base_std, 0.f});
+  plan.push_back({"pos_embed", S, d, base_std, 0.f});
   for (int l = 0; l < L; ++l) {
     const std::string p = "layers." + std::to_string(l) + ".";
     const int kh = static_cast<int>(c.heads[l].size()) * hd, f = c.ffn[l];
-    ok &= append(p + "attn_norm.gain", 1, d, constant(d, 1.0f));
-    ok &= append(p + "attn_norm.bias", 1, d, constant(d, 0.0f));
-    ok &= append(p + "attn.wq", kh, d, normal(kh, d, base_std));
-    ok &= append(p + "attn.wk", kh, d, normal(kh, d, base_std));
-    ok &= append(p + "attn.wv", kh, d, normal(kh, d, base_std));
-    ok &= append(p + "attn.wo", d, kh, normal(d, kh, resid_std));
-    ok &= append(p + "ffn_norm.gain", 1, d, constant(d, 1.0f));
-    ok &= append(p + "ffn_norm.bias", 1, d, constant(d, 0.0f));
-    ok &= append(p + "ffn.w_in", f, d, normal(f, d, base_std));
-    ok &= append(p + "ffn.w_out", d, f, normal(d, f, resid_std));
+    plan.push_back({p + "attn_norm.gain", 1, d, 0.0, 1.f});
+    plan.push_back({p + "attn_norm.bias", 1, d, 0.0, 0.f});
+    plan.push_back({p + "attn.wq", kh, d, base_std, 0.f});
+    plan.push_back({p + "attn.wk", kh, d, base_std, 0.f});
+    plan.push_back({p + "attn.wv", kh, d, base_std, 0.f});
+    plan.push_back({p + "attn.wo", d, kh, resid_std, 0.f});
+    plan.push_back({p + "ffn_norm.gain", 1, d, 0.0, 1.f});
+    plan.push_back({p + "ffn_norm.bias", 1, d, 0.0, 0.f});
+    plan.push_back({p + "ffn.w_in", f, d, base_std, 0.f});
+    plan.push_back({p + "ffn.w_out", d, f, resid_std, 0.f});
   }
-  ok &= append("final_norm.gain", 1, d, constant(d, 1.0f));
-  ok &= append("final_norm.bias", 1, d, constant(d, 0.0f));
-  if (!ok) return 1;
-  const auto bytes = serialize(c, ts, blob, "", "");
-  *out = static_cast<uint8_t*>(std::malloc(bytes.size()));
-  std::memcpy(*out, bytes.data(), bytes.size());
-  *out_len = bytes.size();
+  plan.push_back({"final_norm.gain", 1, d, 0.0, 1.f});
+  plan.push_back({"final_norm.bias", 1, d, 0.0, 0.f});
+
+  auto enc_of = [&](const Plan& t) {
+    if (!is_weight(t.name) || quant == 0) return 0;
+    if (quant == 8) return 1;
+    if (quant == 4) return 2;
+    return 3;
+  };
+  auto payload_bytes = [](int rows, int cols, int enc) -> uint64_t {
+    const uint64_t r = rows, cc = cols;
+    if (enc == 0) return r * cc * 4;
+    if (enc == 1) return r * cc + r * 4;
+    if (enc == 2) return r * ((cc + 1) / 2) + r * 4;
+    const uint64_t g = cc / 4;
+    return r * (cc / 2) + r * ((g + 1) / 2) + r * 4;
+  };
+  std::vector<Tensor> ts;
+  uint64_t total = 0;
+  for (const auto& t : plan) {
+    const int enc = enc_of(t);
+    if (enc == 3 && t.cols % 4 != 0) return 1;
+    const uint64_t n = payload_bytes(t.rows, t.cols, enc);
+    ts.push_back(Tensor{t.name, t.rows, t.cols, enc, total, n});
+    total += n;
+  }
+  std::vector<uint8_t> empty;
+  const std::vector<uint8_t> head = serialize(c, ts, empty, "", "");
+  uint8_t* buf = static_cast<uint8_t*>(std::malloc(head.size() + total));
+  if (!buf) return 2;
+  std::memcpy(buf, head.data(), head.size());
+  uint8_t* blob = buf + head.size();
+  std::vector<float> w;
+  for (size_t i = 0; i < plan.size(); ++i) {
+    const Plan& t = plan[i];
+    const Tensor& rec = ts[i];
+    const size_t n = static_cast<size_t>(t.rows) * t.cols;
+    w.resize(n);
+    if (t.sd > 0) ns.fill(w.data(), n, t.sd);
+    else std::fill(w.begin(), w.end(), t.value);
+    uint8_t* dst = blob + rec.offset;
+    if (rec.enc == 0) {
+      std::memcpy(dst, w.data(), n * 4);
+      continue;
+    }
+    std::vector<int8_t> codes;
+    std::vector<float> scales;
+    if (rec.enc == 1 || rec.enc == 2) {
+      rtn(w.data(), t.rows, t.cols, rec.enc == 1 ? 127 : 7, codes, scales);
+      size_t o = 0;
+      if (rec.enc == 1) {
+        std::memcpy(dst, codes.data(), codes.size());
+        o = codes.size();
+      } else {
+        const size_t rb = (static_cast<size_t>(t.cols) + 1) / 2;
+        std::memset(dst, 0, t.rows * rb);
+        for (int r = 0; r < t.rows; ++r)
+          for (int j = 0; j < t.cols; ++j) {
+            const auto nib = static_cast<uint8_t>(codes[static_cast<size_t>(r) * t.cols + j] + 8);
+            dst[r * rb + j / 2] |= (j % 2 == 0) ? nib : static_cast<uint8_t>(nib << 4);
+          }
+        o = t.rows * rb;
+      }
+      std::memcpy(dst + o, scales.data(), scales.size() * 4);
+      continue;
+    }
+    // sparse24_q8: magnitude 2:4 then RTN q8 on the sparsified weights (compress.cpp:86-136)
+    std::vector<uint8_t> mask;
+    magnitude24(w, t.rows, t.cols, mask);
+    rtn(w.data(), t.rows, t.cols, 127, codes, scales);
+    const size_t groups = t.cols / 4, irb = (groups + 1) / 2;
+    int8_t* kept = reinterpret_cast<int8_t*>(dst);
+    uint8_t* idx = dst + static_cast<size_t>(t.rows) * groups * 2;
+    std::memset(idx, 0, t.rows * irb);
+    for (int r = 0; r < t.rows; ++r)
+      for (size_t g = 0; g < groups; ++g) {
+        int found = 0;
+        uint8_t pos[2] = {0, 0};
+        for (int j = 0; j < 4 && found < 2; ++j) {
+          const size_t e = static_cast<size_t>(r) * t.cols + g * 4 + j;
+          if (mask[e]) {
+            kept[(static_cast<size_t>(r) * groups + g) * 2 + found] = codes[e];
+            pos[found++] = static_cast<uint8_t>(j);
+          }
+        }
+        const auto nib = static_cast<uint8_t>(pos[0] | (pos[1] << 2));
+        idx[r * irb + g / 2] |= (g % 2 == 0) ? nib : static_cast<uint8_t>(nib << 4);
+      }
+    std::memcpy(idx + t.rows * irb, scales.data(), scales.size() * 4);
+  }
+  *out = buf;
+  *out_len = head.size() + total;
   return 0;
 }
 

@@ -139,13 +139,14 @@ class ModelRuntime:
     """iolm::ModelRuntime on a B200. `bundle` is the serialize_bundle byte stream."""
 
     def __init__(self, bundle: bytes, device: int = 0, max_tokens_per_step: int = 0, max_slots: int = 0,
-                 prefix_sharing: bool = True, act_quant: bool = False):
+                 prefix_sharing: bool = True, act_quant: bool = False, kernel_timing: bool = False):
         self._lib = _lib.load()
         opts = _lib.Opts()
         opts.max_tokens_per_step = max_tokens_per_step
         opts.max_slots = max_slots
         opts.prefix_sharing = 0 if prefix_sharing else -1
         opts.act_quant = 1 if act_quant else 0
+        opts.kernel_timing = 1 if kernel_timing else 0
         h = C.c_void_p()
         buf = (C.c_char * len(bundle)).from_buffer_copy(bundle)
         _check(self._lib.iolm_cuda_create(buf, len(bundle), device, C.byref(opts), C.byref(h)))
@@ -179,6 +180,13 @@ class ModelRuntime:
         s = _lib.Stats()
         _check(self._lib.iolm_cuda_last_stats(self._h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in _lib.Stats._fields_}
+
+    def kernel_times(self) -> dict:
+        """Per kernel class of the last call: {name: (ms, algorithmic work, launches)}."""
+        n = len(_lib.KCLASSES)
+        ms, work, cnt = (C.c_double * n)(), (C.c_double * n)(), (C.c_int64 * n)()
+        _check(self._lib.iolm_cuda_kernel_times(self._h, ms, work, cnt, n))
+        return {k: (ms[i], work[i], cnt[i]) for i, k in enumerate(_lib.KCLASSES)}
 
     # ---- forward (runtime.cpp:217-232)
     def forward(self, ids, mask=None, counter: FlopCounter | None = None) -> np.ndarray:
