@@ -133,14 +133,14 @@ const char* iolm_cuda_last_error(void);
 
 /* C[M x N] = A[M x K] * W[N x K]^T with bf16 operands (raw uint16 bit patterns), f32 result,
  * through the production tcgen05 GEMM. epi: 0 f32 store, 2 GELU (result returned as f32 after a
- * bf16 round trip). bn: 128 or 256. */
+ * bf16 round trip). bn: 256 = 2-SM 256x256 tiles (CTA pairs), 128 = single-CTA 128x128 tiles. */
 int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, float* C, int32_t M, int32_t N,
                               int32_t K, int32_t bn, int32_t epi);
 
 /* W8A8 integer GEMM: C_i32[M x N] = A_s8[M x K] * W_s8[N x K]^T through tcgen05 kind::i8.
- * Bit-exact integer accumulators. */
+ * Bit-exact integer accumulators. pair: 1 = 2-SM 256x256 tiles, 0 = single-CTA tiles. */
 int iolm_cuda_debug_gemm_s8(const int8_t* A, const int8_t* W, int32_t* C, int32_t M, int32_t N,
-                            int32_t K);
+                            int32_t K, int32_t pair);
 
 #ifdef __cplusplus
 }

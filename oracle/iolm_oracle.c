@@ -130,15 +130,17 @@ size_t orc_init_dense_params(int V, int d, int L, int H, int F, int S, uint64_t 
 }
 
 /* ------------------------------------------------------------------ numerics (numerics.cpp) */
-/* C[n x N] = A[n x K] * W[N x K]^T, every element summed from 0 in ascending k. */
-static void matmul_wt(const float* A, int n, int K, const float* W, int N, float* Cm) {
+/* C[n x N] = A[n x K] * Wt[K x N] with Wt the transposed weight (runtime.cpp:80-85): the
+ * reference's i-k-j loop, every element summed from 0 in ascending k (numerics.cpp:56-76). */
+static void matmul_wt(const float* A, int n, int K, const float* Wt, int N, float* Cm) {
   for (int i = 0; i < n; ++i) {
     const float* a = A + (size_t)i * K;
     float* c = Cm + (size_t)i * N;
     for (int j = 0; j < N; ++j) c[j] = 0.0f;
     for (int k = 0; k < K; ++k) {
       const float av = a[k];
-      for (int j = 0; j < N; ++j) c[j] += av * W[(size_t)j * K + k];
+      const float* w = Wt + (size_t)k * N;
+      for (int j = 0; j < N; ++j) c[j] += av * w[j];
     }
   }
 }
@@ -182,12 +184,13 @@ typedef struct {
   const float* const* ln1_b;
   const float* const* ln2_g;
   const float* const* ln2_b;
-  const float* const* wq; /* [kh x d] as stored in the bundle ([out x in]) */
+  const float* tok_t;       /* tok_embed^T [d x V] for the tied head */
+  const float* const* wq;   /* transposed: [d x kh] (x * W^T form, runtime.cpp:80-85) */
   const float* const* wk;
   const float* const* wv;
-  const float* const* wo;    /* [d x kh] */
-  const float* const* w_in;  /* [f x d] */
-  const float* const* w_out; /* [d x f] */
+  const float* const* wo;    /* [kh x d] */
+  const float* const* w_in;  /* [d x f] */
+  const float* const* w_out; /* [f x d] */
 } orc_model;
 
 typedef struct {
@@ -315,7 +318,7 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
 
 /* logits_for: y * tok_embed^T (runtime.cpp:213-215). */
 static void logits_for(const orc_model* m, const float* y, int n, float* logits, uint64_t* madds) {
-  matmul_wt(y, n, m->d, m->tok, m->V, logits);
+  matmul_wt(y, n, m->d, m->tok_t, m->V, logits);
   *madds += (uint64_t)n * m->d * m->V;
 }
 

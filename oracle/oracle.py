@@ -95,6 +95,7 @@ class _OrcModel(C.Structure):
         ("tok", C.c_void_p), ("pos", C.c_void_p), ("lnf_g", C.c_void_p), ("lnf_b", C.c_void_p),
         ("ln1_g", C.POINTER(C.c_void_p)), ("ln1_b", C.POINTER(C.c_void_p)),
         ("ln2_g", C.POINTER(C.c_void_p)), ("ln2_b", C.POINTER(C.c_void_p)),
+        ("tok_t", C.c_void_p),
         ("wq", C.POINTER(C.c_void_p)), ("wk", C.POINTER(C.c_void_p)), ("wv", C.POINTER(C.c_void_p)),
         ("wo", C.POINTER(C.c_void_p)), ("w_in", C.POINTER(C.c_void_p)), ("w_out", C.POINTER(C.c_void_p)),
     ]
@@ -146,10 +147,13 @@ class OracleModel:
 
         m.tok, m.pos = ptr(T["tok_embed"]), ptr(T["pos_embed"])
         m.lnf_g, m.lnf_b = ptr(T["final_norm.gain"]), ptr(T["final_norm.bias"])
+        m.tok_t = ptr(np.ascontiguousarray(T["tok_embed"].T))
         for fld, name in [("ln1_g", "attn_norm.gain"), ("ln1_b", "attn_norm.bias"), ("ln2_g", "ffn_norm.gain"),
                           ("ln2_b", "ffn_norm.bias"), ("wq", "attn.wq"), ("wk", "attn.wk"), ("wv", "attn.wv"),
                           ("wo", "attn.wo"), ("w_in", "ffn.w_in"), ("w_out", "ffn.w_out")]:
-            arr = (C.c_void_p * L)(*[ptr(T[f"layers.{l}.{name}"]) for l in range(L)])
+            tr = name.startswith("attn.w") or name.startswith("ffn.w")  # weights go in transposed
+            arr = (C.c_void_p * L)(*[ptr(np.ascontiguousarray(T[f"layers.{l}.{name}"].T) if tr
+                                         else T[f"layers.{l}.{name}"]) for l in range(L)])
             self._keep.append(arr)
             setattr(m, fld, arr)
         self._m = m

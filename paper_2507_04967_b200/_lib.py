@@ -77,7 +77,7 @@ SIGNATURES = {
     "iolm_cuda_debug_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                             C.c_int32, C.c_int32, C.c_int32]),
     "iolm_cuda_debug_gemm_s8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
-                                          C.c_int32]),
+                                          C.c_int32, C.c_int32]),
 }
 
 _LIB = None

@@ -40,7 +40,7 @@ extern "C" int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, f
     CUDA_OK(cudaMemcpy(dA.p, A, sizeof(uint16_t) * M * K, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(dW.p, W, sizeof(uint16_t) * N * K, cudaMemcpyHostToDevice));
     CUtensorMap ta = make_kmajor_map(dA.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, M, 2ull * K, 128);
-    CUtensorMap tb = make_kmajor_map(dW.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, N, 2ull * K, bn);
+    CUtensorMap tb = make_kmajor_map(dW.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, N, 2ull * K, 128);
     iolmk::GemmEpi ep;
     ep.M = M;
     ep.N = N;
@@ -58,7 +58,7 @@ extern "C" int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, f
     } else {
       throw ContractViolation("debug_gemm: unsupported epilogue");
     }
-    launch_gemm_bf16(bn, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
+    launch_gemm(bn == 256, false, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
     CUDA_OK(cudaDeviceSynchronize());
     if (epi == iolmk::EPI_GELU_BF16 || epi == iolmk::EPI_BF16) {
       std::vector<__nv_bfloat16> h(static_cast<size_t>(M) * N);
@@ -67,5 +67,27 @@ extern "C" int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, f
     } else {
       CUDA_OK(cudaMemcpy(C, dC.p, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
     }
+  });
+}
+
+extern "C" int iolm_cuda_debug_gemm_s8(const int8_t* A, const int8_t* W, int32_t* C, int32_t M, int32_t N,
+                                       int32_t K, int32_t pair) {
+  return guarded([&] {
+    if (M <= 0 || N <= 0 || K <= 0 || (K % 16) != 0)
+      throw ContractViolation("debug_gemm_s8: need positive M,N and K % 16 == 0");
+    DevBuf<int8_t> dA(static_cast<size_t>(M) * K), dW(static_cast<size_t>(N) * K);
+    DevBuf<int32_t> dC(static_cast<size_t>(M) * N);
+    CUDA_OK(cudaMemcpy(dA.p, A, static_cast<size_t>(M) * K, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dW.p, W, static_cast<size_t>(N) * K, cudaMemcpyHostToDevice));
+    CUtensorMap ta = make_kmajor_map(dA.p, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, M, K, 128);
+    CUtensorMap tb = make_kmajor_map(dW.p, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, N, K, 128);
+    iolmk::GemmEpi ep;
+    ep.M = M;
+    ep.N = N;
+    ep.out = dC.p;
+    ep.ldo = N;
+    launch_gemm(pair != 0, true, iolmk::EPI_S32, ta, tb, M, N, K, ep, nullptr, sm_count());
+    CUDA_OK(cudaDeviceSynchronize());
+    CUDA_OK(cudaMemcpy(C, dC.p, sizeof(int32_t) * M * N, cudaMemcpyDeviceToHost));
   });
 }

@@ -14,7 +14,9 @@
 // contribution is the reference's closed form (runtime.cpp:311-345).
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -99,13 +101,23 @@ struct Layer {
   int heads = 0, kh = 0, f = 0;
   DevArray<float> ln1_g, ln1_b, ln2_g, ln2_b;
   DevArray<__nv_bfloat16> w_qkv, w_o, w_in, w_out;
-  int bn_qkv = 256, bn_o = 256, bn_in = 256, bn_out = 256;
   CUtensorMap tm_qkv, tm_o, tm_in, tm_out;  // B operands (weights)
   CUtensorMap tm_z, tm_g;                   // A operands with this layer's K extent
   DevArray<__nv_bfloat16> kv;               // paged pool [pages][K|V][heads][PAGE][hd]
 };
 
-int pick_bn(int N) { return N >= 384 ? 256 : 128; }
+// 2-SM 256x256 tiles once both M and N fill at least one pair tile. IOLM_GEMM_TILES=single|pair
+// overrides (A/B measurements).
+bool use_pair(int M, int N) {
+  static const int mode = [] {
+    const char* e = std::getenv("IOLM_GEMM_TILES");
+    if (!e) return 0;
+    return std::string(e) == "single" ? 1 : (std::string(e) == "pair" ? 2 : 0);
+  }();
+  if (mode == 1) return false;
+  if (mode == 2) return true;
+  return M >= 256 && N >= 256;
+}
 
 }  // namespace
 
@@ -153,7 +165,7 @@ class Engine {
   void set_prefix_pages(int prefix_pages);
   void add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head);
   void run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits);
-  void gemm(int bn, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
+  void gemm(int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
   uint64_t ref_madds_row(int s0, int advances) const;
   template <typename F>
   void timed(int cat, double work, F&& f);
@@ -287,15 +299,11 @@ void Engine::upload_weights(const BundleView& b) {
     decode_into(p + "ffn.w_in", ly->w_in.p, d_);
     ly->w_out.alloc(static_cast<size_t>(d_) * f_ld);
     decode_into(p + "ffn.w_out", ly->w_out.p, f_ld);
-    ly->bn_qkv = pick_bn(3 * kh);
-    ly->bn_o = pick_bn(d_);
-    ly->bn_in = pick_bn(f);
-    ly->bn_out = pick_bn(d_);
     const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    ly->tm_qkv = make_kmajor_map(ly->w_qkv.p, BF, 2, d_, 3ull * kh, 2ull * d_, ly->bn_qkv);
-    ly->tm_o = make_kmajor_map(ly->w_o.p, BF, 2, kh, d_, 2ull * kh, ly->bn_o);
-    ly->tm_in = make_kmajor_map(ly->w_in.p, BF, 2, d_, f, 2ull * d_, ly->bn_in);
-    ly->tm_out = make_kmajor_map(ly->w_out.p, BF, 2, f, d_, 2ull * f_ld, ly->bn_out);
+    ly->tm_qkv = make_kmajor_map(ly->w_qkv.p, BF, 2, d_, 3ull * kh, 2ull * d_, 128);
+    ly->tm_o = make_kmajor_map(ly->w_o.p, BF, 2, kh, d_, 2ull * kh, 128);
+    ly->tm_in = make_kmajor_map(ly->w_in.p, BF, 2, d_, f, 2ull * d_, 128);
+    ly->tm_out = make_kmajor_map(ly->w_out.p, BF, 2, f, d_, 2ull * f_ld, 128);
     kh_max_ = std::max(kh_max_, kh);
     f_ld_max_ = std::max(f_ld_max_, f_ld);
     layers_.push_back(std::move(ly));
@@ -381,9 +389,8 @@ void Engine::add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p
   }
 }
 
-void Engine::gemm(int bn, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
-                  const GemmEpi& ep) {
-  launch_gemm_bf16(bn, epi, A, B, M, N, K, ep, stream_, sms_);
+void Engine::gemm(int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep) {
+  launch_gemm(use_pair(M, N), false, epi, A, B, M, N, K, ep, stream_, sms_);
   ++stats_.kernel_launches;
 }
 
@@ -461,7 +468,7 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     ep.hd = hd_;
     ep.heads = ly.heads;
     ep.page_size = PAGE;
-    timed(1, 2.0 * dT * 3 * ly.kh * d_, [&] { gemm(ly.bn_qkv, iolmk::EPI_QKV, tm_h_, ly.tm_qkv, T, 3 * ly.kh, d_, ep); });
+    timed(1, 2.0 * dT * 3 * ly.kh * d_, [&] { gemm(iolmk::EPI_QKV, tm_h_, ly.tm_qkv, T, 3 * ly.kh, d_, ep); });
     // attention
     AttnParams ap{};
     ap.q = q_.p;
@@ -492,7 +499,7 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     eo.N = d_;
     eo.out = x_.p;
     eo.ldo = d_;
-    timed(4, 2.0 * dT * d_ * ly.kh, [&] { gemm(ly.bn_o, iolmk::EPI_RESID_F32, ly.tm_z, ly.tm_o, T, d_, ly.kh, eo); });
+    timed(4, 2.0 * dT * d_ * ly.kh, [&] { gemm(iolmk::EPI_RESID_F32, ly.tm_z, ly.tm_o, T, d_, ly.kh, eo); });
     // h = LN2(x)
     timed(5, dT * d_ * 6.0, [&] { launch_ln(x_.p, T, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_); });
     ++stats_.kernel_launches;
@@ -502,9 +509,9 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     ei.N = ly.f;
     ei.out = g_.p;
     ei.ldo = f_ld_max_;
-    timed(6, 2.0 * dT * ly.f * d_, [&] { gemm(ly.bn_in, iolmk::EPI_GELU_BF16, tm_h_, ly.tm_in, T, ly.f, d_, ei); });
+    timed(6, 2.0 * dT * ly.f * d_, [&] { gemm(iolmk::EPI_GELU_BF16, tm_h_, ly.tm_in, T, ly.f, d_, ei); });
     // x += g * Wout^T
-    timed(7, 2.0 * dT * d_ * ly.f, [&] { gemm(ly.bn_out, iolmk::EPI_RESID_F32, ly.tm_g, ly.tm_out, T, d_, ly.f, eo); });
+    timed(7, 2.0 * dT * d_ * ly.f, [&] { gemm(iolmk::EPI_RESID_F32, ly.tm_g, ly.tm_out, T, d_, ly.f, eo); });
     if (l + 1 < L_) {
       timed(5, dT * d_ * 6.0, [&] {
         launch_ln(x_.p, T, d_, layers_[l + 1]->ln1_g.p, layers_[l + 1]->ln1_b.p, h_.p, d_, stream_);

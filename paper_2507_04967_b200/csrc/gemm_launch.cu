@@ -1,4 +1,7 @@
 // Host launchers for the tcgen05 GEMM instantiations.
+//   bf16 x bf16 -> fp32 (kind::f16) and s8 x s8 -> s32 (kind::i8, W8A8), each as
+//   2-SM pairs (CG = 2, 256 x 256 tiles, clusters of 2) or single-CTA (CG = 1, 128 x 128 tiles).
+// Every TMA box is 128 rows x 128 bytes, so one tensor map per operand serves both shapes.
 #include "gemm_sm100.cuh"
 #include "launch.hpp"
 
@@ -6,46 +9,65 @@ namespace iolmh {
 
 using namespace iolmk;
 
-template <int BN, int EPI>
-static void launch_one(const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
-                       const GemmEpi& ep, cudaStream_t st, int grid_cap) {
-  using Cfg = GemmCfg<BN>;
+template <int BN, int EPI, int CG, bool I8>
+static void launch_one(const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep,
+                       cudaStream_t st, int grid_cap) {
+  using Cfg = GemmCfg<BN, CG>;
+  auto kern = gemm_tn_kernel<BN, EPI, CG, I8>;
   static bool configured = false;
   if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(Cfg::SMEM)));
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM)));
     configured = true;
   }
-  const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < grid_cap ? tiles : grid_cap;
-  if (grid <= 0) return;
-  gemm_bf16_tn_kernel<BN, EPI><<<grid, 192, Cfg::SMEM, st>>>(A, B, M, N, K, ep);
-  CUDA_OK(cudaGetLastError());
+  const int tiles = ((M + Cfg::TILE_M - 1) / Cfg::TILE_M) * ((N + BN - 1) / BN);
+  int groups = std::min(tiles, grid_cap / CG);
+  if (groups <= 0) return;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(groups * CG);
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, kern, A, B, M, N, K, ep));
 }
 
-template <int BN>
+template <int BN, int CG, bool I8>
 static void dispatch_epi(int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
                          const GemmEpi& ep, cudaStream_t st, int grid_cap) {
   switch (epi) {
-    case EPI_F32: return launch_one<BN, EPI_F32>(A, B, M, N, K, ep, st, grid_cap);
-    case EPI_BF16: return launch_one<BN, EPI_BF16>(A, B, M, N, K, ep, st, grid_cap);
-    case EPI_GELU_BF16: return launch_one<BN, EPI_GELU_BF16>(A, B, M, N, K, ep, st, grid_cap);
-    case EPI_RESID_F32: return launch_one<BN, EPI_RESID_F32>(A, B, M, N, K, ep, st, grid_cap);
-    case EPI_QKV: return launch_one<BN, EPI_QKV>(A, B, M, N, K, ep, st, grid_cap);
-    default: throw Unsupported("gemm: unknown epilogue");
+    case EPI_F32:
+      if constexpr (!I8) return launch_one<BN, EPI_F32, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
+      break;
+    case EPI_S32:
+      if constexpr (I8) return launch_one<BN, EPI_S32, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
+      break;
+    case EPI_BF16: return launch_one<BN, EPI_BF16, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_GELU_BF16: return launch_one<BN, EPI_GELU_BF16, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_RESID_F32: return launch_one<BN, EPI_RESID_F32, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_QKV: return launch_one<BN, EPI_QKV, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
+    default: break;
   }
+  throw Unsupported("gemm: epilogue not instantiated for this operand type");
 }
 
-void launch_gemm_bf16(int bn, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N,
-                      int K, const GemmEpi& ep, cudaStream_t st, int grid_cap) {
+// pair = true: 2-SM 256x256 tiles; false: single-CTA 128x128 tiles.
+void launch_gemm(bool pair, bool i8, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
+                 const GemmEpi& ep, cudaStream_t st, int grid_cap) {
   if (M <= 0 || N <= 0) return;
-  if (bn == 256)
-    dispatch_epi<256>(epi, A, B, M, N, K, ep, st, grid_cap);
-  else if (bn == 128)
-    dispatch_epi<128>(epi, A, B, M, N, K, ep, st, grid_cap);
-  else
-    throw Unsupported("gemm: BN must be 128 or 256");
+  if (pair) {
+    if (i8) dispatch_epi<256, 2, true>(epi, A, B, M, N, K, ep, st, grid_cap);
+    else dispatch_epi<256, 2, false>(epi, A, B, M, N, K, ep, st, grid_cap);
+  } else {
+    if (i8) dispatch_epi<128, 1, true>(epi, A, B, M, N, K, ep, st, grid_cap);
+    else dispatch_epi<128, 1, false>(epi, A, B, M, N, K, ep, st, grid_cap);
+  }
+  CUDA_OK(cudaGetLastError());
 }
 
 }  // namespace iolmh

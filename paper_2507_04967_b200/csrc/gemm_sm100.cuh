@@ -26,6 +26,7 @@ enum EpiMode : int {
   EPI_GELU_BF16 = 2,  // out bf16 gelu(acc)
   EPI_RESID_F32 = 3,  // resid f32 [M x ldo] += acc   (x += z*Wo^T, x += g*Wout^T)
   EPI_QKV = 4,        // cols [0,kh) -> q bf16; [kh,2kh) -> K pages; [2kh,3kh) -> V pages
+  EPI_S32 = 5,        // raw int32 accumulators [M x ldo] (integer GEMM parity tests)
 };
 
 struct GemmEpi {
@@ -44,15 +45,22 @@ struct GemmEpi {
   const float* w_scale = nullptr;
 };
 
-template <int BN>
+// Tile configuration. CG = 2 runs the 2-SM UMMA: a CTA pair computes a 256 x BN tile, each CTA
+// stages its own 128 rows of A and half (BN/2 rows) of the W tile, the leader CTA issues
+// tcgen05.mma.cta_group::2, and each CTA drains its 128 accumulator lanes from its own TMEM.
+template <int BN, int CG>
 struct GemmCfg {
-  static constexpr int BM = 128;
+  static constexpr int BM = 128;        // rows per CTA
+  static constexpr int TILE_M = BM * CG;
+  static constexpr int BN_CTA = BN / CG;  // W rows staged per CTA
   static constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per operand row
-  static constexpr int STAGES = BN >= 256 ? 4 : 6;
+  static constexpr int STAGES = CG == 2 ? (BN >= 256 ? 6 : 8) : (BN >= 256 ? 4 : 6);
   static constexpr uint32_t A_BYTES = BM * BK_BYTES;
-  static constexpr uint32_t B_BYTES = BN * BK_BYTES;
+  static constexpr uint32_t B_BYTES = BN_CTA * BK_BYTES;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr int EPI_WARPS = 8;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
   static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + 256;
 };
 
@@ -141,11 +149,11 @@ __device__ __forceinline__ void epi_apply(const GemmEpi& ep, int m, int n0, floa
   }
 }
 
-template <int BN, int EPI>
-__global__ void __launch_bounds__(192, 1)
-    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        int M, int N, int K, GemmEpi ep) {
-  using C = GemmCfg<BN>;
+template <int BN, int EPI, int CG, bool I8>
+__global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
+    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, GemmEpi ep) {
+  using C = GemmCfg<BN, CG>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -158,48 +166,66 @@ __global__ void __launch_bounds__(192, 1)
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * STAGES + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (2 * STAGES + 2 + a); };
   const uint32_t tmem_slot = bars + 8u * (2 * STAGES + 4);
-  const uint32_t* tmem_slot_ptr =
-      reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - raw));
+  const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - raw));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 1);
+      mbar_init(full_bar(s), CG);  // leader: one arrive per producer of the pair
       mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 4);
+      mbar_init(tempty_bar(a), C::EPI_WARPS * CG);
     }
     mbar_fence_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc2(tmem_slot, C::TMEM_COLS);
+    else tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
 
-  const int m_tiles = (M + C::BM - 1) / C::BM;
+  const int m_tiles = (M + C::TILE_M - 1) / C::TILE_M;
   const int n_tiles = (N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
-  const int kbs = (K * 2 + C::BK_BYTES - 1) / C::BK_BYTES;  // 64 bf16 elements per block
+  const int kbs = (K * (I8 ? 1 : 2) + C::BK_BYTES - 1) / C::BK_BYTES;  // 128-byte K blocks
+  constexpr int KELEMS = I8 ? 128 : 64;                                // K elements per block
+  const int group = blockIdx.x / CG, n_groups = gridDim.x / CG;
 
   if (warp == 0) {
     if (lane == 0) {
+      const uint32_t leader_full0 = CG == 2 ? mapa_shared(full_bar(0), 0) : full_bar(0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = group; tile < num_tiles; tile += n_groups) {
         const int mt = tile / n_tiles;
         const int nt = tile - mt * n_tiles;
+        const int arow = mt * C::TILE_M + static_cast<int>(rank) * C::BM;
+        const int brow = nt * BN + static_cast<int>(rank) * C::BN_CTA;
         for (int kb = 0; kb < kbs; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
-          mbar_expect_tx(full_bar(stage), C::STAGE_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, full_bar(stage), kb * 64, mt * C::BM);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, full_bar(stage), kb * 64, nt * BN);
+          if constexpr (CG == 2) {
+            const uint32_t lf = leader_full0 + 8u * stage;
+            if (leader) mbar_expect_tx(full_bar(stage), 2 * C::STAGE_BYTES);
+            tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, lf, kb * KELEMS, arow);
+            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, lf, kb * KELEMS, brow);
+            if (!leader) mbar_arrive_cluster(lf);
+          } else {
+            mbar_expect_tx(full_bar(stage), C::STAGE_BYTES);
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, full_bar(stage), kb * KELEMS, arow);
+            tma_load_2d(sB + stage * C::B_BYTES, &tmB, full_bar(stage), kb * KELEMS, brow);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -209,13 +235,13 @@ __global__ void __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16(128, BN, 1);
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = I8 ? idesc_i8(128 * CG, BN) : idesc_f16(128 * CG, BN, 1);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = group; tile < num_tiles; tile += n_groups) {
         mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -225,57 +251,91 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t ad = smem_desc_k_sw128(sA + stage * C::A_BYTES);
           const uint64_t bd = smem_desc_k_sw128(sB + stage * C::B_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_f16(d, ad + 2u * kk, bd + 2u * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
-          umma_commit(empty_bar(stage));
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
+            if constexpr (CG == 2) {
+              if constexpr (I8) umma_i8_pair(d, ad + 2u * kk, bd + 2u * kk, idesc, accum);
+              else umma_f16_pair(d, ad + 2u * kk, bd + 2u * kk, idesc, accum);
+            } else {
+              if constexpr (I8) umma_i8(d, ad + 2u * kk, bd + 2u * kk, idesc, accum);
+              else umma_f16(d, ad + 2u * kk, bd + 2u * kk, idesc, accum);
+            }
+          }
+          if constexpr (CG == 2) umma_commit_pair_mc(empty_bar(stage), 0x3);
+          else umma_commit(empty_bar(stage));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        umma_commit(tfull_bar(acc));
+        if constexpr (CG == 2) umma_commit_pair_mc(tfull_bar(acc), 0x3);
+        else umma_commit(tfull_bar(acc));
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1u;
       }
     }
     __syncwarp();
   } else {
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int e = warp - 2;
+    const int q = warp & 3;             // TMEM lane quarter this warp may access
+    const int c_begin = (e >> 2) * (BN / 2);  // column half handled by this warp
+    const uint32_t leader_tempty0 = CG == 2 ? mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int tile = group; tile < num_tiles; tile += n_groups) {
       const int mt = tile / n_tiles;
       const int nt = tile - mt * n_tiles;
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
-      const int m = mt * C::BM + q * 32 + lane;
-      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                             static_cast<uint32_t>(acc * BN);
+      const int m = mt * C::TILE_M + static_cast<int>(rank) * C::BM + q * 32 + lane;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        const int n0 = nt * BN + c * 32;
+      for (int c = c_begin; c < c_begin + BN / 2; c += 32) {
+        const int n0 = nt * BN + c;
         if (n0 >= N) break;  // warp-uniform
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tbase + c * 32, r);
+        tmem_ld_32x32b_x32(tbase + c, r);
         tmem_ld_wait();
         if (m < M) {
-          float v[32];
+          if constexpr (EPI == EPI_S32) {
+            int32_t* o = static_cast<int32_t*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          epi_apply<EPI>(ep, m, n0, v);
+            for (int j = 0; j < 32; ++j)
+              if (n0 + j < N) o[j] = static_cast<int32_t>(r[j]);
+          } else {
+            float v[32];
+            if constexpr (I8) {
+              const float sa = ep.a_scale[m];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int n = min(n0 + j, N - 1);
+                v[j] = static_cast<float>(static_cast<int32_t>(r[j])) * sa * ep.w_scale[n];
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            }
+            epi_apply<EPI>(ep, m, n0, v);
+          }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar(acc));
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(leader_tempty0 + 8u * acc);
+        else mbar_arrive(tempty_bar(acc));
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1u;
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if constexpr (CG == 2) tmem_dealloc2(tmem_base, C::TMEM_COLS);
+    else tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 

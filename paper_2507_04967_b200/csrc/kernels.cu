@@ -117,137 +117,159 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // 64 queries of one group x one head per CTA (4 warps x 16 query rows). Key blocks of 64 positions
 // aligned to absolute position 0, so a query's arithmetic depends only on its own position and the
-// K/V values (never on how the step was composed): batch-invariant.
+// K/V values (never on how the step was composed): batch-invariant. K/V blocks stream through a
+// two-stage cp.async ring (zero-filled past the last key).
 template <int HD>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
   constexpr int LD = HD + 8;
   constexpr int KB = 64;
   extern __shared__ __align__(16) uint8_t attn_smem[];
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(attn_smem);
-  __nv_bfloat16* sK = sQ + 64 * LD;
-  __nv_bfloat16* sV = sK + KB * LD;
+  __nv_bfloat16* sKV = sQ + 64 * LD;  // [stage][K|V][KB][LD]
   const AttnGroup grp = p.groups[blockIdx.x];
   const int head = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
+  const int last_key = grp.pos0 + grp.nq - 1;
+  const size_t head_off = static_cast<size_t>(head) * PAGE * HD;
+  const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
+  const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
+  const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
 
+  auto issue_block = [&](int kb, int stage) {
+    __nv_bfloat16* sK = sKV + static_cast<size_t>(stage) * 2 * KB * LD;
+    __nv_bfloat16* sV = sK + KB * LD;
+    for (int idx = tid; idx < KB * (HD / 8); idx += 128) {
+      const int r = idx / (HD / 8), c = (idx % (HD / 8)) * 8;
+      const int pos = kb * KB + r;
+      const bool ok = pos <= last_key;
+      const __nv_bfloat16* base =
+          ok ? p.kv + static_cast<size_t>(pt[pos / PAGE]) * page_stride + head_off + (pos % PAGE) * HD + c : p.kv;
+      cp_async16(sK + r * LD + c, base, ok);
+      cp_async16(sV + r * LD + c, ok ? base + v_off : p.kv, ok);
+    }
+  };
   for (int idx = tid; idx < 64 * (HD / 8); idx += 128) {
     const int r = idx / (HD / 8), c = (idx % (HD / 8)) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < grp.nq)
-      v = *reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(grp.m0 + r) * p.ldq + head * HD + c);
-    *reinterpret_cast<uint4*>(sQ + r * LD + c) = v;
+    const bool ok = r < grp.nq;
+    cp_async16(sQ + r * LD + c, ok ? p.q + static_cast<size_t>(grp.m0 + r) * p.ldq + head * HD + c : p.q, ok);
   }
-  __syncthreads();
-  uint32_t qf[HD / 16][4];
-#pragma unroll
-  for (int kc = 0; kc < HD / 16; ++kc)
-    ldsm_x4(qf[kc], sQ + (warp * 16 + (lane & 15)) * LD + kc * 16 + (lane >> 4) * 8);
+  issue_block(0, 0);
+  cp_async_commit();
 
-  const int last_key = grp.pos0 + grp.nq - 1;
   const int qpos0 = grp.pos0 + warp * 16 + gq;  // rows gq and gq+8 of this warp
   const int qpos1 = qpos0 + 8;
   const int warp_max_pos = grp.pos0 + min(grp.nq - 1, warp * 16 + 15);
+  const bool warp_active = warp * 16 < grp.nq;
   float m_i[2] = {-INFINITY, -INFINITY};
   float l_i[2] = {0.f, 0.f};
   float o[HD / 8][4];
 #pragma unroll
   for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  uint32_t qf[HD / 16][4];
 
-  const size_t head_off = static_cast<size_t>(head) * PAGE * HD;
-  const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
-  const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
-  const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
   const int nblocks = last_key / KB + 1;
   for (int kb = 0; kb < nblocks; ++kb) {
-    __syncthreads();
-    for (int idx = tid; idx < KB * (HD / 8); idx += 128) {
-      const int r = idx / (HD / 8), c = (idx % (HD / 8)) * 8;
-      const int pos = kb * KB + r;
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (pos <= last_key) {
-        const int pg = pt[pos / PAGE];
-        const __nv_bfloat16* base = p.kv + static_cast<size_t>(pg) * page_stride + head_off + (pos % PAGE) * HD + c;
-        kv = *reinterpret_cast<const uint4*>(base);
-        vv = *reinterpret_cast<const uint4*>(base + v_off);
-      }
-      *reinterpret_cast<uint4*>(sK + r * LD + c) = kv;
-      *reinterpret_cast<uint4*>(sV + r * LD + c) = vv;
+    if (kb + 1 < nblocks) {
+      issue_block(kb + 1, (kb + 1) & 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    if (kb * KB > warp_max_pos || warp * 16 >= grp.nq) continue;  // warp-uniform: nothing visible
-
-    float s[KB / 8][4];
+    if (kb == 0) {
 #pragma unroll
-    for (int i = 0; i < KB / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+      for (int kc = 0; kc < HD / 16; ++kc)
+        ldsm_x4(qf[kc], sQ + (warp * 16 + (lane & 15)) * LD + kc * 16 + (lane >> 4) * 8);
+    }
+    const __nv_bfloat16* sK = sKV + static_cast<size_t>(kb & 1) * 2 * KB * LD;
+    const __nv_bfloat16* sV = sK + KB * LD;
+    if (warp_active && kb * KB <= warp_max_pos) {  // warp-uniform
+      float s[KB / 8][4];
 #pragma unroll
-    for (int kc = 0; kc < HD / 16; ++kc) {
+      for (int i = 0; i < KB / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
 #pragma unroll
-      for (int np = 0; np < KB / 16; ++np) {
-        uint32_t b[4];
-        ldsm_x4(b, sK + (np * 16 + (lane & 7) + (lane >> 4) * 8) * LD + kc * 16 + ((lane >> 3) & 1) * 8);
-        mma_bf16(s[2 * np], qf[kc], b[0], b[1]);
-        mma_bf16(s[2 * np + 1], qf[kc], b[2], b[3]);
+      for (int kc = 0; kc < HD / 16; ++kc) {
+#pragma unroll
+        for (int np = 0; np < KB / 16; ++np) {
+          uint32_t b[4];
+          ldsm_x4(b, sK + (np * 16 + (lane & 7) + (lane >> 4) * 8) * LD + kc * 16 + ((lane >> 3) & 1) * 8);
+          mma_bf16(s[2 * np], qf[kc], b[0], b[1]);
+          mma_bf16(s[2 * np + 1], qf[kc], b[2], b[3]);
+        }
+      }
+      float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int nt = 0; nt < KB / 8; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = kb * KB + nt * 8 + 2 * tq + (e & 1);
+          const int qp = e < 2 ? qpos0 : qpos1;
+          bool ok = key <= qp;
+          if (p.key_mask) ok = ok && p.key_mask[key];
+          const float v = ok ? s[nt][e] * p.scale_log2 : -INFINITY;
+          s[nt][e] = v;
+          mx[e >> 1] = fmaxf(mx[e >> 1], v);
+        }
+      }
+      float alpha[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+        const float mnew = fmaxf(m_i[r], mx[r]);
+        alpha[r] = mnew == -INFINITY ? 1.f : exp2f(m_i[r] - mnew);
+        m_i[r] = mnew;
+        l_i[r] *= alpha[r];
+      }
+#pragma unroll
+      for (int nt = 0; nt < KB / 8; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float mm = m_i[e >> 1];
+          const float pv = mm == -INFINITY ? 0.f : exp2f(s[nt][e] - mm);
+          s[nt][e] = pv;
+          l_i[e >> 1] += pv;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) {
+        o[i][0] *= alpha[0];
+        o[i][1] *= alpha[0];
+        o[i][2] *= alpha[1];
+        o[i][3] *= alpha[1];
+      }
+#pragma unroll
+      for (int kc = 0; kc < KB / 16; ++kc) {
+        uint32_t a[4];
+        a[0] = pack_bf16x2(s[2 * kc][0], s[2 * kc][1]);
+        a[1] = pack_bf16x2(s[2 * kc][2], s[2 * kc][3]);
+        a[2] = pack_bf16x2(s[2 * kc + 1][0], s[2 * kc + 1][1]);
+        a[3] = pack_bf16x2(s[2 * kc + 1][2], s[2 * kc + 1][3]);
+#pragma unroll
+        for (int dn = 0; dn < HD / 16; ++dn) {
+          uint32_t b[4];
+          ldsm_x4_t(b, sV + (kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LD + dn * 16 + (lane >> 4) * 8);
+          mma_bf16(o[2 * dn], a, b[0], b[1]);
+          mma_bf16(o[2 * dn + 1], a, b[2], b[3]);
+        }
       }
     }
-    float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-    for (int nt = 0; nt < KB / 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = kb * KB + nt * 8 + 2 * tq + (e & 1);
-        const int qp = e < 2 ? qpos0 : qpos1;
-        bool ok = key <= qp;
-        if (p.key_mask) ok = ok && p.key_mask[key];
-        const float v = ok ? s[nt][e] * p.scale_log2 : -INFINITY;
-        s[nt][e] = v;
-        mx[e >> 1] = fmaxf(mx[e >> 1], v);
-      }
-    }
-    float alpha[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-      const float mnew = fmaxf(m_i[r], mx[r]);
-      alpha[r] = mnew == -INFINITY ? 1.f : exp2f(m_i[r] - mnew);
-      m_i[r] = mnew;
-      l_i[r] *= alpha[r];
-    }
-#pragma unroll
-    for (int nt = 0; nt < KB / 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float mm = m_i[e >> 1];
-        const float pv = mm == -INFINITY ? 0.f : exp2f(s[nt][e] - mm);
-        s[nt][e] = pv;
-        l_i[e >> 1] += pv;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < HD / 8; ++i) {
-      o[i][0] *= alpha[0];
-      o[i][1] *= alpha[0];
-      o[i][2] *= alpha[1];
-      o[i][3] *= alpha[1];
-    }
-#pragma unroll
-    for (int kc = 0; kc < KB / 16; ++kc) {
-      uint32_t a[4];
-      a[0] = pack_bf16x2(s[2 * kc][0], s[2 * kc][1]);
-      a[1] = pack_bf16x2(s[2 * kc][2], s[2 * kc][3]);
-      a[2] = pack_bf16x2(s[2 * kc + 1][0], s[2 * kc + 1][1]);
-      a[3] = pack_bf16x2(s[2 * kc + 1][2], s[2 * kc + 1][3]);
-#pragma unroll
-      for (int dn = 0; dn < HD / 16; ++dn) {
-        uint32_t b[4];
-        ldsm_x4_t(b, sV + (kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LD + dn * 16 + (lane >> 4) * 8);
-        mma_bf16(o[2 * dn], a, b[0], b[1]);
-        mma_bf16(o[2 * dn + 1], a, b[2], b[3]);
-      }
-    }
+    __syncthreads();  // stage kb&1 is refilled by the next iteration's prefetch
   }
   float inv[2];
 #pragma unroll
@@ -271,84 +293,115 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
 }
 
 // ------------------------------------------------------------------ attention (decode)
-// One warp per (sequence, head), single query at position pos0. Keys in absolute 32-position
-// chunks: lane j scores key chunk*32+j, then the warp accumulates p*V with lanes owning dims.
+// One warp per (sequence, head), single query at position pos0. A key row of HD bf16 is read by
+// LPK = HD/8 lanes with one 16-byte load each, so a warp covers KPI = 32/LPK keys per load and
+// issues 8 independent K loads + 8 independent V loads per lane per chunk of CHUNK = 8*KPI keys.
+// Scores are reduced inside each lane group; p*V accumulates per lane over its own keys and the
+// KPI partial sums are combined once at the end. Chunks are aligned to absolute positions, so the
+// arithmetic of a query never depends on the batch it was scheduled in.
 template <int HD>
 __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
-  constexpr int DPL = HD >= 32 ? HD / 32 : 1;  // dims per lane in the PV accumulation
-  __shared__ __align__(16) float sq[4][HD];
+  constexpr int LPK = HD / 8;      // lanes per key row
+  constexpr int KPI = 32 / LPK;    // keys per warp-wide load
+  constexpr int IT = 8;            // loads per lane per chunk
+  constexpr int CHUNK = KPI * IT;  // keys per chunk
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * 4 + warp;
   if (item >= p.n_groups * p.heads) return;
   const int gi = item / p.heads, head = item - gi * p.heads;
   const AttnGroup grp = p.groups[gi];
-  const __nv_bfloat16* qr = p.q + static_cast<size_t>(grp.m0) * p.ldq + head * HD;
-  for (int i = lane; i < HD; i += 32) sq[warp][i] = __bfloat162float(qr[i]) * p.scale_log2;
-  __syncwarp();
+  const int sub = lane % LPK;   // which 8-dim slice of the key row
+  const int kin = lane / LPK;   // which key of the KPI keys per load
+  float qv[8];
+  {
+    const uint4 u = *reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(grp.m0) * p.ldq + head * HD + sub * 8);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h2[j]);
+      qv[2 * j] = f.x * p.scale_log2;
+      qv[2 * j + 1] = f.y * p.scale_log2;
+    }
+  }
   const int last = grp.pos0;
-  const size_t head_off = static_cast<size_t>(head) * PAGE * HD;
+  const size_t head_off = static_cast<size_t>(head) * PAGE * HD + sub * 8;
   const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
   const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
   const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
   float m = -INFINITY, l = 0.f;
-  float acc[DPL];
+  float acc[8];
 #pragma unroll
-  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
-  for (int c0 = 0; c0 <= last; c0 += 32) {
-    const int key = c0 + lane;
-    float s = -INFINITY;
-    if (key <= last && (!p.key_mask || p.key_mask[key])) {
-      const __nv_bfloat16* kr =
-          p.kv + static_cast<size_t>(pt[key / PAGE]) * page_stride + head_off + (key % PAGE) * HD;
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  for (int c0 = 0; c0 <= last; c0 += CHUNK) {
+    uint4 kr[IT], vr[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int key = c0 + it * KPI + kin;
+      kr[it] = make_uint4(0, 0, 0, 0);
+      vr[it] = make_uint4(0, 0, 0, 0);
+      if (key <= last) {
+        const __nv_bfloat16* base = p.kv + static_cast<size_t>(pt[key / PAGE]) * page_stride + head_off +
+                                    (key % PAGE) * HD;
+        kr[it] = *reinterpret_cast<const uint4*>(base);
+        vr[it] = *reinterpret_cast<const uint4*>(base + v_off);
+      }
+    }
+    float sc[IT];
+    float cmax = -INFINITY;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&kr[it]);
       float dot = 0.f;
 #pragma unroll
-      for (int c = 0; c < HD; c += 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(kr + c);
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = __bfloat1622float2(h2[j]);
-          dot = fmaf(f.x, sq[warp][c + 2 * j], dot);
-          dot = fmaf(f.y, sq[warp][c + 2 * j + 1], dot);
-        }
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h2[j]);
+        dot = fmaf(f.x, qv[2 * j], dot);
+        dot = fmaf(f.y, qv[2 * j + 1], dot);
       }
-      s = dot;
-    }
-    float cm = s;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
-    const float mnew = fmaxf(m, cm);
+      for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      const int key = c0 + it * KPI + kin;
+      const bool ok = key <= last && (!p.key_mask || p.key_mask[key]);
+      sc[it] = ok ? dot : -INFINITY;
+      cmax = fmaxf(cmax, sc[it]);
+    }
+#pragma unroll
+    for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    const float mnew = fmaxf(m, cmax);
     const float alpha = mnew == -INFINITY ? 1.f : exp2f(m - mnew);
-    const float pj = mnew == -INFINITY ? 0.f : exp2f(s - mnew);
-    float ps = pj;
+    float psum = 0.f;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-    l = l * alpha + ps;
-    m = mnew;
+    for (int j = 0; j < 8; ++j) acc[j] *= alpha;
 #pragma unroll
-    for (int i = 0; i < DPL; ++i) acc[i] *= alpha;
-    const int nk = min(32, last - c0 + 1);
-    for (int j = 0; j < nk; ++j) {
-      const float w = __shfl_sync(0xffffffffu, pj, j);
-      const int kk = c0 + j;
-      const __nv_bfloat16* vr =
-          p.kv + static_cast<size_t>(pt[kk / PAGE]) * page_stride + v_off + head_off + (kk % PAGE) * HD;
-      if (DPL == 2) {
-        const float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(vr)[lane]);
-        acc[0] = fmaf(w, f.x, acc[0]);
-        acc[DPL - 1] = fmaf(w, f.y, acc[DPL - 1]);
-      } else {
+    for (int it = 0; it < IT; ++it) {
+      const float pj = mnew == -INFINITY ? 0.f : exp2f(sc[it] - mnew);
+      psum += pj;
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&vr[it]);
 #pragma unroll
-        for (int i = 0; i < DPL; ++i)
-          if (lane * DPL + i < HD) acc[i] = fmaf(w, __bfloat162float(vr[lane * DPL + i]), acc[i]);
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h2[j]);
+        acc[2 * j] = fmaf(pj, f.x, acc[2 * j]);
+        acc[2 * j + 1] = fmaf(pj, f.y, acc[2 * j + 1]);
       }
     }
-  }
-  const float inv = l > 0.f ? 1.f / l : 0.f;
-  __nv_bfloat16* zr = p.z + static_cast<size_t>(grp.m0) * p.ldz + head * HD;
 #pragma unroll
-  for (int i = 0; i < DPL; ++i)
-    if (lane * DPL + i < HD) zr[lane * DPL + i] = __float2bfloat16_rn(acc[i] * inv);
+    for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
+    l = l * alpha + psum;
+    m = mnew;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int o = LPK; o < 32; o <<= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  if (kin == 0) {
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    uint4 w;
+    w.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+    w.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+    w.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+    w.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+    *reinterpret_cast<uint4*>(p.z + static_cast<size_t>(grp.m0) * p.ldz + head * HD + sub * 8) = w;
+  }
 }
 
 // ------------------------------------------------------------------ head + argmax
@@ -511,11 +564,24 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
   if (M <= 0) return;
   const unsigned grid = blocks_for(M, 8);
   const int nv = (d / 4 + 31) / 32;
-  if (nv <= 4) ln_kernel<4><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh);
-  else if (nv <= 8) ln_kernel<8><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh);
-  else if (nv <= 16) ln_kernel<16><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh);
-  else if (nv <= 32) ln_kernel<32><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh);
-  else throw Unsupported("layernorm: d_model > 4096");
+#define LNK(V) ln_kernel<V><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh)
+  switch (nv) {
+    case 1: LNK(1); break;
+    case 2: LNK(2); break;
+    case 3: LNK(3); break;
+    case 4: LNK(4); break;
+    case 5: LNK(5); break;
+    case 6: LNK(6); break;
+    case 8: LNK(8); break;
+    case 10: LNK(10); break;
+    case 12: LNK(12); break;
+    case 16: LNK(16); break;
+    default:
+      if (nv <= 16) LNK(16);
+      else if (nv <= 32) LNK(32);
+      else throw Unsupported("layernorm: d_model > 4096");
+  }
+#undef LNK
   CUDA_OK(cudaGetLastError());
 }
 
@@ -528,11 +594,18 @@ void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_
 #define EMB(V)                                                                                          \
   embed_ln_kernel<V><<<grid, 256, 0, st>>>(ids, tok_src, tok_slot, tok_pos, last_tok, M, d, tok_embed, \
                                            pos_embed, x, g, b, h, ldh)
-  if (nv <= 4) EMB(4);
-  else if (nv <= 8) EMB(8);
-  else if (nv <= 16) EMB(16);
-  else if (nv <= 32) EMB(32);
-  else throw Unsupported("embed: d_model > 4096");
+  switch (nv) {
+    case 1: EMB(1); break;
+    case 2: EMB(2); break;
+    case 4: EMB(4); break;
+    case 8: EMB(8); break;
+    case 10: EMB(10); break;
+    case 16: EMB(16); break;
+    default:
+      if (nv <= 16) EMB(16);
+      else if (nv <= 32) EMB(32);
+      else throw Unsupported("embed: d_model > 4096");
+  }
 #undef EMB
   CUDA_OK(cudaGetLastError());
 }
@@ -540,7 +613,7 @@ void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_
 void launch_attention(const AttnParams& prefill, const AttnParams& decode, int hd, cudaStream_t st) {
 #define ATT(HD)                                                                                     \
   do {                                                                                              \
-    constexpr int smem = 3 * 64 * (HD + 8) * 2;                                                     \
+    constexpr int smem = 5 * 64 * (HD + 8) * 2;                                                     \
     static bool cfg = false;                                                                        \
     if (!cfg) {                                                                                     \
       CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD>,                                         \

@@ -53,7 +53,8 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define CUDA_OK(x) ::iolmh::cuda_check((x), #x, __FILE__, __LINE__)
 
 // ---- launchers (gemm_launch.cu, kernels.cu)
-void launch_gemm_bf16(int bn, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N,
-                      int K, const iolmk::GemmEpi& ep, cudaStream_t st, int grid_cap);
+// pair: 2-SM 256x256 tiles (clusters of 2) vs single-CTA 128x128 tiles; i8: W8A8 kind::i8.
+void launch_gemm(bool pair, bool i8, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
+                 const iolmk::GemmEpi& ep, cudaStream_t st, int grid_cap);
 
 }  // namespace iolmh

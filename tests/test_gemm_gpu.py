@@ -57,3 +57,21 @@ def test_gemm_gelu_resid(engine_lib):
     out, a, w = run_gemm(engine_lib, A, W, 128, 3, base)
     ref = base + a.astype(np.float64) @ w.astype(np.float64).T
     assert np.abs(out - ref).max() < 1e-4
+
+
+@pytest.mark.parametrize("M,N,K,pair", [
+    (128, 128, 128, 0), (300, 3840, 1280, 1), (1000, 1280, 5120, 1), (77, 200, 640, 0), (513, 2560, 2560, 1),
+    (4096, 5120, 1280, 1),
+])
+def test_gemm_s8_bitexact(engine_lib, M, N, K, pair):
+    """W8A8 integer GEMM (tcgen05 kind::i8): int32 accumulators bit-identical to the CPU
+    restatement (oracle.gemm_s8)."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(M + N + K)
+    A = rng.integers(-127, 128, size=(M, K), dtype=np.int8)
+    W = rng.integers(-127, 128, size=(N, K), dtype=np.int8)
+    out = np.zeros((M, N), np.int32)
+    st = engine_lib.iolm_cuda_debug_gemm_s8(A.ctypes.data, W.ctypes.data, out.ctypes.data, M, N, K, pair)
+    assert st == 0, engine_lib.iolm_cuda_last_error()
+    ref = O.gemm_s8(A, W)
+    assert np.array_equal(out, ref)
