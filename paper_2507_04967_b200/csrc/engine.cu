@@ -9,16 +9,21 @@
 //     of newly admitted rows, so every GEMM runs at M = thousands of rows. The common prompt prefix
 //     of the call is prefilled once into shared KV pages that every row's page table references.
 //   * K/V live in a paged bf16 pool (16-token pages); attention reads through per-slot page tables.
+//   * steps are pipelined: whether a row keeps decoding is decided by its emitted count and its
+//     length alone, except for EOS, so step k+1 is planned and launched before step k's tokens are
+//     read back. A row that hits EOS gets one speculative token in the next step; it is discarded.
+//     Generated token ids stay on the device (per-slot register written by the argmax kernel).
 // Output semantics follow batch_decode exactly (runtime.cpp:280-307): argmax (ties -> lowest id),
 // stop on EOS / budget before emitting, stop on a full context after emitting; the FlopCounter
 // contribution is the reference's closed form (runtime.cpp:311-345).
 #include <algorithm>
-#include <chrono>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
-#include <string>
 #include <memory>
 #include <mutex>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "bundle.hpp"
@@ -96,6 +101,7 @@ struct PinnedArray {
 };
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
+size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
 struct Layer {
   int heads = 0, kh = 0, f = 0;
@@ -119,6 +125,43 @@ bool use_pair(int M, int N) {
   return M >= 256 && N >= 256;
 }
 
+// Host-side description of one engine step.
+struct Step {
+  std::vector<int64_t> tok_src;  // >= 0: index into the id table; -1: slot's last generated token
+  std::vector<int> tok_slot, tok_pos;
+  std::vector<AttnGroup> pre, dec;
+  std::vector<int> head_rows, head_slot;
+  std::vector<int64_t> head_owner;  // caller row index per head row (host only)
+  void clear() {
+    tok_src.clear();
+    tok_slot.clear();
+    tok_pos.clear();
+    pre.clear();
+    dec.clear();
+    head_rows.clear();
+    head_slot.clear();
+    head_owner.clear();
+  }
+  int T() const { return static_cast<int>(tok_src.size()); }
+};
+
+// Device + pinned-host buffers of one in-flight step (double-buffered by step parity).
+struct StepBuffers {
+  PinnedArray<uint8_t> h_meta;  // packed metadata staging
+  DevArray<uint8_t> d_meta;
+  DevArray<int32_t> d_next;
+  PinnedArray<int32_t> h_next;
+  cudaEvent_t done = nullptr;
+  // device views into d_meta for the current step
+  const int64_t* tok_src = nullptr;
+  const int *tok_slot = nullptr, *tok_pos = nullptr, *head_rows = nullptr, *head_slot = nullptr;
+  const AttnGroup *pre = nullptr, *dec = nullptr;
+  Step step;
+  ~StepBuffers() {
+    if (done) cudaEventDestroy(done);
+  }
+};
+
 }  // namespace
 
 class Engine {
@@ -140,36 +183,22 @@ class Engine {
   void forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds);
 
   std::mutex mu;
+  double kms_[IOLM_KCLASSES] = {}, kwork_[IOLM_KCLASSES] = {};
+  int64_t kcount_[IOLM_KCLASSES] = {};
 
  private:
-  struct Step {
-    std::vector<int64_t> tok_src;
-    std::vector<int> tok_slot, tok_pos;
-    std::vector<AttnGroup> pre, dec;
-    std::vector<int> head_rows, head_slot;
-    void clear() {
-      tok_src.clear();
-      tok_slot.clear();
-      tok_pos.clear();
-      pre.clear();
-      dec.clear();
-      head_rows.clear();
-      head_slot.clear();
-    }
-    int T() const { return static_cast<int>(tok_src.size()); }
-  };
-
   void reset_counters();
   void upload_weights(const BundleView& b);
   void alloc_runtime();
   void set_prefix_pages(int prefix_pages);
-  void add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head);
-  void run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits);
+  static void add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head,
+                          int64_t owner);
+  void launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits);
   void gemm(int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
   uint64_t ref_madds_row(int s0, int advances) const;
   template <typename F>
   void timed(int cat, double work, F&& f);
-  void collect_times();
+  void collect_times(int64_t upto_step);
 
   ModelConfig cfg_;
   uint64_t hash_ = 0;
@@ -182,20 +211,18 @@ class Engine {
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   iolm_cuda_stats stats_{};
+  int64_t step_seq_ = 0;  // steps launched on this engine (kernel-timing bookkeeping)
+
   // kernel-class timing (opts.kernel_timing)
   bool ktime_ = false;
   std::vector<cudaEvent_t> kev_;
+  std::vector<int> kev_free_;
   struct KPending {
-    int cat, ev;
+    int cat, ev0, ev1;
     double work;
+    int64_t step;
   };
   std::vector<KPending> kpend_;
-
- public:
-  double kms_[IOLM_KCLASSES] = {}, kwork_[IOLM_KCLASSES] = {};
-  int64_t kcount_[IOLM_KCLASSES] = {};
-
- private:
 
   std::vector<std::unique_ptr<Layer>> layers_;
   DevArray<float> tok_embed_, tok_embed_t_, pos_embed_, lnf_g_, lnf_b_;
@@ -203,23 +230,18 @@ class Engine {
   DevArray<__nv_bfloat16> h_, q_, z_, g_;
   CUtensorMap tm_h_;
   DevArray<int> page_table_;
-  DevArray<int64_t> d_tok_src_;
-  DevArray<int> d_tok_slot_, d_tok_pos_, d_head_rows_, d_head_slot_;
-  DevArray<AttnGroup> d_pre_, d_dec_;
-  DevArray<int32_t> d_next_, d_last_tok_, d_ids_;
+  StepBuffers sbuf_[2];
+  DevArray<int32_t> d_last_tok_, d_ids_;
   DevArray<int64_t> d_offsets_;
   DevArray<int> d_scalar_;
   DevArray<float> d_logits_;
   DevArray<uint8_t> d_mask_;
-  PinnedArray<int32_t> h_next_;
-  PinnedArray<int32_t> h_ids_stage_;
 };
 
 Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opts* opts) {
   if (!bytes || len == 0) throw ContractViolation("iolm_cuda_create: empty bundle");
   BundleView b = parse_bundle(bytes, len);
   cfg_ = b.config;
-  hash_ = b.hash = fnv1a64(bytes, len);
   d_ = cfg_.d_model;
   L_ = cfg_.n_layers;
   V_ = cfg_.vocab_size;
@@ -250,8 +272,16 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
     madds_A_ += 4ull * d_ * kh + 2ull * d_ * cfg_.layer_ffn(l);
     madds_B_ += kh;
   }
-  upload_weights(b);
-  alloc_runtime();
+  // The FNV-1a hash of the serialized bundle is inherently sequential; overlap it with the upload.
+  std::thread hasher([&] { hash_ = fnv1a64(bytes, len); });
+  try {
+    upload_weights(b);
+    alloc_runtime();
+  } catch (...) {
+    hasher.join();
+    throw;
+  }
+  hasher.join();
 }
 
 void Engine::upload_weights(const BundleView& b) {
@@ -325,15 +355,16 @@ void Engine::alloc_runtime() {
     ly->tm_z = make_kmajor_map(z_.p, BF, 2, ly->kh, T, 2ull * kh_max_, 128);
     ly->tm_g = make_kmajor_map(g_.p, BF, 2, ly->f, T, 2ull * f_ld_max_, 128);
   }
-  d_tok_src_.alloc(T);
-  d_tok_slot_.alloc(T);
-  d_tok_pos_.alloc(T);
-  d_head_rows_.alloc(T);
-  d_head_slot_.alloc(T);
-  d_pre_.alloc(T);
-  d_dec_.alloc(T);
-  d_next_.alloc(T);
-  h_next_.ensure(T);
+  // packed step metadata: tok_src i64[T], tok_slot/pos i32[T], groups 2 x [T], head rows/slots i32[T]
+  const size_t meta_bytes = align16(T * 8) + 2 * align16(T * 4) + 2 * align16(T * sizeof(AttnGroup)) +
+                            2 * align16(T * 4) + 64;
+  for (auto& sb : sbuf_) {
+    sb.h_meta.ensure(meta_bytes);
+    sb.d_meta.alloc(meta_bytes);
+    sb.d_next.alloc(T);
+    sb.h_next.ensure(T);
+    CUDA_OK(cudaEventCreateWithFlags(&sb.done, cudaEventDisableTiming));
+  }
   d_logits_.alloc(T * V_);
   d_mask_.alloc(S_);
   d_scalar_.alloc(4);
@@ -345,7 +376,7 @@ void Engine::alloc_runtime() {
   size_t free_b = 0, total_b = 0;
   CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
   const size_t cap = static_cast<size_t>(0.7 * static_cast<double>(free_b)) / std::max<size_t>(bytes_per_slot, 1);
-  if (max_slots_ <= 0) max_slots_ = 2048;
+  if (max_slots_ <= 0) max_slots_ = 2560;
   max_slots_ = static_cast<int>(std::min<size_t>(max_slots_, cap > 1 ? cap - 1 : 0));
   if (max_slots_ < 1) throw OutOfMemory("KV pool: not enough device memory for one sequence");
   prefix_slot_ = max_slots_;
@@ -374,7 +405,8 @@ void Engine::set_prefix_pages(int prefix_pages) {
   cur_prefix_pages_ = prefix_pages;
 }
 
-void Engine::add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head) {
+void Engine::add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head,
+                         int64_t owner) {
   const int m0 = s.T();
   for (int p = p_begin; p < p_end; ++p) {
     s.tok_src.push_back(src_base + p);
@@ -386,6 +418,7 @@ void Engine::add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p
   if (want_head) {
     s.head_rows.push_back(m0 + (p_end - p_begin) - 1);
     s.head_slot.push_back(slot);
+    s.head_owner.push_back(owner);
   }
 }
 
@@ -400,56 +433,83 @@ void Engine::timed(int cat, double work, F&& f) {
     f();
     return;
   }
-  const int i = static_cast<int>(kpend_.size()) * 2;
-  while (static_cast<int>(kev_.size()) < i + 2) {
-    cudaEvent_t e;
-    CUDA_OK(cudaEventCreate(&e));
-    kev_.push_back(e);
-  }
-  CUDA_OK(cudaEventRecord(kev_[i], stream_));
+  auto get_ev = [&] {
+    if (kev_free_.empty()) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreate(&e));
+      kev_.push_back(e);
+      kev_free_.push_back(static_cast<int>(kev_.size()) - 1);
+    }
+    const int i = kev_free_.back();
+    kev_free_.pop_back();
+    return i;
+  };
+  const int a = get_ev(), b = get_ev();
+  CUDA_OK(cudaEventRecord(kev_[a], stream_));
   f();
-  CUDA_OK(cudaEventRecord(kev_[i + 1], stream_));
-  kpend_.push_back({cat, i, work});
+  CUDA_OK(cudaEventRecord(kev_[b], stream_));
+  kpend_.push_back({cat, a, b, work, step_seq_});
 }
 
-void Engine::collect_times() {
+// Accumulates the durations of every timed launch of steps <= upto_step (already complete).
+void Engine::collect_times(int64_t upto_step) {
   if (!ktime_ || kpend_.empty()) return;
-  CUDA_OK(cudaStreamSynchronize(stream_));
+  std::vector<KPending> keep;
   for (const auto& k : kpend_) {
+    if (k.step > upto_step) {
+      keep.push_back(k);
+      continue;
+    }
     float ms = 0.f;
-    CUDA_OK(cudaEventElapsedTime(&ms, kev_[k.ev], kev_[k.ev + 1]));
+    CUDA_OK(cudaEventSynchronize(kev_[k.ev1]));
+    CUDA_OK(cudaEventElapsedTime(&ms, kev_[k.ev0], kev_[k.ev1]));
     kms_[k.cat] += ms;
     kwork_[k.cat] += k.work;
     kcount_[k.cat] += 1;
+    kev_free_.push_back(k.ev0);
+    kev_free_.push_back(k.ev1);
   }
-  kpend_.clear();
+  kpend_.swap(keep);
 }
 
-void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits) {
+// Packs the step's metadata into the pinned staging buffer, copies it with ONE async H2D, runs
+// the layer stack, the head + argmax, copies the generated ids back (async) and records sb.done.
+void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits) {
+  const Step& s = sb.step;
   const int T = s.T();
-  auto h2d = [&](void* dst, const void* src, size_t bytes) {
-    if (bytes) CUDA_OK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_));
+  const int R = static_cast<int>(s.head_rows.size());
+  uint8_t* h = sb.h_meta.p;
+  uint8_t* d = sb.d_meta.p;
+  size_t off = 0;
+  auto put = [&](const void* src, size_t bytes) {
+    if (bytes) std::memcpy(h + off, src, bytes);
+    const uint8_t* dev = d + off;
+    off = align16(off + bytes);
+    return dev;
   };
-  h2d(d_tok_src_.p, s.tok_src.data(), T * sizeof(int64_t));
-  h2d(d_tok_slot_.p, s.tok_slot.data(), T * sizeof(int));
-  h2d(d_tok_pos_.p, s.tok_pos.data(), T * sizeof(int));
-  h2d(d_pre_.p, s.pre.data(), s.pre.size() * sizeof(AttnGroup));
-  h2d(d_dec_.p, s.dec.data(), s.dec.size() * sizeof(AttnGroup));
-  h2d(d_head_rows_.p, s.head_rows.data(), s.head_rows.size() * sizeof(int));
-  h2d(d_head_slot_.p, s.head_slot.data(), s.head_slot.size() * sizeof(int));
+  sb.tok_src = reinterpret_cast<const int64_t*>(put(s.tok_src.data(), T * sizeof(int64_t)));
+  sb.tok_slot = reinterpret_cast<const int*>(put(s.tok_slot.data(), T * sizeof(int)));
+  sb.tok_pos = reinterpret_cast<const int*>(put(s.tok_pos.data(), T * sizeof(int)));
+  sb.pre = reinterpret_cast<const AttnGroup*>(put(s.pre.data(), s.pre.size() * sizeof(AttnGroup)));
+  sb.dec = reinterpret_cast<const AttnGroup*>(put(s.dec.data(), s.dec.size() * sizeof(AttnGroup)));
+  sb.head_rows = reinterpret_cast<const int*>(put(s.head_rows.data(), R * sizeof(int)));
+  sb.head_slot = reinterpret_cast<const int*>(put(s.head_slot.data(), R * sizeof(int)));
+  CUDA_OK(cudaMemcpyAsync(d, h, off, cudaMemcpyHostToDevice, stream_));
 
   const double dT = static_cast<double>(T);
   timed(0, dT * d_ * 14.0, [&] {
-    launch_embed_ln(d_ids, d_tok_src_.p, d_tok_slot_.p, d_tok_pos_.p, d_last_tok_.p, T, d_, tok_embed_.p,
-                    pos_embed_.p, x_.p, layers_[0]->ln1_g.p, layers_[0]->ln1_b.p, h_.p, d_, stream_);
+    launch_embed_ln(d_ids, sb.tok_src, sb.tok_slot, sb.tok_pos, d_last_tok_.p, T, d_, tok_embed_.p, pos_embed_.p,
+                    x_.p, layers_[0]->ln1_g.p, layers_[0]->ln1_b.p, h_.p, d_, stream_);
   });
   ++stats_.kernel_launches;
   // algorithmic attention work of this step (per head): prefill FLOPs 4*hd*sum(pos+1),
   // decode K+V bytes 2*2*hd*(pos+1)
   double pre_keys = 0, dec_keys = 0;
-  for (const auto& g : s.pre)
-    for (int i = 0; i < g.nq; ++i) pre_keys += g.pos0 + i + 1;
-  for (const auto& g : s.dec) dec_keys += g.pos0 + 1;
+  if (ktime_) {
+    for (const auto& g : s.pre)
+      for (int i = 0; i < g.nq; ++i) pre_keys += g.pos0 + i + 1;
+    for (const auto& g : s.dec) dec_keys += g.pos0 + 1;
+  }
   const float scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(hd_));
   for (int l = 0; l < L_; ++l) {
     Layer& ly = *layers_[l];
@@ -460,8 +520,8 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     ep.out = q_.p;
     ep.ldo = kh_max_;
     ep.kv_layer = ly.kv.p;
-    ep.tok_slot = d_tok_slot_.p;
-    ep.tok_pos = d_tok_pos_.p;
+    ep.tok_slot = sb.tok_slot;
+    ep.tok_pos = sb.tok_pos;
     ep.page_table = page_table_.p;
     ep.max_pages = pps_;
     ep.kh = ly.kh;
@@ -469,7 +529,6 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     ep.heads = ly.heads;
     ep.page_size = PAGE;
     timed(1, 2.0 * dT * 3 * ly.kh * d_, [&] { gemm(iolmk::EPI_QKV, tm_h_, ly.tm_qkv, T, 3 * ly.kh, d_, ep); });
-    // attention
     AttnParams ap{};
     ap.q = q_.p;
     ap.ldq = kh_max_;
@@ -481,18 +540,20 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
     ap.heads = ly.heads;
     ap.key_mask = d_key_mask;
     ap.scale_log2 = scale_log2;
-    AttnParams pre = ap, dec = ap;
-    pre.groups = d_pre_.p;
+    AttnParams pre = ap, dec = ap, none = ap;
+    pre.groups = sb.pre;
     pre.n_groups = static_cast<int>(s.pre.size());
-    dec.groups = d_dec_.p;
+    dec.groups = sb.dec;
     dec.n_groups = static_cast<int>(s.dec.size());
-    {
-      AttnParams none = pre;
-      none.n_groups = 0;
-      if (pre.n_groups) timed(2, 4.0 * hd_ * ly.heads * pre_keys, [&] { launch_attention(pre, none, hd_, stream_); });
-      if (dec.n_groups) timed(3, 4.0 * hd_ * ly.heads * dec_keys, [&] { launch_attention(none, dec, hd_, stream_); });
+    none.n_groups = 0;
+    if (pre.n_groups) {
+      timed(2, 4.0 * hd_ * ly.heads * pre_keys, [&] { launch_attention(pre, none, hd_, stream_); });
+      ++stats_.kernel_launches;
     }
-    stats_.kernel_launches += (pre.n_groups > 0) + (dec.n_groups > 0);
+    if (dec.n_groups) {
+      timed(3, 4.0 * hd_ * ly.heads * dec_keys, [&] { launch_attention(none, dec, hd_, stream_); });
+      ++stats_.kernel_launches;
+    }
     // x += z * Wo^T
     GemmEpi eo;
     eo.M = T;
@@ -519,18 +580,18 @@ void Engine::run_step(const Step& s, const int32_t* d_ids, const uint8_t* d_key_
       ++stats_.kernel_launches;
     }
   }
-  const int R = static_cast<int>(s.head_rows.size());
   if (R > 0) {
     timed(8, static_cast<double>(R) * d_ * 4.0 + static_cast<double>(V_) * d_ * 4.0, [&] {
-      launch_head(x_.p, d_, d_head_rows_.p, R, lnf_g_.p, lnf_b_.p, tok_embed_t_.p, V_, d_head_slot_.p, d_next_.p,
+      launch_head(x_.p, d_, sb.head_rows, R, lnf_g_.p, lnf_b_.p, tok_embed_t_.p, V_, sb.head_slot, sb.d_next.p,
                   d_last_tok_.p, d_logits, stream_);
     });
     ++stats_.kernel_launches;
-    CUDA_OK(cudaMemcpyAsync(h_next_.p, d_next_.p, R * sizeof(int32_t), cudaMemcpyDeviceToHost, stream_));
+    CUDA_OK(cudaMemcpyAsync(sb.h_next.p, sb.d_next.p, R * sizeof(int32_t), cudaMemcpyDeviceToHost, stream_));
   }
+  CUDA_OK(cudaEventRecord(sb.done, stream_));
   ++stats_.steps;
   stats_.tokens += T;
-  collect_times();
+  ++step_seq_;
 }
 
 uint64_t Engine::ref_madds_row(int s0, int advances) const {
@@ -597,83 +658,119 @@ void Engine::decode(const int32_t* ids, bool ids_on_device, const int64_t* offse
   const int P = prefix_pages * PAGE;
   set_prefix_pages(prefix_pages);
 
-  Step s;
+  int parity = 0;
   if (P > 0) {  // shared prefix: K/V only, computed once per call
-    s.clear();
-    add_prefill(s, prefix_slot_, offsets[0], 0, P, false);
-    run_step(s, d_ids, nullptr, nullptr);
+    StepBuffers& sb = sbuf_[parity];
+    sb.step.clear();
+    add_prefill(sb.step, prefix_slot_, offsets[0], 0, P, false, -1);
+    launch_step(sb, d_ids, nullptr, nullptr);
     stats_.prefix_tokens += P;
+    parity ^= 1;
   }
 
   struct RowState {
-    int slot = -1, s0 = 0, cur = 0, emitted = 0;
+    int slot = -1, s0 = 0;
+    int cur_plan = 0;    // sequence length after every planned step
+    int heads_plan = 0;  // token predictions planned
+    int emitted = 0;     // tokens confirmed and emitted
+    bool done = false;
   };
   std::vector<RowState> rows(n_rows);
-  std::vector<int> slot_row(max_slots_, -1);
   std::vector<int> free_slots;
   for (int sl = max_slots_ - 1; sl >= 0; --sl) free_slots.push_back(sl);
-  std::vector<int> decode_slots, next_decode;
+  std::vector<int64_t> live;  // rows with a token prediction in the last planned step
+  std::vector<int64_t> next_live;
   int64_t next_row = 0;
   uint64_t madd_total = 0;
-  while (next_row < n_rows || !decode_slots.empty()) {
-    s.clear();
-    for (int sl : decode_slots) {
-      RowState& r = rows[slot_row[sl]];
-      const int m = s.T();
-      s.tok_src.push_back(-1);  // token comes from the slot's last argmax (device register)
-      s.tok_slot.push_back(sl);
-      s.tok_pos.push_back(r.cur);
-      s.dec.push_back(AttnGroup{sl, m, 1, r.cur});
-      s.head_rows.push_back(m);
-      s.head_slot.push_back(sl);
-      ++r.cur;  // sequence length after this step's advance
-    }
-    stats_.decode_tokens += s.T();
-    while (next_row < n_rows && !free_slots.empty()) {
-      const int len = static_cast<int>(offsets[next_row + 1] - offsets[next_row]);
-      if (s.T() + (len - P) > T_max_) break;
-      const int sl = free_slots.back();
-      free_slots.pop_back();
-      slot_row[sl] = static_cast<int>(next_row);
-      rows[next_row].slot = sl;
-      rows[next_row].s0 = len;
-      rows[next_row].cur = len;
-      add_prefill(s, sl, offsets[next_row], P, len, true);
-      stats_.prefill_tokens += len - P;
-      ++next_row;
-    }
-    if (s.T() == 0) throw CudaError("scheduler stalled (no slot or token budget)");
-    run_step(s, d_ids, nullptr, nullptr);
-    CUDA_OK(cudaStreamSynchronize(stream_));
-    next_decode.clear();
-    for (size_t i = 0; i < s.head_slot.size(); ++i) {
-      const int sl = s.head_slot[i];
-      const int ri = slot_row[sl];
+  StepBuffers* inflight = nullptr;
+
+  // Results of one completed step: emit tokens, finish rows (EOS / budget / full context).
+  auto process = [&](StepBuffers& sb) {
+    CUDA_OK(cudaEventSynchronize(sb.done));
+    const Step& st = sb.step;
+    for (size_t i = 0; i < st.head_owner.size(); ++i) {
+      const int64_t ri = st.head_owner[i];
       RowState& r = rows[ri];
-      const int nxt = h_next_.p[i];
-      int advances = -1;  // >= 0 once the row is finished: advances the reference performs
+      if (r.done) continue;  // speculative token after an EOS
+      const int nxt = sb.h_next.p[i];
+      int advances = -1;
       if (nxt == IOLM_EOS || r.emitted == max_new) {
         advances = r.emitted;  // stop before emitting (runtime.cpp:287-290)
       } else {
         out_ids[static_cast<size_t>(ri) * max_new + r.emitted] = nxt;
         ++r.emitted;
-        if (r.cur == S_) {
-          advances = r.emitted - 1;  // context full: stop without advancing (runtime.cpp:293-296)
-        } else if (r.emitted == max_new) {
-          advances = r.emitted;  // the reference advances once more and discards the logits
-        } else {
-          next_decode.push_back(sl);
-        }
+        if (r.s0 + r.emitted - 1 == S_) advances = r.emitted - 1;  // full context (runtime.cpp:293-296)
+        else if (r.emitted == max_new) advances = r.emitted;     // reference advances once more
       }
       if (advances >= 0) {
+        r.done = true;
         out_len[ri] = r.emitted;
         madd_total += ref_madds_row(r.s0, advances);
-        slot_row[sl] = -1;
-        free_slots.push_back(sl);
       }
     }
-    decode_slots.swap(next_decode);
+  };
+
+  while (next_row < n_rows || !live.empty()) {
+    StepBuffers& sb = sbuf_[parity];
+    Step& s = sb.step;
+    s.clear();
+    // (a) one generated token for every row whose previous prediction will be emitted and fed
+    //     back; rows that stop here release their slot (stream order protects its pages)
+    next_live.clear();
+    for (int64_t ri : live) {
+      RowState& r = rows[ri];
+      if (r.done || r.heads_plan >= max_new || r.cur_plan >= S_) {
+        free_slots.push_back(r.slot);
+        r.slot = -1;
+        continue;
+      }
+      const int m = s.T();
+      s.tok_src.push_back(-1);  // token from the slot's last argmax (device register)
+      s.tok_slot.push_back(r.slot);
+      s.tok_pos.push_back(r.cur_plan);
+      s.dec.push_back(AttnGroup{r.slot, m, 1, r.cur_plan});
+      s.head_rows.push_back(m);
+      s.head_slot.push_back(r.slot);
+      s.head_owner.push_back(ri);
+      ++r.cur_plan;
+      ++r.heads_plan;
+      next_live.push_back(ri);
+    }
+    stats_.decode_tokens += s.T();
+    // (b) admit new rows while slots and the token budget allow
+    while (next_row < n_rows && !free_slots.empty()) {
+      const int len = static_cast<int>(offsets[next_row + 1] - offsets[next_row]);
+      if (s.T() + (len - P) > T_max_) break;
+      RowState& r = rows[next_row];
+      r.slot = free_slots.back();
+      free_slots.pop_back();
+      r.s0 = len;
+      r.cur_plan = len;
+      r.heads_plan = 1;
+      add_prefill(s, r.slot, offsets[next_row], P, len, true, next_row);
+      stats_.prefill_tokens += len - P;
+      next_live.push_back(next_row);
+      ++next_row;
+    }
+    live.swap(next_live);
+    if (s.T() == 0) {
+      if (inflight) {  // only finished rows left in flight
+        process(*inflight);
+        inflight = nullptr;
+        continue;
+      }
+      throw CudaError("scheduler stalled (no slot or token budget)");
+    }
+    launch_step(sb, d_ids, nullptr, nullptr);
+    if (inflight) {
+      process(*inflight);
+      collect_times(step_seq_ - 2);
+    }
+    inflight = &sb;
+    parity ^= 1;
   }
+  if (inflight) process(*inflight);
+  collect_times(step_seq_);
   if (madds) *madds = madd_total;
   CUDA_OK(cudaEventRecord(ev1_, stream_));
   CUDA_OK(cudaEventSynchronize(ev1_));
@@ -700,16 +797,19 @@ void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logi
     dmask = d_mask_.p;
   }
   set_prefix_pages(0);
-  Step s;
-  add_prefill(s, 0, 0, 0, n, false);
+  StepBuffers& sb = sbuf_[0];
+  sb.step.clear();
+  add_prefill(sb.step, 0, 0, 0, n, false, -1);
   for (int i = 0; i < n; ++i) {
-    s.head_rows.push_back(i);
-    s.head_slot.push_back(0);
+    sb.step.head_rows.push_back(i);
+    sb.step.head_slot.push_back(0);
+    sb.step.head_owner.push_back(0);
   }
-  run_step(s, d_ids_.p, dmask, d_logits_.p);
+  launch_step(sb, d_ids_.p, dmask, d_logits_.p);
   CUDA_OK(cudaMemcpyAsync(logits, d_logits_.p, sizeof(float) * n * V_, cudaMemcpyDeviceToHost, stream_));
   CUDA_OK(cudaEventRecord(ev1_, stream_));
   CUDA_OK(cudaEventSynchronize(ev1_));
+  collect_times(step_seq_);
   float ms = 0.f;
   CUDA_OK(cudaEventElapsedTime(&ms, ev0_, ev1_));
   stats_.device_ms = ms;

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), CG);  // leader: one arrive per producer of the pair
+      mbar_init(full_bar(s), 1);  // pair: the leader's expect_tx covers both CTAs' bytes
       mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -217,10 +217,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
           mbar_wait(empty_bar(stage), phase ^ 1u);
           if constexpr (CG == 2) {
             const uint32_t lf = leader_full0 + 8u * stage;
+            // The peer's bytes may land on the leader's barrier before the leader's expect_tx of
+            // the same phase: the transaction count goes transiently negative, which the
+            // barrier allows; the phase cannot complete before the leader's arrive.
             if (leader) mbar_expect_tx(full_bar(stage), 2 * C::STAGE_BYTES);
             tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, lf, kb * KELEMS, arow);
             tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, lf, kb * KELEMS, brow);
-            if (!leader) mbar_arrive_cluster(lf);
           } else {
             mbar_expect_tx(full_bar(stage), C::STAGE_BYTES);
             tma_load_2d(sA + stage * C::A_BYTES, &tmA, full_bar(stage), kb * KELEMS, arow);
@@ -285,9 +287,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     for (int tile = group; tile < num_tiles; tile += n_groups) {
       const int mt = tile / n_tiles;
       const int nt = tile - mt * n_tiles;
+      const int m = mt * C::TILE_M + static_cast<int>(rank) * C::BM + q * 32 + lane;
+      if constexpr (EPI == EPI_RESID_F32) {
+        // warm L2 with this thread's residual row segment while the MMAs of the tile run
+        if (m < M) {
+          const float* xr = static_cast<const float*>(ep.out) + static_cast<size_t>(m) * ep.ldo + nt * BN + c_begin;
+#pragma unroll
+          for (int c = 0; c < BN / 2; c += 32)
+            if (nt * BN + c_begin + c < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + c));
+        }
+      }
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
-      const int m = mt * C::TILE_M + static_cast<int>(rank) * C::BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
       for (int c = c_begin; c < c_begin + BN / 2; c += 32) {

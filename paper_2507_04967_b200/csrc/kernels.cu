@@ -293,114 +293,170 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
 }
 
 // ------------------------------------------------------------------ attention (decode)
-// One warp per (sequence, head), single query at position pos0. A key row of HD bf16 is read by
-// LPK = HD/8 lanes with one 16-byte load each, so a warp covers KPI = 32/LPK keys per load and
-// issues 8 independent K loads + 8 independent V loads per lane per chunk of CHUNK = 8*KPI keys.
-// Scores are reduced inside each lane group; p*V accumulates per lane over its own keys and the
-// KPI partial sums are combined once at the end. Chunks are aligned to absolute positions, so the
-// arithmetic of a query never depends on the batch it was scheduled in.
+// One CTA per (decode sequence, group of HG heads). In the paged pool a page's K rows for all heads
+// are one contiguous block ([head][PAGE][HD]) and so are its V rows, so the CTA streams each page of
+// its head group with two bulk async copies into a DSTAGES-deep smem ring (a dedicated producer
+// warp; completion on mbarriers) while 8 compute warps run the online softmax from smem. Key rows
+// are read by LPK = HD/8 lanes x 16 B, KPI = 32/LPK keys per instruction. Work is chunked by page
+// (absolute 16-position blocks), so a query's arithmetic never depends on the batch composition.
+constexpr int DSTAGES = 2;
+constexpr int DEC_WARPS = 8;
 template <int HD>
-__global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
-  constexpr int LPK = HD / 8;      // lanes per key row
-  constexpr int KPI = 32 / LPK;    // keys per warp-wide load
-  constexpr int IT = 8;            // loads per lane per chunk
-  constexpr int CHUNK = KPI * IT;  // keys per chunk
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item = blockIdx.x * 4 + warp;
-  if (item >= p.n_groups * p.heads) return;
-  const int gi = item / p.heads, head = item - gi * p.heads;
+struct DecCfg {
+  static constexpr int HG_MAX = HD >= 128 ? 8 : (HD == 64 ? 16 : 32);  // heads per CTA
+  static constexpr int HEADS_PER_WARP = (HG_MAX + DEC_WARPS - 1) / DEC_WARPS;
+  static constexpr size_t SMEM_MAX = 256 + DSTAGES * 2 * HG_MAX * PAGE * HD * 2;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(32 * (DEC_WARPS + 1)) attn_decode_kernel(AttnParams p, int hg, int n_hgroups) {
+  using C = DecCfg<HD>;
+  constexpr int LPK = HD / 8;
+  constexpr int KPI = 32 / LPK;
+  constexpr int ITERS = PAGE / KPI;  // KPI <= 16 = PAGE for HD >= 16
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const uint32_t sbase = (smem_u32(dsm) + 127u) & ~127u;
+  uint8_t* gbase = dsm + (sbase - smem_u32(dsm));
+  const uint32_t HALF = static_cast<uint32_t>(hg) * PAGE * HD * 2;  // K (or V) bytes per page per group
+  const uint32_t STAGE = 2 * HALF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + DSTAGES * STAGE);  // full[DSTAGES], empty[DSTAGES]
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + DSTAGES);
+
+  const int gi = blockIdx.x / n_hgroups;
+  const int hgi = blockIdx.x - gi * n_hgroups;
   const AttnGroup grp = p.groups[gi];
-  const int sub = lane % LPK;   // which 8-dim slice of the key row
-  const int kin = lane / LPK;   // which key of the KPI keys per load
-  float qv[8];
-  {
-    const uint4 u = *reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(grp.m0) * p.ldq + head * HD + sub * 8);
-    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __bfloat1622float2(h2[j]);
-      qv[2 * j] = f.x * p.scale_log2;
-      qv[2 * j + 1] = f.y * p.scale_log2;
-    }
-  }
+  const int h0 = hgi * hg;
+  const int nh = min(hg, p.heads - h0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int last = grp.pos0;
-  const size_t head_off = static_cast<size_t>(head) * PAGE * HD + sub * 8;
-  const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
-  const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
+  const int npages = last / PAGE + 1;
+  const uint32_t half_bytes = static_cast<uint32_t>(nh) * PAGE * HD * 2;
   const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
-  float m = -INFINITY, l = 0.f;
-  float acc[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-  for (int c0 = 0; c0 <= last; c0 += CHUNK) {
-    uint4 kr[IT], vr[IT];
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int key = c0 + it * KPI + kin;
-      kr[it] = make_uint4(0, 0, 0, 0);
-      vr[it] = make_uint4(0, 0, 0, 0);
-      if (key <= last) {
-        const __nv_bfloat16* base = p.kv + static_cast<size_t>(pt[key / PAGE]) * page_stride + head_off +
-                                    (key % PAGE) * HD;
-        kr[it] = *reinterpret_cast<const uint4*>(base);
-        vr[it] = *reinterpret_cast<const uint4*>(base + v_off);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DSTAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, DEC_WARPS);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == DEC_WARPS) {  // producer
+    if (lane == 0) {
+      const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
+      const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
+      for (int pg = 0; pg < npages; ++pg) {
+        const int s = pg % DSTAGES;
+        mbar_wait(empty0 + 8 * s, ((pg / DSTAGES) & 1) ^ 1u);
+        const __nv_bfloat16* src =
+            p.kv + static_cast<size_t>(pt[pg]) * page_stride + static_cast<size_t>(h0) * PAGE * HD;
+        mbar_expect_tx(full0 + 8 * s, 2 * half_bytes);
+        bulk_load(sbase + s * STAGE, src, half_bytes, full0 + 8 * s);
+        bulk_load(sbase + s * STAGE + HALF, src + v_off, half_bytes, full0 + 8 * s);
       }
     }
-    float sc[IT];
-    float cmax = -INFINITY;
+    return;
+  }
+
+  const int sub = lane % LPK, kin = lane / LPK;
+  float qv[C::HEADS_PER_WARP][8];
+  float m[C::HEADS_PER_WARP], l[C::HEADS_PER_WARP], acc[C::HEADS_PER_WARP][8];
 #pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&kr[it]);
-      float dot = 0.f;
+  for (int j = 0; j < C::HEADS_PER_WARP; ++j) {
+    const int h = warp + j * DEC_WARPS;
+    m[j] = -INFINITY;
+    l[j] = 0.f;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h2[j]);
-        dot = fmaf(f.x, qv[2 * j], dot);
-        dot = fmaf(f.y, qv[2 * j + 1], dot);
-      }
+    for (int e = 0; e < 8; ++e) acc[j][e] = 0.f;
+    if (h < nh) {
+      const uint4 u =
+          *reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(grp.m0) * p.ldq + (h0 + h) * HD + sub * 8);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-      for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      const int key = c0 + it * KPI + kin;
-      const bool ok = key <= last && (!p.key_mask || p.key_mask[key]);
-      sc[it] = ok ? dot : -INFINITY;
-      cmax = fmaxf(cmax, sc[it]);
-    }
-#pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-    const float mnew = fmaxf(m, cmax);
-    const float alpha = mnew == -INFINITY ? 1.f : exp2f(m - mnew);
-    float psum = 0.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] *= alpha;
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const float pj = mnew == -INFINITY ? 0.f : exp2f(sc[it] - mnew);
-      psum += pj;
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&vr[it]);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h2[j]);
-        acc[2 * j] = fmaf(pj, f.x, acc[2 * j]);
-        acc[2 * j + 1] = fmaf(pj, f.y, acc[2 * j + 1]);
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h2[e]);
+        qv[j][2 * e] = f.x * p.scale_log2;
+        qv[j][2 * e + 1] = f.y * p.scale_log2;
       }
     }
+  }
+  for (int pg = 0; pg < npages; ++pg) {
+    const int s = pg % DSTAGES;
+    mbar_wait(full0 + 8 * s, (pg / DSTAGES) & 1);
+    const __nv_bfloat16* sK = reinterpret_cast<const __nv_bfloat16*>(gbase + s * STAGE);
+    const __nv_bfloat16* sV = reinterpret_cast<const __nv_bfloat16*>(gbase + s * STAGE + HALF);
 #pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
-    l = l * alpha + psum;
-    m = mnew;
+    for (int j = 0; j < C::HEADS_PER_WARP; ++j) {
+      const int h = warp + j * DEC_WARPS;
+      if (h >= nh) break;  // warp-uniform
+      float sc[ITERS];
+      float cmax = -INFINITY;
+#pragma unroll
+      for (int it = 0; it < ITERS; ++it) {
+        const int kr = it * KPI + kin;  // key row within the page
+        const uint4 u = *reinterpret_cast<const uint4*>(sK + (static_cast<size_t>(h) * PAGE + kr) * HD + sub * 8);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        float dot = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          dot = fmaf(f.x, qv[j][2 * e], dot);
+          dot = fmaf(f.y, qv[j][2 * e + 1], dot);
+        }
+#pragma unroll
+        for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        const int key = pg * PAGE + kr;
+        const bool ok = key <= last && (!p.key_mask || p.key_mask[key]);
+        sc[it] = ok ? dot : -INFINITY;
+        cmax = fmaxf(cmax, sc[it]);
+      }
+#pragma unroll
+      for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+      const float mnew = fmaxf(m[j], cmax);
+      const float alpha = mnew == -INFINITY ? 1.f : exp2f(m[j] - mnew);
+      float psum = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[j][e] *= alpha;
+#pragma unroll
+      for (int it = 0; it < ITERS; ++it) {
+        const float pj = mnew == -INFINITY ? 0.f : exp2f(sc[it] - mnew);
+        psum += pj;
+        const int kr = it * KPI + kin;
+        const uint4 u = *reinterpret_cast<const uint4*>(sV + (static_cast<size_t>(h) * PAGE + kr) * HD + sub * 8);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          acc[j][2 * e] = fmaf(pj, f.x, acc[j][2 * e]);
+          acc[j][2 * e + 1] = fmaf(pj, f.y, acc[j][2 * e + 1]);
+        }
+      }
+#pragma unroll
+      for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
+      l[j] = l[j] * alpha + psum;
+      m[j] = mnew;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * s);
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < C::HEADS_PER_WARP; ++j) {
+    const int h = warp + j * DEC_WARPS;
+    if (h >= nh) break;
 #pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-  if (kin == 0) {
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    uint4 w;
-    w.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
-    w.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
-    w.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
-    w.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
-    *reinterpret_cast<uint4*>(p.z + static_cast<size_t>(grp.m0) * p.ldz + head * HD + sub * 8) = w;
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int o = LPK; o < 32; o <<= 1) acc[j][e] += __shfl_xor_sync(0xffffffffu, acc[j][e], o);
+    if (kin == 0) {
+      const float inv = l[j] > 0.f ? 1.f / l[j] : 0.f;
+      uint4 w;
+      w.x = pack_bf16x2(acc[j][0] * inv, acc[j][1] * inv);
+      w.y = pack_bf16x2(acc[j][2] * inv, acc[j][3] * inv);
+      w.z = pack_bf16x2(acc[j][4] * inv, acc[j][5] * inv);
+      w.w = pack_bf16x2(acc[j][6] * inv, acc[j][7] * inv);
+      *reinterpret_cast<uint4*>(p.z + static_cast<size_t>(grp.m0) * p.ldz + (h0 + h) * HD + sub * 8) = w;
+    }
   }
 }
 
@@ -622,9 +678,21 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
     }                                                                                               \
     if (prefill.n_groups > 0)                                                                       \
       attn_prefill_kernel<HD><<<dim3(prefill.n_groups, prefill.heads), 128, smem, st>>>(prefill);   \
-    if (decode.n_groups > 0)                                                                        \
-      attn_decode_kernel<HD><<<blocks_for(static_cast<int64_t>(decode.n_groups) * decode.heads, 4), \
-                               128, 0, st>>>(decode);                                               \
+    if (decode.n_groups > 0) {                                                                      \
+      using DC = DecCfg<HD>;                                                                        \
+      static bool dcfg = false;                                                                     \
+      if (!dcfg) {                                                                                  \
+        CUDA_OK(cudaFuncSetAttribute(attn_decode_kernel<HD>,                                        \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,                   \
+                                     static_cast<int>(DC::SMEM_MAX)));                              \
+        dcfg = true;                                                                                \
+      }                                                                                             \
+      const int ngrp = (decode.heads + DC::HG_MAX - 1) / DC::HG_MAX;                                \
+      const int hg = (decode.heads + ngrp - 1) / ngrp;                                              \
+      const size_t sm = 256 + static_cast<size_t>(DSTAGES) * 2 * hg * PAGE * HD * 2;                 \
+      attn_decode_kernel<HD><<<decode.n_groups * ngrp, 32 * (DEC_WARPS + 1), sm, st>>>(             \
+          decode, hg, ngrp);                                                                        \
+    }                                                                                               \
   } while (0)
   switch (hd) {
     case 16: ATT(16); break;

@@ -73,6 +73,14 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   return p;
 }
 
+// Non-tensor bulk copy global -> this CTA's smem, completion counted on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- clusters (CTA pairs)
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -230,10 +238,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Reference: 0.5*x*(1+tanh(0.7978845608028654*(x+0.044715*x^3))) (numerics.cpp:179-184). The SFU
+// tanh (max rel. error ~2^-11) is below the bf16 rounding (2^-9) the result is stored with.
 __device__ __forceinline__ float gelu_tanh(float x) {
-  // Reference: 0.5*x*(1+tanh(0.7978845608028654*(x+0.044715*x^3))) (numerics.cpp:179-184).
   const float inner = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-  return 0.5f * x * (1.0f + tanhf(inner));
+  return 0.5f * x * (1.0f + tanh_fast(inner));
 }
 
 }  // namespace iolmk
