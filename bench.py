@@ -117,6 +117,7 @@ def dist_setup():
             import torch
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
+        _cpu_group()  # collective: created by every rank up front
     return world, rank, local
 
 
@@ -149,6 +150,39 @@ def allreduce_sum(world, value: float, device=None) -> float:
 def step_rows(step: int, world: int, rank: int, B: int) -> int:
     """First global table row of (step, rank): weak scaling, no row reused."""
     return (step * world + rank) * B
+
+
+def gather_token_column(world: int, rank: int, out_ids: np.ndarray, out_len: np.ndarray):
+    """The only cross-GPU exchange of the job: every rank's generated-token column
+    (int32[rows x max_new] + int32 len[rows], host memory) is gathered to rank 0 over the CPU
+    (gloo) group. Returns the concatenation in rank order on rank 0, None elsewhere."""
+    if world == 1:
+        return out_ids, out_len
+    import torch
+    import torch.distributed as dist
+    ids_t = torch.from_numpy(np.ascontiguousarray(out_ids, dtype=np.int32))
+    len_t = torch.from_numpy(np.ascontiguousarray(out_len, dtype=np.int32))
+    grp = _cpu_group()
+    if rank == 0:
+        ids_l = [torch.empty_like(ids_t) for _ in range(world)]
+        len_l = [torch.empty_like(len_t) for _ in range(world)]
+        dist.gather(ids_t, ids_l, dst=0, group=grp)
+        dist.gather(len_t, len_l, dst=0, group=grp)
+        return torch.cat(ids_l).numpy(), torch.cat(len_l).numpy()
+    dist.gather(ids_t, None, dst=0, group=grp)
+    dist.gather(len_t, None, dst=0, group=grp)
+    return None
+
+
+_CPU_GROUP = None
+
+
+def _cpu_group():
+    global _CPU_GROUP
+    import torch.distributed as dist
+    if _CPU_GROUP is None:
+        _CPU_GROUP = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else dist.group.WORLD
+    return _CPU_GROUP
 
 
 # --------------------------------------------------------------------------- CPU reference
@@ -273,8 +307,12 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    gathered_rows = 0
     for k in range(W, W + K):
         o2, ln2, _ = run(k, False)
+        g = gather_token_column(world, rank, o2, ln2)  # output column -> rank 0 (timed, part of e2e)
+        if g is not None:
+            gathered_rows += len(g[1])
     e1.record()
     torch.cuda.synchronize()
     barrier(world)
@@ -350,6 +388,7 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
         "clocks": clk,
         "cpu_baseline": cpu,
         "mean_new_tokens_per_row": emitted / (B * K),
+        "rows_gathered_on_rank0": gathered_rows,
         "engine_device_ms": eng_ms,
         "setup_s": setup_s,
     }

@@ -1,0 +1,180 @@
+// iolm_cuda_runtime.hpp - header-only C++ shim: the public surface of iolm::ModelRuntime
+// (/root/reference/proj/include/iolm/runtime.hpp:37-60) on top of the C ABI in iolm_cuda.h.
+//
+//   iolm::cuda::ModelRuntime rt(serialized_bundle_bytes);        // ModelRuntime(bundle)
+//   rt.config(); rt.bundle_hash();                                // runtime.hpp:41-42
+//   rt.forward(ids, mask, counter);                               // runtime.hpp:48-49
+//   rt.greedy_decode(prompt, n, counter);                         // runtime.hpp:54-55
+//   rt.batch_decode(prompts, n, counter);                         // runtime.hpp:59-60
+//
+// Tokenization (BOS + one id per ASCII byte), the per-prompt length check, rendering of emitted ids
+// and the error classes follow the reference (runtime.cpp:241-309, tokenizer.cpp:10-36,
+// common.hpp:16-89). Define IOLM_CUDA_WITH_REFERENCE_TYPES before including this header (with the
+// reference's include/ on the path) to get a constructor from iolm::ModelBundle, results as
+// iolm::Matrix and errors thrown as the reference's own exception classes - see INTEGRATION.md.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "iolm_cuda.h"
+
+#ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
+#include "iolm/common.hpp"
+#include "iolm/matrix.hpp"
+#include "iolm/model.hpp"
+#endif
+
+namespace iolm::cuda {
+
+#ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
+using Error = iolm::Error;
+using ContractViolation = iolm::ContractViolation;
+using SequenceTooLong = iolm::SequenceTooLong;
+using CorruptHeader = iolm::CorruptHeader;
+using TruncatedBlob = iolm::TruncatedBlob;
+using UnknownEncoding = iolm::UnknownEncoding;
+using FlopCounter = iolm::FlopCounter;
+#else
+struct Error : std::runtime_error {
+  explicit Error(const std::string& w) : std::runtime_error(w) {}
+};
+struct ContractViolation : Error {
+  using Error::Error;
+};
+struct SequenceTooLong : Error {
+  using Error::Error;
+};
+struct CorruptHeader : Error {
+  using Error::Error;
+};
+struct TruncatedBlob : Error {
+  using Error::Error;
+};
+struct UnknownEncoding : Error {
+  using Error::Error;
+};
+class FlopCounter {
+ public:
+  void add(uint64_t m) { t_ += m; }
+  uint64_t total() const { return t_; }
+  void reset() { t_ = 0; }
+
+ private:
+  uint64_t t_ = 0;
+};
+#endif
+// GPU-side failures have no reference counterpart (the reference is CPU-only).
+struct GpuError : Error {
+  explicit GpuError(const std::string& w) : Error(w) {}
+};
+
+inline void check(int st) {
+  if (st == IOLM_OK) return;
+  const std::string msg = iolm_cuda_last_error();
+  switch (st) {
+    case IOLM_E_CONTRACT: throw ContractViolation(msg);
+    case IOLM_E_SEQ_TOO_LONG: throw SequenceTooLong(msg);
+    case IOLM_E_CORRUPT_HEADER: throw CorruptHeader(msg);
+    case IOLM_E_TRUNCATED_BLOB: throw TruncatedBlob(msg);
+    case IOLM_E_UNKNOWN_ENCODING: throw UnknownEncoding(msg);
+    default: throw GpuError(msg);
+  }
+}
+
+struct Config {
+  int vocab_size, d_model, n_layers, n_heads, d_ff, max_seq_len, head_dim;
+};
+
+class ModelRuntime {
+ public:
+  explicit ModelRuntime(std::span<const uint8_t> bundle_bytes, int device = 0, const iolm_cuda_opts* opts = nullptr) {
+    check(iolm_cuda_create(bundle_bytes.data(), bundle_bytes.size(), device, opts, &ctx_));
+    iolm_cuda_model_config c{};
+    check(iolm_cuda_config(ctx_, &c));
+    cfg_ = {c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.d_ff, c.max_seq_len, c.head_dim};
+  }
+#ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
+  // Drop-in for ModelRuntime(const ModelBundle&): the bundle is handed over in its canonical
+  // serialized form (model.cpp:311-346), so bundle_hash() is the reference's exactly.
+  explicit ModelRuntime(const iolm::ModelBundle& bundle, int device = 0)
+      : ModelRuntime(std::span<const uint8_t>(iolm::serialize_bundle(bundle)), device) {}
+#endif
+  ModelRuntime(const ModelRuntime&) = delete;
+  ModelRuntime& operator=(const ModelRuntime&) = delete;
+  ~ModelRuntime() { iolm_cuda_destroy(ctx_); }
+
+  const Config& config() const { return cfg_; }
+  uint64_t bundle_hash() const {
+    uint64_t h = 0;
+    check(iolm_cuda_bundle_hash(ctx_, &h));
+    return h;
+  }
+
+  // Logits for every position, row-major [ids.size() x 131].
+  std::vector<float> forward(std::span<const int> ids, std::span<const uint8_t> mask, FlopCounter& counter) const {
+    if (ids.empty()) throw ContractViolation("forward: empty sequence");
+    if (!mask.empty() && mask.size() != ids.size()) throw ContractViolation("forward: mask length mismatch");
+    std::vector<int32_t> v(ids.begin(), ids.end());
+    std::vector<float> out(ids.size() * static_cast<size_t>(cfg_.vocab_size));
+    uint64_t madds = 0;
+    check(iolm_cuda_forward_logits(ctx_, v.data(), mask.empty() ? nullptr : mask.data(),
+                                   static_cast<int32_t>(v.size()), out.data(), &madds));
+    counter.add(madds);
+    return out;
+  }
+
+  std::string greedy_decode(std::string_view prompt, int max_new_tokens, FlopCounter& counter) const {
+    const std::string p(prompt);
+    return batch_decode(std::span<const std::string>(&p, 1), max_new_tokens, counter)[0];
+  }
+
+  std::vector<std::string> batch_decode(std::span<const std::string> prompts, int max_new_tokens,
+                                        FlopCounter& counter) const {
+    if (prompts.empty()) throw ContractViolation("batch_decode: batch size must be >= 1");
+    if (max_new_tokens < 0) throw ContractViolation("batch_decode: max_new_tokens must be >= 0");
+    std::vector<std::string> out(prompts.size());
+    if (max_new_tokens == 0) return out;
+    std::vector<int32_t> ids;
+    std::vector<int64_t> offsets{0};
+    for (size_t i = 0; i < prompts.size(); ++i) {  // encode + length check in prompt order
+      ids.push_back(IOLM_BOS);
+      for (size_t j = 0; j < prompts[i].size(); ++j) {
+        const auto b = static_cast<unsigned char>(prompts[i][j]);
+        if (b > 127)
+          throw ContractViolation("Tokenizer: non-ASCII byte " + std::to_string(b) + " at offset " + std::to_string(j));
+        ids.push_back(b);
+      }
+      const int64_t len = static_cast<int64_t>(ids.size()) - offsets.back();
+      if (len > cfg_.max_seq_len)
+        throw SequenceTooLong("batch_decode: prompt " + std::to_string(i) + " needs " + std::to_string(len) +
+                              " tokens, max_seq_len is " + std::to_string(cfg_.max_seq_len));
+      offsets.push_back(static_cast<int64_t>(ids.size()));
+    }
+    const size_t n = prompts.size();
+    std::vector<int32_t> gen(n * static_cast<size_t>(max_new_tokens)), len(n);
+    uint64_t madds = 0;
+    int64_t bad = -1;
+    check(iolm_cuda_decode(ctx_, ids.data(), offsets.data(), static_cast<int64_t>(n), max_new_tokens, gen.data(),
+                           len.data(), &madds, &bad));
+    counter.add(madds);
+    for (size_t i = 0; i < n; ++i)
+      for (int t = 0; t < len[i]; ++t) {
+        const int32_t id = gen[i * max_new_tokens + t];
+        if (id >= 0 && id <= 127) out[i].push_back(static_cast<char>(id));  // PAD/BOS render nothing
+      }
+    return out;
+  }
+
+  iolm_cuda_ctx* handle() const { return ctx_; }
+
+ private:
+  iolm_cuda_ctx* ctx_ = nullptr;
+  Config cfg_{};
+};
+
+}  // namespace iolm::cuda

@@ -1,0 +1,86 @@
+// Drop-in check at the C++ level (GPU box): the reference's own ModelBundle (ToyModelParams::init)
+// goes into iolm::cuda::ModelRuntime (include/iolm_cuda_runtime.hpp) in place of
+// iolm::ModelRuntime; both run side by side in one process and must agree on bundle_hash, FlopCounter
+// madds, error classes, greedy outputs (ties excepted) and logits (rel-L2 <= 1e-2).
+// Built by oracle/Makefile (target dropin) against oracle/_ref/libiolm_ref.so - test only.
+#define IOLM_CUDA_WITH_REFERENCE_TYPES
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "iolm/runtime.hpp"
+#include "iolm/tokenizer.hpp"
+#include "iolm/train.hpp"
+#include "iolm_cuda_runtime.hpp"
+
+static int fails = 0;
+#define EXPECT(c, msg)                           \
+  do {                                           \
+    if (!(c)) {                                  \
+      std::printf("FAIL %s (line %d)\n", msg, __LINE__); \
+      ++fails;                                   \
+    }                                            \
+  } while (0)
+
+int main() {
+  iolm::Rng rng(42);
+  const auto bundle = iolm::ToyModelParams::init(iolm::ModelConfig::reference(), rng).to_bundle();
+  iolm::ModelRuntime cpu(bundle);
+  iolm::cuda::ModelRuntime gpu(bundle);
+  EXPECT(cpu.bundle_hash() == gpu.bundle_hash(), "bundle_hash");
+
+  std::vector<std::string> prompts;
+  iolm::Rng prng(7);
+  for (int i = 0; i < 24; ++i) {
+    std::string p = "summarize in five words, plain:";
+    for (int j = 0; j < 64; ++j) p.push_back(static_cast<char>(32 + prng.next_below(95)));
+    prompts.push_back(p);
+  }
+  prompts.push_back("");
+  iolm::FlopCounter c1, c2;
+  const auto a = cpu.batch_decode(prompts, 8, c1);
+  const auto b = gpu.batch_decode(prompts, 8, c2);
+  int same = 0;
+  for (size_t i = 0; i < a.size(); ++i) same += a[i] == b[i];
+  EXPECT(same >= static_cast<int>(a.size()) - 1, "batch_decode agreement");
+  EXPECT(c1.total() == c2.total(), "FlopCounter madds");
+  std::printf("batch_decode: %d/%zu identical, madds %llu vs %llu\n", same, a.size(),
+              static_cast<unsigned long long>(c1.total()), static_cast<unsigned long long>(c2.total()));
+
+  std::vector<int> ids = {iolm::Tokenizer::kBos};
+  for (char ch : prompts[0]) ids.push_back(ch);
+  iolm::FlopCounter f1, f2;
+  const auto la = cpu.forward(ids, {}, f1);
+  const auto lb = gpu.forward(ids, {}, f2);
+  double worst = 0;
+  for (size_t t = 0; t < ids.size(); ++t) {
+    double num = 0, den = 0;
+    for (int v = 0; v < 131; ++v) {
+      const double x = la.at(static_cast<int>(t), v), y = lb[t * 131 + v];
+      num += (x - y) * (x - y);
+      den += x * x;
+    }
+    worst = std::max(worst, std::sqrt(num / den));
+  }
+  EXPECT(worst <= 1e-2, "forward logits rel-L2");
+  EXPECT(f1.total() == f2.total(), "forward madds");
+  std::printf("forward: worst rel-L2 %.3e\n", worst);
+
+  bool threw = false;
+  try {
+    gpu.batch_decode(std::vector<std::string>{"ok", std::string(200, 'x')}, 4, c2);
+  } catch (const iolm::SequenceTooLong&) {
+    threw = true;
+  }
+  EXPECT(threw, "SequenceTooLong");
+  threw = false;
+  try {
+    gpu.batch_decode(std::vector<std::string>{}, 4, c2);
+  } catch (const iolm::ContractViolation&) {
+    threw = true;
+  }
+  EXPECT(threw, "ContractViolation");
+  std::printf(fails ? "DROPIN FAIL\n" : "DROPIN OK\n");
+  return fails ? 1 : 0;
+}

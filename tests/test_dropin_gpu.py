@@ -1,0 +1,20 @@
+"""The reference's own C++ ModelBundle through the C++ shim (include/iolm_cuda_runtime.hpp), side by
+side with iolm::ModelRuntime in one process (tests/cpp/dropin_test.cpp, built by oracle/Makefile)."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+BIN = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "dropin_test"
+
+
+@pytest.mark.skipif(not BIN.exists(), reason="drop-in binary not built (needs /root/reference at build time)")
+def test_cpp_dropin_against_reference_runtime():
+    res = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0 and "DROPIN OK" in res.stdout, res.stdout + res.stderr
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()
