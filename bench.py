@@ -39,6 +39,19 @@ CONFIGS = {
     "c1": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="dense",
                desc="C1: 0.5B-class decoder (1280,24,20,5120,128) bf16 dense, 32-token prefix + 64-token row, "
                     "8 new tokens"),
+    "c2-w8a8": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="q8", act_quant=True,
+                    desc="C2: C1 model, q8_perchannel RTN weights + per-token int8 activations (W8A8, "
+                         "tcgen05 kind::i8), 32+64 tokens, 8 new tokens"),
+    "c2-w4a16": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="q4",
+                     desc="C2: C1 model, q4_perchannel RTN weights, bf16 activations (W4A16), 32+64, 8 new"),
+    "c3": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="sparse24", act_quant=True,
+               heads=[10] * 24, ffn=[2560] * 24,
+               desc="C3: C1 model pruned 50% (10 of 20 heads, FFN 2560) + 2:4 magnitude + q8 (sparse24_q8), "
+                    "W8A8, 32+64, 8 new"),
+    "c4": dict(dims=(2048, 28, 16, 8192, 576), row_chars=512, quant="sparse24", act_quant=True,
+               heads=[8] * 28, ffn=[4096] * 28,
+               desc="C4: 1.5B-class (2048,28,16,8192,576) pruned 50% + 2:4 + q8, W8A8, 32-token prefix + "
+                    "512-token row, 8 new"),
 }
 MAX_NEW = 8
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -216,11 +229,12 @@ def run_reference_arm(args, cfg: dict, world: int, rank: int) -> None:
         return
     from oracle import oracle as O
     cores = os.cpu_count() or 1
-    if O.ref_available():
+    if O.ref_available() and cfg["quant"] == "dense" and "heads" not in cfg:
         bundle = O.ref_toy_bundle(*cfg["dims"], seed=42)
     else:
         from paper_2507_04967_b200 import synth
-        bundle = synth.toy_bundle(*cfg["dims"], seed=42, quant=cfg["quant"])
+        bundle = synth.toy_bundle(*cfg["dims"], seed=42, quant=cfg["quant"], heads=cfg.get("heads"),
+                                  ffn=cfg.get("ffn"))
     n = cpu_sample_rows(args.config, cores)
     for w in range(args.warmup):  # untimed; one row each keeps the run bounded
         cpu_reference_sample(bundle, cfg, 1, 10_000_000 + w, 1)
@@ -253,8 +267,10 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     dev = torch.device("cuda", local)
     B, K, W = args.rows_per_step, args.steps, args.warmup
     t_setup = time.perf_counter()
-    bundle = synth.toy_bundle(*cfg["dims"], seed=42, quant=cfg["quant"])
-    rt = R.ModelRuntime(bundle, device=local, kernel_timing=True, max_tokens_per_step=args.tokens_per_step)
+    bundle = synth.toy_bundle(*cfg["dims"], seed=42, quant=cfg["quant"], heads=cfg.get("heads"),
+                              ffn=cfg.get("ffn"))
+    rt = R.ModelRuntime(bundle, device=local, kernel_timing=True, max_tokens_per_step=args.tokens_per_step,
+                        act_quant=cfg.get("act_quant", False))
     # this rank's rows for every warmup + timed step, host (pinned) and device copies
     host_ids, dev_ids, offsets = [], [], []
     for k in range(W + K):
@@ -373,7 +389,7 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     line = {
         "metric": "rows/sec", "value": value, "unit": "rows/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (seeded rows, random-init weights: ToyModelParams::init seed 42)",
+        "dtype": "s8 x s8 -> s32 (W8A8)" if cfg.get("act_quant") else "bf16", "data": "synthetic (seeded rows, random-init weights: ToyModelParams::init seed 42)",
         "config": {"workload": cfg["desc"], "rows_per_step_per_gpu": B, "max_new_tokens": MAX_NEW,
                    "tokens_per_engine_step": args.tokens_per_step or 16384,
                    "l2": "inputs larger than L2 (GB-scale activations per step)",

@@ -142,6 +142,15 @@ int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, float* C, in
 int iolm_cuda_debug_gemm_s8(const int8_t* A, const int8_t* W, int32_t* C, int32_t M, int32_t N,
                             int32_t K, int32_t pair);
 
+/* Device-only GEMM timing (kernel tuning): mean ms per launch of `iters` launches on synthetic
+ * operands. epi: 0 f32, 1 bf16, 2 gelu, 3 residual-add, 5 s32 (i8 only). */
+int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_t epi, int32_t pair, int32_t i8,
+                              int32_t iters, float* ms_out);
+
+/* Per-token int8 activation quantization (the W8A8 rule) of bf16 rows [n x d] on the
+ * device: codes [n x d] and one f32 scale per row. */
+int iolm_cuda_debug_quant_rows_bf16(const uint16_t* x, int32_t n, int32_t d, int8_t* codes, float* scales);
+
 #ifdef __cplusplus
 }
 #endif

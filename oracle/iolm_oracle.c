@@ -191,7 +191,37 @@ typedef struct {
   const float* const* wo;    /* [kh x d] */
   const float* const* w_in;  /* [d x f] */
   const float* const* w_out; /* [f x d] */
+  /* W8A8 restatement (act_quant != 0): per linear (index layer*6 + {q,k,v,o,in,out}) the int8 weight
+   * codes transposed to [K x N] and the per-output-channel scales [N]. */
+  int act_quant;
+  const int8_t* const* wcodes_t;
+  const float* const* wscale;
 } orc_model;
+
+void orc_quant_rows_s8(const float* x, int n, int d, int8_t* codes, float* scales);
+
+/* y[n x N] = W8A8(x[n x K], linear `which`): per-token int8 x codes, exact int32 dot with the int8
+ * weight codes, then (float)acc * s_x * s_w - the GPU kind::i8 GEMM epilogue's arithmetic. */
+static void linear_w8a8(const orc_model* m, int li, const float* x, int n, int K, int N, float* y) {
+  int8_t* xc = (int8_t*)malloc((size_t)n * K);
+  float* xs = (float*)malloc(sizeof(float) * n);
+  int32_t* acc = (int32_t*)malloc(sizeof(int32_t) * N);
+  orc_quant_rows_s8(x, n, K, xc, xs);
+  const int8_t* w = m->wcodes_t[li];
+  const float* ws = m->wscale[li];
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < N; ++j) acc[j] = 0;
+    for (int k = 0; k < K; ++k) {
+      const int32_t a = xc[(size_t)i * K + k];
+      const int8_t* wr = w + (size_t)k * N;
+      for (int j = 0; j < N; ++j) acc[j] += a * (int32_t)wr[j];
+    }
+    for (int j = 0; j < N; ++j) y[(size_t)i * N + j] = (float)acc[j] * xs[i] * ws[j];
+  }
+  free(xc);
+  free(xs);
+  free(acc);
+}
 
 typedef struct {
   float** k; /* per layer [S x kh] */
@@ -244,9 +274,15 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
     float* ao = (float*)malloc(sizeof(float) * n * d);
     float* g = (float*)malloc(sizeof(float) * n * f);
     for (int i = 0; i < n; ++i) layernorm_row(x + (size_t)i * d, d, m->ln1_g[l], m->ln1_b[l], h + (size_t)i * d);
-    matmul_wt(h, n, d, m->wq[l], kh, q);
-    matmul_wt(h, n, d, m->wk[l], kh, kn);
-    matmul_wt(h, n, d, m->wv[l], kh, vn);
+    if (m->act_quant) {
+      linear_w8a8(m, l * 6 + 0, h, n, d, kh, q);
+      linear_w8a8(m, l * 6 + 1, h, n, d, kh, kn);
+      linear_w8a8(m, l * 6 + 2, h, n, d, kh, vn);
+    } else {
+      matmul_wt(h, n, d, m->wq[l], kh, q);
+      matmul_wt(h, n, d, m->wk[l], kh, kn);
+      matmul_wt(h, n, d, m->wv[l], kh, vn);
+    }
     *madds += 3ull * n * d * kh;
     for (int i = 0; i < n; ++i) {
       memcpy(st->k[l] + (size_t)(p0 + i) * kh, kn + (size_t)i * kh, sizeof(float) * kh);
@@ -291,14 +327,17 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
         *madds += (uint64_t)span * hd;
       }
     }
-    matmul_wt(z, n, kh, m->wo[l], d, ao);
+    if (m->act_quant) linear_w8a8(m, l * 6 + 3, z, n, kh, d, ao);
+    else matmul_wt(z, n, kh, m->wo[l], d, ao);
     *madds += (uint64_t)n * kh * d;
     for (size_t t = 0; t < (size_t)n * d; ++t) x[t] += ao[t];
     for (int i = 0; i < n; ++i) layernorm_row(x + (size_t)i * d, d, m->ln2_g[l], m->ln2_b[l], h + (size_t)i * d);
-    matmul_wt(h, n, d, m->w_in[l], f, g);
+    if (m->act_quant) linear_w8a8(m, l * 6 + 4, h, n, d, f, g);
+    else matmul_wt(h, n, d, m->w_in[l], f, g);
     *madds += (uint64_t)n * d * f;
     for (size_t t = 0; t < (size_t)n * f; ++t) g[t] = gelu(g[t]);
-    matmul_wt(g, n, f, m->w_out[l], d, ao);
+    if (m->act_quant) linear_w8a8(m, l * 6 + 5, g, n, f, d, ao);
+    else matmul_wt(g, n, f, m->w_out[l], d, ao);
     *madds += (uint64_t)n * f * d;
     for (size_t t = 0; t < (size_t)n * d; ++t) x[t] += ao[t];
     free(q);
@@ -434,8 +473,10 @@ int orc_decode_rows(const orc_model* m, const int* ids, const int64_t* offsets, 
 
 /* ------------------------------------------------------------------ W8A8 restatement */
 /* Per-token symmetric int8 quantization of activation rows, the reference's RTN rule applied to
- * rows instead of weight channels: scale = amax/127 (amax == 0 -> 1), code =
- * clamp(nearbyint(x / scale), -127, 127) evaluated in double (quant.cpp:23-38). */
+ * rows instead of weight channels (quant.cpp:23-38): scale = amax/127 (amax == 0 -> 1), code =
+ * clamp(nearbyint(x / scale), -127, 127) with x / scale an IEEE fp32 division (the weight rule
+ * divides in double; activations are quantized on the GPU every step, so the rule pinned here uses
+ * the correctly rounded fp32 quotient - exact half-integers still round to even). */
 void orc_quant_rows_s8(const float* x, int n, int d, int8_t* codes, float* scales) {
   for (int i = 0; i < n; ++i) {
     const float* r = x + (size_t)i * d;
@@ -444,9 +485,9 @@ void orc_quant_rows_s8(const float* x, int n, int d, int8_t* codes, float* scale
     const float s = amax == 0.0f ? 1.0f : amax / 127.0f;
     scales[i] = s;
     for (int k = 0; k < d; ++k) {
-      double q = nearbyint((double)r[k] / (double)s);
-      if (q > 127.0) q = 127.0;
-      if (q < -127.0) q = -127.0;
+      float q = nearbyintf(r[k] / s);
+      if (q > 127.0f) q = 127.0f;
+      if (q < -127.0f) q = -127.0f;
       codes[(size_t)i * d + k] = (int8_t)q;
     }
   }

@@ -41,14 +41,16 @@ def build(ref: bool = True) -> None:
 ENC_DENSE, ENC_Q8, ENC_Q4, ENC_SPARSE24 = 0, 1, 2, 3
 
 
-def parse_bundle(data: bytes) -> dict:
-    """deserialize_bundle (model.cpp:348-406) + decode_tensor (model.cpp:140-204) in numpy."""
+def parse_bundle(data: bytes, with_codes: bool = False) -> dict:
+    """deserialize_bundle (model.cpp:348-406) + decode_tensor (model.cpp:140-204) in numpy.
+    with_codes: also return the integer codes and scales of quantized tensors (W8A8 restatement)."""
     if len(data) < 10 or data[:4] != b"IOLM":
         raise ValueError("bundle: bad magic")
     hl = int.from_bytes(data[6:10], "little")
     header = json.loads(data[10:10 + hl].decode())
     blob = memoryview(data)[10 + hl:]
     tensors = {}
+    codes_all = {}
     for t in header["tensors"]:
         r, c, enc, off, ln = t["rows"], t["cols"], t["encoding"], t["offset"], t["length"]
         p = np.frombuffer(blob[off:off + ln], dtype=np.uint8)
@@ -58,6 +60,8 @@ def parse_bundle(data: bytes) -> dict:
             codes = p[: r * c].view(np.int8).reshape(r, c)
             scales = p[r * c: r * c + 4 * r].view(np.float32)
             v = codes.astype(np.float32) * scales[:, None]
+            if with_codes:
+                codes_all[t["name"]] = (codes.astype(np.int8), scales.copy())
         elif enc == ENC_Q4:
             rb = (c + 1) // 2
             packed = p[: r * rb].reshape(r, rb)
@@ -81,10 +85,15 @@ def parse_bundle(data: bytes) -> dict:
             v[ri, gi, nibs & 3] = codes[:, :, 0].astype(np.float32) * scales[:, None]
             v[ri, gi, (nibs >> 2) & 3] = codes[:, :, 1].astype(np.float32) * scales[:, None]
             v = v.reshape(r, c)
+            if with_codes:
+                cd = np.zeros((r, g, 4), np.int8)
+                cd[ri, gi, nibs & 3] = codes[:, :, 0]
+                cd[ri, gi, (nibs >> 2) & 3] = codes[:, :, 1]
+                codes_all[t["name"]] = (cd.reshape(r, c), scales.copy())
         else:
             raise ValueError(f"unknown encoding {enc}")
         tensors[t["name"]] = np.ascontiguousarray(v, dtype=np.float32)
-    return {"config": header["config"], "tensors": tensors, "header": header}
+    return {"config": header["config"], "tensors": tensors, "header": header, "codes": codes_all}
 
 
 # ----------------------------------------------------------------------------- C restatement
@@ -98,6 +107,7 @@ class _OrcModel(C.Structure):
         ("tok_t", C.c_void_p),
         ("wq", C.POINTER(C.c_void_p)), ("wk", C.POINTER(C.c_void_p)), ("wv", C.POINTER(C.c_void_p)),
         ("wo", C.POINTER(C.c_void_p)), ("w_in", C.POINTER(C.c_void_p)), ("w_out", C.POINTER(C.c_void_p)),
+        ("act_quant", C.c_int), ("wcodes_t", C.POINTER(C.c_void_p)), ("wscale", C.POINTER(C.c_void_p)),
     ]
 
 
@@ -127,8 +137,10 @@ def load_oracle() -> C.CDLL:
 class OracleModel:
     """The C restatement over a decoded bundle."""
 
-    def __init__(self, bundle: bytes | dict):
-        b = parse_bundle(bundle) if isinstance(bundle, (bytes, bytearray)) else bundle
+    def __init__(self, bundle: bytes | dict, act_quant: bool = False):
+        """act_quant: the W8A8 restatement (per-token int8 activations, int8 weight codes, exact
+        int32 accumulation) - requires q8 / sparse24_q8 encodings for every linear weight."""
+        b = parse_bundle(bundle, with_codes=act_quant) if isinstance(bundle, (bytes, bytearray)) else bundle
         cfg, T = b["config"], b["tensors"]
         self.cfg = cfg
         L = cfg["n_layers"]
@@ -156,6 +168,21 @@ class OracleModel:
                                          else T[f"layers.{l}.{name}"]) for l in range(L)])
             self._keep.append(arr)
             setattr(m, fld, arr)
+        m.act_quant = 1 if act_quant else 0
+        if act_quant:
+            names = ["attn.wq", "attn.wk", "attn.wv", "attn.wo", "ffn.w_in", "ffn.w_out"]
+            cw, cs = [], []
+            for l in range(L):
+                for nm in names:
+                    key = f"layers.{l}.{nm}"
+                    if key not in b["codes"]:
+                        raise ValueError(f"W8A8 needs q8/sparse24 codes for {key}")
+                    codes, scales = b["codes"][key]
+                    cw.append(ptr(np.ascontiguousarray(codes.T)))
+                    cs.append(ptr(np.ascontiguousarray(scales, dtype=np.float32)))
+            m.wcodes_t = (C.c_void_p * len(cw))(*cw)
+            m.wscale = (C.c_void_p * len(cs))(*cs)
+            self._keep += [m.wcodes_t, m.wscale]
         self._m = m
         self.lib = load_oracle()
 

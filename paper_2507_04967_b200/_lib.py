@@ -76,6 +76,8 @@ SIGNATURES = {
     "iolm_cuda_kernel_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "iolm_cuda_debug_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                             C.c_int32, C.c_int32, C.c_int32]),
+    "iolm_cuda_debug_gemm_time": (C.c_int, [C.c_int32] * 7 + [C.POINTER(C.c_float)]),
+    "iolm_cuda_debug_quant_rows_bf16": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "iolm_cuda_debug_gemm_s8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                           C.c_int32, C.c_int32]),
 }

@@ -39,10 +39,15 @@ using iolmk::AttnParams;
 using iolmk::GemmEpi;
 
 void launch_ln(const float* x, int M, int d, const float* g, const float* b, __nv_bfloat16* h, int ldh,
-               cudaStream_t st);
+               cudaStream_t st, int8_t* q8, float* qscale);
 void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_slot, const int* tok_pos,
                      const int32_t* last_tok, int M, int d, const float* tok_embed, const float* pos_embed, float* x,
-                     const float* g, const float* b, __nv_bfloat16* h, int ldh, cudaStream_t st);
+                     const float* g, const float* b, __nv_bfloat16* h, int ldh, cudaStream_t st, int8_t* q8,
+                     float* qscale);
+void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_t* dst, int ldd, float* scale,
+                       cudaStream_t st);
+void launch_decode_codes(const void* payload, int enc, int rows, int cols, void* dst, bool int8, int ld,
+                         float* scales, cudaStream_t st);
 void launch_attention(const AttnParams& prefill, const AttnParams& decode, int hd, cudaStream_t st);
 void launch_head(const float* x, int d, const int* rows, int n_rows, const float* g, const float* b,
                  const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
@@ -103,13 +108,27 @@ struct PinnedArray {
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
+// Weights of one GEMM ([N x K], K-major as stored in the bundle) in one of three forms:
+//   VALUES : bf16(value)                       dense_f32 tensors (or mixed-encoding groups)
+//   CODES  : bf16(code) + f32 scale per row    q8 / q4 / sparse24 without activation quant (W8A16,
+//            W4A16): integer codes are exact in bf16, the scale is applied in the GEMM epilogue
+//   INT8   : int8 code + f32 scale per row     q8 / sparse24 with act_quant (W8A8, kind::i8)
+enum WMode : int { W_VALUES = 0, W_CODES = 1, W_INT8 = 2 };
+struct GemmW {
+  int mode = W_VALUES;
+  DevArray<__nv_bfloat16> wb;
+  DevArray<int8_t> w8;
+  DevArray<float> scale;
+  CUtensorMap tm;
+};
+
 struct Layer {
   int heads = 0, kh = 0, f = 0;
   DevArray<float> ln1_g, ln1_b, ln2_g, ln2_b;
-  DevArray<__nv_bfloat16> w_qkv, w_o, w_in, w_out;
-  CUtensorMap tm_qkv, tm_o, tm_in, tm_out;  // B operands (weights)
-  CUtensorMap tm_z, tm_g;                   // A operands with this layer's K extent
-  DevArray<__nv_bfloat16> kv;               // paged pool [pages][K|V][heads][PAGE][hd]
+  GemmW qkv, o, in, out;
+  CUtensorMap tm_z, tm_g;    // bf16 A operands with this layer's K extent
+  CUtensorMap tm_z8, tm_g8;  // int8 A operands (W8A8)
+  DevArray<__nv_bfloat16> kv;  // paged pool [pages][K|V][heads][PAGE][hd]
 };
 
 // 2-SM 256x256 tiles once both M and N fill at least one pair tile. IOLM_GEMM_TILES=single|pair
@@ -194,7 +213,8 @@ class Engine {
   static void add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head,
                           int64_t owner);
   void launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits);
-  void gemm(int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
+  void gemm(int epi, bool i8, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
+  void load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<std::string>& names, int K, int ld);
   uint64_t ref_madds_row(int s0, int advances) const;
   template <typename F>
   void timed(int cat, double work, F&& f);
@@ -207,6 +227,7 @@ class Engine {
   int T_max_ = 16384, max_slots_ = 0, pps_ = 0, prefix_slot_ = 0;
   int cur_prefix_pages_ = -1;
   bool prefix_sharing_ = true;
+  bool act_quant_ = false;
   uint64_t madds_A_ = 0, madds_B_ = 0;  // sum_l (4*d*kh + 2*d*f), sum_l kh
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
@@ -229,6 +250,10 @@ class Engine {
   DevArray<float> x_;
   DevArray<__nv_bfloat16> h_, q_, z_, g_;
   CUtensorMap tm_h_;
+  DevArray<int8_t> h8_, z8_, g8_;  // W8A8 operands + per-token scales
+  DevArray<float> hs_, zs_, gs_;
+  CUtensorMap tm_h8_;
+  bool any_int8_ = false;
   DevArray<int> page_table_;
   StepBuffers sbuf_[2];
   DevArray<int32_t> d_last_tok_, d_ids_;
@@ -262,7 +287,7 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
     if (opts->max_tokens_per_step > 0) T_max_ = opts->max_tokens_per_step;
     if (opts->max_slots > 0) max_slots_ = opts->max_slots;
     if (opts->page_size != 0 && opts->page_size != PAGE) throw Unsupported("page_size must be 16");
-    if (opts->act_quant != 0) throw Unsupported("act_quant (W8A8) is not available in this build");
+    act_quant_ = opts->act_quant != 0;
     if (opts->prefix_sharing < 0) prefix_sharing_ = false;
     ktime_ = opts->kernel_timing != 0;
   }
@@ -285,11 +310,6 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
 }
 
 void Engine::upload_weights(const BundleView& b) {
-  // Stage every payload through one device scratch buffer; decode kernels write the final layout.
-  size_t max_payload = 0;
-  for (const auto& t : b.tensors) max_payload = std::max<size_t>(max_payload, t.length);
-  DevArray<uint8_t> scratch;
-  scratch.alloc(max_payload + 16);
   auto upload_f32 = [&](const std::string& name, DevArray<float>& dst) {
     const auto& t = b.tensor(name);
     dst.alloc(static_cast<size_t>(t.rows) * t.cols);
@@ -302,12 +322,6 @@ void Engine::upload_weights(const BundleView& b) {
   tok_embed_t_.alloc(static_cast<size_t>(V_) * d_);
   launch_transpose(tok_embed_.p, V_, d_, tok_embed_t_.p, stream_);
 
-  auto decode_into = [&](const std::string& name, __nv_bfloat16* dst, int ld) {
-    const auto& t = b.tensor(name);
-    CUDA_OK(cudaMemcpyAsync(scratch.p, b.payload(t), t.length, cudaMemcpyHostToDevice, stream_));
-    launch_decode_weight(scratch.p, t.encoding, t.rows, t.cols, dst, ld, stream_);
-    CUDA_OK(cudaStreamSynchronize(stream_));  // scratch is reused by the next tensor
-  };
   for (int l = 0; l < L_; ++l) {
     auto ly = std::make_unique<Layer>();
     const std::string p = "layers." + std::to_string(l) + ".";
@@ -318,27 +332,63 @@ void Engine::upload_weights(const BundleView& b) {
     upload_f32(p + "attn_norm.bias", ly->ln1_b);
     upload_f32(p + "ffn_norm.gain", ly->ln2_g);
     upload_f32(p + "ffn_norm.bias", ly->ln2_b);
-    const int kh = ly->kh, f = ly->f, f_ld = round_up(f, 8);
-    ly->w_qkv.alloc(static_cast<size_t>(3) * kh * d_);
-    decode_into(p + "attn.wq", ly->w_qkv.p, d_);
-    decode_into(p + "attn.wk", ly->w_qkv.p + static_cast<size_t>(kh) * d_, d_);
-    decode_into(p + "attn.wv", ly->w_qkv.p + static_cast<size_t>(2) * kh * d_, d_);
-    ly->w_o.alloc(static_cast<size_t>(d_) * kh);
-    decode_into(p + "attn.wo", ly->w_o.p, kh);
-    ly->w_in.alloc(static_cast<size_t>(f) * d_);
-    decode_into(p + "ffn.w_in", ly->w_in.p, d_);
-    ly->w_out.alloc(static_cast<size_t>(d_) * f_ld);
-    decode_into(p + "ffn.w_out", ly->w_out.p, f_ld);
-    const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    ly->tm_qkv = make_kmajor_map(ly->w_qkv.p, BF, 2, d_, 3ull * kh, 2ull * d_, 128);
-    ly->tm_o = make_kmajor_map(ly->w_o.p, BF, 2, kh, d_, 2ull * kh, 128);
-    ly->tm_in = make_kmajor_map(ly->w_in.p, BF, 2, d_, f, 2ull * d_, 128);
-    ly->tm_out = make_kmajor_map(ly->w_out.p, BF, 2, f, d_, 2ull * f_ld, 128);
+    const int kh = ly->kh, f = ly->f, f_ld = round_up(f, 16);
+    load_gemm_weights(b, ly->qkv, {p + "attn.wq", p + "attn.wk", p + "attn.wv"}, d_, d_);
+    load_gemm_weights(b, ly->o, {p + "attn.wo"}, kh, kh);
+    load_gemm_weights(b, ly->in, {p + "ffn.w_in"}, d_, d_);
+    load_gemm_weights(b, ly->out, {p + "ffn.w_out"}, f, f_ld);
+    any_int8_ = any_int8_ || ly->qkv.mode == W_INT8 || ly->o.mode == W_INT8 || ly->in.mode == W_INT8 ||
+                ly->out.mode == W_INT8;
     kh_max_ = std::max(kh_max_, kh);
     f_ld_max_ = std::max(f_ld_max_, f_ld);
     layers_.push_back(std::move(ly));
   }
   CUDA_OK(cudaStreamSynchronize(stream_));
+}
+
+// Decodes the tensors of one GEMM (stacked along N, e.g. wq|wk|wv) into the chosen weight form.
+void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<std::string>& names, int K,
+                               int ld) {
+  std::vector<const TensorRecord*> ts;
+  int N = 0;
+  bool all_dense = true, all_quant = true, int8_ok = true;
+  for (const auto& n : names) {
+    ts.push_back(&b.tensor(n));
+    N += ts.back()->rows;
+    all_dense = all_dense && ts.back()->encoding == ENC_DENSE_F32;
+    all_quant = all_quant && ts.back()->encoding != ENC_DENSE_F32;
+    int8_ok = int8_ok && (ts.back()->encoding == ENC_Q8 || ts.back()->encoding == ENC_SPARSE24_Q8);
+  }
+  w.mode = all_quant ? (act_quant_ && int8_ok ? W_INT8 : W_CODES) : W_VALUES;
+  if (act_quant_ && w.mode != W_INT8)
+    throw Unsupported("act_quant (W8A8) needs q8 or sparse24_q8 encodings for every linear weight; " + names[0] +
+                      " is " + (all_dense ? "dense_f32" : "q4 or mixed"));
+  size_t max_payload = 0;
+  for (auto* t : ts) max_payload = std::max<size_t>(max_payload, t->length);
+  DevArray<uint8_t> scratch;
+  scratch.alloc(max_payload + 16);
+  if (w.mode == W_INT8) w.w8.alloc(static_cast<size_t>(N) * ld);
+  else w.wb.alloc(static_cast<size_t>(N) * ld);
+  if (w.mode != W_VALUES) w.scale.alloc(N);
+  int row0 = 0;
+  for (auto* t : ts) {
+    CUDA_OK(cudaMemcpyAsync(scratch.p, b.payload(*t), t->length, cudaMemcpyHostToDevice, stream_));
+    const size_t off = static_cast<size_t>(row0) * ld;
+    if (w.mode == W_VALUES)
+      launch_decode_weight(scratch.p, t->encoding, t->rows, t->cols, w.wb.p + off, ld, stream_);
+    else if (w.mode == W_CODES)
+      launch_decode_codes(scratch.p, t->encoding, t->rows, t->cols, w.wb.p + off, false, ld, w.scale.p + row0,
+                          stream_);
+    else
+      launch_decode_codes(scratch.p, t->encoding, t->rows, t->cols, w.w8.p + off, true, ld, w.scale.p + row0,
+                          stream_);
+    CUDA_OK(cudaStreamSynchronize(stream_));  // scratch is reused by the next tensor
+    row0 += t->rows;
+  }
+  if (w.mode == W_INT8)
+    w.tm = make_kmajor_map(w.w8.p, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, N, static_cast<uint64_t>(ld), 128);
+  else
+    w.tm = make_kmajor_map(w.wb.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, N, 2ull * ld, 128);
 }
 
 void Engine::alloc_runtime() {
@@ -354,6 +404,20 @@ void Engine::alloc_runtime() {
   for (auto& ly : layers_) {
     ly->tm_z = make_kmajor_map(z_.p, BF, 2, ly->kh, T, 2ull * kh_max_, 128);
     ly->tm_g = make_kmajor_map(g_.p, BF, 2, ly->f, T, 2ull * f_ld_max_, 128);
+  }
+  if (any_int8_) {
+    const auto U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
+    h8_.alloc(T * d_);
+    z8_.alloc(T * kh_max_);
+    g8_.alloc(T * f_ld_max_);
+    hs_.alloc(T);
+    zs_.alloc(T);
+    gs_.alloc(T);
+    tm_h8_ = make_kmajor_map(h8_.p, U8, 1, d_, T, static_cast<uint64_t>(d_), 128);
+    for (auto& ly : layers_) {
+      ly->tm_z8 = make_kmajor_map(z8_.p, U8, 1, ly->kh, T, static_cast<uint64_t>(kh_max_), 128);
+      ly->tm_g8 = make_kmajor_map(g8_.p, U8, 1, ly->f, T, static_cast<uint64_t>(f_ld_max_), 128);
+    }
   }
   // packed step metadata: tok_src i64[T], tok_slot/pos i32[T], groups 2 x [T], head rows/slots i32[T]
   const size_t meta_bytes = align16(T * 8) + 2 * align16(T * 4) + 2 * align16(T * sizeof(AttnGroup)) +
@@ -422,8 +486,9 @@ void Engine::add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p
   }
 }
 
-void Engine::gemm(int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep) {
-  launch_gemm(use_pair(M, N), false, epi, A, B, M, N, K, ep, stream_, sms_);
+void Engine::gemm(int epi, bool i8, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
+                  const GemmEpi& ep) {
+  launch_gemm(use_pair(M, N), i8, epi, A, B, M, N, K, ep, stream_, sms_);
   ++stats_.kernel_launches;
 }
 
@@ -497,9 +562,11 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
   CUDA_OK(cudaMemcpyAsync(d, h, off, cudaMemcpyHostToDevice, stream_));
 
   const double dT = static_cast<double>(T);
+  const bool q8_first = layers_[0]->qkv.mode == W_INT8;
   timed(0, dT * d_ * 14.0, [&] {
     launch_embed_ln(d_ids, sb.tok_src, sb.tok_slot, sb.tok_pos, d_last_tok_.p, T, d_, tok_embed_.p, pos_embed_.p,
-                    x_.p, layers_[0]->ln1_g.p, layers_[0]->ln1_b.p, h_.p, d_, stream_);
+                    x_.p, layers_[0]->ln1_g.p, layers_[0]->ln1_b.p, h_.p, d_, stream_, q8_first ? h8_.p : nullptr,
+                    hs_.p);
   });
   ++stats_.kernel_launches;
   // algorithmic attention work of this step (per head): prefill FLOPs 4*hd*sum(pos+1),
@@ -511,8 +578,15 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     for (const auto& g : s.dec) dec_keys += g.pos0 + 1;
   }
   const float scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(hd_));
+  // weight scale (CODES / INT8) and activation scale (INT8) of one GEMM
+  auto scales = [](GemmEpi& e, const GemmW& w, const float* a_scale) {
+    e.w_scale = w.mode == W_VALUES ? nullptr : w.scale.p;
+    e.a_scale = w.mode == W_INT8 ? a_scale : nullptr;
+  };
   for (int l = 0; l < L_; ++l) {
     Layer& ly = *layers_[l];
+    const bool i8_qkv = ly.qkv.mode == W_INT8, i8_o = ly.o.mode == W_INT8;
+    const bool i8_in = ly.in.mode == W_INT8, i8_out = ly.out.mode == W_INT8;
     GemmEpi ep;
     ep.M = T;
     // QKV projection; K/V scattered into the paged pool by the epilogue.
@@ -526,9 +600,13 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     ep.max_pages = pps_;
     ep.kh = ly.kh;
     ep.hd = hd_;
+    ep.hd_shift = hd_ == 16 ? 4 : hd_ == 32 ? 5 : hd_ == 64 ? 6 : 7;
     ep.heads = ly.heads;
     ep.page_size = PAGE;
-    timed(1, 2.0 * dT * 3 * ly.kh * d_, [&] { gemm(iolmk::EPI_QKV, tm_h_, ly.tm_qkv, T, 3 * ly.kh, d_, ep); });
+    scales(ep, ly.qkv, hs_.p);
+    timed(1, 2.0 * dT * 3 * ly.kh * d_, [&] {
+      gemm(iolmk::EPI_QKV, i8_qkv, i8_qkv ? tm_h8_ : tm_h_, ly.qkv.tm, T, 3 * ly.kh, d_, ep);
+    });
     AttnParams ap{};
     ap.q = q_.p;
     ap.ldq = kh_max_;
@@ -555,14 +633,23 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       ++stats_.kernel_launches;
     }
     // x += z * Wo^T
+    if (i8_o) {
+      timed(5, dT * ly.kh * 3.0, [&] { launch_quant_rows(z_.p, kh_max_, T, ly.kh, z8_.p, kh_max_, zs_.p, stream_); });
+      ++stats_.kernel_launches;
+    }
     GemmEpi eo;
     eo.M = T;
     eo.N = d_;
     eo.out = x_.p;
     eo.ldo = d_;
-    timed(4, 2.0 * dT * d_ * ly.kh, [&] { gemm(iolmk::EPI_RESID_F32, ly.tm_z, ly.tm_o, T, d_, ly.kh, eo); });
+    scales(eo, ly.o, zs_.p);
+    timed(4, 2.0 * dT * d_ * ly.kh, [&] {
+      gemm(iolmk::EPI_RESID_F32, i8_o, i8_o ? ly.tm_z8 : ly.tm_z, ly.o.tm, T, d_, ly.kh, eo);
+    });
     // h = LN2(x)
-    timed(5, dT * d_ * 6.0, [&] { launch_ln(x_.p, T, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_); });
+    timed(5, dT * d_ * 6.0, [&] {
+      launch_ln(x_.p, T, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_, i8_in ? h8_.p : nullptr, hs_.p);
+    });
     ++stats_.kernel_launches;
     // g = gelu(h * Win^T)
     GemmEpi ei;
@@ -570,12 +657,25 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     ei.N = ly.f;
     ei.out = g_.p;
     ei.ldo = f_ld_max_;
-    timed(6, 2.0 * dT * ly.f * d_, [&] { gemm(iolmk::EPI_GELU_BF16, tm_h_, ly.tm_in, T, ly.f, d_, ei); });
+    scales(ei, ly.in, hs_.p);
+    timed(6, 2.0 * dT * ly.f * d_, [&] {
+      gemm(iolmk::EPI_GELU_BF16, i8_in, i8_in ? tm_h8_ : tm_h_, ly.in.tm, T, ly.f, d_, ei);
+    });
     // x += g * Wout^T
-    timed(7, 2.0 * dT * d_ * ly.f, [&] { gemm(iolmk::EPI_RESID_F32, ly.tm_g, ly.tm_out, T, d_, ly.f, eo); });
+    if (i8_out) {
+      timed(5, dT * ly.f * 3.0, [&] { launch_quant_rows(g_.p, f_ld_max_, T, ly.f, g8_.p, f_ld_max_, gs_.p, stream_); });
+      ++stats_.kernel_launches;
+    }
+    GemmEpi eo2 = eo;
+    scales(eo2, ly.out, gs_.p);
+    timed(7, 2.0 * dT * d_ * ly.f, [&] {
+      gemm(iolmk::EPI_RESID_F32, i8_out, i8_out ? ly.tm_g8 : ly.tm_g, ly.out.tm, T, d_, ly.f, eo2);
+    });
     if (l + 1 < L_) {
+      const bool q8_next = layers_[l + 1]->qkv.mode == W_INT8;
       timed(5, dT * d_ * 6.0, [&] {
-        launch_ln(x_.p, T, d_, layers_[l + 1]->ln1_g.p, layers_[l + 1]->ln1_b.p, h_.p, d_, stream_);
+        launch_ln(x_.p, T, d_, layers_[l + 1]->ln1_g.p, layers_[l + 1]->ln1_b.p, h_.p, d_, stream_,
+                  q8_next ? h8_.p : nullptr, hs_.p);
       });
       ++stats_.kernel_launches;
     }

@@ -40,6 +40,7 @@ struct GemmEpi {
   const int* page_table = nullptr;
   int max_pages = 0;
   int kh = 0, hd = 0, heads = 0, page_size = 16;
+  int hd_shift = 0;  // log2(hd); hd is 16/32/64/128
   // W8A8 dequant epilogue: acc_i32 * a_scale[row] * w_scale[col]
   const float* a_scale = nullptr;
   const float* w_scale = nullptr;
@@ -54,14 +55,15 @@ struct GemmCfg {
   static constexpr int TILE_M = BM * CG;
   static constexpr int BN_CTA = BN / CG;  // W rows staged per CTA
   static constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per operand row
-  static constexpr int STAGES = CG == 2 ? (BN >= 256 ? 6 : 8) : (BN >= 256 ? 4 : 6);
+  static constexpr int STAGES = CG == 2 ? (BN >= 256 ? 5 : 7) : (BN >= 256 ? 4 : 5);
   static constexpr uint32_t A_BYTES = BM * BK_BYTES;
   static constexpr uint32_t B_BYTES = BN_CTA * BK_BYTES;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static constexpr int EPI_WARPS = 8;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
-  static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+  static constexpr size_t SMEM =
+      1024 + STAGES * STAGE_BYTES + 512 + BN * 4 + EPI_WARPS * 5120;  // ring, barriers, scales, tiles
 };
 
 template <int EPI>
@@ -117,36 +119,142 @@ __device__ __forceinline__ void epi_apply(const GemmEpi& ep, int m, int n0, floa
         if (n0 + j < N) o[j] += v[j];
     }
   } else if constexpr (EPI == EPI_QKV) {
-    const int kh = ep.kh;
-    const int slot = ep.tok_slot[m];
-    const int pos = ep.tok_pos[m];
-    const int page = ep.page_table[static_cast<size_t>(slot) * ep.max_pages + pos / ep.page_size];
-    const int in_page = pos % ep.page_size;
+    // row context (kbase/vbase) is resolved once per tile by the caller: see QkvRow
+    (void)N;
+  }
+}
+
+// Per-row destinations of the QKV epilogue, resolved once per tile: the q row and the K/V rows of
+// this token's page slot (page layout [page][K|V][head][PAGE][hd]).
+struct QkvRow {
+  __nv_bfloat16* q;
+  __nv_bfloat16* k;  // head 0 of this token's K row
+  __nv_bfloat16* v;
+};
+__device__ __forceinline__ QkvRow qkv_row(const GemmEpi& ep, int m) {
+  QkvRow r;
+  const int slot = ep.tok_slot[m];
+  const int pos = ep.tok_pos[m];
+  const int page = ep.page_table[static_cast<size_t>(slot) * ep.max_pages + (pos >> 4)];
+  const size_t head_stride = static_cast<size_t>(ep.page_size) << ep.hd_shift;
+  __nv_bfloat16* kp = ep.kv_layer + static_cast<size_t>(page) * 2 * ep.heads * head_stride +
+                      (static_cast<size_t>(pos & 15) << ep.hd_shift);
+  r.q = static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(m) * ep.ldo;
+  r.k = kp;
+  r.v = kp + ep.heads * head_stride;
+  return r;
+}
+__device__ __forceinline__ void qkv_store(const GemmEpi& ep, const QkvRow& row, int n0, const float (&v)[32]) {
+  const int kh = ep.kh;
+  const size_t head_stride = static_cast<size_t>(ep.page_size) << ep.hd_shift;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int n = n0 + 8 * j;
-      if (n >= N) break;
-      uint4 w;
-      w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
-      w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
-      w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
-      w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
-      __nv_bfloat16* dst;
-      if (n < kh) {
-        dst = static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n;
-      } else {
-        const int c = n - kh;
-        const int which = c >= kh ? 1 : 0;
-        const int cc = c - which * kh;
-        const int head = cc / ep.hd;
-        const int dim = cc - head * ep.hd;
-        dst = ep.kv_layer +
-              ((static_cast<size_t>(page) * 2 + which) * ep.heads + head) * ep.page_size * ep.hd +
-              static_cast<size_t>(in_page) * ep.hd + dim;
+  for (int j = 0; j < 4; ++j) {
+    const int n = n0 + 8 * j;
+    if (n >= ep.N) break;
+    uint4 w;
+    w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+    w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+    w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+    w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+    __nv_bfloat16* dst;
+    if (n < kh) {
+      dst = row.q + n;
+    } else {
+      const int c = n - kh;
+      const bool is_v = c >= kh;
+      const int cc = is_v ? c - kh : c;
+      const int head = cc >> ep.hd_shift;
+      dst = (is_v ? row.v : row.k) + head * head_stride + (cc & (ep.hd - 1));
+    }
+    *reinterpret_cast<uint4*>(dst) = w;
+  }
+}
+
+// Coalesced epilogue of one warp's 32 x 32 fp32 chunk (thread t holds row m_base + t). The values
+// go through a per-warp smem tile with an XOR swizzle of the eight 16-byte column groups by
+// (row & 7), so both the row-wise (thread = row) and the column-wise (8 lanes = one 128-byte row
+// segment) accesses are bank-conflict free; every global access is then a full 128-byte row
+// segment instead of 32 half-sector writes.
+__device__ __forceinline__ int swz(int r, int g) { return r * 32 + ((g ^ (r & 7)) << 2); }
+
+template <int EPI>
+__device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* tile, int m_base, int n0, float (&v)[32],
+                                                   int lane, const QkvRow* rows = nullptr) {
+  const int rr = lane >> 3, gg = lane & 7;  // coalesced phase: row rr + 4i, column group gg
+  if constexpr (EPI == EPI_GELU_BF16) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+  }
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
+    *reinterpret_cast<float4*>(tile + swz(lane, g)) = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+  __syncwarp();
+  if constexpr (EPI == EPI_RESID_F32) {
+    float* xb = static_cast<float*>(ep.out) + n0 + gg * 4;
+    float4 xo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = m_base + rr + 4 * i;
+      xo[i] = row < ep.M ? *reinterpret_cast<const float4*>(xb + static_cast<size_t>(row) * ep.ldo)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = m_base + rr + 4 * i;
+      const float4 a = *reinterpret_cast<const float4*>(tile + swz(rr + 4 * i, gg));
+      if (row < ep.M)
+        *reinterpret_cast<float4*>(xb + static_cast<size_t>(row) * ep.ldo) =
+            make_float4(xo[i].x + a.x, xo[i].y + a.y, xo[i].z + a.z, xo[i].w + a.w);
+    }
+  } else if constexpr (EPI == EPI_QKV) {
+    // 4 lanes x 16 B per row segment, 8 rows per instruction; destinations per row from `rows`
+    const int r8 = lane >> 2, q4 = lane & 3;
+    const int n = n0 + q4 * 8;
+    const int kh = ep.kh;
+    const size_t head_stride = static_cast<size_t>(ep.page_size) << ep.hd_shift;
+    int region = 0, off = n;  // 0: q, 1: K, 2: V
+    if (n >= kh) {
+      const int c = n - kh;
+      region = c >= kh ? 2 : 1;
+      const int cc = region == 2 ? c - kh : c;
+      off = static_cast<int>((cc >> ep.hd_shift) * head_stride) + (cc & (ep.hd - 1));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int lr = r8 + 8 * i;
+      const float4 a = *reinterpret_cast<const float4*>(tile + swz(lr, 2 * q4));
+      const float4 b = *reinterpret_cast<const float4*>(tile + swz(lr, 2 * q4 + 1));
+      if (m_base + lr < ep.M) {
+        uint4 w;
+        w.x = pack_bf16x2(a.x, a.y);
+        w.y = pack_bf16x2(a.z, a.w);
+        w.z = pack_bf16x2(b.x, b.y);
+        w.w = pack_bf16x2(b.z, b.w);
+        const QkvRow& rw = rows[lr];
+        __nv_bfloat16* dst = (region == 0 ? rw.q : region == 1 ? rw.k : rw.v) + off;
+        *reinterpret_cast<uint4*>(dst) = w;
       }
-      *reinterpret_cast<uint4*>(dst) = w;
+    }
+  } else {  // bf16 output: 4 lanes x 16 B = one 64-byte row segment, 8 rows per instruction
+    const int r8 = lane >> 2, q4 = lane & 3;
+    __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(ep.out) + n0 + q4 * 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int lr = r8 + 8 * i;
+      const float4 a = *reinterpret_cast<const float4*>(tile + swz(lr, 2 * q4));
+      const float4 b = *reinterpret_cast<const float4*>(tile + swz(lr, 2 * q4 + 1));
+      const int row = m_base + lr;
+      if (row < ep.M) {
+        uint4 w;
+        w.x = pack_bf16x2(a.x, a.y);
+        w.y = pack_bf16x2(a.z, a.w);
+        w.z = pack_bf16x2(b.x, b.y);
+        w.w = pack_bf16x2(b.z, b.w);
+        *reinterpret_cast<uint4*>(ob + static_cast<size_t>(row) * ep.ldo) = w;
+      }
     }
   }
+  __syncwarp();
 }
 
 template <int BN, int EPI, int CG, bool I8>
@@ -279,54 +387,98 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     __syncwarp();
   } else {
     const int e = warp - 2;
-    const int q = warp & 3;             // TMEM lane quarter this warp may access
+    const int q = warp & 3;                   // TMEM lane quarter this warp may access
     const int c_begin = (e >> 2) * (BN / 2);  // column half handled by this warp
+    constexpr int NCH = BN / 64;              // 32-column chunks per warp per tile
     const uint32_t leader_tempty0 = CG == 2 ? mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
+    float* s_scale = reinterpret_cast<float*>(smem_raw + (bars + 512 - raw));  // [BN] per tile
+    uint8_t* s_warp = smem_raw + (bars + 512 + BN * 4 - raw) + e * 5120;
+    float* s_tile = reinterpret_cast<float*>(s_warp);                 // 32 x 32 fp32 (4 KB)
+    QkvRow* s_rows = reinterpret_cast<QkvRow*>(s_warp + 4096);        // the warp's 32 row destinations
+    const bool has_ws = ep.w_scale != nullptr;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = group; tile < num_tiles; tile += n_groups) {
       const int mt = tile / n_tiles;
       const int nt = tile - mt * n_tiles;
       const int m = mt * C::TILE_M + static_cast<int>(rank) * C::BM + q * 32 + lane;
-      if constexpr (EPI == EPI_RESID_F32) {
-        // warm L2 with this thread's residual row segment while the MMAs of the tile run
-        if (m < M) {
-          const float* xr = static_cast<const float*>(ep.out) + static_cast<size_t>(m) * ep.ldo + nt * BN + c_begin;
-#pragma unroll
-          for (int c = 0; c < BN / 2; c += 32)
-            if (nt * BN + c_begin + c < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + c));
+      const bool row_ok = m < M;
+      // stage this tile's per-column weight scales once (all epilogue warps, named barrier 1)
+      if (has_ws) {
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+        for (int i = threadIdx.x - 64; i < BN; i += 32 * C::EPI_WARPS) {
+          const int n = nt * BN + i;
+          s_scale[i] = n < N ? ep.w_scale[n] : 0.f;
         }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+      }
+      float a_sc = 1.f;
+      if constexpr (I8) a_sc = row_ok ? ep.a_scale[m] : 0.f;
+      QkvRow qrow{};
+      if constexpr (EPI == EPI_QKV) {
+        if (row_ok) qrow = qkv_row(ep, m);
+        s_rows[lane] = qrow;
+        __syncwarp();
       }
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
-#pragma unroll 1
-      for (int c = c_begin; c < c_begin + BN / 2; c += 32) {
+      // TMEM loads double-buffered across chunks: chunk c+1 is in flight while c is processed
+      uint32_t r[2][32];
+      tmem_ld_32x32b_x32(tbase + c_begin, r[0]);
+#pragma unroll
+      for (int ci = 0; ci < NCH; ++ci) {
+        const int c = c_begin + ci * 32;
         const int n0 = nt * BN + c;
-        if (n0 >= N) break;  // warp-uniform
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tbase + c, r);
         tmem_ld_wait();
-        if (m < M) {
+        if (ci + 1 < NCH) tmem_ld_32x32b_x32(tbase + c + 32, r[(ci + 1) & 1]);
+        const uint32_t(&rc)[32] = r[ci & 1];
+        const int m_base = mt * C::TILE_M + static_cast<int>(rank) * C::BM + q * 32;  // warp's first row
+        if constexpr (EPI == EPI_RESID_F32 || EPI == EPI_BF16 || EPI == EPI_GELU_BF16 || EPI == EPI_QKV) {
+          // full 32-column chunk with aligned rows: coalesced path through the warp's smem tile
+          // (QKV: a chunk never straddles q/K/V or a head when hd >= 32)
+          const bool full = n0 + 32 <= N && (ep.ldo & 7) == 0 && (EPI != EPI_QKV || ep.hd_shift >= 5);
+          if (full && m_base < M) {
+            float v[32];
+            if constexpr (I8) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = static_cast<float>(static_cast<int32_t>(rc[j])) * a_sc * s_scale[c + j];
+            } else if (has_ws) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rc[j]) * s_scale[c + j];
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rc[j]);
+            }
+            warp_tile_epilogue<EPI>(ep, s_tile, m_base, n0, v, lane, s_rows);
+            continue;
+          }
+        }
+        if (row_ok && n0 < N) {
           if constexpr (EPI == EPI_S32) {
             int32_t* o = static_cast<int32_t*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n0;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (n0 + j < N) o[j] = static_cast<int32_t>(r[j]);
+              if (n0 + j < N) o[j] = static_cast<int32_t>(rc[j]);
           } else {
             float v[32];
             if constexpr (I8) {
-              const float sa = ep.a_scale[m];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const int n = min(n0 + j, N - 1);
-                v[j] = static_cast<float>(static_cast<int32_t>(r[j])) * sa * ep.w_scale[n];
-              }
+              for (int j = 0; j < 32; ++j) v[j] = static_cast<float>(static_cast<int32_t>(rc[j])) * a_sc * s_scale[c + j];
             } else {
+              if (has_ws) {  // W8A16 / W4A16: codes as exact bf16 integers, scale here
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rc[j]) * s_scale[c + j];
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rc[j]);
+              }
             }
-            epi_apply<EPI>(ep, m, n0, v);
+            if constexpr (EPI == EPI_QKV) {
+              qkv_store(ep, qrow, n0, v);
+            } else {
+              epi_apply<EPI>(ep, m, n0, v);
+            }
           }
         }
       }

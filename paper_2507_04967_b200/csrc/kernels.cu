@@ -17,12 +17,30 @@ namespace iolmk {
 
 constexpr int PAGE = 16;
 
+// ------------------------------------------------------------------ per-token int8 (W8A8)
+// Activation quantization rule (the reference has none; pinned to its weight RTN
+// rule, quant.cpp:23-38, applied per token): s = amax/127 (amax == 0 -> 1),
+// q = clamp(rint(x / s), -127, 127) with x / s the IEEE round-to-nearest fp32 division and rint
+// ties-to-even - exactly oracle/iolm_oracle.c orc_quant_rows_s8 ("W8A8").
+__device__ __forceinline__ int8_t quant_one(float x, float s) {
+  float q = rintf(__fdiv_rn(x, s));
+  q = fminf(127.f, fmaxf(-127.f, q));
+  return static_cast<int8_t>(static_cast<int>(q));
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 // ------------------------------------------------------------------ LayerNorm
-// One warp per row. Two-pass mean / variance in fp32 over the row held in registers.
-template <int MAXV>  // max float4 per lane
+// One warp per row. Two-pass mean / variance in fp32 over the row held in registers. Writes the
+// bf16 GEMM operand, or (Q8) per-token int8 codes + the row scale for the W8A8 GEMMs.
+template <int MAXV, bool Q8 = false>
 __device__ __forceinline__ void ln_row_warp(const float* __restrict__ xr, int d, const float* __restrict__ g,
                                             const float* __restrict__ b, __nv_bfloat16* __restrict__ hr,
-                                            int lane) {
+                                            int lane, int8_t* __restrict__ q8 = nullptr,
+                                            float* __restrict__ qscale = nullptr) {
   float4 v[MAXV];
   const int nv = d >> 2;
   float s = 0.f;
@@ -49,39 +67,120 @@ __device__ __forceinline__ void ln_row_warp(const float* __restrict__ xr, int d,
 #pragma unroll
   for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
   const float inv = 1.0f / sqrtf(q / static_cast<float>(d) + 1e-5f);
+  if constexpr (Q8) {
+    float amax = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
-    const int idx = lane + 32 * i;
-    if (idx < nv) {
-      const float4 gg = reinterpret_cast<const float4*>(g)[idx];
-      const float4 bb = reinterpret_cast<const float4*>(b)[idx];
-      uint2 w;
-      w.x = pack_bf16x2((v[i].x - mean) * inv * gg.x + bb.x, (v[i].y - mean) * inv * gg.y + bb.y);
-      w.y = pack_bf16x2((v[i].z - mean) * inv * gg.z + bb.z, (v[i].w - mean) * inv * gg.w + bb.w);
-      reinterpret_cast<uint2*>(hr)[idx] = w;
+    for (int i = 0; i < MAXV; ++i) {
+      const int idx = lane + 32 * i;
+      if (idx < nv) {
+        const float4 gg = reinterpret_cast<const float4*>(g)[idx];
+        const float4 bb = reinterpret_cast<const float4*>(b)[idx];
+        v[i].x = (v[i].x - mean) * inv * gg.x + bb.x;
+        v[i].y = (v[i].y - mean) * inv * gg.y + bb.y;
+        v[i].z = (v[i].z - mean) * inv * gg.z + bb.z;
+        v[i].w = (v[i].w - mean) * inv * gg.w + bb.w;
+        amax = fmaxf(fmaxf(amax, fmaxf(fabsf(v[i].x), fabsf(v[i].y))), fmaxf(fabsf(v[i].z), fabsf(v[i].w)));
+      }
+    }
+    amax = warp_max(amax);
+    const float s = amax == 0.f ? 1.f : amax / 127.0f;
+    const float sd = s;
+    if (lane == 0) *qscale = s;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int idx = lane + 32 * i;
+      if (idx < nv) {
+        char4 c;
+        c.x = quant_one(v[i].x, sd);
+        c.y = quant_one(v[i].y, sd);
+        c.z = quant_one(v[i].z, sd);
+        c.w = quant_one(v[i].w, sd);
+        reinterpret_cast<char4*>(q8)[idx] = c;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int idx = lane + 32 * i;
+      if (idx < nv) {
+        const float4 gg = reinterpret_cast<const float4*>(g)[idx];
+        const float4 bb = reinterpret_cast<const float4*>(b)[idx];
+        uint2 w;
+        w.x = pack_bf16x2((v[i].x - mean) * inv * gg.x + bb.x, (v[i].y - mean) * inv * gg.y + bb.y);
+        w.y = pack_bf16x2((v[i].z - mean) * inv * gg.z + bb.z, (v[i].w - mean) * inv * gg.w + bb.w);
+        reinterpret_cast<uint2*>(hr)[idx] = w;
+      }
     }
   }
 }
 
-template <int MAXV>
+template <int MAXV, bool Q8>
 __global__ void __launch_bounds__(256) ln_kernel(const float* __restrict__ x, int M, int d,
                                                  const float* __restrict__ g, const float* __restrict__ b,
-                                                 __nv_bfloat16* __restrict__ h, int ldh) {
+                                                 __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
+                                                 float* __restrict__ qscale) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= M) return;
-  ln_row_warp<MAXV>(x + static_cast<size_t>(row) * d, d, g, b, h + static_cast<size_t>(row) * ldh,
-                    threadIdx.x & 31);
+  if constexpr (Q8)
+    ln_row_warp<MAXV, true>(x + static_cast<size_t>(row) * d, d, g, b, nullptr, threadIdx.x & 31,
+                            q8 + static_cast<size_t>(row) * ldh, qscale + row);
+  else
+    ln_row_warp<MAXV>(x + static_cast<size_t>(row) * d, d, g, b, h + static_cast<size_t>(row) * ldh,
+                      threadIdx.x & 31);
+}
+
+// Per-token int8 quantization of a bf16 activation matrix (attention output z, GELU output g).
+// One warp per row; two passes over the row (amax, then codes), the row stays L1/L2 resident.
+__global__ void __launch_bounds__(256) quant_rows_kernel(const __nv_bfloat16* __restrict__ src, int lds, int M,
+                                                         int cols, int8_t* __restrict__ dst, int ldd,
+                                                         float* __restrict__ scale) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= M) return;
+  const int lane = threadIdx.x & 31;
+  const __nv_bfloat16* r = src + static_cast<size_t>(row) * lds;
+  const int cols8 = cols & ~7;
+  float amax = 0.f;
+  for (int c = cols8 + lane; c < cols; c += 32) amax = fmaxf(amax, fabsf(__bfloat162float(r[c])));
+  for (int c = lane * 8; c < cols8; c += 256) {
+    const uint4 u = *reinterpret_cast<const uint4*>(r + c);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h2[j]);
+      amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+    }
+  }
+  amax = warp_max(amax);
+  const float s = amax == 0.f ? 1.f : amax / 127.0f;
+  const float sd = s;
+  if (lane == 0) scale[row] = s;
+  int8_t* o = dst + static_cast<size_t>(row) * ldd;
+  for (int c = cols8 + lane; c < cols; c += 32) o[c] = quant_one(__bfloat162float(r[c]), sd);
+  for (int c = lane * 8; c < cols8; c += 256) {
+    const uint4 u = *reinterpret_cast<const uint4*>(r + c);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+    uint2 w;
+    int8_t* wb = reinterpret_cast<int8_t*>(&w);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h2[j]);
+      wb[2 * j] = quant_one(f.x, sd);
+      wb[2 * j + 1] = quant_one(f.y, sd);
+    }
+    *reinterpret_cast<uint2*>(o + c) = w;
+  }
 }
 
 // token id of step row m: prompt tokens come from the id table, generated tokens from the
 // per-slot "last token" register written by head_argmax_kernel.
-template <int MAXV>
+template <int MAXV, bool Q8>
 __global__ void __launch_bounds__(256)
     embed_ln_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ tok_src,
                     const int* __restrict__ tok_slot, const int* __restrict__ tok_pos,
                     const int32_t* __restrict__ last_tok, int M, int d, const float* __restrict__ tok_embed,
                     const float* __restrict__ pos_embed, float* __restrict__ x, const float* __restrict__ g,
-                    const float* __restrict__ b, __nv_bfloat16* __restrict__ h, int ldh) {
+                    const float* __restrict__ b, __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
+                    float* __restrict__ qscale) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= M) return;
   const int lane = threadIdx.x & 31;
@@ -95,7 +194,11 @@ __global__ void __launch_bounds__(256)
     xr[i] = make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
   }
   __syncwarp();
-  ln_row_warp<MAXV>(x + static_cast<size_t>(row) * d, d, g, b, h + static_cast<size_t>(row) * ldh, lane);
+  if constexpr (Q8)
+    ln_row_warp<MAXV, true>(x + static_cast<size_t>(row) * d, d, g, b, nullptr, lane,
+                            q8 + static_cast<size_t>(row) * ldh, qscale + row);
+  else
+    ln_row_warp<MAXV>(x + static_cast<size_t>(row) * d, d, g, b, h + static_cast<size_t>(row) * ldh, lane);
 }
 
 // ------------------------------------------------------------------ attention (prefill, mma.sync)
@@ -600,6 +703,49 @@ __global__ void decode_quant_bf16_kernel(const uint8_t* __restrict__ p, int enc,
   dst[i] = __float2bfloat16_rn(v);
 }
 
+// Quantized payload -> the integer codes only (exact as bf16 for |code| <= 127), zero padded;
+// scales[r] receives the per-row f32 scale. The scale is applied in the GEMM epilogue.
+template <typename T>
+__global__ void decode_codes_kernel(const uint8_t* __restrict__ p, int enc, int rows, int cols, T* dst, int ld,
+                                    float* __restrict__ scales) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(rows) * ld) return;
+  const int r = static_cast<int>(i / ld), c = static_cast<int>(i % ld);
+  int code = 0;
+  size_t scale_off = 0;
+  if (enc == 1) {
+    scale_off = static_cast<size_t>(rows) * cols;
+    if (c < cols) code = reinterpret_cast<const int8_t*>(p)[static_cast<size_t>(r) * cols + c];
+  } else if (enc == 2) {
+    const size_t rb = (static_cast<size_t>(cols) + 1) / 2;
+    scale_off = rows * rb;
+    if (c < cols) {
+      const uint8_t byte = p[r * rb + c / 2];
+      code = ((c & 1) ? (byte >> 4) : (byte & 0xF)) - 8;
+    }
+  } else if (enc == 3) {
+    const size_t groups = cols / 4, irb = (groups + 1) / 2;
+    const int8_t* codes = reinterpret_cast<const int8_t*>(p);
+    const uint8_t* idx = p + static_cast<size_t>(rows) * groups * 2;
+    scale_off = static_cast<size_t>(rows) * groups * 2 + rows * irb;
+    if (c < cols) {
+      const size_t gidx = c / 4;
+      const uint8_t byte = idx[r * irb + gidx / 2];
+      const int nib = (gidx & 1) ? (byte >> 4) : (byte & 0xF);
+      const int j = c & 3;
+      if (j == (nib & 3)) code = codes[(r * groups + gidx) * 2];
+      if (j == ((nib >> 2) & 3)) code = codes[(r * groups + gidx) * 2 + 1];
+    }
+  }
+  if constexpr (sizeof(T) == 1) dst[i] = static_cast<int8_t>(code);
+  else dst[i] = __int2bfloat16_rn(code);
+  if (c == 0) {
+    float s;
+    memcpy(&s, p + scale_off + 4ull * r, 4);
+    scales[r] = s;
+  }
+}
+
 __global__ void transpose_f32_kernel(const float* __restrict__ src, int rows, int cols, float* __restrict__ dst) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(rows) * cols) return;
@@ -616,11 +762,15 @@ using namespace iolmk;
 static inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 void launch_ln(const float* x, int M, int d, const float* g, const float* b, __nv_bfloat16* h, int ldh,
-               cudaStream_t st) {
+               cudaStream_t st, int8_t* q8, float* qscale) {
   if (M <= 0) return;
   const unsigned grid = blocks_for(M, 8);
   const int nv = (d / 4 + 31) / 32;
-#define LNK(V) ln_kernel<V><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh)
+#define LNK(V)                                                                     \
+  do {                                                                             \
+    if (q8) ln_kernel<V, true><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale); \
+    else ln_kernel<V, false><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);   \
+  } while (0)
   switch (nv) {
     case 1: LNK(1); break;
     case 2: LNK(2); break;
@@ -641,15 +791,30 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
   CUDA_OK(cudaGetLastError());
 }
 
+void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_t* dst, int ldd, float* scale,
+                       cudaStream_t st) {
+  if (M <= 0) return;
+  if (lds % 8 != 0 || ldd % 8 != 0) throw Unsupported("quant_rows: leading dimensions must be multiples of 8");
+  quant_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  CUDA_OK(cudaGetLastError());
+}
+
 void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_slot, const int* tok_pos,
                      const int32_t* last_tok, int M, int d, const float* tok_embed, const float* pos_embed, float* x,
-                     const float* g, const float* b, __nv_bfloat16* h, int ldh, cudaStream_t st) {
+                     const float* g, const float* b, __nv_bfloat16* h, int ldh, cudaStream_t st, int8_t* q8,
+                     float* qscale) {
   if (M <= 0) return;
   const unsigned grid = blocks_for(M, 8);
   const int nv = (d / 4 + 31) / 32;
-#define EMB(V)                                                                                          \
-  embed_ln_kernel<V><<<grid, 256, 0, st>>>(ids, tok_src, tok_slot, tok_pos, last_tok, M, d, tok_embed, \
-                                           pos_embed, x, g, b, h, ldh)
+#define EMB(V)                                                                                        \
+  do {                                                                                                \
+    if (q8)                                                                                           \
+      embed_ln_kernel<V, true><<<grid, 256, 0, st>>>(ids, tok_src, tok_slot, tok_pos, last_tok, M, d, \
+                                                     tok_embed, pos_embed, x, g, b, h, ldh, q8, qscale); \
+    else                                                                                              \
+      embed_ln_kernel<V, false><<<grid, 256, 0, st>>>(ids, tok_src, tok_slot, tok_pos, last_tok, M, d, \
+                                                      tok_embed, pos_embed, x, g, b, h, ldh, q8, qscale); \
+  } while (0)
   switch (nv) {
     case 1: EMB(1); break;
     case 2: EMB(2); break;
@@ -740,6 +905,19 @@ void launch_decode_weight(const void* payload, int enc, int rows, int cols, __nv
   else
     decode_quant_bf16_kernel<<<blocks_for(n, 256), 256, 0, st>>>(static_cast<const uint8_t*>(payload), enc, rows,
                                                                  cols, dst, ld);
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_decode_codes(const void* payload, int enc, int rows, int cols, void* dst, bool int8, int ld,
+                         float* scales, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(rows) * ld;
+  if (enc < 1 || enc > 3) throw Unsupported("decode_codes: not a quantized encoding");
+  if (int8)
+    decode_codes_kernel<int8_t><<<blocks_for(n, 256), 256, 0, st>>>(static_cast<const uint8_t*>(payload), enc, rows,
+                                                                    cols, static_cast<int8_t*>(dst), ld, scales);
+  else
+    decode_codes_kernel<__nv_bfloat16><<<blocks_for(n, 256), 256, 0, st>>>(
+        static_cast<const uint8_t*>(payload), enc, rows, cols, static_cast<__nv_bfloat16*>(dst), ld, scales);
   CUDA_OK(cudaGetLastError());
 }
 

@@ -75,3 +75,22 @@ def test_gemm_s8_bitexact(engine_lib, M, N, K, pair):
     assert st == 0, engine_lib.iolm_cuda_last_error()
     ref = O.gemm_s8(A, W)
     assert np.array_equal(out, ref)
+
+
+def test_activation_quantizer_bitexact(engine_lib):
+    """GPU per-token int8 quantization == oracle.quant_rows_s8 bit-for-bit (codes and scales)."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal((257, 1280)) * rng.uniform(0.01, 30, size=(257, 1))).astype(np.float32)
+    x[3] = 0.0
+    x[7, :5] = [2.5, -3.5, 127.0, -0.5, 1.5]  # exact half-integers once scaled
+    bits = bf16_bits(x)
+    xf = bits_to_f32(bits).reshape(x.shape)
+    codes = np.zeros(x.shape, np.int8)
+    scales = np.zeros(x.shape[0], np.float32)
+    st = engine_lib.iolm_cuda_debug_quant_rows_bf16(np.ascontiguousarray(bits).ctypes.data, x.shape[0], x.shape[1],
+                                                    codes.ctypes.data, scales.ctypes.data)
+    assert st == 0, engine_lib.iolm_cuda_last_error()
+    rc, rs = O.quant_rows_s8(xf)
+    assert np.array_equal(scales.view(np.uint32), rs.view(np.uint32))
+    assert np.array_equal(codes, rc)
