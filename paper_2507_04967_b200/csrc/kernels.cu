@@ -403,17 +403,15 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
 // are read by LPK = HD/8 lanes x 16 B, KPI = 32/LPK keys per instruction. Work is chunked by page
 // (absolute 16-position blocks), so a query's arithmetic never depends on the batch composition.
 constexpr int DSTAGES = 2;
-constexpr int DEC_WARPS = 8;
 template <int HD>
 struct DecCfg {
-  static constexpr int HG_MAX = HD >= 128 ? 8 : (HD == 64 ? 16 : 32);  // heads per CTA
-  static constexpr int HEADS_PER_WARP = (HG_MAX + DEC_WARPS - 1) / DEC_WARPS;
+  static constexpr int HG_MAX = HD >= 128 ? 8 : 16;  // heads per CTA = compute warps
   static constexpr size_t SMEM_MAX = 256 + DSTAGES * 2 * HG_MAX * PAGE * HD * 2;
 };
 
+// Block = hg compute warps (warp h owns head h0+h) + 1 producer warp.
 template <int HD>
-__global__ void __launch_bounds__(32 * (DEC_WARPS + 1)) attn_decode_kernel(AttnParams p, int hg, int n_hgroups) {
-  using C = DecCfg<HD>;
+__global__ void __launch_bounds__(32 * 17) attn_decode_kernel(AttnParams p, int hg, int n_hgroups) {
   constexpr int LPK = HD / 8;
   constexpr int KPI = 32 / LPK;
   constexpr int ITERS = PAGE / KPI;  // KPI <= 16 = PAGE for HD >= 16
@@ -439,13 +437,13 @@ __global__ void __launch_bounds__(32 * (DEC_WARPS + 1)) attn_decode_kernel(AttnP
   if (threadIdx.x == 0) {
     for (int s = 0; s < DSTAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, DEC_WARPS);
+      mbar_init(empty0 + 8 * s, hg);
     }
     mbar_fence_init();
   }
   __syncthreads();
 
-  if (warp == DEC_WARPS) {  // producer
+  if (warp == hg) {  // producer: two bulk copies (K block, V block of the group) per page
     if (lane == 0) {
       const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
       const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
@@ -462,104 +460,101 @@ __global__ void __launch_bounds__(32 * (DEC_WARPS + 1)) attn_decode_kernel(AttnP
     return;
   }
 
+  const int h = warp;  // this warp's head within the group
+  const bool active = h < nh;
   const int sub = lane % LPK, kin = lane / LPK;
-  float qv[C::HEADS_PER_WARP][8];
-  float m[C::HEADS_PER_WARP], l[C::HEADS_PER_WARP], acc[C::HEADS_PER_WARP][8];
+  float qv[8];
+  float m = -INFINITY, l = 0.f, acc[8];
 #pragma unroll
-  for (int j = 0; j < C::HEADS_PER_WARP; ++j) {
-    const int h = warp + j * DEC_WARPS;
-    m[j] = -INFINITY;
-    l[j] = 0.f;
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  if (active) {
+    const uint4 u =
+        *reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(grp.m0) * p.ldq + (h0 + h) * HD + sub * 8);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[j][e] = 0.f;
-    if (h < nh) {
-      const uint4 u =
-          *reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(grp.m0) * p.ldq + (h0 + h) * HD + sub * 8);
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h2[e]);
-        qv[j][2 * e] = f.x * p.scale_log2;
-        qv[j][2 * e + 1] = f.y * p.scale_log2;
-      }
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h2[e]);
+      qv[2 * e] = f.x * p.scale_log2;
+      qv[2 * e + 1] = f.y * p.scale_log2;
     }
   }
   for (int pg = 0; pg < npages; ++pg) {
     const int s = pg % DSTAGES;
     mbar_wait(full0 + 8 * s, (pg / DSTAGES) & 1);
-    const __nv_bfloat16* sK = reinterpret_cast<const __nv_bfloat16*>(gbase + s * STAGE);
-    const __nv_bfloat16* sV = reinterpret_cast<const __nv_bfloat16*>(gbase + s * STAGE + HALF);
+    if (active) {
+      const __nv_bfloat16* sK = reinterpret_cast<const __nv_bfloat16*>(gbase + s * STAGE) + static_cast<size_t>(h) * PAGE * HD;
+      const __nv_bfloat16* sV = reinterpret_cast<const __nv_bfloat16*>(gbase + s * STAGE + HALF) + static_cast<size_t>(h) * PAGE * HD;
+      uint4 kr[ITERS], vr[ITERS];
 #pragma unroll
-    for (int j = 0; j < C::HEADS_PER_WARP; ++j) {
-      const int h = warp + j * DEC_WARPS;
-      if (h >= nh) break;  // warp-uniform
+      for (int it = 0; it < ITERS; ++it) {
+        kr[it] = *reinterpret_cast<const uint4*>(sK + (it * KPI + kin) * HD + sub * 8);
+        vr[it] = *reinterpret_cast<const uint4*>(sV + (it * KPI + kin) * HD + sub * 8);
+      }
       float sc[ITERS];
       float cmax = -INFINITY;
 #pragma unroll
       for (int it = 0; it < ITERS; ++it) {
-        const int kr = it * KPI + kin;  // key row within the page
-        const uint4 u = *reinterpret_cast<const uint4*>(sK + (static_cast<size_t>(h) * PAGE + kr) * HD + sub * 8);
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&kr[it]);
         float dot = 0.f;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 f = __bfloat1622float2(h2[e]);
-          dot = fmaf(f.x, qv[j][2 * e], dot);
-          dot = fmaf(f.y, qv[j][2 * e + 1], dot);
+          dot = fmaf(f.x, qv[2 * e], dot);
+          dot = fmaf(f.y, qv[2 * e + 1], dot);
         }
+        sc[it] = dot;
+      }
 #pragma unroll
-        for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        const int key = pg * PAGE + kr;
+      for (int o = 1; o < LPK; o <<= 1)
+#pragma unroll
+        for (int it = 0; it < ITERS; ++it) sc[it] += __shfl_xor_sync(0xffffffffu, sc[it], o);
+#pragma unroll
+      for (int it = 0; it < ITERS; ++it) {
+        const int key = pg * PAGE + it * KPI + kin;
         const bool ok = key <= last && (!p.key_mask || p.key_mask[key]);
-        sc[it] = ok ? dot : -INFINITY;
+        sc[it] = ok ? sc[it] : -INFINITY;
         cmax = fmaxf(cmax, sc[it]);
       }
 #pragma unroll
       for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-      const float mnew = fmaxf(m[j], cmax);
-      const float alpha = mnew == -INFINITY ? 1.f : exp2f(m[j] - mnew);
+      const float mnew = fmaxf(m, cmax);
+      const float alpha = mnew == -INFINITY ? 1.f : exp2f(m - mnew);
       float psum = 0.f;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[j][e] *= alpha;
+      for (int e = 0; e < 8; ++e) acc[e] *= alpha;
 #pragma unroll
       for (int it = 0; it < ITERS; ++it) {
         const float pj = mnew == -INFINITY ? 0.f : exp2f(sc[it] - mnew);
         psum += pj;
-        const int kr = it * KPI + kin;
-        const uint4 u = *reinterpret_cast<const uint4*>(sV + (static_cast<size_t>(h) * PAGE + kr) * HD + sub * 8);
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&vr[it]);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 f = __bfloat1622float2(h2[e]);
-          acc[j][2 * e] = fmaf(pj, f.x, acc[j][2 * e]);
-          acc[j][2 * e + 1] = fmaf(pj, f.y, acc[j][2 * e + 1]);
+          acc[2 * e] = fmaf(pj, f.x, acc[2 * e]);
+          acc[2 * e + 1] = fmaf(pj, f.y, acc[2 * e + 1]);
         }
       }
 #pragma unroll
       for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
-      l[j] = l[j] * alpha + psum;
-      m[j] = mnew;
+      l = l * alpha + psum;
+      m = mnew;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * s);
   }
+  if (!active) return;
 #pragma unroll
-  for (int j = 0; j < C::HEADS_PER_WARP; ++j) {
-    const int h = warp + j * DEC_WARPS;
-    if (h >= nh) break;
+  for (int e = 0; e < 8; ++e)
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-#pragma unroll
-      for (int o = LPK; o < 32; o <<= 1) acc[j][e] += __shfl_xor_sync(0xffffffffu, acc[j][e], o);
-    if (kin == 0) {
-      const float inv = l[j] > 0.f ? 1.f / l[j] : 0.f;
-      uint4 w;
-      w.x = pack_bf16x2(acc[j][0] * inv, acc[j][1] * inv);
-      w.y = pack_bf16x2(acc[j][2] * inv, acc[j][3] * inv);
-      w.z = pack_bf16x2(acc[j][4] * inv, acc[j][5] * inv);
-      w.w = pack_bf16x2(acc[j][6] * inv, acc[j][7] * inv);
-      *reinterpret_cast<uint4*>(p.z + static_cast<size_t>(grp.m0) * p.ldz + (h0 + h) * HD + sub * 8) = w;
-    }
+    for (int o = LPK; o < 32; o <<= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+  if (kin == 0) {
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    uint4 w;
+    w.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+    w.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+    w.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+    w.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+    *reinterpret_cast<uint4*>(p.z + static_cast<size_t>(grp.m0) * p.ldz + (h0 + h) * HD + sub * 8) = w;
   }
 }
 
@@ -598,15 +593,54 @@ __global__ void __launch_bounds__(256)
   for (int r = nr; r < HEAD_ROWS; ++r)
     for (int i = threadIdx.x; i < d; i += blockDim.x) sy[r * d + i] = 0.f;
   __syncthreads();
-  for (int v = threadIdx.x; v < V; v += blockDim.x) {
-    float acc[HEAD_ROWS];
+  // logits = y * E^T: E^T streamed through a 2-stage cp.async ring of KC-row chunks (16-byte
+  // copies, the next chunk in flight during the FMAs); each thread owns one vocabulary column and
+  // accumulates all HEAD_ROWS rows in fp32, 4 k at a time.
+  constexpr int KC = 64;
+  float* set0 = slog + HEAD_ROWS * V;  // [2][KC][V]
+  const int chunk_floats = KC * V;     // multiple of 4 (KC = 64)
+  float acc[HEAD_ROWS];
 #pragma unroll
-    for (int r = 0; r < HEAD_ROWS; ++r) acc[r] = 0.f;
-    for (int k = 0; k < d; ++k) {
-      const float e = embed_t[static_cast<size_t>(k) * V + v];
-#pragma unroll
-      for (int r = 0; r < HEAD_ROWS; ++r) acc[r] = fmaf(sy[r * d + k], e, acc[r]);
+  for (int r = 0; r < HEAD_ROWS; ++r) acc[r] = 0.f;
+  const int v = threadIdx.x;
+  const int nchunks = (d + KC - 1) / KC;
+  auto issue = [&](int c) {
+    const int k0 = c * KC;
+    const int nf = min(KC, d - k0) * V;  // d % 4 == 0, V*kc*4 bytes 16-aligned when kc % 4 == 0
+    float* dst = set0 + (c & 1) * chunk_floats;
+    const float* src = embed_t + static_cast<size_t>(k0) * V;
+    for (int i = threadIdx.x * 4; i < nf; i += blockDim.x * 4) cp_async16(dst + i, src + i, true);
+    cp_async_commit();
+  };
+  issue(0);
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      issue(c + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    __syncthreads();
+    const int k0 = c * KC;
+    const int kc = min(KC, d - k0);
+    const float* set = set0 + (c & 1) * chunk_floats;
+    if (v < V) {
+      for (int k = 0; k < kc; k += 4) {
+        const float e0 = set[k * V + v], e1 = set[(k + 1) * V + v], e2 = set[(k + 2) * V + v],
+                    e3 = set[(k + 3) * V + v];
+#pragma unroll
+        for (int r = 0; r < HEAD_ROWS; ++r) {
+          const float4 y4 = *reinterpret_cast<const float4*>(sy + r * d + k0 + k);
+          acc[r] = fmaf(y4.x, e0, acc[r]);
+          acc[r] = fmaf(y4.y, e1, acc[r]);
+          acc[r] = fmaf(y4.z, e2, acc[r]);
+          acc[r] = fmaf(y4.w, e3, acc[r]);
+        }
+      }
+    }
+    __syncthreads();  // stage (c & 1) is refilled by the next iteration's prefetch
+  }
+  if (v < V) {
 #pragma unroll
     for (int r = 0; r < HEAD_ROWS; ++r) slog[r * V + v] = acc[r];
   }
@@ -855,7 +889,7 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
       const int ngrp = (decode.heads + DC::HG_MAX - 1) / DC::HG_MAX;                                \
       const int hg = (decode.heads + ngrp - 1) / ngrp;                                              \
       const size_t sm = 256 + static_cast<size_t>(DSTAGES) * 2 * hg * PAGE * HD * 2;                 \
-      attn_decode_kernel<HD><<<decode.n_groups * ngrp, 32 * (DEC_WARPS + 1), sm, st>>>(             \
+      attn_decode_kernel<HD><<<decode.n_groups * ngrp, 32 * (hg + 1), sm, st>>>(                    \
           decode, hg, ngrp);                                                                        \
     }                                                                                               \
   } while (0)
@@ -874,7 +908,9 @@ void launch_head(const float* x, int d, const int* rows, int n_rows, const float
                  const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
                  float* logits_out, cudaStream_t st) {
   if (n_rows <= 0) return;
-  const size_t smem = sizeof(float) * HEAD_ROWS * (d + V);
+  if (V > 256) throw Unsupported("head: vocabulary larger than the CTA");
+  if (d % 4 != 0) throw Unsupported("head: d_model must be a multiple of 4");
+  const size_t smem = sizeof(float) * (HEAD_ROWS * (d + V) + 2 * 64 * V) + 16;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     CUDA_OK(cudaFuncSetAttribute(head_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
