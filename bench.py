@@ -345,7 +345,7 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     # dominant kernel class by device time
     dom = max(kt.items(), key=lambda kv: kv[1][0])
     name, (kms, work, cnt) = dom
-    hbm_classes = {"attn_decode", "ln", "embed_ln", "head"}
+    hbm_classes = {"attn_decode", "ln", "embed_ln", "head", "quant"}
     if name in hbm_classes:
         achieved = work / (kms / 1000.0) / 1e9
         peak = peaks["hbm_gbs"]

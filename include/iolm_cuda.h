@@ -120,10 +120,11 @@ int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* out);
 
 /* Per kernel-class device time of the last call, recorded with CUDA events on the engine stream
  * when opts.kernel_timing = 1. Classes (index): 0 embed+LN1, 1 QKV GEMM, 2 prefill attention,
- * 3 decode attention, 4 Wo GEMM, 5 LN, 6 W_in GEMM, 7 W_out GEMM, 8 head+argmax.
+ * 3 decode attention, 4 Wo GEMM, 5 LN, 6 W_in GEMM, 7 W_out GEMM, 8 head+argmax,
+ * 9 int8 row quantization (W8A8).
  * ms[i]: summed launch durations; work[i]: algorithmic FLOPs (GEMMs, attention) or bytes (LN,
- * head, embed) of those launches; launches[i]: launch count. n: capacity of the arrays (>= 9). */
-#define IOLM_KCLASSES 9
+ * head, embed) of those launches; launches[i]: launch count. n: capacity of the arrays (>= 10). */
+#define IOLM_KCLASSES 10
 int iolm_cuda_kernel_times(const iolm_cuda_ctx* ctx, double* ms, double* work, int64_t* launches, int32_t n);
 
 /* Thread-local message for the last non-OK status. */

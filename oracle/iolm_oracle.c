@@ -472,20 +472,22 @@ int orc_decode_rows(const orc_model* m, const int* ids, const int64_t* offsets, 
 }
 
 /* ------------------------------------------------------------------ W8A8 restatement */
-/* Per-token symmetric int8 quantization of activation rows, the reference's RTN rule applied to
- * rows instead of weight channels (quant.cpp:23-38): scale = amax/127 (amax == 0 -> 1), code =
- * clamp(nearbyint(x / scale), -127, 127) with x / scale an IEEE fp32 division (the weight rule
- * divides in double; activations are quantized on the GPU every step, so the rule pinned here uses
- * the correctly rounded fp32 quotient - exact half-integers still round to even). */
+/* Per-token symmetric int8 quantization of activation rows, modelled on the reference's RTN rule
+ * (quant.cpp:23-38) applied to rows: scale = amax/127 (amax == 0 -> 1); inv = 1/scale (fp32);
+ * code = clamp(nearbyint(x * inv), -127, 127) with the fp32 product (round-to-nearest-even).
+ * The reference has no activation quantization; this is the rule the GPU W8A8 path
+ * implements (kernels.cu quant_one), pinned here bit-for-bit. */
 void orc_quant_rows_s8(const float* x, int n, int d, int8_t* codes, float* scales) {
   for (int i = 0; i < n; ++i) {
     const float* r = x + (size_t)i * d;
     float amax = 0.0f;
     for (int k = 0; k < d; ++k) amax = fmaxf(amax, fabsf(r[k]));
     const float s = amax == 0.0f ? 1.0f : amax / 127.0f;
+    const float inv = 1.0f / s;
     scales[i] = s;
     for (int k = 0; k < d; ++k) {
-      float q = nearbyintf(r[k] / s);
+      const float y = r[k] * inv;
+      float q = nearbyintf(y);
       if (q > 127.0f) q = 127.0f;
       if (q < -127.0f) q = -127.0f;
       codes[(size_t)i * d + k] = (int8_t)q;

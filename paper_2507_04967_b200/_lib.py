@@ -24,7 +24,7 @@ IOLM_E_UNKNOWN_ENCODING = 8
 
 VOCAB, PAD, BOS, EOS = 131, 128, 129, 130
 KCLASSES = ["embed_ln", "gemm_qkv", "attn_prefill", "attn_decode", "gemm_o", "ln", "gemm_in",
-            "gemm_out", "head"]
+            "gemm_out", "head", "quant"]
 
 
 class Opts(C.Structure):

@@ -634,7 +634,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     }
     // x += z * Wo^T
     if (i8_o) {
-      timed(5, dT * ly.kh * 3.0, [&] { launch_quant_rows(z_.p, kh_max_, T, ly.kh, z8_.p, kh_max_, zs_.p, stream_); });
+      timed(9, dT * ly.kh * 3.0, [&] { launch_quant_rows(z_.p, kh_max_, T, ly.kh, z8_.p, kh_max_, zs_.p, stream_); });
       ++stats_.kernel_launches;
     }
     GemmEpi eo;
@@ -663,7 +663,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     });
     // x += g * Wout^T
     if (i8_out) {
-      timed(5, dT * ly.f * 3.0, [&] { launch_quant_rows(g_.p, f_ld_max_, T, ly.f, g8_.p, f_ld_max_, gs_.p, stream_); });
+      timed(9, dT * ly.f * 3.0, [&] { launch_quant_rows(g_.p, f_ld_max_, T, ly.f, g8_.p, f_ld_max_, gs_.p, stream_); });
       ++stats_.kernel_launches;
     }
     GemmEpi eo2 = eo;

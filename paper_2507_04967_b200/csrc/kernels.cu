@@ -6,6 +6,7 @@
 //   head_argmax       final LN + tied head (fp32) + greedy argmax           (runtime.cpp:202-215,
 //                                                                            numerics.cpp:190-197)
 //   lcp / decode helpers
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -18,14 +19,15 @@ namespace iolmk {
 constexpr int PAGE = 16;
 
 // ------------------------------------------------------------------ per-token int8 (W8A8)
-// Activation quantization rule (the reference has none; pinned to its weight RTN
-// rule, quant.cpp:23-38, applied per token): s = amax/127 (amax == 0 -> 1),
-// q = clamp(rint(x / s), -127, 127) with x / s the IEEE round-to-nearest fp32 division and rint
-// ties-to-even - exactly oracle/iolm_oracle.c orc_quant_rows_s8 ("W8A8").
-__device__ __forceinline__ int8_t quant_one(float x, float s) {
-  float q = rintf(__fdiv_rn(x, s));
-  q = fminf(127.f, fmaxf(-127.f, q));
-  return static_cast<int8_t>(static_cast<int>(q));
+// Activation quantization rule (the reference has none; modelled on its RTN weight
+// rule, quant.cpp:23-38, applied per token): s = amax/127 (amax == 0 -> 1), inv = 1/s (IEEE fp32),
+// q = clamp(rint(x * inv)) with the fp32 product rounded to nearest-even - one FMUL + one
+// cvt.rni.sat.s8.f32 per element. |x * inv| <= 127 * (1 + 2^-22), so the saturation never clips a
+// code. Restated bit-for-bit in oracle/iolm_oracle.c orc_quant_rows_s8.
+__device__ __forceinline__ int8_t quant_one(float x, float /*s*/, float inv_s) {
+  int r;
+  asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(r) : "f"(x * inv_s));
+  return static_cast<int8_t>(r);
 }
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -85,16 +87,17 @@ __device__ __forceinline__ void ln_row_warp(const float* __restrict__ xr, int d,
     amax = warp_max(amax);
     const float s = amax == 0.f ? 1.f : amax / 127.0f;
     const float sd = s;
+    const float inv_sd = 1.0f / s;
     if (lane == 0) *qscale = s;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
       const int idx = lane + 32 * i;
       if (idx < nv) {
         char4 c;
-        c.x = quant_one(v[i].x, sd);
-        c.y = quant_one(v[i].y, sd);
-        c.z = quant_one(v[i].z, sd);
-        c.w = quant_one(v[i].w, sd);
+        c.x = quant_one(v[i].x, sd, inv_sd);
+        c.y = quant_one(v[i].y, sd, inv_sd);
+        c.z = quant_one(v[i].z, sd, inv_sd);
+        c.w = quant_one(v[i].w, sd, inv_sd);
         reinterpret_cast<char4*>(q8)[idx] = c;
       }
     }
@@ -129,8 +132,66 @@ __global__ void __launch_bounds__(256) ln_kernel(const float* __restrict__ x, in
                       threadIdx.x & 31);
 }
 
+// Bandwidth-oriented LayerNorm: persistent CTAs, a producer warp streams groups of 8 consecutive x
+// rows (one contiguous block) with cp.async.bulk into an LN_STAGES-deep smem ring; each of the 8
+// compute warps normalises one row of the group from smem (same arithmetic as ln_row_warp).
+constexpr int LN_STAGES = 2;
+template <int MAXV, bool Q8>
+__global__ void __launch_bounds__(288) ln_bulk_kernel(const float* __restrict__ x, int M, int d,
+                                                      const float* __restrict__ g, const float* __restrict__ b,
+                                                      __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
+                                                      float* __restrict__ qscale) {
+  extern __shared__ __align__(128) uint8_t lsm[];
+  const uint32_t sbase = (smem_u32(lsm) + 127u) & ~127u;
+  float* ring = reinterpret_cast<float*>(lsm + (sbase - smem_u32(lsm)));
+  const int group_floats = 8 * d;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + LN_STAGES * group_floats);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + LN_STAGES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ngroups = (M + 7) / 8;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < LN_STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 8) {
+    if (lane == 0) {
+      int it = 0;
+      for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x, ++it) {
+        const int s = it % LN_STAGES;
+        mbar_wait(empty0 + 8 * s, ((it / LN_STAGES) & 1) ^ 1u);
+        const int rows = min(8, M - gi * 8);
+        const uint32_t bytes = static_cast<uint32_t>(rows) * d * 4;
+        mbar_expect_tx(full0 + 8 * s, bytes);
+        bulk_load(smem_u32(ring + s * group_floats), x + static_cast<size_t>(gi) * 8 * d, bytes, full0 + 8 * s);
+      }
+    }
+    return;
+  }
+  int it = 0;
+  for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x, ++it) {
+    const int s = it % LN_STAGES;
+    mbar_wait(full0 + 8 * s, (it / LN_STAGES) & 1);
+    const int row = gi * 8 + warp;
+    if (row < M) {
+      const float* xr = ring + s * group_floats + warp * d;
+      if constexpr (Q8)
+        ln_row_warp<MAXV, true>(xr, d, g, b, nullptr, lane, q8 + static_cast<size_t>(row) * ldh, qscale + row);
+      else
+        ln_row_warp<MAXV>(xr, d, g, b, h + static_cast<size_t>(row) * ldh, lane);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * s);
+  }
+}
+
 // Per-token int8 quantization of a bf16 activation matrix (attention output z, GELU output g).
-// One warp per row; two passes over the row (amax, then codes), the row stays L1/L2 resident.
+// One warp per row. CH > 0: the row (cols = 256*CH, multiple of 8) stays in registers between the
+// amax and the code pass; CH == 0: generic two-pass version (any width).
+template <int CH>
 __global__ void __launch_bounds__(256) quant_rows_kernel(const __nv_bfloat16* __restrict__ src, int lds, int M,
                                                          int cols, int8_t* __restrict__ dst, int ldd,
                                                          float* __restrict__ scale) {
@@ -138,36 +199,71 @@ __global__ void __launch_bounds__(256) quant_rows_kernel(const __nv_bfloat16* __
   if (row >= M) return;
   const int lane = threadIdx.x & 31;
   const __nv_bfloat16* r = src + static_cast<size_t>(row) * lds;
-  const int cols8 = cols & ~7;
-  float amax = 0.f;
-  for (int c = cols8 + lane; c < cols; c += 32) amax = fmaxf(amax, fabsf(__bfloat162float(r[c])));
-  for (int c = lane * 8; c < cols8; c += 256) {
-    const uint4 u = *reinterpret_cast<const uint4*>(r + c);
-    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __bfloat1622float2(h2[j]);
-      amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
-    }
-  }
-  amax = warp_max(amax);
-  const float s = amax == 0.f ? 1.f : amax / 127.0f;
-  const float sd = s;
-  if (lane == 0) scale[row] = s;
   int8_t* o = dst + static_cast<size_t>(row) * ldd;
-  for (int c = cols8 + lane; c < cols; c += 32) o[c] = quant_one(__bfloat162float(r[c]), sd);
-  for (int c = lane * 8; c < cols8; c += 256) {
-    const uint4 u = *reinterpret_cast<const uint4*>(r + c);
-    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-    uint2 w;
-    int8_t* wb = reinterpret_cast<int8_t*>(&w);
+  if constexpr (CH > 0) {
+    uint4 u[CH];
+    float amax = 0.f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __bfloat1622float2(h2[j]);
-      wb[2 * j] = quant_one(f.x, sd);
-      wb[2 * j + 1] = quant_one(f.y, sd);
+    for (int i = 0; i < CH; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      u[i] = c < cols ? *reinterpret_cast<const uint4*>(r + c) : make_uint4(0, 0, 0, 0);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h2[j]);
+        amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+      }
     }
-    *reinterpret_cast<uint2*>(o + c) = w;
+    amax = warp_max(amax);
+    const float sd = amax == 0.f ? 1.f : amax / 127.0f;
+    const float inv_sd = 1.0f / sd;
+    if (lane == 0) scale[row] = sd;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      if (c >= cols) break;
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+      uint2 w;
+      int8_t* wb = reinterpret_cast<int8_t*>(&w);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h2[j]);
+        wb[2 * j] = quant_one(f.x, sd, inv_sd);
+        wb[2 * j + 1] = quant_one(f.y, sd, inv_sd);
+      }
+      *reinterpret_cast<uint2*>(o + c) = w;
+    }
+  } else {
+    const int cols8 = cols & ~7;
+    float amax = 0.f;
+    for (int c = cols8 + lane; c < cols; c += 32) amax = fmaxf(amax, fabsf(__bfloat162float(r[c])));
+    for (int c = lane * 8; c < cols8; c += 256) {
+      const uint4 u = *reinterpret_cast<const uint4*>(r + c);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h2[j]);
+        amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+      }
+    }
+    amax = warp_max(amax);
+    const float sd = amax == 0.f ? 1.f : amax / 127.0f;
+    const float inv_sd = 1.0f / sd;
+    if (lane == 0) scale[row] = sd;
+    for (int c = cols8 + lane; c < cols; c += 32) o[c] = quant_one(__bfloat162float(r[c]), sd, inv_sd);
+    for (int c = lane * 8; c < cols8; c += 256) {
+      const uint4 u = *reinterpret_cast<const uint4*>(r + c);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+      uint2 w;
+      int8_t* wb = reinterpret_cast<int8_t*>(&w);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h2[j]);
+        wb[2 * j] = quant_one(f.x, sd, inv_sd);
+        wb[2 * j + 1] = quant_one(f.y, sd, inv_sd);
+      }
+      *reinterpret_cast<uint2*>(o + c) = w;
+    }
   }
 }
 
@@ -202,6 +298,11 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------------ attention (prefill, mma.sync)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -316,17 +417,31 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
         }
       }
       float mx[2] = {-INFINITY, -INFINITY};
+      // blocks entirely below the warp's first query need no causal mask (warp-uniform test)
+      const bool full_block = !p.key_mask && kb * KB + KB - 1 <= grp.pos0 + warp * 16;
+      if (full_block) {
 #pragma unroll
-      for (int nt = 0; nt < KB / 8; ++nt) {
+        for (int nt = 0; nt < KB / 8; ++nt) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int key = kb * KB + nt * 8 + 2 * tq + (e & 1);
-          const int qp = e < 2 ? qpos0 : qpos1;
-          bool ok = key <= qp;
-          if (p.key_mask) ok = ok && p.key_mask[key];
-          const float v = ok ? s[nt][e] * p.scale_log2 : -INFINITY;
-          s[nt][e] = v;
-          mx[e >> 1] = fmaxf(mx[e >> 1], v);
+          for (int e = 0; e < 4; ++e) {
+            const float v = s[nt][e] * p.scale_log2;
+            s[nt][e] = v;
+            mx[e >> 1] = fmaxf(mx[e >> 1], v);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < KB / 8; ++nt) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int key = kb * KB + nt * 8 + 2 * tq + (e & 1);
+            const int qp = e < 2 ? qpos0 : qpos1;
+            bool ok = key <= qp;
+            if (p.key_mask) ok = ok && p.key_mask[key];
+            const float v = ok ? s[nt][e] * p.scale_log2 : -INFINITY;
+            s[nt][e] = v;
+            mx[e >> 1] = fmaxf(mx[e >> 1], v);
+          }
         }
       }
       float alpha[2];
@@ -339,12 +454,14 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
         m_i[r] = mnew;
         l_i[r] *= alpha[r];
       }
+      // rows with no visible key yet (m == -inf) contribute exact zeros: ex2(-inf) = +0
+      const float msub0 = m_i[0] == -INFINITY ? 0.f : m_i[0];
+      const float msub1 = m_i[1] == -INFINITY ? 0.f : m_i[1];
 #pragma unroll
       for (int nt = 0; nt < KB / 8; ++nt) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float mm = m_i[e >> 1];
-          const float pv = mm == -INFINITY ? 0.f : exp2f(s[nt][e] - mm);
+          const float pv = ex2_approx(s[nt][e] - (e < 2 ? msub0 : msub1));
           s[nt][e] = pv;
           l_i[e >> 1] += pv;
         }
@@ -798,8 +915,39 @@ static inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigne
 void launch_ln(const float* x, int M, int d, const float* g, const float* b, __nv_bfloat16* h, int ldh,
                cudaStream_t st, int8_t* q8, float* qscale) {
   if (M <= 0) return;
-  const unsigned grid = blocks_for(M, 8);
   const int nv = (d / 4 + 31) / 32;
+  const size_t bsmem = 256 + static_cast<size_t>(LN_STAGES) * 8 * d * 4;
+  // the bulk-streamed variant pays off for the int8 (W8A8) output; the bf16 output keeps the
+  // register-resident one-warp-per-row kernel (measured faster at d = 1280)
+  if (q8 && d % 128 == 0 && (nv == 10 || nv == 16 || nv == 8 || nv == 4) && bsmem <= 200 * 1024) {
+    static int sms = 0;
+    if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int per_sm = bsmem <= 100 * 1024 ? 2 : 1;
+    const int grid_b = std::min<int>((M + 7) / 8, sms * per_sm);
+#define LNB(V)                                                                                          \
+  do {                                                                                                  \
+    static bool cfg = false;                                                                            \
+    if (!cfg) {                                                                                         \
+      CUDA_OK(cudaFuncSetAttribute(ln_bulk_kernel<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   200 * 1024));                                                        \
+      CUDA_OK(cudaFuncSetAttribute(ln_bulk_kernel<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   200 * 1024));                                                        \
+      cfg = true;                                                                                       \
+    }                                                                                                   \
+    if (q8) ln_bulk_kernel<V, true><<<grid_b, 288, bsmem, st>>>(x, M, d, g, b, h, ldh, q8, qscale);      \
+    else ln_bulk_kernel<V, false><<<grid_b, 288, bsmem, st>>>(x, M, d, g, b, h, ldh, q8, qscale);        \
+  } while (0)
+    switch (nv) {
+      case 4: LNB(4); break;
+      case 8: LNB(8); break;
+      case 10: LNB(10); break;
+      default: LNB(16); break;
+    }
+#undef LNB
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
+  const unsigned grid = blocks_for(M, 8);
 #define LNK(V)                                                                     \
   do {                                                                             \
     if (q8) ln_kernel<V, true><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale); \
@@ -829,7 +977,15 @@ void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_
                        cudaStream_t st) {
   if (M <= 0) return;
   if (lds % 8 != 0 || ldd % 8 != 0) throw Unsupported("quant_rows: leading dimensions must be multiples of 8");
-  quant_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  const unsigned grid = blocks_for(M, 8);
+  const int ch = (cols + 255) / 256;
+  if (cols % 8 != 0) quant_rows_kernel<0><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  else if (ch <= 4) quant_rows_kernel<4><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  else if (ch <= 8) quant_rows_kernel<8><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  else if (ch <= 12) quant_rows_kernel<12><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  else if (ch <= 16) quant_rows_kernel<16><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  else if (ch <= 20) quant_rows_kernel<20><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  else quant_rows_kernel<0><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
   CUDA_OK(cudaGetLastError());
 }
 

@@ -110,7 +110,8 @@ def test_c1_generator_and_forward_golden():
 
 
 def test_rtn_activation_quantizer_kats():
-    """SPEC.md quantize_rtn examples (round-half-even, zero row -> scale 1), applied per token."""
+    """SPEC.md quantize_rtn examples (round-half-even, zero row -> scale 1), applied per token with
+    the pinned W8A8 form q = rint(x * (1/s))."""
     codes, scales = O.quant_rows_s8(np.array([[0, 0, 0], [1.0, -2.0, 0.5]], np.float32))
     assert scales[0] == 1.0 and codes[0].tolist() == [0, 0, 0]
     assert scales[1] == np.float32(2.0) / np.float32(127.0)
