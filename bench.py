@@ -236,8 +236,9 @@ def run_reference_arm(args, cfg: dict, world: int, rank: int) -> None:
         bundle = synth.toy_bundle(*cfg["dims"], seed=42, quant=cfg["quant"], heads=cfg.get("heads"),
                                   ffn=cfg.get("ffn"))
     n = cpu_sample_rows(args.config, cores)
-    for w in range(args.warmup):  # untimed; one row each keeps the run bounded
-        cpu_reference_sample(bundle, cfg, 1, 10_000_000 + w, 1)
+    # untimed warm-up: W rows of the same workload, one per thread, run concurrently
+    if args.warmup > 0:
+        cpu_reference_sample(bundle, cfg, args.warmup, 10_000_000, args.warmup)
     rates, kinds, secs = [], [], 0.0
     for k in range(args.steps):
         r, kind, dt, _ = cpu_reference_sample(bundle, cfg, n, step_rows(k, 1, 0, n), cores)
