@@ -1029,6 +1029,8 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
     if (!cfg) {                                                                                     \
       CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD>,                                         \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));             \
+      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD>,                                         \
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));           \
       cfg = true;                                                                                   \
     }                                                                                               \
     if (prefill.n_groups > 0)                                                                       \
@@ -1040,6 +1042,8 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
         CUDA_OK(cudaFuncSetAttribute(attn_decode_kernel<HD>,                                        \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,                   \
                                      static_cast<int>(DC::SMEM_MAX)));                              \
+        CUDA_OK(cudaFuncSetAttribute(attn_decode_kernel<HD>,                                        \
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));         \
         dcfg = true;                                                                                \
       }                                                                                             \
       const int ngrp = (decode.heads + DC::HG_MAX - 1) / DC::HG_MAX;                                \
