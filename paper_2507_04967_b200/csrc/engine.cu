@@ -129,6 +129,7 @@ struct Layer {
   CUtensorMap tm_z, tm_g;    // bf16 A operands with this layer's K extent
   CUtensorMap tm_z8, tm_g8;  // int8 A operands (W8A8)
   DevArray<__nv_bfloat16> kv;  // paged pool [pages][K|V][heads][PAGE][hd]
+  CUtensorMap tm_kv;             // the pool as rows of hd (prefill attention TMA)
 };
 
 // 2-SM 256x256 tiles once both M and N fill at least one pair tile. IOLM_GEMM_TILES=single|pair
@@ -249,7 +250,7 @@ class Engine {
   DevArray<float> tok_embed_, tok_embed_t_, pos_embed_, lnf_g_, lnf_b_;
   DevArray<float> x_;
   DevArray<__nv_bfloat16> h_, q_, z_, g_;
-  CUtensorMap tm_h_;
+  CUtensorMap tm_h_, tm_q_;
   DevArray<int8_t> h8_, z8_, g8_;  // W8A8 operands + per-token scales
   DevArray<float> hs_, zs_, gs_;
   CUtensorMap tm_h8_;
@@ -401,6 +402,7 @@ void Engine::alloc_runtime() {
   CUDA_OK(cudaMemset(z_.p, 0, T * kh_max_ * sizeof(__nv_bfloat16)));
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   tm_h_ = make_kmajor_map(h_.p, BF, 2, d_, T, 2ull * d_, 128);
+  tm_q_ = make_rows_map_bf16(q_.p, kh_max_, T, 2ull * kh_max_, std::min(hd_, 64), 64);
   for (auto& ly : layers_) {
     ly->tm_z = make_kmajor_map(z_.p, BF, 2, ly->kh, T, 2ull * kh_max_, 128);
     ly->tm_g = make_kmajor_map(g_.p, BF, 2, ly->f, T, 2ull * f_ld_max_, 128);
@@ -449,6 +451,8 @@ void Engine::alloc_runtime() {
     const size_t elems = pages * 2 * ly->heads * PAGE * hd_;
     ly->kv.alloc(elems);
     CUDA_OK(cudaMemset(ly->kv.p, 0, elems * sizeof(__nv_bfloat16)));
+    ly->tm_kv = make_rows_map_bf16(ly->kv.p, hd_, pages * 2 * ly->heads * PAGE, 2ull * hd_,
+                                   std::min(hd_, 64), PAGE);
   }
   page_table_.alloc(static_cast<size_t>(max_slots_ + 1) * pps_);
   d_last_tok_.alloc(max_slots_ + 1);
@@ -608,6 +612,8 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       gemm(iolmk::EPI_QKV, i8_qkv, i8_qkv ? tm_h8_ : tm_h_, ly.qkv.tm, T, 3 * ly.kh, d_, ep);
     });
     AttnParams ap{};
+    ap.q_map = tm_q_;
+    ap.kv_map = ly.tm_kv;
     ap.q = q_.p;
     ap.ldq = kh_max_;
     ap.z = z_.p;

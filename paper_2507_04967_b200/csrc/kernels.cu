@@ -332,136 +332,188 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// 64 queries of one group x one head per CTA (4 warps x 16 query rows). Key blocks of 64 positions
-// aligned to absolute position 0, so a query's arithmetic depends only on its own position and the
-// K/V values (never on how the step was composed): batch-invariant. K/V blocks stream through a
-// two-stage cp.async ring (zero-filled past the last key).
+// 64 queries of one group x one head per CTA (4 warps x 16 query rows). Keys stream in blocks of
+// PF_KB = 32 absolute positions (two KV pages): thread 0 issues one TMA per page slab (the pool is a
+// 2D tensor of HD-wide rows, swizzled like the GEMM operands) into a PF_ST-deep ring with mbarrier
+// completion, so no thread computes a load address and no warp waits on another at a CTA barrier.
+// Work is skipped per 16-key chunk (one page) beyond a warp's last query, and the causal mask is
+// applied only in chunks that straddle the diagonal. A query's arithmetic depends only on its own
+// position and the K/V values (chunks are aligned to absolute positions): batch-invariant.
+constexpr int PF_KB = 32;
 template <int HD>
-__global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
-  constexpr int LD = HD + 8;
-  constexpr int KB = 64;
-  extern __shared__ __align__(16) uint8_t attn_smem[];
-  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(attn_smem);
-  __nv_bfloat16* sKV = sQ + 64 * LD;  // [stage][K|V][KB][LD]
+struct PfCfg {
+  static constexpr int CB = HD < 64 ? HD : 64;   // elements per TMA box row (<= 128 B)
+  static constexpr int CBB = CB * 2;             // bytes per box row = swizzle span
+  static constexpr int NCB = HD / CB;            // boxes per HD-wide row
+  static constexpr uint32_t SWM = CBB == 128 ? 7 : (CBB == 64 ? 3 : 1);
+  static constexpr int ST = HD >= 128 ? 3 : 4;   // ring depth (blocks in flight)
+  static constexpr int MINB = HD >= 128 ? 3 : 5; // resident CTAs per SM (smem-limited)
+  static constexpr uint32_t Q_BYTES = 64 * HD * 2;
+  static constexpr uint32_t KT_BYTES = PF_KB * HD * 2;  // one K (or V) tile
+  static constexpr uint32_t STAGE_BYTES = 2 * KT_BYTES;
+  static constexpr size_t SMEM = 1024 + Q_BYTES + ST * STAGE_BYTES + 64;
+};
+
+// Byte offset of element (r, c) in a [R x HD] bf16 tile stored as NCB swizzled [R x CB] boxes.
+template <int HD>
+__device__ __forceinline__ uint32_t pf_off(int R, int r, int c) {
+  using C = PfCfg<HD>;
+  const uint32_t b = static_cast<uint32_t>(c / C::CB) * R * C::CBB + r * C::CBB + (c % C::CB) * 2;
+  return b ^ (((b >> 7) & C::SWM) << 4);
+}
+
+template <int HD, bool MASK>
+__global__ void __launch_bounds__(128, PfCfg<HD>::MINB) attn_prefill_kernel(const __grid_constant__ AttnParams p) {
+  using C = PfCfg<HD>;
+  constexpr int ST = C::ST;
+  extern __shared__ __align__(1024) uint8_t pf_smem[];
+  const uint32_t sraw = smem_u32(pf_smem);
+  const uint32_t sQ = (sraw + 1023u) & ~1023u;
+  uint8_t* gQ = pf_smem + (sQ - sraw);
+  const uint32_t sKV = sQ + C::Q_BYTES;
+  const uint32_t bars = sKV + ST * C::STAGE_BYTES;  // full[ST], empty[ST], q
   const AttnGroup grp = p.groups[blockIdx.x];
   const int head = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int last_key = grp.pos0 + grp.nq - 1;
-  const size_t head_off = static_cast<size_t>(head) * PAGE * HD;
-  const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
-  const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
+  const int nblocks = last_key / PF_KB + 1;
   const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
 
-  auto issue_block = [&](int kb, int stage) {
-    __nv_bfloat16* sK = sKV + static_cast<size_t>(stage) * 2 * KB * LD;
-    __nv_bfloat16* sV = sK + KB * LD;
-    for (int idx = tid; idx < KB * (HD / 8); idx += 128) {
-      const int r = idx / (HD / 8), c = (idx % (HD / 8)) * 8;
-      const int pos = kb * KB + r;
-      const bool ok = pos <= last_key;
-      const __nv_bfloat16* base =
-          ok ? p.kv + static_cast<size_t>(pt[pos / PAGE]) * page_stride + head_off + (pos % PAGE) * HD + c : p.kv;
-      cp_async16(sK + r * LD + c, base, ok);
-      cp_async16(sV + r * LD + c, ok ? base + v_off : p.kv, ok);
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(bars + 8 * s, 1);
+      mbar_init(bars + 8 * (ST + s), 4);
+    }
+    mbar_init(bars + 16 * ST, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  // warp 0 is also the producer: lanes hold 32 page ids at a time, lane 0 issues the TMAs
+  int pid_base = -(1 << 20), pid = 0;
+  auto issue_block = [&](int kb) {
+    const uint32_t full = bars + 8 * (kb % ST);
+    const uint32_t dst = sKV + (kb % ST) * C::STAGE_BYTES;
+    const int pg0 = kb * (PF_KB / PAGE);
+    const int npg = min(PF_KB / PAGE, last_key / PAGE - pg0 + 1);
+    if (pg0 + npg > pid_base + 32 || pg0 < pid_base) {
+      pid_base = pg0;
+      pid = pid_base + lane < p.max_pages ? __ldg(pt + pid_base + lane) : 0;
+    }
+    if (lane == 0) mbar_expect_tx(full, npg * 2 * PAGE * HD * 2);
+    for (int j = 0; j < npg; ++j) {
+      const int page = __shfl_sync(0xffffffffu, pid, pg0 + j - pid_base);
+      if (lane == 0) {
+        const int rk = ((page * 2 + 0) * p.heads + head) * PAGE;
+        const int rv = rk + p.heads * PAGE;
+#pragma unroll
+        for (int cb = 0; cb < C::NCB; ++cb) {
+          const uint32_t o = cb * PF_KB * C::CBB + j * PAGE * C::CBB;
+          tma_load_2d(dst + o, &p.kv_map, full, cb * C::CB, rk);
+          tma_load_2d(dst + C::KT_BYTES + o, &p.kv_map, full, cb * C::CB, rv);
+        }
+      }
     }
   };
-  for (int idx = tid; idx < 64 * (HD / 8); idx += 128) {
-    const int r = idx / (HD / 8), c = (idx % (HD / 8)) * 8;
-    const bool ok = r < grp.nq;
-    cp_async16(sQ + r * LD + c, ok ? p.q + static_cast<size_t>(grp.m0 + r) * p.ldq + head * HD + c : p.q, ok);
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&p.kv_map);
+      mbar_expect_tx(bars + 16 * ST, C::Q_BYTES);
+#pragma unroll
+      for (int cb = 0; cb < C::NCB; ++cb)
+        tma_load_2d(sQ + cb * 64 * C::CBB, &p.q_map, bars + 16 * ST, head * HD + cb * C::CB, grp.m0);
+    }
+    for (int kb = 0; kb < min(ST, nblocks); ++kb) issue_block(kb);
   }
-  issue_block(0, 0);
-  cp_async_commit();
 
-  const int qpos0 = grp.pos0 + warp * 16 + gq;  // rows gq and gq+8 of this warp
-  const int qpos1 = qpos0 + 8;
-  const int warp_max_pos = grp.pos0 + min(grp.nq - 1, warp * 16 + 15);
+  const int qrow0 = warp * 16 + gq;  // this thread's rows qrow0 and qrow0 + 8
+  const int qpos0 = grp.pos0 + qrow0, qpos1 = qpos0 + 8;
   const bool warp_active = warp * 16 < grp.nq;
+  const int warp_min_pos = grp.pos0 + warp * 16;
+  const int warp_max_pos = grp.pos0 + min(grp.nq - 1, warp * 16 + 15);
   float m_i[2] = {-INFINITY, -INFINITY};
   float l_i[2] = {0.f, 0.f};
   float o[HD / 8][4];
 #pragma unroll
   for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   uint32_t qf[HD / 16][4];
+  if (warp_active) {
+    mbar_wait(bars + 16 * ST, 0);
+#pragma unroll
+    for (int kc = 0; kc < HD / 16; ++kc)
+      ldsm_x4(qf[kc], gQ + pf_off<HD>(64, warp * 16 + (lane & 15), kc * 16 + (lane >> 4) * 8));
+  }
 
-  const int nblocks = last_key / KB + 1;
   for (int kb = 0; kb < nblocks; ++kb) {
-    if (kb + 1 < nblocks) {
-      issue_block(kb + 1, (kb + 1) & 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    if (warp == 0 && kb >= 1 && kb - 1 + ST < nblocks) {
+      // refill the stage block kb-1 used once every warp has released it
+      mbar_wait(bars + 8 * (ST + (kb - 1) % ST), ((kb - 1) / ST) & 1);
+      issue_block(kb - 1 + ST);
     }
-    __syncthreads();
-    if (kb == 0) {
+    mbar_wait(bars + 8 * (kb % ST), (kb / ST) & 1);
+    const int key0 = kb * PF_KB;
+    if (warp_active && key0 <= warp_max_pos) {  // warp-uniform
+      const uint8_t* sK = pf_smem + (sKV + (kb % ST) * C::STAGE_BYTES - sraw);
+      const uint8_t* sV = sK + C::KT_BYTES;
+      const bool need1 = key0 + 16 <= warp_max_pos;  // second 16-key chunk visible to this warp
+      float s[4][4];
 #pragma unroll
-      for (int kc = 0; kc < HD / 16; ++kc)
-        ldsm_x4(qf[kc], sQ + (warp * 16 + (lane & 15)) * LD + kc * 16 + (lane >> 4) * 8);
-    }
-    const __nv_bfloat16* sK = sKV + static_cast<size_t>(kb & 1) * 2 * KB * LD;
-    const __nv_bfloat16* sV = sK + KB * LD;
-    if (warp_active && kb * KB <= warp_max_pos) {  // warp-uniform
-      float s[KB / 8][4];
-#pragma unroll
-      for (int i = 0; i < KB / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+      for (int i = 0; i < 4; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
 #pragma unroll
       for (int kc = 0; kc < HD / 16; ++kc) {
 #pragma unroll
-        for (int np = 0; np < KB / 16; ++np) {
+        for (int np = 0; np < 2; ++np) {
+          if (np == 1 && !need1) break;
           uint32_t b[4];
-          ldsm_x4(b, sK + (np * 16 + (lane & 7) + (lane >> 4) * 8) * LD + kc * 16 + ((lane >> 3) & 1) * 8);
+          ldsm_x4(b, sK + pf_off<HD>(PF_KB, np * 16 + (lane & 7) + (lane >> 4) * 8, kc * 16 + ((lane >> 3) & 1) * 8));
           mma_bf16(s[2 * np], qf[kc], b[0], b[1]);
           mma_bf16(s[2 * np + 1], qf[kc], b[2], b[3]);
         }
       }
+      // chunks entirely at or below the warp's first query need no causal mask (warp-uniform)
+      const bool full0 = !MASK && key0 + 15 <= warp_min_pos;
+      const bool full1 = !MASK && key0 + 31 <= warp_min_pos;
       float mx[2] = {-INFINITY, -INFINITY};
-      // blocks entirely below the warp's first query need no causal mask (warp-uniform test)
-      const bool full_block = !p.key_mask && kb * KB + KB - 1 <= grp.pos0 + warp * 16;
-      if (full_block) {
 #pragma unroll
-        for (int nt = 0; nt < KB / 8; ++nt) {
+      for (int nt = 0; nt < 4; ++nt) {
+        const bool full = nt < 2 ? full0 : full1;
+        if (nt >= 2 && !need1) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float v = s[nt][e] * p.scale_log2;
-            s[nt][e] = v;
-            mx[e >> 1] = fmaxf(mx[e >> 1], v);
-          }
+          for (int e = 0; e < 4; ++e) s[nt][e] = -INFINITY;
+          continue;
         }
-      } else {
 #pragma unroll
-        for (int nt = 0; nt < KB / 8; ++nt) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int key = kb * KB + nt * 8 + 2 * tq + (e & 1);
-            const int qp = e < 2 ? qpos0 : qpos1;
-            bool ok = key <= qp;
-            if (p.key_mask) ok = ok && p.key_mask[key];
-            const float v = ok ? s[nt][e] * p.scale_log2 : -INFINITY;
+        for (int e = 0; e < 4; ++e) {
+          float v = s[nt][e];
+          if (!full) {
+            const int key = key0 + nt * 8 + 2 * tq + (e & 1);
+            bool ok = key <= (e < 2 ? qpos0 : qpos1);
+            if (MASK) ok = ok && key <= last_key && p.key_mask[key];
+            v = ok ? v : -INFINITY;
             s[nt][e] = v;
-            mx[e >> 1] = fmaxf(mx[e >> 1], v);
           }
+          mx[e >> 1] = fmaxf(mx[e >> 1], v);
         }
       }
-      float alpha[2];
+      float alpha[2], msub[2];
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
         mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-        const float mnew = fmaxf(m_i[r], mx[r]);
-        alpha[r] = mnew == -INFINITY ? 1.f : exp2f(m_i[r] - mnew);
+        const float mnew = fmaxf(m_i[r], mx[r] * p.scale_log2);
+        alpha[r] = mnew == -INFINITY ? 1.f : ex2_approx(m_i[r] - mnew);
         m_i[r] = mnew;
         l_i[r] *= alpha[r];
+        // rows with no visible key yet contribute exact zeros: ex2(-inf) = +0
+        msub[r] = mnew == -INFINITY ? 0.f : mnew;
       }
-      // rows with no visible key yet (m == -inf) contribute exact zeros: ex2(-inf) = +0
-      const float msub0 = m_i[0] == -INFINITY ? 0.f : m_i[0];
-      const float msub1 = m_i[1] == -INFINITY ? 0.f : m_i[1];
 #pragma unroll
-      for (int nt = 0; nt < KB / 8; ++nt) {
+      for (int nt = 0; nt < 4; ++nt) {
+        if (nt >= 2 && !need1) break;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float pv = ex2_approx(s[nt][e] - (e < 2 ? msub0 : msub1));
+          const float pv = ex2_approx(fmaf(s[nt][e], p.scale_log2, -msub[e >> 1]));
           s[nt][e] = pv;
           l_i[e >> 1] += pv;
         }
@@ -474,7 +526,8 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
         o[i][3] *= alpha[1];
       }
 #pragma unroll
-      for (int kc = 0; kc < KB / 16; ++kc) {
+      for (int kc = 0; kc < 2; ++kc) {
+        if (kc == 1 && !need1) break;
         uint32_t a[4];
         a[0] = pack_bf16x2(s[2 * kc][0], s[2 * kc][1]);
         a[1] = pack_bf16x2(s[2 * kc][2], s[2 * kc][3]);
@@ -483,14 +536,16 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
 #pragma unroll
         for (int dn = 0; dn < HD / 16; ++dn) {
           uint32_t b[4];
-          ldsm_x4_t(b, sV + (kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LD + dn * 16 + (lane >> 4) * 8);
+          ldsm_x4_t(b, sV + pf_off<HD>(PF_KB, kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, dn * 16 + (lane >> 4) * 8));
           mma_bf16(o[2 * dn], a, b[0], b[1]);
           mma_bf16(o[2 * dn + 1], a, b[2], b[3]);
         }
       }
     }
-    __syncthreads();  // stage kb&1 is refilled by the next iteration's prefetch
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bars + 8 * (ST + kb % ST));
   }
+  if (!warp_active) return;
   float inv[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -499,16 +554,23 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
     l += __shfl_xor_sync(0xffffffffu, l, 2);
     inv[r] = l > 0.f ? 1.f / l : 0.f;
   }
-  const int r0 = warp * 16 + gq;
+  // stage the warp's 16 x HD output tile in its own (consumed) Q rows, then coalesced 16-B stores
 #pragma unroll
   for (int i = 0; i < HD / 8; ++i) {
-    const int col = head * HD + i * 8 + 2 * tq;
-    if (r0 < grp.nq)
-      *reinterpret_cast<uint32_t*>(p.z + static_cast<size_t>(grp.m0 + r0) * p.ldz + col) =
-          pack_bf16x2(o[i][0] * inv[0], o[i][1] * inv[0]);
-    if (r0 + 8 < grp.nq)
-      *reinterpret_cast<uint32_t*>(p.z + static_cast<size_t>(grp.m0 + r0 + 8) * p.ldz + col) =
-          pack_bf16x2(o[i][2] * inv[1], o[i][3] * inv[1]);
+    const int col = i * 8 + 2 * tq;
+    *reinterpret_cast<uint32_t*>(gQ + pf_off<HD>(64, qrow0, col)) = pack_bf16x2(o[i][0] * inv[0], o[i][1] * inv[0]);
+    *reinterpret_cast<uint32_t*>(gQ + pf_off<HD>(64, qrow0 + 8, col)) = pack_bf16x2(o[i][2] * inv[1], o[i][3] * inv[1]);
+  }
+  __syncwarp();
+  constexpr int CPR = HD / 8;  // 16-B chunks per row
+#pragma unroll
+  for (int it = 0; it < 16 * CPR / 32; ++it) {
+    const int idx = it * 32 + lane;
+    const int r = idx / CPR, c = (idx % CPR) * 8;
+    const int row = warp * 16 + r;
+    if (row < grp.nq)
+      *reinterpret_cast<uint4*>(p.z + static_cast<size_t>(grp.m0 + row) * p.ldz + head * HD + c) =
+          *reinterpret_cast<const uint4*>(gQ + pf_off<HD>(64, row, c));
   }
 }
 
@@ -1024,17 +1086,24 @@ void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_
 void launch_attention(const AttnParams& prefill, const AttnParams& decode, int hd, cudaStream_t st) {
 #define ATT(HD)                                                                                     \
   do {                                                                                              \
-    constexpr int smem = 5 * 64 * (HD + 8) * 2;                                                     \
+    constexpr int smem = static_cast<int>(PfCfg<HD>::SMEM);                                         \
     static bool cfg = false;                                                                        \
     if (!cfg) {                                                                                     \
-      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD>,                                         \
+      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD, false>,                                  \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));             \
-      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD>,                                         \
+      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD, true>,                                   \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));             \
+      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD, false>,                                  \
                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100));           \
       cfg = true;                                                                                   \
     }                                                                                               \
-    if (prefill.n_groups > 0)                                                                       \
-      attn_prefill_kernel<HD><<<dim3(prefill.n_groups, prefill.heads), 128, smem, st>>>(prefill);   \
+    if (prefill.n_groups > 0) {                                                                     \
+      const dim3 grid(prefill.n_groups, prefill.heads);                                             \
+      if (prefill.key_mask)                                                                         \
+        attn_prefill_kernel<HD, true><<<grid, 128, smem, st>>>(prefill);                            \
+      else                                                                                          \
+        attn_prefill_kernel<HD, false><<<grid, 128, smem, st>>>(prefill);                           \
+    }                                                                                               \
     if (decode.n_groups > 0) {                                                                      \
       using DC = DecCfg<HD>;                                                                        \
       static bool dcfg = false;                                                                     \

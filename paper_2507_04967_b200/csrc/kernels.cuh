@@ -1,6 +1,7 @@
 // Non-GEMM kernels of the prompt() hot path (declarations + parameter blocks).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 namespace iolmk {
@@ -16,6 +17,8 @@ struct AttnGroup {
 };
 
 struct AttnParams {
+  CUtensorMap q_map;   // prefill: q buffer [T x ldq] as [CB-wide swizzled boxes x 64 rows]
+  CUtensorMap kv_map;  // prefill: layer pool as rows of hd ([page][K|V][heads][PAGE] rows), 16-row boxes
   const __nv_bfloat16* q;  // [T x ldq] (head h at columns h*hd ..)
   int ldq;
   __nv_bfloat16* z;  // [T x ldz] output

@@ -48,4 +48,29 @@ inline CUtensorMap make_kmajor_map(const void* ptr, CUtensorMapDataType dt, int 
   return m;
 }
 
+// bf16 row tensor [rows x inner] read in boxes of box_inner elements x box_rows, swizzled over the
+// box's row span (128/64/32 B -> SWIZZLE_128B/64B/32B). Used by the prefill attention for the q
+// buffer and the paged KV pool.
+inline CUtensorMap make_rows_map_bf16(const void* ptr, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
+                                      uint32_t box_inner, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  const uint32_t span = box_inner * 2;
+  const CUtensorMapSwizzle sw = span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : span == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : span == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                             : CU_TENSOR_MAP_SWIZZLE_NONE;
+  if (sw == CU_TENSOR_MAP_SWIZZLE_NONE || (row_stride_bytes % 16) != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
+    throw std::runtime_error("row TMA map: unsupported box width or misaligned tensor");
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed with code " + std::to_string(r));
+  return m;
+}
+
 }  // namespace iolmh
