@@ -49,6 +49,7 @@ void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_
 void launch_decode_codes(const void* payload, int enc, int rows, int cols, void* dst, bool int8, int ld,
                          float* scales, cudaStream_t st);
 void launch_attention(const AttnParams& prefill, const AttnParams& decode, int hd, cudaStream_t st);
+int decode_heads_per_cta(int heads, int hd);
 void launch_head(const float* x, int d, const int* rows, int n_rows, const float* g, const float* b,
                  const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
                  float* logits_out, cudaStream_t st);
@@ -129,7 +130,7 @@ struct Layer {
   CUtensorMap tm_z, tm_g;    // bf16 A operands with this layer's K extent
   CUtensorMap tm_z8, tm_g8;  // int8 A operands (W8A8)
   DevArray<__nv_bfloat16> kv;  // paged pool [pages][K|V][heads][PAGE][hd]
-  CUtensorMap tm_kv;             // the pool as rows of hd (prefill attention TMA)
+  CUtensorMap tm_kv, tm_kvg;     // the pool as rows of hd (prefill / decode attention TMA boxes)
 };
 
 // 2-SM 256x256 tiles once both M and N fill at least one pair tile. IOLM_GEMM_TILES=single|pair
@@ -453,6 +454,8 @@ void Engine::alloc_runtime() {
     CUDA_OK(cudaMemset(ly->kv.p, 0, elems * sizeof(__nv_bfloat16)));
     ly->tm_kv = make_rows_map_bf16(ly->kv.p, hd_, pages * 2 * ly->heads * PAGE, 2ull * hd_,
                                    std::min(hd_, 64), PAGE);
+    ly->tm_kvg = make_rows_map_bf16(ly->kv.p, hd_, pages * 2 * ly->heads * PAGE, 2ull * hd_, std::min(hd_, 64),
+                                    decode_heads_per_cta(ly->heads, hd_) * PAGE);
   }
   page_table_.alloc(static_cast<size_t>(max_slots_ + 1) * pps_);
   d_last_tok_.alloc(max_slots_ + 1);
@@ -614,6 +617,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     AttnParams ap{};
     ap.q_map = tm_q_;
     ap.kv_map = ly.tm_kv;
+    ap.kvg_map = ly.tm_kvg;
     ap.q = q_.p;
     ap.ldq = kh_max_;
     ap.z = z_.p;

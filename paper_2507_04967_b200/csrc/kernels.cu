@@ -575,32 +575,37 @@ __global__ void __launch_bounds__(128, PfCfg<HD>::MINB) attn_prefill_kernel(cons
 }
 
 // ------------------------------------------------------------------ attention (decode)
-// One CTA per (decode sequence, group of HG heads). In the paged pool a page's K rows for all heads
-// are one contiguous block ([head][PAGE][HD]) and so are its V rows, so the CTA streams each page of
-// its head group with two bulk async copies into a DSTAGES-deep smem ring (a dedicated producer
-// warp; completion on mbarriers) while 8 compute warps run the online softmax from smem. Key rows
-// are read by LPK = HD/8 lanes x 16 B, KPI = 32/LPK keys per instruction. Work is chunked by page
-// (absolute 16-position blocks), so a query's arithmetic never depends on the batch composition.
+// One CTA per (decode sequence, group of hg heads). A page's K rows for heads h0 .. h0+hg-1 are one
+// contiguous run of hg*PAGE pool rows (and so are its V rows), so a producer warp moves each page
+// of the group with two swizzled TMA boxes into a DSTAGES-deep ring (mbarrier completion) while one
+// compute warp per head runs the online softmax on the tensor cores: S^T = K q (m16n8k16 with q as
+// the single live B column) and O^T += V^T p^T (V through ldmatrix.trans, p as the live B column),
+// so a 16-key page costs 2*HD/16 MMAs and HD/8 ldmatrix per warp instead of per-lane dot products.
+// Work is chunked by page (absolute 16-position blocks), so a query's arithmetic never depends on
+// the batch composition.
 constexpr int DSTAGES = 2;
 template <int HD>
 struct DecCfg {
   static constexpr int HG_MAX = HD >= 128 ? 8 : 16;  // heads per CTA = compute warps
-  static constexpr size_t SMEM_MAX = 256 + DSTAGES * 2 * HG_MAX * PAGE * HD * 2;
+  static constexpr size_t smem(int hg) {
+    return 1024 + static_cast<size_t>(DSTAGES) * 2 * hg * PAGE * HD * 2 + 16 * DSTAGES + hg * HD * 2;
+  }
 };
 
 // Block = hg compute warps (warp h owns head h0+h) + 1 producer warp.
 template <int HD>
-__global__ void __launch_bounds__(32 * 17) attn_decode_kernel(AttnParams p, int hg, int n_hgroups) {
-  constexpr int LPK = HD / 8;
-  constexpr int KPI = 32 / LPK;
-  constexpr int ITERS = PAGE / KPI;  // KPI <= 16 = PAGE for HD >= 16
-  extern __shared__ __align__(128) uint8_t dsm[];
-  const uint32_t sbase = (smem_u32(dsm) + 127u) & ~127u;
-  uint8_t* gbase = dsm + (sbase - smem_u32(dsm));
-  const uint32_t HALF = static_cast<uint32_t>(hg) * PAGE * HD * 2;  // K (or V) bytes per page per group
+__global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_constant__ AttnParams p, int hg,
+                                                              int n_hgroups) {
+  using C = PfCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  const uint32_t sraw = smem_u32(dsm);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  uint8_t* gbase = dsm + (sbase - sraw);
+  const int R = hg * PAGE;                            // rows of one K (or V) tile
+  const uint32_t HALF = static_cast<uint32_t>(R) * HD * 2;
   const uint32_t STAGE = 2 * HALF;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + DSTAGES * STAGE);  // full[DSTAGES], empty[DSTAGES]
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + DSTAGES);
+  const uint32_t full0 = sbase + DSTAGES * STAGE, empty0 = full0 + 8 * DSTAGES;
+  __nv_bfloat16* sOut = reinterpret_cast<__nv_bfloat16*>(gbase + DSTAGES * STAGE + 16 * DSTAGES);
 
   const int gi = blockIdx.x / n_hgroups;
   const int hgi = blockIdx.x - gi * n_hgroups;
@@ -610,8 +615,6 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(AttnParams p, int 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int last = grp.pos0;
   const int npages = last / PAGE + 1;
-  const uint32_t half_bytes = static_cast<uint32_t>(nh) * PAGE * HD * 2;
-  const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < DSTAGES; ++s) {
@@ -622,18 +625,25 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(AttnParams p, int 
   }
   __syncthreads();
 
-  if (warp == hg) {  // producer: two bulk copies (K block, V block of the group) per page
-    if (lane == 0) {
-      const size_t page_stride = static_cast<size_t>(2) * p.heads * PAGE * HD;
-      const size_t v_off = static_cast<size_t>(p.heads) * PAGE * HD;
-      for (int pg = 0; pg < npages; ++pg) {
+  if (warp == hg) {  // producer: lanes hold 32 page ids at a time, lane 0 issues the boxes
+    const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
+    if (lane == 0) tma_prefetch_desc(&p.kvg_map);
+    int pid = 0;
+    for (int pg = 0; pg < npages; ++pg) {
+      if ((pg & 31) == 0) pid = pg + lane < p.max_pages ? __ldg(pt + pg + lane) : 0;
+      const int page = __shfl_sync(0xffffffffu, pid, pg & 31);
+      if (lane == 0) {
         const int s = pg % DSTAGES;
         mbar_wait(empty0 + 8 * s, ((pg / DSTAGES) & 1) ^ 1u);
-        const __nv_bfloat16* src =
-            p.kv + static_cast<size_t>(pt[pg]) * page_stride + static_cast<size_t>(h0) * PAGE * HD;
-        mbar_expect_tx(full0 + 8 * s, 2 * half_bytes);
-        bulk_load(sbase + s * STAGE, src, half_bytes, full0 + 8 * s);
-        bulk_load(sbase + s * STAGE + HALF, src + v_off, half_bytes, full0 + 8 * s);
+        mbar_expect_tx(full0 + 8 * s, STAGE);
+        const int rk = (page * 2 * p.heads + h0) * PAGE;
+        const int rv = rk + p.heads * PAGE;
+        const uint32_t dst = sbase + s * STAGE;
+#pragma unroll
+        for (int cb = 0; cb < C::NCB; ++cb) {
+          tma_load_2d(dst + cb * R * C::CBB, &p.kvg_map, full0 + 8 * s, cb * C::CB, rk);
+          tma_load_2d(dst + HALF + cb * R * C::CBB, &p.kvg_map, full0 + 8 * s, cb * C::CB, rv);
+        }
       }
     }
     return;
@@ -641,100 +651,87 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(AttnParams p, int 
 
   const int h = warp;  // this warp's head within the group
   const bool active = h < nh;
-  const int sub = lane % LPK, kin = lane / LPK;
-  float qv[8];
-  float m = -INFINITY, l = 0.f, acc[8];
+  const int gq = lane >> 2, tq = lane & 3;
+  // q as column 0 of the B operand: lanes with gq == 0 hold dims 16ks + 2tq (+1) and 16ks + 8 + 2tq (+1)
+  uint32_t qb[HD / 16][2];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-  if (active) {
-    const uint4 u =
-        *reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(grp.m0) * p.ldq + (h0 + h) * HD + sub * 8);
-    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+  for (int ks = 0; ks < HD / 16; ++ks) qb[ks][0] = qb[ks][1] = 0u;
+  if (active && gq == 0) {
+    const __nv_bfloat16* qr = p.q + static_cast<size_t>(grp.m0) * p.ldq + (h0 + h) * HD;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(h2[e]);
-      qv[2 * e] = f.x * p.scale_log2;
-      qv[2 * e + 1] = f.y * p.scale_log2;
+    for (int ks = 0; ks < HD / 16; ++ks) {
+      qb[ks][0] = *reinterpret_cast<const uint32_t*>(qr + ks * 16 + 2 * tq);
+      qb[ks][1] = *reinterpret_cast<const uint32_t*>(qr + ks * 16 + 8 + 2 * tq);
     }
   }
+  float o[HD / 16][4];
+#pragma unroll
+  for (int i = 0; i < HD / 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m = -INFINITY, l = 0.f;
   for (int pg = 0; pg < npages; ++pg) {
     const int s = pg % DSTAGES;
     mbar_wait(full0 + 8 * s, (pg / DSTAGES) & 1);
     if (active) {
-      const __nv_bfloat16* sK = reinterpret_cast<const __nv_bfloat16*>(gbase + s * STAGE) + static_cast<size_t>(h) * PAGE * HD;
-      const __nv_bfloat16* sV = reinterpret_cast<const __nv_bfloat16*>(gbase + s * STAGE + HALF) + static_cast<size_t>(h) * PAGE * HD;
-      uint4 kr[ITERS], vr[ITERS];
+      const uint8_t* sK = gbase + s * STAGE;
+      const uint8_t* sV = sK + HALF;
+      float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int it = 0; it < ITERS; ++it) {
-        kr[it] = *reinterpret_cast<const uint4*>(sK + (it * KPI + kin) * HD + sub * 8);
-        vr[it] = *reinterpret_cast<const uint4*>(sV + (it * KPI + kin) * HD + sub * 8);
+      for (int ks = 0; ks < HD / 16; ++ks) {
+        uint32_t a[4];
+        ldsm_x4(a, sK + pf_off<HD>(R, h * PAGE + (lane & 15), ks * 16 + (lane >> 4) * 8));
+        mma_bf16(sc, a, qb[ks][0], qb[ks][1]);
       }
-      float sc[ITERS];
-      float cmax = -INFINITY;
+      // lanes tq == 0: sc[0] = score of key gq, sc[2] = score of key gq + 8 (of this page)
+      const int key0 = pg * PAGE + gq, key1 = key0 + 8;
+      const bool ok0 = key0 <= last && (!p.key_mask || p.key_mask[key0]);
+      const bool ok1 = key1 <= last && (!p.key_mask || p.key_mask[key1]);
+      const float s0 = ok0 ? sc[0] * p.scale_log2 : -INFINITY;
+      const float s1 = ok1 ? sc[2] * p.scale_log2 : -INFINITY;
+      float cmax = fmaxf(s0, s1);
 #pragma unroll
-      for (int it = 0; it < ITERS; ++it) {
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&kr[it]);
-        float dot = 0.f;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(h2[e]);
-          dot = fmaf(f.x, qv[2 * e], dot);
-          dot = fmaf(f.y, qv[2 * e + 1], dot);
-        }
-        sc[it] = dot;
-      }
-#pragma unroll
-      for (int o = 1; o < LPK; o <<= 1)
-#pragma unroll
-        for (int it = 0; it < ITERS; ++it) sc[it] += __shfl_xor_sync(0xffffffffu, sc[it], o);
-#pragma unroll
-      for (int it = 0; it < ITERS; ++it) {
-        const int key = pg * PAGE + it * KPI + kin;
-        const bool ok = key <= last && (!p.key_mask || p.key_mask[key]);
-        sc[it] = ok ? sc[it] : -INFINITY;
-        cmax = fmaxf(cmax, sc[it]);
-      }
-#pragma unroll
-      for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+      for (int off = 4; off < 32; off <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, off));
       const float mnew = fmaxf(m, cmax);
-      const float alpha = mnew == -INFINITY ? 1.f : exp2f(m - mnew);
-      float psum = 0.f;
+      const float alpha = mnew == -INFINITY ? 1.f : ex2_approx(m - mnew);
+      const float msub = mnew == -INFINITY ? 0.f : mnew;
+      const float p0 = ex2_approx(s0 - msub), p1 = ex2_approx(s1 - msub);
+      float psum = p0 + p1;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] *= alpha;
-#pragma unroll
-      for (int it = 0; it < ITERS; ++it) {
-        const float pj = mnew == -INFINITY ? 0.f : exp2f(sc[it] - mnew);
-        psum += pj;
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&vr[it]);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(h2[e]);
-          acc[2 * e] = fmaf(pj, f.x, acc[2 * e]);
-          acc[2 * e + 1] = fmaf(pj, f.y, acc[2 * e + 1]);
-        }
-      }
-#pragma unroll
-      for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
+      for (int off = 4; off < 32; off <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, off);
       l = l * alpha + psum;
       m = mnew;
+      // p^T as column 0 of the B operand: lane t < 4 needs keys 2t, 2t+1 (b0) and 8+2t, 9+2t (b1)
+      const uint32_t pk = pack_bf16x2(p0, p1);
+      const uint32_t u = __shfl_sync(0xffffffffu, pk, (lane & 3) * 8);
+      const uint32_t w = __shfl_sync(0xffffffffu, pk, (lane & 3) * 8 + 4);
+      const uint32_t b0 = lane < 4 ? __byte_perm(u, w, 0x5410) : 0u;
+      const uint32_t b1 = lane < 4 ? __byte_perm(u, w, 0x7632) : 0u;
+#pragma unroll
+      for (int mt = 0; mt < HD / 16; ++mt) {
+        o[mt][0] *= alpha;
+        o[mt][2] *= alpha;
+        uint32_t a[4];
+        ldsm_x4_t(a, sV + pf_off<HD>(R, h * PAGE + (lane & 7) + (lane >> 4) * 8, mt * 16 + ((lane >> 3) & 1) * 8));
+        mma_bf16(o[mt], a, b0, b1);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * s);
   }
   if (!active) return;
+  // lanes tq == 0 hold O[16mt + gq] (o[mt][0]) and O[16mt + gq + 8] (o[mt][2])
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  __nv_bfloat16* so = sOut + h * HD;
+  if (tq == 0) {
 #pragma unroll
-  for (int e = 0; e < 8; ++e)
-#pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
-  if (kin == 0) {
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    uint4 w;
-    w.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
-    w.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
-    w.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
-    w.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
-    *reinterpret_cast<uint4*>(p.z + static_cast<size_t>(grp.m0) * p.ldz + (h0 + h) * HD + sub * 8) = w;
+    for (int mt = 0; mt < HD / 16; ++mt) {
+      so[mt * 16 + gq] = __float2bfloat16_rn(o[mt][0] * inv);
+      so[mt * 16 + gq + 8] = __float2bfloat16_rn(o[mt][2] * inv);
+    }
   }
+  __syncwarp();
+  if (lane < HD / 8)
+    *reinterpret_cast<uint4*>(p.z + static_cast<size_t>(grp.m0) * p.ldz + (h0 + h) * HD + lane * 8) =
+        *reinterpret_cast<const uint4*>(so + lane * 8);
 }
 
 // ------------------------------------------------------------------ head + argmax
@@ -972,6 +969,12 @@ __global__ void transpose_f32_kernel(const float* __restrict__ src, int rows, in
 namespace iolmh {
 using namespace iolmk;
 
+int decode_heads_per_cta(int heads, int hd) {
+  const int hmax = hd >= 128 ? 8 : 16;
+  const int ngrp = (heads + hmax - 1) / hmax;
+  return (heads + ngrp - 1) / ngrp;
+}
+
 static inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 void launch_ln(const float* x, int M, int d, const float* g, const float* b, __nv_bfloat16* h, int ldh,
@@ -1105,21 +1108,19 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
         attn_prefill_kernel<HD, false><<<grid, 128, smem, st>>>(prefill);                           \
     }                                                                                               \
     if (decode.n_groups > 0) {                                                                      \
-      using DC = DecCfg<HD>;                                                                        \
-      static bool dcfg = false;                                                                     \
-      if (!dcfg) {                                                                                  \
+      const int hg = decode_heads_per_cta(decode.heads, HD);                                        \
+      const int ngrp = (decode.heads + hg - 1) / hg;                                                \
+      const size_t sm = DecCfg<HD>::smem(hg);                                                       \
+      static size_t dcfg = 0;                                                                       \
+      if (sm > dcfg) {                                                                              \
         CUDA_OK(cudaFuncSetAttribute(attn_decode_kernel<HD>,                                        \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,                   \
-                                     static_cast<int>(DC::SMEM_MAX)));                              \
+                                     static_cast<int>(DecCfg<HD>::smem(DecCfg<HD>::HG_MAX))));      \
         CUDA_OK(cudaFuncSetAttribute(attn_decode_kernel<HD>,                                        \
                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));         \
-        dcfg = true;                                                                                \
+        dcfg = DecCfg<HD>::smem(DecCfg<HD>::HG_MAX);                                                \
       }                                                                                             \
-      const int ngrp = (decode.heads + DC::HG_MAX - 1) / DC::HG_MAX;                                \
-      const int hg = (decode.heads + ngrp - 1) / ngrp;                                              \
-      const size_t sm = 256 + static_cast<size_t>(DSTAGES) * 2 * hg * PAGE * HD * 2;                 \
-      attn_decode_kernel<HD><<<decode.n_groups * ngrp, 32 * (hg + 1), sm, st>>>(                    \
-          decode, hg, ngrp);                                                                        \
+      attn_decode_kernel<HD><<<decode.n_groups * ngrp, 32 * (hg + 1), sm, st>>>(decode, hg, ngrp);  \
     }                                                                                               \
   } while (0)
   switch (hd) {

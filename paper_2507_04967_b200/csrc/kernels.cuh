@@ -19,6 +19,7 @@ struct AttnGroup {
 struct AttnParams {
   CUtensorMap q_map;   // prefill: q buffer [T x ldq] as [CB-wide swizzled boxes x 64 rows]
   CUtensorMap kv_map;  // prefill: layer pool as rows of hd ([page][K|V][heads][PAGE] rows), 16-row boxes
+  CUtensorMap kvg_map; // decode: the same rows in boxes of decode_heads_per_cta(heads, hd) * PAGE rows
   const __nv_bfloat16* q;  // [T x ldq] (head h at columns h*hd ..)
   int ldq;
   __nv_bfloat16* z;  // [T x ldz] output
