@@ -392,7 +392,7 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "s8 x s8 -> s32 (W8A8)" if cfg.get("act_quant") else "bf16", "data": "synthetic (seeded rows, random-init weights: ToyModelParams::init seed 42)",
         "config": {"workload": cfg["desc"], "rows_per_step_per_gpu": B, "max_new_tokens": MAX_NEW,
-                   "tokens_per_engine_step": args.tokens_per_step or 16384,
+                   "tokens_per_engine_step": args.tokens_per_step or "SMs/2 x 256 (18944 on B200)",
                    "l2": "inputs larger than L2 (GB-scale activations per step)",
                    "parallelism": f"rows range-partitioned over {world} GPU(s), full replica each"},
         "e2e": {"value": e2e, "unit": "rows/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

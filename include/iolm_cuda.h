@@ -43,7 +43,7 @@ typedef struct iolm_cuda_ctx iolm_cuda_ctx;
 
 /* Engine options. Zero means "default" for every field. */
 typedef struct iolm_cuda_opts {
-  int32_t max_tokens_per_step; /* continuous-batching token budget per engine step (default 16384) */
+  int32_t max_tokens_per_step; /* continuous-batching token budget per engine step (default: SMs/2 x 256) */
   int32_t max_slots;           /* sequences resident in the paged KV pool (default: derived) */
   int32_t page_size;           /* KV page size in tokens (default 16) */
   int32_t act_quant;           /* 1: W8A8 int8 activations for q8 / sparse24 weights (default 0) */

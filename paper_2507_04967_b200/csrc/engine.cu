@@ -226,7 +226,7 @@ class Engine {
   uint64_t hash_ = 0;
   int device_ = 0, sms_ = 148;
   int d_ = 0, L_ = 0, V_ = 0, S_ = 0, hd_ = 0, kh_max_ = 0, f_ld_max_ = 0;
-  int T_max_ = 16384, max_slots_ = 0, pps_ = 0, prefix_slot_ = 0;
+  int T_max_ = 0, max_slots_ = 0, pps_ = 0, prefix_slot_ = 0;
   int cur_prefix_pages_ = -1;
   bool prefix_sharing_ = true;
   bool act_quant_ = false;
@@ -293,6 +293,9 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
     if (opts->prefix_sharing < 0) prefix_sharing_ = false;
     ktime_ = opts->kernel_timing != 0;
   }
+  // Default token budget: one 256-row GEMM M-tile per SM pair (74 x 256 = 18944 on a 148-SM B200),
+  // so every projection's tile count is a whole number of waves of the persistent GEMM grid.
+  if (T_max_ <= 0) T_max_ = std::max(1, sms_ / 2) * 256;
   T_max_ = std::max(round_up(T_max_, 128), round_up(S_, 128));
   for (int l = 0; l < L_; ++l) {
     const uint64_t kh = static_cast<uint64_t>(cfg_.layer_heads(l)) * hd_;

@@ -7,6 +7,7 @@
 //                                                                            numerics.cpp:190-197)
 //   lcp / decode helpers
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 #include <cmath>
 
@@ -577,25 +578,25 @@ __global__ void __launch_bounds__(128, PfCfg<HD>::MINB) attn_prefill_kernel(cons
 // ------------------------------------------------------------------ attention (decode)
 // One CTA per (decode sequence, group of hg heads). A page's K rows for heads h0 .. h0+hg-1 are one
 // contiguous run of hg*PAGE pool rows (and so are its V rows), so a producer warp moves each page
-// of the group with two swizzled TMA boxes into a DSTAGES-deep ring (mbarrier completion) while one
+// of the group with two swizzled TMA boxes into an nst-deep ring (mbarrier completion) while one
 // compute warp per head runs the online softmax on the tensor cores: S^T = K q (m16n8k16 with q as
 // the single live B column) and O^T += V^T p^T (V through ldmatrix.trans, p as the live B column),
 // so a 16-key page costs 2*HD/16 MMAs and HD/8 ldmatrix per warp instead of per-lane dot products.
 // Work is chunked by page (absolute 16-position blocks), so a query's arithmetic never depends on
 // the batch composition.
-constexpr int DSTAGES = 2;
+constexpr int DSTAGES_MAX = 4;
 template <int HD>
 struct DecCfg {
   static constexpr int HG_MAX = HD >= 128 ? 8 : 16;  // heads per CTA = compute warps
-  static constexpr size_t smem(int hg) {
-    return 1024 + static_cast<size_t>(DSTAGES) * 2 * hg * PAGE * HD * 2 + 16 * DSTAGES + hg * HD * 2;
+  static constexpr size_t smem(int hg, int nst) {
+    return 1024 + static_cast<size_t>(nst) * 2 * hg * PAGE * HD * 2 + 16 * DSTAGES_MAX + hg * HD * 2;
   }
 };
 
 // Block = hg compute warps (warp h owns head h0+h) + 1 producer warp.
 template <int HD>
 __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_constant__ AttnParams p, int hg,
-                                                              int n_hgroups) {
+                                                              int n_hgroups, int nst) {
   using C = PfCfg<HD>;
   extern __shared__ __align__(1024) uint8_t dsm[];
   const uint32_t sraw = smem_u32(dsm);
@@ -604,8 +605,8 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
   const int R = hg * PAGE;                            // rows of one K (or V) tile
   const uint32_t HALF = static_cast<uint32_t>(R) * HD * 2;
   const uint32_t STAGE = 2 * HALF;
-  const uint32_t full0 = sbase + DSTAGES * STAGE, empty0 = full0 + 8 * DSTAGES;
-  __nv_bfloat16* sOut = reinterpret_cast<__nv_bfloat16*>(gbase + DSTAGES * STAGE + 16 * DSTAGES);
+  const uint32_t full0 = sbase + nst * STAGE, empty0 = full0 + 8 * DSTAGES_MAX;
+  __nv_bfloat16* sOut = reinterpret_cast<__nv_bfloat16*>(gbase + nst * STAGE + 16 * DSTAGES_MAX);
 
   const int gi = blockIdx.x / n_hgroups;
   const int hgi = blockIdx.x - gi * n_hgroups;
@@ -617,7 +618,7 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
   const int npages = last / PAGE + 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < DSTAGES; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, hg);
     }
@@ -628,13 +629,13 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
   if (warp == hg) {  // producer: lanes hold 32 page ids at a time, lane 0 issues the boxes
     const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
     if (lane == 0) tma_prefetch_desc(&p.kvg_map);
-    int pid = 0;
+    int pid = 0, s = 0;
+    uint32_t ph = 0;
     for (int pg = 0; pg < npages; ++pg) {
       if ((pg & 31) == 0) pid = pg + lane < p.max_pages ? __ldg(pt + pg + lane) : 0;
       const int page = __shfl_sync(0xffffffffu, pid, pg & 31);
       if (lane == 0) {
-        const int s = pg % DSTAGES;
-        mbar_wait(empty0 + 8 * s, ((pg / DSTAGES) & 1) ^ 1u);
+        mbar_wait(empty0 + 8 * s, ph ^ 1u);
         mbar_expect_tx(full0 + 8 * s, STAGE);
         const int rk = (page * 2 * p.heads + h0) * PAGE;
         const int rv = rk + p.heads * PAGE;
@@ -645,6 +646,7 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
           tma_load_2d(dst + HALF + cb * R * C::CBB, &p.kvg_map, full0 + 8 * s, cb * C::CB, rv);
         }
       }
+      if (++s == nst) s = 0, ph ^= 1u;
     }
     return;
   }
@@ -668,9 +670,10 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
 #pragma unroll
   for (int i = 0; i < HD / 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m = -INFINITY, l = 0.f;
+  int s = 0;
+  uint32_t ph = 0;
   for (int pg = 0; pg < npages; ++pg) {
-    const int s = pg % DSTAGES;
-    mbar_wait(full0 + 8 * s, (pg / DSTAGES) & 1);
+    mbar_wait(full0 + 8 * s, ph);
     if (active) {
       const uint8_t* sK = gbase + s * STAGE;
       const uint8_t* sV = sK + HALF;
@@ -716,6 +719,7 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * s);
+    if (++s == nst) s = 0, ph ^= 1u;
   }
   if (!active) return;
   // lanes tq == 0 hold O[16mt + gq] (o[mt][0]) and O[16mt + gq + 8] (o[mt][2])
@@ -969,8 +973,18 @@ __global__ void transpose_f32_kernel(const float* __restrict__ src, int rows, in
 namespace iolmh {
 using namespace iolmk;
 
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+// decode attention CTA shape (IOLM_DEC_HG / IOLM_DEC_STAGES override, for A/B measurements)
+static int decode_stages() {
+  static const int v = std::max(2, std::min(DSTAGES_MAX, env_int("IOLM_DEC_STAGES", 3)));
+  return v;
+}
 int decode_heads_per_cta(int heads, int hd) {
-  const int hmax = hd >= 128 ? 8 : 16;
+  static const int cap = env_int("IOLM_DEC_HG", 0);
+  const int hmax = std::min(hd >= 128 ? 8 : 16, cap > 0 ? cap : 5);
   const int ngrp = (heads + hmax - 1) / hmax;
   return (heads + ngrp - 1) / ngrp;
 }
@@ -1110,17 +1124,17 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
     if (decode.n_groups > 0) {                                                                      \
       const int hg = decode_heads_per_cta(decode.heads, HD);                                        \
       const int ngrp = (decode.heads + hg - 1) / hg;                                                \
-      const size_t sm = DecCfg<HD>::smem(hg);                                                       \
+      const int nst = decode_stages();                                                              \
+      const size_t sm = DecCfg<HD>::smem(hg, nst);                                                  \
       static size_t dcfg = 0;                                                                       \
       if (sm > dcfg) {                                                                              \
         CUDA_OK(cudaFuncSetAttribute(attn_decode_kernel<HD>,                                        \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,                   \
-                                     static_cast<int>(DecCfg<HD>::smem(DecCfg<HD>::HG_MAX))));      \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm))); \
         CUDA_OK(cudaFuncSetAttribute(attn_decode_kernel<HD>,                                        \
                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));         \
-        dcfg = DecCfg<HD>::smem(DecCfg<HD>::HG_MAX);                                                \
+        dcfg = sm;                                                                                  \
       }                                                                                             \
-      attn_decode_kernel<HD><<<decode.n_groups * ngrp, 32 * (hg + 1), sm, st>>>(decode, hg, ngrp);  \
+      attn_decode_kernel<HD><<<decode.n_groups * ngrp, 32 * (hg + 1), sm, st>>>(decode, hg, ngrp, nst); \
     }                                                                                               \
   } while (0)
   switch (hd) {
