@@ -355,6 +355,12 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
         achieved = work / (kms / 1000.0) / 1e12
         peak = peaks["bf16_tflops_sustained"]
         unit, bound = "TFLOP/s", "tensor"
+        if cfg.get("act_quant"):
+            # int8 GEMMs: kind::i8 dense = 2x and 2:4 sparse kind::i8 = 4x the bf16 rate (datasheet
+            # ratios applied to the measured sustained bf16 peak; FLOPs counted dense-equivalent)
+            mult = 4.0 if cfg["quant"] == "sparse24" else 2.0
+            peak *= mult
+            peak_src = f"{peak_src} x {mult:g} (int8{' 2:4 sparse' if mult == 4 else ''} datasheet ratio)"
     traffic = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
@@ -392,7 +398,9 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "s8 x s8 -> s32 (W8A8)" if cfg.get("act_quant") else "bf16", "data": "synthetic (seeded rows, random-init weights: ToyModelParams::init seed 42)",
         "config": {"workload": cfg["desc"], "rows_per_step_per_gpu": B, "max_new_tokens": MAX_NEW,
-                   "tokens_per_engine_step": args.tokens_per_step or "SMs/2 x 256 (18944 on B200)",
+                   "tokens_per_engine_step": args.tokens_per_step or (
+                       "SMs/2 x 224 (16576 on B200: whole waves of the 2:4 sparse kernel's 224-token tiles)"
+                       if cfg["quant"] == "sparse24" and cfg.get("act_quant") else "SMs/2 x 256 (18944 on B200)"),
                    "l2": "inputs larger than L2 (GB-scale activations per step)",
                    "parallelism": f"rows range-partitioned over {world} GPU(s), full replica each"},
         "e2e": {"value": e2e, "unit": "rows/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

@@ -50,7 +50,8 @@ typedef struct iolm_cuda_opts {
   int32_t prefix_sharing;      /* -1: off; 0/1: share the common prompt prefix KV (default on) */
   int32_t use_cuda_graph;      /* reserved */
   int32_t kernel_timing;       /* 1: time every kernel class with CUDA events (iolm_cuda_kernel_times) */
-  int32_t reserved[9];
+  int32_t sparse_mma;          /* -1: expand sparse24_q8 to dense int8; 0/1: 2:4 sparse tensor cores (W8A8) */
+  int32_t reserved[8];
 } iolm_cuda_opts;
 
 /* ModelConfig (proj/include/iolm/model.hpp:20-41); per-layer lists are queried separately. */
@@ -150,6 +151,15 @@ int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_t epi, int3
 
 /* Per-token int8 activation quantization (the W8A8 rule) of bf16 rows [n x d] on the
  * device: codes [n x d] and one f32 scale per row. */
+/* 2:4 sparse W8A8 GEMM on the sparse tensor cores (tcgen05.mma.sp kind::i8): X_s8 [T x K] times a
+ * sparse24_q8 tensor payload W [N x K] exactly as stored in a bundle (proj/src/model.cpp:255-290).
+ * epi 5: raw int32 accumulators -> out_s32 [T x N] (bit-exact); epi 0: acc * a_scale[t] * w_scale[n]
+ * -> out_f32 (w_scale = the payload's per-row scales). K % 16 == 0. */
+int iolm_cuda_debug_gemm_sp24(const int8_t* X, const uint8_t* payload, int32_t T, int32_t N, int32_t K,
+                              int32_t epi, const float* a_scale, int32_t* out_s32, float* out_f32);
+/* Device-only timing of the sparse GEMM: mean ms per launch (epi as in debug_gemm_time). */
+int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, float* ms_out);
+
 int iolm_cuda_debug_quant_rows_bf16(const uint16_t* x, int32_t n, int32_t d, int8_t* codes, float* scales);
 
 #ifdef __cplusplus

@@ -36,7 +36,8 @@ class Opts(C.Structure):
         ("prefix_sharing", C.c_int32),
         ("use_cuda_graph", C.c_int32),
         ("kernel_timing", C.c_int32),
-        ("reserved", C.c_int32 * 9),
+        ("sparse_mma", C.c_int32),
+        ("reserved", C.c_int32 * 8),
     ]
 
 
@@ -80,6 +81,9 @@ SIGNATURES = {
     "iolm_cuda_debug_quant_rows_bf16": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "iolm_cuda_debug_gemm_s8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                           C.c_int32, C.c_int32]),
+    "iolm_cuda_debug_gemm_sp24": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                            C.c_void_p, C.c_void_p, C.c_void_p]),
+    "iolm_cuda_debug_gemm_sp24_time": (C.c_int, [C.c_int32] * 5 + [C.POINTER(C.c_float)]),
 }
 
 _LIB = None

@@ -4,6 +4,7 @@
 
 #include "capi_util.hpp"
 #include "launch.hpp"
+#include "sparse24.hpp"
 #include "tma_host.hpp"
 
 namespace iolmh {
@@ -144,6 +145,87 @@ extern "C" int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_
     launch_gemm(pair != 0, i8 != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
     CUDA_OK(cudaEventRecord(e0));
     for (int i = 0; i < iters; ++i) launch_gemm(pair != 0, i8 != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
+    CUDA_OK(cudaEventRecord(e1));
+    CUDA_OK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_out = ms / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+// 2:4 sparse W8A8 GEMM through the sparse tensor cores: X_s8 [T x K] times the sparse24_q8 payload
+// W [N x K] (the bundle's own bytes, proj/src/model.cpp:255-290). epi 5: raw int32 accumulators
+// into out_s32 [T x N]; epi 0: acc * a_scale[t] * w_scale[n] into out_f32 (w_scale from the payload).
+extern "C" int iolm_cuda_debug_gemm_sp24(const int8_t* X, const uint8_t* payload, int32_t T, int32_t N, int32_t K,
+                                         int32_t epi, const float* a_scale, int32_t* out_s32, float* out_f32) {
+  return guarded([&] {
+    if (T <= 0 || N <= 0 || K <= 0 || K % 16 != 0)
+      throw ContractViolation("debug_gemm_sp24: need positive T, N and K % 16 == 0");
+    if (epi != iolmk::EPI_S32 && epi != iolmk::EPI_F32) throw ContractViolation("debug_gemm_sp24: epi 0 or 5");
+    if (!sp24_check(payload, N, K)) throw Unsupported("debug_gemm_sp24: positions not ascending");
+    const Sp24Layout l = sp24_layout(N, K);
+    std::vector<int8_t> codes(l.code_bytes(), 0);
+    std::vector<uint8_t> meta(l.meta_bytes(), 0x44);
+    std::vector<float> scales(N);
+    sp24_append(l, payload, N, K, 0, codes.data(), meta.data(), scales.data());
+    DevBuf<int8_t> dX(static_cast<size_t>(T) * K), dW(codes.size());
+    DevBuf<uint8_t> dE(meta.size());
+    DevBuf<float> dS(N), dA(T), dC(static_cast<size_t>(T) * N);
+    CUDA_OK(cudaMemcpy(dX.p, X, static_cast<size_t>(T) * K, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dW.p, codes.data(), codes.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dE.p, meta.data(), meta.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dS.p, scales.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
+    iolmk::GemmEpi ep;
+    ep.M = T;
+    ep.N = N;
+    ep.out = dC.p;
+    ep.ldo = N;
+    if (epi == iolmk::EPI_F32) {
+      CUDA_OK(cudaMemcpy(dA.p, a_scale, sizeof(float) * T, cudaMemcpyHostToDevice));
+      ep.a_scale = dA.p;
+      ep.w_scale = dS.p;
+    }
+    launch_gemm_sp(epi, sp24_codes_map(l, dW.p), sp24_act_map(dX.p, K, T, K), sp24_meta_map(l, dE.p), K,
+                   l.katoms_pad, ep, nullptr, sm_count());
+    CUDA_OK(cudaDeviceSynchronize());
+    if (epi == iolmk::EPI_S32)
+      CUDA_OK(cudaMemcpy(out_s32, dC.p, sizeof(int32_t) * T * N, cudaMemcpyDeviceToHost));
+    else
+      CUDA_OK(cudaMemcpy(out_f32, dC.p, sizeof(float) * T * N, cudaMemcpyDeviceToHost));
+  });
+}
+
+// Device-only timing of the sparse GEMM (kernel tuning): every group keeps positions (0, 1).
+extern "C" int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
+                                              float* ms_out) {
+  return guarded([&] {
+    if (T <= 0 || N <= 0 || K <= 0 || K % 16 != 0 || iters <= 0) throw ContractViolation("debug_gemm_sp24_time");
+    const Sp24Layout l = sp24_layout(N, K);
+    DevBuf<int8_t> dX(static_cast<size_t>(T) * K), dW(l.code_bytes());
+    DevBuf<uint8_t> dE(l.meta_bytes());
+    DevBuf<float> dS(N), dA(T), dC(static_cast<size_t>(T) * N);
+    CUDA_OK(cudaMemset(dX.p, 0x11, static_cast<size_t>(T) * K));
+    CUDA_OK(cudaMemset(dW.p, 0x13, l.code_bytes()));
+    CUDA_OK(cudaMemset(dE.p, 0x44, l.meta_bytes()));
+    CUDA_OK(cudaMemset(dS.p, 0, sizeof(float) * N));
+    CUDA_OK(cudaMemset(dA.p, 0, sizeof(float) * T));
+    CUDA_OK(cudaMemset(dC.p, 0, sizeof(float) * T * N));
+    iolmk::GemmEpi ep;
+    ep.M = T;
+    ep.N = N;
+    ep.out = dC.p;
+    ep.ldo = N;
+    ep.a_scale = dA.p;
+    ep.w_scale = dS.p;
+    const CUtensorMap ta = sp24_codes_map(l, dW.p), tb = sp24_act_map(dX.p, K, T, K), te = sp24_meta_map(l, dE.p);
+    cudaEvent_t e0, e1;
+    CUDA_OK(cudaEventCreate(&e0));
+    CUDA_OK(cudaEventCreate(&e1));
+    launch_gemm_sp(epi, ta, tb, te, K, l.katoms_pad, ep, nullptr, sm_count());
+    CUDA_OK(cudaEventRecord(e0));
+    for (int i = 0; i < iters; ++i) launch_gemm_sp(epi, ta, tb, te, K, l.katoms_pad, ep, nullptr, sm_count());
     CUDA_OK(cudaEventRecord(e1));
     CUDA_OK(cudaEventSynchronize(e1));
     float ms = 0;

@@ -30,6 +30,7 @@
 #include "capi_util.hpp"
 #include "kernels.cuh"
 #include "launch.hpp"
+#include "sparse24.hpp"
 #include "tma_host.hpp"
 
 namespace iolmh {
@@ -114,13 +115,20 @@ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 //   CODES  : bf16(code) + f32 scale per row    q8 / q4 / sparse24 without activation quant (W8A16,
 //            W4A16): integer codes are exact in bf16, the scale is applied in the GEMM epilogue
 //   INT8   : int8 code + f32 scale per row     q8 / sparse24 with act_quant (W8A8, kind::i8)
-enum WMode : int { W_VALUES = 0, W_CODES = 1, W_INT8 = 2 };
+//   SP24   : kept int8 codes [N x K/2] + 2:4 metadata + f32 scale per row: sparse24_q8 with
+//            act_quant on the sparse tensor cores (tcgen05.mma.sp kind::i8, gemm_sp_sm100.cuh)
+enum WMode : int { W_VALUES = 0, W_CODES = 1, W_INT8 = 2, W_SP24 = 3 };
 struct GemmW {
   int mode = W_VALUES;
   DevArray<__nv_bfloat16> wb;
   DevArray<int8_t> w8;
   DevArray<float> scale;
   CUtensorMap tm;
+  // W_SP24
+  DevArray<uint8_t> meta;
+  Sp24Layout sl;
+  CUtensorMap tm_e;
+  bool int8() const { return mode == W_INT8 || mode == W_SP24; }
 };
 
 struct Layer {
@@ -129,6 +137,7 @@ struct Layer {
   GemmW qkv, o, in, out;
   CUtensorMap tm_z, tm_g;    // bf16 A operands with this layer's K extent
   CUtensorMap tm_z8, tm_g8;  // int8 A operands (W8A8)
+  CUtensorMap tm_z8s, tm_g8s;  // the same in the sparse kernel's 112-row boxes
   DevArray<__nv_bfloat16> kv;  // paged pool [pages][K|V][heads][PAGE][hd]
   CUtensorMap tm_kv, tm_kvg;     // the pool as rows of hd (prefill / decode attention TMA boxes)
 };
@@ -216,6 +225,9 @@ class Engine {
                           int64_t owner);
   void launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits);
   void gemm(int epi, bool i8, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
+  // one projection: dense (A = activations, B = weights) or 2:4 sparse (weights are the MMA's A)
+  void gemm_w(int epi, const GemmW& w, const CUtensorMap& act, const CUtensorMap& act_sp, int M, int N, int K,
+              const GemmEpi& ep);
   void load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<std::string>& names, int K, int ld);
   uint64_t ref_madds_row(int s0, int advances) const;
   template <typename F>
@@ -230,6 +242,7 @@ class Engine {
   int cur_prefix_pages_ = -1;
   bool prefix_sharing_ = true;
   bool act_quant_ = false;
+  bool sparse_mma_ = true;
   uint64_t madds_A_ = 0, madds_B_ = 0;  // sum_l (4*d*kh + 2*d*f), sum_l kh
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
@@ -254,7 +267,7 @@ class Engine {
   CUtensorMap tm_h_, tm_q_;
   DevArray<int8_t> h8_, z8_, g8_;  // W8A8 operands + per-token scales
   DevArray<float> hs_, zs_, gs_;
-  CUtensorMap tm_h8_;
+  CUtensorMap tm_h8_, tm_h8s_;
   bool any_int8_ = false;
   DevArray<int> page_table_;
   StepBuffers sbuf_[2];
@@ -292,10 +305,12 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
     act_quant_ = opts->act_quant != 0;
     if (opts->prefix_sharing < 0) prefix_sharing_ = false;
     ktime_ = opts->kernel_timing != 0;
+    if (opts->sparse_mma < 0) sparse_mma_ = false;
   }
   // Default token budget: one 256-row GEMM M-tile per SM pair (74 x 256 = 18944 on a 148-SM B200),
   // so every projection's tile count is a whole number of waves of the persistent GEMM grid.
-  if (T_max_ <= 0) T_max_ = std::max(1, sms_ / 2) * 256;
+  const bool auto_budget = T_max_ <= 0;
+  if (auto_budget) T_max_ = std::max(1, sms_ / 2) * 256;
   T_max_ = std::max(round_up(T_max_, 128), round_up(S_, 128));
   for (int l = 0; l < L_; ++l) {
     const uint64_t kh = static_cast<uint64_t>(cfg_.layer_heads(l)) * hd_;
@@ -306,6 +321,12 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
   std::thread hasher([&] { hash_ = fnv1a64(bytes, len); });
   try {
     upload_weights(b);
+    // All projections on the 2:4 sparse kernel (224-token pair tiles): whole waves of that grid.
+    bool all_sp = true;
+    for (const auto& ly : layers_)
+      all_sp = all_sp && ly->qkv.mode == W_SP24 && ly->o.mode == W_SP24 && ly->in.mode == W_SP24 &&
+               ly->out.mode == W_SP24;
+    if (auto_budget && all_sp) T_max_ = std::max(std::max(1, sms_ / 2) * 224, round_up(S_, 32));
     alloc_runtime();
   } catch (...) {
     hasher.join();
@@ -342,8 +363,7 @@ void Engine::upload_weights(const BundleView& b) {
     load_gemm_weights(b, ly->o, {p + "attn.wo"}, kh, kh);
     load_gemm_weights(b, ly->in, {p + "ffn.w_in"}, d_, d_);
     load_gemm_weights(b, ly->out, {p + "ffn.w_out"}, f, f_ld);
-    any_int8_ = any_int8_ || ly->qkv.mode == W_INT8 || ly->o.mode == W_INT8 || ly->in.mode == W_INT8 ||
-                ly->out.mode == W_INT8;
+    any_int8_ = any_int8_ || ly->qkv.int8() || ly->o.int8() || ly->in.int8() || ly->out.int8();
     kh_max_ = std::max(kh_max_, kh);
     f_ld_max_ = std::max(f_ld_max_, f_ld);
     layers_.push_back(std::move(ly));
@@ -356,15 +376,40 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
                                int ld) {
   std::vector<const TensorRecord*> ts;
   int N = 0;
-  bool all_dense = true, all_quant = true, int8_ok = true;
+  bool all_dense = true, all_quant = true, int8_ok = true, sp_ok = act_quant_ && sparse_mma_;
   for (const auto& n : names) {
     ts.push_back(&b.tensor(n));
     N += ts.back()->rows;
     all_dense = all_dense && ts.back()->encoding == ENC_DENSE_F32;
     all_quant = all_quant && ts.back()->encoding != ENC_DENSE_F32;
     int8_ok = int8_ok && (ts.back()->encoding == ENC_Q8 || ts.back()->encoding == ENC_SPARSE24_Q8);
+    sp_ok = sp_ok && ts.back()->encoding == ENC_SPARSE24_Q8 &&
+            sp24_check(b.payload(*ts.back()), ts.back()->rows, ts.back()->cols);
   }
   w.mode = all_quant ? (act_quant_ && int8_ok ? W_INT8 : W_CODES) : W_VALUES;
+  if (w.mode == W_INT8 && sp_ok) {
+    // 2:4 sparse tensor cores: the bundle's kept codes and position nibbles are repacked on the host
+    w.mode = W_SP24;
+    w.sl = sp24_layout(N, K);
+    std::vector<int8_t> codes(w.sl.code_bytes(), 0);
+    std::vector<uint8_t> meta(w.sl.meta_bytes(), 0x44);
+    std::vector<float> scales(N);
+    int row0 = 0;
+    for (auto* t : ts) {
+      sp24_append(w.sl, b.payload(*t), t->rows, t->cols, row0, codes.data(), meta.data(), scales.data());
+      row0 += t->rows;
+    }
+    w.w8.alloc(codes.size());
+    w.meta.alloc(meta.size());
+    w.scale.alloc(N);
+    CUDA_OK(cudaMemcpy(w.w8.p, codes.data(), codes.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(w.meta.p, meta.data(), meta.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(w.scale.p, scales.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
+    w.tm = sp24_codes_map(w.sl, w.w8.p);
+    w.tm_e = sp24_meta_map(w.sl, w.meta.p);
+    (void)ld;
+    return;
+  }
   if (act_quant_ && w.mode != W_INT8)
     throw Unsupported("act_quant (W8A8) needs q8 or sparse24_q8 encodings for every linear weight; " + names[0] +
                       " is " + (all_dense ? "dense_f32" : "q4 or mixed"));
@@ -420,9 +465,12 @@ void Engine::alloc_runtime() {
     zs_.alloc(T);
     gs_.alloc(T);
     tm_h8_ = make_kmajor_map(h8_.p, U8, 1, d_, T, static_cast<uint64_t>(d_), 128);
+    tm_h8s_ = sp24_act_map(h8_.p, d_, static_cast<int>(T), d_);
     for (auto& ly : layers_) {
       ly->tm_z8 = make_kmajor_map(z8_.p, U8, 1, ly->kh, T, static_cast<uint64_t>(kh_max_), 128);
       ly->tm_g8 = make_kmajor_map(g8_.p, U8, 1, ly->f, T, static_cast<uint64_t>(f_ld_max_), 128);
+      ly->tm_z8s = sp24_act_map(z8_.p, ly->kh, static_cast<int>(T), kh_max_);
+      ly->tm_g8s = sp24_act_map(g8_.p, ly->f, static_cast<int>(T), f_ld_max_);
     }
   }
   // packed step metadata: tok_src i64[T], tok_slot/pos i32[T], groups 2 x [T], head rows/slots i32[T]
@@ -502,6 +550,16 @@ void Engine::gemm(int epi, bool i8, const CUtensorMap& A, const CUtensorMap& B, 
   ++stats_.kernel_launches;
 }
 
+void Engine::gemm_w(int epi, const GemmW& w, const CUtensorMap& act, const CUtensorMap& act_sp, int M, int N, int K,
+                    const GemmEpi& ep) {
+  if (w.mode == W_SP24) {
+    launch_gemm_sp(epi, w.tm, act_sp, w.tm_e, K, w.sl.katoms_pad, ep, stream_, sms_);
+    ++stats_.kernel_launches;
+  } else {
+    gemm(epi, w.mode == W_INT8, act, w.tm, M, N, K, ep);
+  }
+}
+
 template <typename F>
 void Engine::timed(int cat, double work, F&& f) {
   if (!ktime_) {
@@ -572,7 +630,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
   CUDA_OK(cudaMemcpyAsync(d, h, off, cudaMemcpyHostToDevice, stream_));
 
   const double dT = static_cast<double>(T);
-  const bool q8_first = layers_[0]->qkv.mode == W_INT8;
+  const bool q8_first = layers_[0]->qkv.int8();
   timed(0, dT * d_ * 14.0, [&] {
     launch_embed_ln(d_ids, sb.tok_src, sb.tok_slot, sb.tok_pos, d_last_tok_.p, T, d_, tok_embed_.p, pos_embed_.p,
                     x_.p, layers_[0]->ln1_g.p, layers_[0]->ln1_b.p, h_.p, d_, stream_, q8_first ? h8_.p : nullptr,
@@ -591,12 +649,12 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
   // weight scale (CODES / INT8) and activation scale (INT8) of one GEMM
   auto scales = [](GemmEpi& e, const GemmW& w, const float* a_scale) {
     e.w_scale = w.mode == W_VALUES ? nullptr : w.scale.p;
-    e.a_scale = w.mode == W_INT8 ? a_scale : nullptr;
+    e.a_scale = w.int8() ? a_scale : nullptr;
   };
   for (int l = 0; l < L_; ++l) {
     Layer& ly = *layers_[l];
-    const bool i8_qkv = ly.qkv.mode == W_INT8, i8_o = ly.o.mode == W_INT8;
-    const bool i8_in = ly.in.mode == W_INT8, i8_out = ly.out.mode == W_INT8;
+    const bool i8_qkv = ly.qkv.int8(), i8_o = ly.o.int8();
+    const bool i8_in = ly.in.int8(), i8_out = ly.out.int8();
     GemmEpi ep;
     ep.M = T;
     // QKV projection; K/V scattered into the paged pool by the epilogue.
@@ -615,7 +673,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     ep.page_size = PAGE;
     scales(ep, ly.qkv, hs_.p);
     timed(1, 2.0 * dT * 3 * ly.kh * d_, [&] {
-      gemm(iolmk::EPI_QKV, i8_qkv, i8_qkv ? tm_h8_ : tm_h_, ly.qkv.tm, T, 3 * ly.kh, d_, ep);
+      gemm_w(iolmk::EPI_QKV, ly.qkv, i8_qkv ? tm_h8_ : tm_h_, tm_h8s_, T, 3 * ly.kh, d_, ep);
     });
     AttnParams ap{};
     ap.q_map = tm_q_;
@@ -657,7 +715,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     eo.ldo = d_;
     scales(eo, ly.o, zs_.p);
     timed(4, 2.0 * dT * d_ * ly.kh, [&] {
-      gemm(iolmk::EPI_RESID_F32, i8_o, i8_o ? ly.tm_z8 : ly.tm_z, ly.o.tm, T, d_, ly.kh, eo);
+      gemm_w(iolmk::EPI_RESID_F32, ly.o, i8_o ? ly.tm_z8 : ly.tm_z, ly.tm_z8s, T, d_, ly.kh, eo);
     });
     // h = LN2(x)
     timed(5, dT * d_ * 6.0, [&] {
@@ -672,7 +730,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     ei.ldo = f_ld_max_;
     scales(ei, ly.in, hs_.p);
     timed(6, 2.0 * dT * ly.f * d_, [&] {
-      gemm(iolmk::EPI_GELU_BF16, i8_in, i8_in ? tm_h8_ : tm_h_, ly.in.tm, T, ly.f, d_, ei);
+      gemm_w(iolmk::EPI_GELU_BF16, ly.in, i8_in ? tm_h8_ : tm_h_, tm_h8s_, T, ly.f, d_, ei);
     });
     // x += g * Wout^T
     if (i8_out) {
@@ -682,10 +740,10 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     GemmEpi eo2 = eo;
     scales(eo2, ly.out, gs_.p);
     timed(7, 2.0 * dT * d_ * ly.f, [&] {
-      gemm(iolmk::EPI_RESID_F32, i8_out, i8_out ? ly.tm_g8 : ly.tm_g, ly.out.tm, T, d_, ly.f, eo2);
+      gemm_w(iolmk::EPI_RESID_F32, ly.out, i8_out ? ly.tm_g8 : ly.tm_g, ly.tm_g8s, T, d_, ly.f, eo2);
     });
     if (l + 1 < L_) {
-      const bool q8_next = layers_[l + 1]->qkv.mode == W_INT8;
+      const bool q8_next = layers_[l + 1]->qkv.int8();
       timed(5, dT * d_ * 6.0, [&] {
         launch_ln(x_.p, T, d_, layers_[l + 1]->ln1_g.p, layers_[l + 1]->ln1_b.p, h_.p, d_, stream_,
                   q8_next ? h8_.p : nullptr, hs_.p);

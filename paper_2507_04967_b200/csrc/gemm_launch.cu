@@ -51,6 +51,7 @@ static void dispatch_epi(int epi, const CUtensorMap& A, const CUtensorMap& B, in
     case EPI_GELU_BF16: return launch_one<BN, EPI_GELU_BF16, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
     case EPI_RESID_F32: return launch_one<BN, EPI_RESID_F32, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
     case EPI_QKV: return launch_one<BN, EPI_QKV, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_NONE: return launch_one<BN, EPI_NONE, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
     default: break;
   }
   throw Unsupported("gemm: epilogue not instantiated for this operand type");

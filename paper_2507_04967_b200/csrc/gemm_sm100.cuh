@@ -27,6 +27,7 @@ enum EpiMode : int {
   EPI_RESID_F32 = 3,  // resid f32 [M x ldo] += acc   (x += z*Wo^T, x += g*Wout^T)
   EPI_QKV = 4,        // cols [0,kh) -> q bf16; [kh,2kh) -> K pages; [2kh,3kh) -> V pages
   EPI_S32 = 5,        // raw int32 accumulators [M x ldo] (integer GEMM parity tests)
+  EPI_NONE = 6,       // kernel tuning only: accumulators are drained but not read (mainloop rate)
 };
 
 struct GemmEpi {
@@ -55,12 +56,14 @@ struct GemmCfg {
   static constexpr int TILE_M = BM * CG;
   static constexpr int BN_CTA = BN / CG;  // W rows staged per CTA
   static constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per operand row
+  // 8 epilogue warps (2 per TMEM lane quarter). 16 warps were measured too: no gain here (this
+  // epilogue stages through smem and competes with the MMA for it), unlike the sparse kernel's.
+  static constexpr int EPI_WARPS = 8;
   static constexpr int STAGES = CG == 2 ? (BN >= 256 ? 5 : 7) : (BN >= 256 ? 4 : 5);
   static constexpr uint32_t A_BYTES = BM * BK_BYTES;
   static constexpr uint32_t B_BYTES = BN_CTA * BK_BYTES;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
-  static constexpr int EPI_WARPS = 8;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
   static constexpr size_t SMEM =
       1024 + STAGES * STAGE_BYTES + 512 + BN * 4 + EPI_WARPS * 5120;  // ring, barriers, scales, tiles
@@ -388,8 +391,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
   } else {
     const int e = warp - 2;
     const int q = warp & 3;                   // TMEM lane quarter this warp may access
-    const int c_begin = (e >> 2) * (BN / 2);  // column half handled by this warp
-    constexpr int NCH = BN / 64;              // 32-column chunks per warp per tile
+    constexpr int WCOLS = BN / (C::EPI_WARPS / 4);  // columns drained per warp per tile
+    const int c_begin = (e >> 2) * WCOLS;        // this warp's column range
+    constexpr int NCH = WCOLS / 32;              // 32-column chunks per warp per tile
     const uint32_t leader_tempty0 = CG == 2 ? mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
     float* s_scale = reinterpret_cast<float*>(smem_raw + (bars + 512 - raw));  // [BN] per tile
     uint8_t* s_warp = smem_raw + (bars + 512 + BN * 4 - raw) + e * 5120;
@@ -423,6 +427,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      if constexpr (EPI == EPI_NONE) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_remote(leader_tempty0 + 8u * acc);
+          else mbar_arrive(tempty_bar(acc));
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1u;
+        continue;
+      }
       // TMEM loads double-buffered across chunks: chunk c+1 is in flight while c is processed
       uint32_t r[2][32];
       tmem_ld_32x32b_x32(tbase + c_begin, r[0]);
@@ -485,7 +500,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(leader_tempty0 + 8u * acc);
+        if constexpr (CG == 2) mbar_arrive_remote(leader_tempty0 + 8u * acc);
         else mbar_arrive(tempty_bar(acc));
       }
       acc ^= 1;

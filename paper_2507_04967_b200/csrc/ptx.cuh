@@ -99,6 +99,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Arrive on a (possibly remote) cluster mbarrier with the default CTA-scope release: enough to
+// order this warp's completed tcgen05.ld (fenced by tcgen05.fence::before_thread_sync) before the
+// MMA warp's reuse of the accumulator, without waiting for the warp's global stores to drain
+// (a cluster-scope release compiles to a MEMBAR/ERRBAR on every tile).
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // 2-SM TMA load: data lands in this CTA's smem, completion bytes are counted on the pair leader's
 // mbarrier (bar must be the leader's barrier address).
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar,

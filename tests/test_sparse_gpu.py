@@ -1,0 +1,115 @@
+"""2:4 structured-sparse W8A8 on the sparse tensor cores (tcgen05.mma.sp kind::i8).
+
+The sparse kernel consumes the bundle's sparse24_q8 payload as stored (kept codes + position
+nibbles, proj/src/model.cpp:255-290; decode semantics :177-199). Checks:
+* integer accumulators are bit-exact against X_s8 . dense(W)^T (the CPU restatement of
+  decode_tensor's expansion with exact integer sums) over regular, tail and irregular shapes;
+* the scaled epilogue (acc * s_a[token]) * s_w[channel] equals the f32 restatement bit-for-bit;
+* the whole engine with sparse MMAs is bitwise identical (logits and greedy ids) to the same
+  W8A8 engine with the weights expanded to dense int8 (sparse_mma off), including pruned and
+  irregular shapes (C3/C3b), and batch invariance holds.
+"""
+import numpy as np
+import pytest
+
+from paper_2507_04967_b200 import runtime as R
+from paper_2507_04967_b200 import synth
+
+pytestmark = pytest.mark.gpu
+TOY = (128, 4, 4, 512, 160)
+PAIRS = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
+
+
+def make_sparse24(rng, N, K):
+    """A sparse24_q8 tensor payload (codes, position nibbles, scales) and its dense int8 twin."""
+    G = K // 4
+    sel = rng.integers(0, 6, size=(N, G))
+    pos = np.array(PAIRS, np.uint8)[sel]                              # [N, G, 2] ascending
+    codes = rng.integers(-127, 128, size=(N, G, 2)).astype(np.int8)
+    nib = (pos[..., 0] | (pos[..., 1] << 2)).astype(np.uint8)         # [N, G]
+    if G % 2:
+        nib = np.concatenate([nib, np.zeros((N, 1), np.uint8)], axis=1)
+    idx = (nib[:, 0::2] | (nib[:, 1::2] << 4)).astype(np.uint8)        # low nibble = even group
+    scales = rng.uniform(1e-3, 2e-2, size=N).astype(np.float32)
+    payload = codes.tobytes() + idx.tobytes() + scales.tobytes()
+    dense = np.zeros((N, G, 4), np.int8)
+    n_i, g_i = np.meshgrid(np.arange(N), np.arange(G), indexing="ij")
+    dense[n_i, g_i, pos[..., 0]] = codes[..., 0]
+    dense[n_i, g_i, pos[..., 1]] = codes[..., 1]
+    return np.frombuffer(payload, np.uint8).copy(), dense.reshape(N, K), scales
+
+
+def run_sp(lib, X, payload, N, epi=5, a_scale=None):
+    T, K = X.shape
+    out_i = np.zeros((T, N), np.int32)
+    out_f = np.zeros((T, N), np.float32)
+    a = np.zeros(T, np.float32) if a_scale is None else np.ascontiguousarray(a_scale, np.float32)
+    st = lib.iolm_cuda_debug_gemm_sp24(np.ascontiguousarray(X).ctypes.data, payload.ctypes.data, T, N, K, epi,
+                                       a.ctypes.data, out_i.ctypes.data, out_f.ctypes.data)
+    assert st == 0, lib.iolm_cuda_last_error()
+    return out_i if epi == 5 else out_f
+
+
+@pytest.mark.parametrize("T,N,K", [
+    (224, 256, 256), (300, 1920, 1280), (1000, 2560, 1280), (77, 1280, 2560), (18944, 384, 640),
+    (513, 130, 2512), (5, 16, 16),
+])
+def test_sp24_s32_bitexact(engine_lib, T, N, K):
+    rng = np.random.default_rng(T + 3 * N + 7 * K)
+    payload, Wd, _ = make_sparse24(rng, N, K)
+    X = rng.integers(-127, 128, size=(T, K)).astype(np.int8)
+    got = run_sp(engine_lib, X, payload, N)
+    want = (X.astype(np.float64) @ Wd.astype(np.float64).T).astype(np.int64)  # exact: |sum| < 2^53
+    assert np.array_equal(got.astype(np.int64), want)
+
+
+def test_sp24_scaled_epilogue_bitexact(engine_lib):
+    rng = np.random.default_rng(11)
+    T, N, K = 450, 640, 1280
+    payload, Wd, scales = make_sparse24(rng, N, K)
+    X = rng.integers(-127, 128, size=(T, K)).astype(np.int8)
+    a = rng.uniform(1e-3, 5e-2, size=T).astype(np.float32)
+    got = run_sp(engine_lib, X, payload, N, epi=0, a_scale=a)
+    acc = (X.astype(np.float64) @ Wd.astype(np.float64).T).astype(np.int64).astype(np.float32)
+    want = (acc * a[:, None]).astype(np.float32) * scales[None, :]
+    assert np.array_equal(got, want.astype(np.float32))
+
+
+def test_sp24_rejects_unordered_positions(engine_lib):
+    rng = np.random.default_rng(5)
+    payload, _, _ = make_sparse24(rng, 16, 64)
+    G = 16
+    payload[16 * G * 2] = 0x01 | (0x4 << 4)  # row 0 group 0: p0 = 1, p1 = 0 (descending)
+    X = np.zeros((8, 64), np.int8)
+    out = np.zeros((8, 16), np.int32)
+    st = engine_lib.iolm_cuda_debug_gemm_sp24(X.ctypes.data, payload.ctypes.data, 8, 16, 64, 5, None,
+                                              out.ctypes.data, None)
+    assert st == 3
+
+
+@pytest.mark.parametrize("heads,ffn", [
+    (None, None),                               # dense shapes
+    ([2, 2, 2, 2], [256, 256, 256, 256]),      # C3-style 50% pruning
+    ([1, 3, 2, 4], [124, 500, 260, 388]),      # C3b irregular (FFN widths % 4 == 0, odd group counts)
+])
+def test_engine_sparse_equals_dense_int8(heads, ffn):
+    b = synth.toy_bundle(*TOY, seed=42, quant="sparse24", heads=heads, ffn=ffn)
+    sp = R.ModelRuntime(b, act_quant=True)
+    dn = R.ModelRuntime(b, act_quant=True, sparse_mma=False)
+    ids, offs = synth.rows(60, 3, 64)
+    for r in range(3):
+        row = ids[offs[r]:offs[r + 1]]
+        assert np.array_equal(sp.forward(row), dn.forward(row))
+    ids, offs = synth.rows(0, 64, 64)
+    gi, gl, gm = sp.decode_token_rows(ids, offs, 8)
+    di, dl, dm = dn.decode_token_rows(ids, offs, 8)
+    assert gm == dm and np.array_equal(gl, dl) and np.array_equal(gi, di)
+
+
+def test_engine_sparse_batch_invariance():
+    b = synth.toy_bundle(*TOY, seed=42, quant="sparse24", heads=[2, 2, 2, 2], ffn=[256] * 4)
+    rt = R.ModelRuntime(b, act_quant=True)
+    prompts = synth.row_strings(900, 16, 64)
+    full = rt.batch_decode(prompts, 8)
+    for i in [0, 7, 15]:
+        assert rt.batch_decode([prompts[i]], 8) == [full[i]]
