@@ -51,7 +51,8 @@ typedef struct iolm_cuda_opts {
   int32_t use_cuda_graph;      /* reserved */
   int32_t kernel_timing;       /* 1: time every kernel class with CUDA events (iolm_cuda_kernel_times) */
   int32_t sparse_mma;          /* -1: expand sparse24_q8 to dense int8; 0/1: 2:4 sparse tensor cores (W8A8) */
-  int32_t reserved[8];
+  int32_t int4_mma;            /* -1: expand q4 codes to bf16 in HBM; 0/1: int4 in HBM, expanded in smem (W4A16) */
+  int32_t reserved[7];
 } iolm_cuda_opts;
 
 /* ModelConfig (proj/include/iolm/model.hpp:20-41); per-layer lists are queried separately. */
@@ -145,7 +146,8 @@ int iolm_cuda_debug_gemm_s8(const int8_t* A, const int8_t* W, int32_t* C, int32_
                             int32_t K, int32_t pair);
 
 /* Device-only GEMM timing (kernel tuning): mean ms per launch of `iters` launches on synthetic
- * operands. epi: 0 f32, 1 bf16, 2 gelu, 3 residual-add, 5 s32 (i8 only). */
+ * operands. epi: 0 f32, 1 bf16, 2 gelu, 3 residual-add, 5 s32 (i8 only), 6 none (mainloop only).
+ * i8: 0 bf16 x bf16, 1 s8 x s8 (W8A8), 2 bf16 x int4 (W4A16, K % 32 == 0). */
 int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_t epi, int32_t pair, int32_t i8,
                               int32_t iters, float* ms_out);
 
@@ -157,6 +159,11 @@ int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_t epi, int3
  * -> out_f32 (w_scale = the payload's per-row scales). K % 16 == 0. */
 int iolm_cuda_debug_gemm_sp24(const int8_t* X, const uint8_t* payload, int32_t T, int32_t N, int32_t K,
                               int32_t epi, const float* a_scale, int32_t* out_s32, float* out_f32);
+/* W4A16 GEMM: C[M x N] = A_bf16[M x K] * (codes(W) * scale)^T with W a q4_perchannel tensor payload
+ * exactly as stored in a bundle (nibble rows + per-row f32 scales, proj/src/model.cpp:164-176); the
+ * int4 codes are expanded to bf16 inside the kernel. epi 0: f32 out. pair as in debug_gemm_s8. */
+int iolm_cuda_debug_gemm_w4(const uint16_t* A, const uint8_t* payload, float* C, int32_t M, int32_t N, int32_t K,
+                            int32_t pair);
 /* Device-only timing of the sparse GEMM: mean ms per launch (epi as in debug_gemm_time). */
 int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, float* ms_out);
 

@@ -37,7 +37,8 @@ class Opts(C.Structure):
         ("use_cuda_graph", C.c_int32),
         ("kernel_timing", C.c_int32),
         ("sparse_mma", C.c_int32),
-        ("reserved", C.c_int32 * 8),
+        ("int4_mma", C.c_int32),
+        ("reserved", C.c_int32 * 7),
     ]
 
 
@@ -83,6 +84,8 @@ SIGNATURES = {
                                           C.c_int32, C.c_int32]),
     "iolm_cuda_debug_gemm_sp24": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                             C.c_void_p, C.c_void_p, C.c_void_p]),
+    "iolm_cuda_debug_gemm_w4": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                          C.c_int32]),
     "iolm_cuda_debug_gemm_sp24_time": (C.c_int, [C.c_int32] * 5 + [C.POINTER(C.c_float)]),
 }
 

@@ -120,31 +120,39 @@ extern "C" int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_
   return guarded([&] {
     if (M <= 0 || N <= 0 || K <= 0 || iters <= 0) throw ContractViolation("debug_gemm_time: bad sizes");
     const size_t eb = i8 ? 1 : 2;
-    DevBuf<uint8_t> dA(static_cast<size_t>(M) * K * eb), dW(static_cast<size_t>(N) * K * eb);
+    if (i8 == 2 && K % 32 != 0) throw ContractViolation("debug_gemm_time: W4 needs K % 32 == 0");
+    DevBuf<uint8_t> dA(static_cast<size_t>(M) * K * 2), dW(static_cast<size_t>(N) * K * eb);
     DevBuf<float> dC(static_cast<size_t>(M) * N), ws(N), as(M);
-    CUDA_OK(cudaMemset(dA.p, 0x11, static_cast<size_t>(M) * K * eb));
+    CUDA_OK(cudaMemset(dA.p, 0x11, static_cast<size_t>(M) * K * 2));
     CUDA_OK(cudaMemset(dW.p, 0x13, static_cast<size_t>(N) * K * eb));
     CUDA_OK(cudaMemset(dC.p, 0, sizeof(float) * M * N));
     CUDA_OK(cudaMemset(ws.p, 0, sizeof(float) * N));
     CUDA_OK(cudaMemset(as.p, 0, sizeof(float) * M));
     const auto dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    CUtensorMap ta = make_kmajor_map(dA.p, dt, static_cast<int>(eb), K, M, eb * K, 128);
-    CUtensorMap tb = make_kmajor_map(dW.p, dt, static_cast<int>(eb), K, N, eb * K, 128);
+    const bool w4 = i8 == 2;  // W4A16: bf16 activations, packed int4 weights (K/2 bytes per row)
+    const auto dt_a = w4 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : dt;
+    const size_t eb_a = w4 ? 2 : eb;
+    if (w4) i8 = 0;
+    CUtensorMap ta = make_kmajor_map(dA.p, dt_a, static_cast<int>(eb_a), K, M, eb_a * K, 128);
+    CUtensorMap tb = w4 ? make_w4_map(dW.p, K, N, static_cast<uint64_t>(K) / 2)
+                        : make_kmajor_map(dW.p, dt, static_cast<int>(eb), K, N, eb * K, 128);
     iolmk::GemmEpi ep;
     ep.M = M;
     ep.N = N;
     ep.out = dC.p;
     ep.ldo = N;
-    if (i8) {
-      ep.a_scale = as.p;
-      ep.w_scale = ws.p;
-    }
+    if (i8 || w4) ep.w_scale = ws.p;
+    if (i8) ep.a_scale = as.p;
     cudaEvent_t e0, e1;
     CUDA_OK(cudaEventCreate(&e0));
     CUDA_OK(cudaEventCreate(&e1));
-    launch_gemm(pair != 0, i8 != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
+    auto go = [&] {
+      if (w4) launch_gemm_w4(pair != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
+      else launch_gemm(pair != 0, i8 != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
+    };
+    go();
     CUDA_OK(cudaEventRecord(e0));
-    for (int i = 0; i < iters; ++i) launch_gemm(pair != 0, i8 != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
+    for (int i = 0; i < iters; ++i) go();
     CUDA_OK(cudaEventRecord(e1));
     CUDA_OK(cudaEventSynchronize(e1));
     float ms = 0;
@@ -233,5 +241,30 @@ extern "C" int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, i
     *ms_out = ms / iters;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+  });
+}
+
+extern "C" int iolm_cuda_debug_gemm_w4(const uint16_t* A, const uint8_t* payload, float* C, int32_t M, int32_t N,
+                                       int32_t K, int32_t pair) {
+  return guarded([&] {
+    if (M <= 0 || N <= 0 || K <= 0 || K % 8 != 0) throw ContractViolation("debug_gemm_w4: need K % 8 == 0");
+    const size_t rb = static_cast<size_t>(K + 1) / 2, ld4 = (rb + 15) / 16 * 16;
+    DevBuf<uint16_t> dA(static_cast<size_t>(M) * K);
+    DevBuf<uint8_t> dW(static_cast<size_t>(N) * ld4);
+    DevBuf<float> dS(N), dC(static_cast<size_t>(M) * N);
+    CUDA_OK(cudaMemcpy(dA.p, A, sizeof(uint16_t) * M * K, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy2D(dW.p, ld4, payload, rb, rb, N, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dS.p, payload + rb * N, sizeof(float) * N, cudaMemcpyHostToDevice));
+    CUtensorMap ta = make_kmajor_map(dA.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, M, 2ull * K, 128);
+    CUtensorMap tb = make_w4_map(dW.p, K, N, ld4);
+    iolmk::GemmEpi ep;
+    ep.M = M;
+    ep.N = N;
+    ep.out = dC.p;
+    ep.ldo = N;
+    ep.w_scale = dS.p;
+    launch_gemm_w4(pair != 0, iolmk::EPI_F32, ta, tb, M, N, K, ep, nullptr, sm_count());
+    CUDA_OK(cudaDeviceSynchronize());
+    CUDA_OK(cudaMemcpy(C, dC.p, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
   });
 }

@@ -117,14 +117,17 @@ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 //   INT8   : int8 code + f32 scale per row     q8 / sparse24 with act_quant (W8A8, kind::i8)
 //   SP24   : kept int8 codes [N x K/2] + 2:4 metadata + f32 scale per row: sparse24_q8 with
 //            act_quant on the sparse tensor cores (tcgen05.mma.sp kind::i8, gemm_sp_sm100.cuh)
-enum WMode : int { W_VALUES = 0, W_CODES = 1, W_INT8 = 2, W_SP24 = 3 };
+//   INT4   : packed q4 nibbles [N x ceil(K/2)] + f32 scale per row: W4A16, the codes are expanded
+//            to bf16 inside the GEMM (shared memory), never in HBM
+enum WMode : int { W_VALUES = 0, W_CODES = 1, W_INT8 = 2, W_SP24 = 3, W_INT4 = 4 };
 struct GemmW {
   int mode = W_VALUES;
   DevArray<__nv_bfloat16> wb;
   DevArray<int8_t> w8;
   DevArray<float> scale;
   CUtensorMap tm;
-  // W_SP24
+  // W_SP24 (metadata) / W_INT4 (packed nibbles)
+  DevArray<uint8_t> w4;
   DevArray<uint8_t> meta;
   Sp24Layout sl;
   CUtensorMap tm_e;
@@ -243,6 +246,7 @@ class Engine {
   bool prefix_sharing_ = true;
   bool act_quant_ = false;
   bool sparse_mma_ = true;
+  bool int4_mma_ = true;
   uint64_t madds_A_ = 0, madds_B_ = 0;  // sum_l (4*d*kh + 2*d*f), sum_l kh
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
@@ -306,6 +310,7 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
     if (opts->prefix_sharing < 0) prefix_sharing_ = false;
     ktime_ = opts->kernel_timing != 0;
     if (opts->sparse_mma < 0) sparse_mma_ = false;
+    if (opts->int4_mma < 0) int4_mma_ = false;
   }
   // Default token budget: one 256-row GEMM M-tile per SM pair (74 x 256 = 18944 on a 148-SM B200),
   // so every projection's tile count is a whole number of waves of the persistent GEMM grid.
@@ -377,12 +382,14 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
   std::vector<const TensorRecord*> ts;
   int N = 0;
   bool all_dense = true, all_quant = true, int8_ok = true, sp_ok = act_quant_ && sparse_mma_;
+  bool q4_ok = !act_quant_ && int4_mma_;
   for (const auto& n : names) {
     ts.push_back(&b.tensor(n));
     N += ts.back()->rows;
     all_dense = all_dense && ts.back()->encoding == ENC_DENSE_F32;
     all_quant = all_quant && ts.back()->encoding != ENC_DENSE_F32;
     int8_ok = int8_ok && (ts.back()->encoding == ENC_Q8 || ts.back()->encoding == ENC_SPARSE24_Q8);
+    q4_ok = q4_ok && ts.back()->encoding == ENC_Q4;
     sp_ok = sp_ok && ts.back()->encoding == ENC_SPARSE24_Q8 &&
             sp24_check(b.payload(*ts.back()), ts.back()->rows, ts.back()->cols);
   }
@@ -407,6 +414,25 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
     CUDA_OK(cudaMemcpy(w.scale.p, scales.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
     w.tm = sp24_codes_map(w.sl, w.w8.p);
     w.tm_e = sp24_meta_map(w.sl, w.meta.p);
+    (void)ld;
+    return;
+  }
+  if (w.mode == W_CODES && q4_ok) {
+    // W4A16: the bundle's nibble rows (ceil(K/2) bytes, low nibble = even column) re-pitched to 16 B
+    w.mode = W_INT4;
+    const size_t rb = static_cast<size_t>(K + 1) / 2, ld4 = (rb + 15) / 16 * 16;
+    w.w4.alloc(static_cast<size_t>(N) * ld4);
+    w.scale.alloc(N);
+    CUDA_OK(cudaMemset(w.w4.p, 0x88, static_cast<size_t>(N) * ld4));  // pad bytes: codes 0
+    int row0 = 0;
+    for (auto* t : ts) {
+      const uint8_t* pl = b.payload(*t);
+      CUDA_OK(cudaMemcpy2D(w.w4.p + static_cast<size_t>(row0) * ld4, ld4, pl, rb, rb, t->rows, cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(w.scale.p + row0, pl + static_cast<size_t>(t->rows) * rb, sizeof(float) * t->rows,
+                         cudaMemcpyHostToDevice));
+      row0 += t->rows;
+    }
+    w.tm = make_w4_map(w.w4.p, static_cast<uint64_t>(K), static_cast<uint64_t>(N), ld4);
     (void)ld;
     return;
   }
@@ -554,6 +580,9 @@ void Engine::gemm_w(int epi, const GemmW& w, const CUtensorMap& act, const CUten
                     const GemmEpi& ep) {
   if (w.mode == W_SP24) {
     launch_gemm_sp(epi, w.tm, act_sp, w.tm_e, K, w.sl.katoms_pad, ep, stream_, sms_);
+    ++stats_.kernel_launches;
+  } else if (w.mode == W_INT4) {
+    launch_gemm_w4(use_pair(M, N), epi, act, w.tm, M, N, K, ep, stream_, sms_);
     ++stats_.kernel_launches;
   } else {
     gemm(epi, w.mode == W_INT8, act, w.tm, M, N, K, ep);

@@ -9,11 +9,11 @@ namespace iolmh {
 
 using namespace iolmk;
 
-template <int BN, int EPI, int CG, bool I8>
+template <int BN, int EPI, int CG, bool I8, bool W4 = false>
 static void launch_one(const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep,
                        cudaStream_t st, int grid_cap) {
-  using Cfg = GemmCfg<BN, CG>;
-  auto kern = gemm_tn_kernel<BN, EPI, CG, I8>;
+  using Cfg = GemmCfg<BN, CG, W4>;
+  auto kern = gemm_tn_kernel<BN, EPI, CG, I8, W4>;
   static bool configured = false;
   if (!configured) {
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM)));
@@ -55,6 +55,30 @@ static void dispatch_epi(int epi, const CUtensorMap& A, const CUtensorMap& B, in
     default: break;
   }
   throw Unsupported("gemm: epilogue not instantiated for this operand type");
+}
+
+// W4A16: B is the packed int4 weight map (make_w4_map), expanded to bf16 in shared memory.
+template <int BN, int CG>
+static void dispatch_w4(int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep,
+                        cudaStream_t st, int grid_cap) {
+  switch (epi) {
+    case EPI_F32: return launch_one<BN, EPI_F32, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_BF16: return launch_one<BN, EPI_BF16, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_GELU_BF16: return launch_one<BN, EPI_GELU_BF16, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_RESID_F32: return launch_one<BN, EPI_RESID_F32, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_QKV: return launch_one<BN, EPI_QKV, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_NONE: return launch_one<BN, EPI_NONE, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
+    default: break;
+  }
+  throw Unsupported("gemm_w4: epilogue not instantiated");
+}
+
+void launch_gemm_w4(bool pair, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
+                    const GemmEpi& ep, cudaStream_t st, int grid_cap) {
+  if (M <= 0 || N <= 0) return;
+  if (pair) dispatch_w4<256, 2>(epi, A, B, M, N, K, ep, st, grid_cap);
+  else dispatch_w4<128, 1>(epi, A, B, M, N, K, ep, st, grid_cap);
+  CUDA_OK(cudaGetLastError());
 }
 
 // pair = true: 2-SM 256x256 tiles; false: single-CTA 128x128 tiles.

@@ -50,7 +50,11 @@ struct GemmEpi {
 // Tile configuration. CG = 2 runs the 2-SM UMMA: a CTA pair computes a 256 x BN tile, each CTA
 // stages its own 128 rows of A and half (BN/2 rows) of the W tile, the leader CTA issues
 // tcgen05.mma.cta_group::2, and each CTA drains its 128 accumulator lanes from its own TMEM.
-template <int BN, int CG>
+// W4 = true: W4A16. The weights stay int4 (the bundle's q4 nibbles, re-pitched) in HBM; TMA
+// stages the packed tile (BN_CTA rows x 32 B per 64 K) and CONV_WARPS converter warps expand it
+// in shared memory into the bf16 SWIZZLE_128B operand tile the MMA reads (code - 8, exact in bf16;
+// the per-channel scale is applied in the epilogue as for the other code forms).
+template <int BN, int CG, bool W4 = false>
 struct GemmCfg {
   static constexpr int BM = 128;        // rows per CTA
   static constexpr int TILE_M = BM * CG;
@@ -64,10 +68,38 @@ struct GemmCfg {
   static constexpr uint32_t B_BYTES = BN_CTA * BK_BYTES;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
-  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
-  static constexpr size_t SMEM =
-      1024 + STAGES * STAGE_BYTES + 512 + BN * 4 + EPI_WARPS * 5120;  // ring, barriers, scales, tiles
+  static constexpr int CONV_WARPS = W4 ? 4 : 0;
+  static constexpr uint32_t RAW_BYTES = W4 ? BN_CTA * 32 : 0;  // packed int4 per stage
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS + 32 * CONV_WARPS;
+  static constexpr size_t SMEM = 1024 + STAGES * (STAGE_BYTES + RAW_BYTES) + 512 + BN * 4 +
+                                 EPI_WARPS * 5120;  // rings, barriers, scales, tiles
+  static_assert(!W4 || BN_CTA == 128, "W4 converter maps one thread per staged weight row");
 };
+
+// Expands 4 packed bytes (8 int4 codes, low nibble first) into 4 bf16x2 words of (nibble - 8):
+// bf16(128 + n) has bit pattern 0x4300 | n, and 128 + n - 136 is exact in bf16. Byte permutes build
+// the 0x43nn halves (12 instructions per 8 codes).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ void int4x8_to_bf16(uint32_t x, uint32_t (&w)[4]) {
+  const uint32_t lo = x & 0x0F0F0F0Fu, hi = (x >> 4) & 0x0F0F0F0Fu;  // codes 0,2,4,6 / 1,3,5,7
+  const uint32_t u = prmt(lo, hi, 0x5140u), v = prmt(lo, hi, 0x7362u);  // codes 0..3 / 4..7 in order
+  const uint32_t c43 = 0x43434343u;
+  const uint32_t t[4] = {prmt(u, c43, 0x4140u), prmt(u, c43, 0x4342u), prmt(v, c43, 0x4140u),
+                         prmt(v, c43, 0x4342u)};
+  const __nv_bfloat162 off = __floats2bfloat162_rn(136.f, 136.f);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&t[i]), off);
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 template <int EPI>
 __device__ __forceinline__ void epi_apply(const GemmEpi& ep, int m, int n0, float (&v)[32]) {
@@ -260,24 +292,26 @@ __device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* til
   __syncwarp();
 }
 
-template <int BN, int EPI, int CG, bool I8>
-__global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
+template <int BN, int EPI, int CG, bool I8, bool W4 = false>
+__global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, GemmEpi ep) {
-  using C = GemmCfg<BN, CG>;
+  using C = GemmCfg<BN, CG, W4>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   const uint32_t sA = base;
   const uint32_t sB = base + STAGES * C::A_BYTES;
-  const uint32_t bars = sB + STAGES * C::B_BYTES;
+  const uint32_t sRaw = sB + STAGES * C::B_BYTES;  // W4: packed int4 staging ring
+  const uint32_t bars = sRaw + STAGES * C::RAW_BYTES;
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * STAGES + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (2 * STAGES + 2 + a); };
   const uint32_t tmem_slot = bars + 8u * (2 * STAGES + 4);
   const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - raw));
+  auto raw_full_bar = [&](int s) { return bars + 8u * (2 * STAGES + 5 + s); };  // W4, CTA-local
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -286,8 +320,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 1);  // pair: the leader's expect_tx covers both CTAs' bytes
+      // pair: the leader's expect_tx covers both CTAs' TMA bytes; W4 adds one arrival per CTA
+      // from the converter warp that expanded that CTA's B tile of the stage
+      mbar_init(full_bar(s), W4 ? 1 + CG : 1);
       mbar_init(empty_bar(s), 1);
+      if constexpr (W4) mbar_init(raw_full_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
@@ -326,7 +363,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         const int brow = nt * BN + static_cast<int>(rank) * C::BN_CTA;
         for (int kb = 0; kb < kbs; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
-          if constexpr (CG == 2) {
+          if constexpr (W4) {
+            // A as usual; the packed weight tile goes to this CTA's raw ring (local barrier)
+            mbar_expect_tx(raw_full_bar(stage), C::RAW_BYTES);
+            tma_load_2d(sRaw + stage * C::RAW_BYTES, &tmB, raw_full_bar(stage), kb * 32, brow);
+            if constexpr (CG == 2) {
+              if (leader) mbar_expect_tx(full_bar(stage), 2 * C::A_BYTES);
+              tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, leader_full0 + 8u * stage, kb * KELEMS, arow);
+            } else {
+              mbar_expect_tx(full_bar(stage), C::A_BYTES);
+              tma_load_2d(sA + stage * C::A_BYTES, &tmA, full_bar(stage), kb * KELEMS, arow);
+            }
+          } else if constexpr (CG == 2) {
             const uint32_t lf = leader_full0 + 8u * stage;
             // The peer's bytes may land on the leader's barrier before the leader's expect_tx of
             // the same phase: the transaction count goes transiently negative, which the
@@ -359,7 +407,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         tc_fence_after();
         const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
         for (int kb = 0; kb < kbs; ++kb) {
-          mbar_wait(full_bar(stage), phase);
+          if constexpr (W4 && CG == 2) mbar_wait_acq_cluster(full_bar(stage), phase);  // peer converters
+          else mbar_wait(full_bar(stage), phase);
           tc_fence_after();
           const uint64_t ad = smem_desc_k_sw128(sA + stage * C::A_BYTES);
           const uint64_t bd = smem_desc_k_sw128(sB + stage * C::B_BYTES);
@@ -388,6 +437,48 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       }
     }
     __syncwarp();
+  } else if (W4 && warp >= 2 + C::EPI_WARPS) {
+    // converters: warp cw expands every CONV_WARPS-th stage on its own (4 stages in flight, so the
+    // per-stage fence / barrier latency of one warp overlaps the others' conversion work). Lane l
+    // expands rows l, l + 32, l + 64, l + 96: 32 packed bytes (64 codes) -> one 128-byte
+    // SWIZZLE_128B row of the B tile (16-byte chunk c lands at chunk c ^ (r & 7)).
+    const int cw = warp - (2 + C::EPI_WARPS);
+    const uint32_t leader_full0 = CG == 2 ? mapa_shared(full_bar(0), 0) : full_bar(0);
+    int stage = 0, seq = 0;
+    uint32_t phase = 0;
+    for (int tile = group; tile < num_tiles; tile += n_groups) {
+      for (int kb = 0; kb < kbs; ++kb, ++seq) {
+        if (seq % C::CONV_WARPS == cw) {
+          mbar_wait(raw_full_bar(stage), phase);
+          const uint4* src = reinterpret_cast<const uint4*>(smem_raw + (sRaw + stage * C::RAW_BYTES - raw));
+          uint8_t* dst = smem_raw + (sB + stage * C::B_BYTES - raw);
+#pragma unroll
+          for (int i = 0; i < C::BN_CTA / 32; ++i) {
+            const int r = lane + 32 * i;
+            const uint4 p0 = src[2 * r], p1 = src[2 * r + 1];
+            const uint32_t words[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+            uint8_t* dst_row = dst + r * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              uint32_t w[4];
+              int4x8_to_bf16(words[c], w);
+              *reinterpret_cast<uint4*>(dst_row + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+          if constexpr (CG == 2) fence_release_smem_cluster();  // ... and to the leader's MMA issue
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_relaxed_cluster(leader_full0 + 8u * stage);
+            else mbar_arrive(full_bar(stage));
+          }
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
   } else {
     const int e = warp - 2;
     const int q = warp & 3;                   // TMEM lane quarter this warp may access

@@ -56,5 +56,8 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 // pair: 2-SM 256x256 tiles (clusters of 2) vs single-CTA 128x128 tiles; i8: W8A8 kind::i8.
 void launch_gemm(bool pair, bool i8, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
                  const iolmk::GemmEpi& ep, cudaStream_t st, int grid_cap);
+// W4A16: B = packed int4 weights [N x ceil(K/2) bytes] (make_w4_map), expanded to bf16 in smem.
+void launch_gemm_w4(bool pair, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
+                    const iolmk::GemmEpi& ep, cudaStream_t st, int grid_cap);
 
 }  // namespace iolmh

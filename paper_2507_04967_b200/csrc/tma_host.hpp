@@ -73,4 +73,24 @@ inline CUtensorMap make_rows_map_bf16(const void* ptr, uint64_t inner, uint64_t 
   return m;
 }
 
+// Packed int4 weights [rows x ceil(K/2) bytes] (two codes per byte, low nibble = even column: the
+// bundle's q4 layout, model.cpp:164-176) read in unswizzled boxes of 32 bytes (64 codes) x 128 rows.
+// Out-of-bounds bytes read as 0 (codes -8): they only ever meet zero-filled activations (k >= K) or
+// output columns the epilogue masks (n >= N).
+inline CUtensorMap make_w4_map(const void* ptr, uint64_t K, uint64_t rows, uint64_t row_stride_bytes) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(K + 1) / 2, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t es[2] = {1, 1};
+  if ((row_stride_bytes % 16) != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
+    throw std::runtime_error("int4 weight map must be 16-byte aligned with a 16-byte row stride");
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (int4 weights) failed with code " + std::to_string(r));
+  return m;
+}
+
 }  // namespace iolmh
