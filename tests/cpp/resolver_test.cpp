@@ -1,0 +1,192 @@
+// Streaming prompt() resolver (include/iolm_cuda_resolver.hpp) against the reference executor
+// (iolm::execute -> PromptResolver, /root/reference/proj/src/exec.cpp:84-159, :353-370).
+//
+// CPU build (default): the resolver drives the reference's own iolm::ModelRuntime, so every output
+// must be IDENTICAL to iolm::execute's, and so must the ExecStats it maintains (model_invocations,
+// cache_hits, cache_misses) for every batch size, cache capacity (incl. eviction) and device batch
+// size - the scenarios of proj/tests/test_query.cpp:375-431 plus streaming take_ready().
+// GPU build (-DWITH_GPU): the same scenarios with iolm::cuda::ModelRuntime (B200) as the model;
+// stats must still match the reference exactly, outputs must equal the GPU's own batch_decode of
+// the distinct prompts (batch invariance) and agree with the CPU reference on >= 95% of rows.
+// Built by oracle/Makefile (targets resolver / resolver_gpu) - test only.
+#define IOLM_CUDA_WITH_REFERENCE_TYPES
+#include <algorithm>
+#include <cstdio>
+#include <type_traits>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "iolm/exec.hpp"
+#include "iolm/rng.hpp"
+#include "iolm/sql.hpp"
+#include "iolm/table.hpp"
+#include "iolm/train.hpp"
+#include "iolm_cuda_resolver.hpp"
+
+static int fails = 0;
+#define EXPECT(c, msg)                                      \
+  do {                                                      \
+    if (!(c)) {                                             \
+      std::printf("FAIL %s (line %d)\n", msg, __LINE__);    \
+      ++fails;                                              \
+    }                                                       \
+  } while (0)
+
+namespace {
+
+iolm::Table words_table(int n, uint64_t seed) {
+  iolm::Table t;
+  t.name = "t";
+  iolm::Column c;
+  c.name = "w";
+  c.type = iolm::ColumnType::text;
+  iolm::Rng rng(seed);
+  for (int i = 0; i < n; ++i) {
+    std::string s;
+    for (int j = 0; j < 1 + static_cast<int>(rng.next_below(10)); ++j)
+      s.push_back(static_cast<char>('a' + rng.next_below(26)));
+    if (i % 2 == 1) s = c.texts[rng.next_below(c.texts.size())];  // ~50% duplicates
+    c.texts.push_back(s);
+  }
+  t.columns.push_back(c);
+  t.row_count = static_cast<size_t>(n);
+  return t;
+}
+
+struct RefRun {
+  std::vector<std::string> out;
+  iolm::ExecStats stats;
+};
+
+RefRun run_reference(const iolm::ModelRuntime& cpu, const iolm::Table& t, int batch, size_t capacity, int max_new) {
+  const iolm::QueryPlan plan = iolm::parse_query("SELECT prompt('echo ' || w) AS r FROM t");
+  iolm::PromptCache cache(capacity);
+  iolm::ExecOptions opts;
+  opts.batch_size = batch;
+  opts.max_new_tokens = max_new;
+  opts.cache_capacity = capacity;
+  RefRun r;
+  iolm::FlopCounter fc;
+  const iolm::Table out = iolm::execute(plan, {{"t", t}}, cpu, cache, opts, r.stats, fc);
+  r.out = out.columns[0].texts;
+  return r;
+}
+
+}  // namespace
+
+int main() {
+  iolm::Rng wrng(21);
+  const auto bundle = iolm::ToyModelParams::init(iolm::ModelConfig::dense(32, 2, 2, 64, 96), wrng).to_bundle();
+  const iolm::ModelRuntime cpu(bundle);
+#ifdef WITH_GPU
+  const iolm::cuda::ModelRuntime model(bundle);
+#else
+  const iolm::ModelRuntime& model = cpu;
+#endif
+  using Resolver = iolm::cuda::StreamingPromptResolver<std::remove_cv_t<std::remove_reference_t<decltype(model)>>,
+                                                       iolm::FlopCounter>;
+  const iolm::Table t = words_table(40, 5);
+  std::vector<std::string> prompts;
+  for (const auto& w : t.columns[0].texts) prompts.push_back("echo " + w);
+  const size_t distinct = std::set<std::string>(prompts.begin(), prompts.end()).size();
+
+  int scenarios = 0;
+  size_t agree = 0, total = 0;
+  for (int batch : {1, 4, 16, 64})
+    for (size_t capacity : {size_t{0}, size_t{3}, size_t{1024}})
+      for (size_t device_batch : {size_t{1}, size_t{7}, size_t{100000}}) {
+        const RefRun ref = run_reference(cpu, t, batch, capacity, 6);
+        iolm::cuda::PromptCache cache(capacity);
+        iolm::cuda::ResolverStats st;
+        iolm::FlopCounter fc;
+        Resolver res(model, cache, batch, 6, st, fc, device_batch);
+        const auto out = res.resolve(prompts);
+        ++scenarios;
+        EXPECT(out.size() == ref.out.size(), "row count");
+        EXPECT(st.model_invocations == ref.stats.model_invocations, "model_invocations");
+        EXPECT(st.cache_hits == ref.stats.cache_hits, "cache_hits");
+        EXPECT(st.cache_misses == ref.stats.cache_misses, "cache_misses");
+        if (capacity == 1024) EXPECT(st.model_invocations == distinct, "invocation law: distinct prompts");
+#ifdef WITH_GPU
+        // outputs = the GPU's own decode of each distinct prompt (batch invariance), rows aligned
+        const std::set<std::string> uset(prompts.begin(), prompts.end());
+        const std::vector<std::string> uniq(uset.begin(), uset.end());
+        iolm::FlopCounter f2;
+        const auto solo = model.batch_decode(std::span<const std::string>(uniq), 6, f2);
+        for (size_t i = 0; i < prompts.size(); ++i) {
+          const size_t k = std::lower_bound(uniq.begin(), uniq.end(), prompts[i]) - uniq.begin();
+          EXPECT(out[i] == solo[k], "gpu output = gpu batch_decode of the distinct prompt");
+          agree += out[i] == ref.out[i];
+          ++total;
+        }
+#else
+        EXPECT(out == ref.out, "outputs identical to iolm::execute");
+#endif
+      }
+
+  // streaming: rows pushed one at a time, outputs drained as they complete
+  {
+    const RefRun ref = run_reference(cpu, t, 16, 1024, 6);
+    iolm::cuda::PromptCache cache(1024);
+    iolm::cuda::ResolverStats st;
+    iolm::FlopCounter fc;
+    Resolver res(model, cache, 16, 6, st, fc, 5);
+    std::vector<std::string> got;
+    for (const auto& p : prompts) {
+      res.push(p);
+      for (auto& s : res.take_ready()) got.push_back(std::move(s));
+    }
+    res.finish();
+    for (auto& s : res.take_ready()) got.push_back(std::move(s));
+    EXPECT(got.size() == prompts.size(), "streaming row count");
+    EXPECT(st.model_invocations == ref.stats.model_invocations && st.cache_hits == ref.stats.cache_hits,
+           "streaming stats");
+#ifndef WITH_GPU
+    EXPECT(got == ref.out, "streaming outputs");
+#endif
+    // the same cache serves a second identical query entirely from hits
+    iolm::cuda::ResolverStats st2;
+    Resolver res2(model, cache, 16, 6, st2, fc, 5);
+    const auto again = res2.resolve(prompts);
+    EXPECT(st2.model_invocations == 0 && st2.cache_hits == prompts.size(), "second query all hits");
+    EXPECT(again == got, "second query outputs");
+  }
+
+  // SequenceTooLong carries the first row of the failing reference flush window
+  {
+    iolm::Table t2 = t;
+    t2.columns[0].texts.resize(20);
+    t2.columns[0].texts[17] = std::string(200, 'x');  // "echo " + 200 chars > max_seq_len 96
+    t2.row_count = 20;
+    std::string ref_msg, got_msg;
+    try {
+      run_reference(cpu, t2, 2, 0, 6);
+    } catch (const iolm::SequenceTooLong& e) {
+      ref_msg = e.what();
+    }
+    std::vector<std::string> p3;
+    for (const auto& w : t2.columns[0].texts) p3.push_back("echo " + w);
+    iolm::cuda::PromptCache cache(0);
+    iolm::cuda::ResolverStats st;
+    iolm::FlopCounter fc;
+    Resolver res(model, cache, 2, 6, st, fc, 100000);
+    try {
+      res.resolve(p3);
+    } catch (const iolm::SequenceTooLong& e) {
+      got_msg = e.what();
+    }
+    const auto tail = [](const std::string& s) { return s.substr(s.rfind(" (row ") == std::string::npos ? 0 : s.rfind(" (row ")); };
+    EXPECT(!ref_msg.empty() && !got_msg.empty(), "SequenceTooLong raised by both");
+    std::printf("SequenceTooLong: reference \"%s\" / resolver \"%s\"\n", ref_msg.c_str(), got_msg.c_str());
+    EXPECT(tail(ref_msg) == tail(got_msg), "SequenceTooLong row suffix");
+  }
+
+#ifdef WITH_GPU
+  std::printf("gpu vs cpu reference agreement %zu/%zu rows\n", agree, total);
+  EXPECT(agree * 100 >= total * 95, "gpu vs cpu agreement >= 95%");
+#endif
+  std::printf("%d scenarios, %d failures\n", scenarios, fails);
+  if (fails == 0) std::printf("RESOLVER OK\n");
+  return fails == 0 ? 0 : 1;
+}
