@@ -127,6 +127,9 @@ int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* out);
  * ms[i]: summed launch durations; work[i]: algorithmic FLOPs (GEMMs, attention) or bytes (LN,
  * head, embed) of those launches; launches[i]: launch count. n: capacity of the arrays (>= 10). */
 #define IOLM_KCLASSES 10
+/* Turns the per-kernel CUDA-event timing of opts.kernel_timing on or off for subsequent calls
+ * (the events cost ~3% of a step, so throughput runs leave it off and time a separate pass). */
+int iolm_cuda_set_kernel_timing(iolm_cuda_ctx* ctx, int32_t on);
 int iolm_cuda_kernel_times(const iolm_cuda_ctx* ctx, double* ms, double* work, int64_t* launches, int32_t n);
 
 /* Thread-local message for the last non-OK status. */

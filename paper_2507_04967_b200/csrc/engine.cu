@@ -216,6 +216,7 @@ class Engine {
   void forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds);
 
   std::mutex mu;
+  void set_kernel_timing(bool on) { ktime_ = on; }
   double kms_[IOLM_KCLASSES] = {}, kwork_[IOLM_KCLASSES] = {};
   int64_t kcount_[IOLM_KCLASSES] = {};
 
@@ -1108,6 +1109,14 @@ extern "C" int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* o
   return guarded([&] {
     if (!ctx || !out) throw iolmh::ContractViolation("null argument");
     *out = ctx->eng->stats();
+  });
+}
+
+extern "C" int iolm_cuda_set_kernel_timing(iolm_cuda_ctx* ctx, int32_t on) {
+  return guarded([&] {
+    if (!ctx) throw iolmh::ContractViolation("null argument");
+    std::lock_guard<std::mutex> lk(ctx->eng->mu);
+    ctx->eng->set_kernel_timing(on != 0);
   });
 }
 

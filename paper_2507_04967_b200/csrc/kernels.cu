@@ -39,21 +39,42 @@ __device__ __forceinline__ float warp_max(float v) {
 // ------------------------------------------------------------------ LayerNorm
 // One warp per row. Two-pass mean / variance in fp32 over the row held in registers. Writes the
 // bf16 GEMM operand, or (Q8) per-token int8 codes + the row scale for the W8A8 GEMMs.
+template <int MAXV>
+__device__ __forceinline__ void ln_load_row(const float* __restrict__ xr, int d, int lane, float4 (&v)[MAXV]) {
+  const int nv = d >> 2;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int idx = lane + 32 * i;
+    if (idx < nv) v[i] = reinterpret_cast<const float4*>(xr)[idx];
+  }
+}
+
+template <int MAXV, bool Q8 = false>
+__device__ __forceinline__ void ln_finish_row(float4 (&v)[MAXV], int d, const float* __restrict__ g,
+                                              const float* __restrict__ b, __nv_bfloat16* __restrict__ hr,
+                                              int lane, int8_t* __restrict__ q8 = nullptr,
+                                              float* __restrict__ qscale = nullptr);
+
 template <int MAXV, bool Q8 = false>
 __device__ __forceinline__ void ln_row_warp(const float* __restrict__ xr, int d, const float* __restrict__ g,
                                             const float* __restrict__ b, __nv_bfloat16* __restrict__ hr,
                                             int lane, int8_t* __restrict__ q8 = nullptr,
                                             float* __restrict__ qscale = nullptr) {
   float4 v[MAXV];
+  ln_load_row<MAXV>(xr, d, lane, v);
+  ln_finish_row<MAXV, Q8>(v, d, g, b, hr, lane, q8, qscale);
+}
+
+template <int MAXV, bool Q8>
+__device__ __forceinline__ void ln_finish_row(float4 (&v)[MAXV], int d, const float* __restrict__ g,
+                                              const float* __restrict__ b, __nv_bfloat16* __restrict__ hr,
+                                              int lane, int8_t* __restrict__ q8, float* __restrict__ qscale) {
   const int nv = d >> 2;
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
     const int idx = lane + 32 * i;
-    if (idx < nv) {
-      v[i] = reinterpret_cast<const float4*>(xr)[idx];
-      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-    }
+    if (idx < nv) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -118,8 +139,10 @@ __device__ __forceinline__ void ln_row_warp(const float* __restrict__ xr, int d,
   }
 }
 
+// 4 resident CTAs (32 rows in flight per SM): the kernel is bound by the latency of its row loads
+// (ncu: 65% long-scoreboard stalls at 3 CTAs / 24 warps), so the register cap buys occupancy.
 template <int MAXV, bool Q8>
-__global__ void __launch_bounds__(256) ln_kernel(const float* __restrict__ x, int M, int d,
+__global__ void __launch_bounds__(256, MAXV <= 10 ? 4 : 2) ln_kernel(const float* __restrict__ x, int M, int d,
                                                  const float* __restrict__ g, const float* __restrict__ b,
                                                  __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
                                                  float* __restrict__ qscale) {
@@ -131,6 +154,31 @@ __global__ void __launch_bounds__(256) ln_kernel(const float* __restrict__ x, in
   else
     ln_row_warp<MAXV>(x + static_cast<size_t>(row) * d, d, g, b, h + static_cast<size_t>(row) * ldh,
                       threadIdx.x & 31);
+}
+
+// Streaming LayerNorm: persistent warps walk rows gw, gw + nw, ... and load row i+1 into registers
+// before normalising row i, so every warp always has a row's loads in flight (the one-row-per-warp
+// kernel above idles its memory traffic during each row's reductions). Same arithmetic.
+template <int MAXV, bool Q8>
+__global__ void __launch_bounds__(256, 2) ln_stream_kernel(const float* __restrict__ x, int M, int d,
+                                                           const float* __restrict__ g, const float* __restrict__ b,
+                                                           __nv_bfloat16* __restrict__ h, int ldh,
+                                                           int8_t* __restrict__ q8, float* __restrict__ qscale) {
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * 8;
+  int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  float4 cur[MAXV], nxt[MAXV];
+  if (row < M) ln_load_row<MAXV>(x + static_cast<size_t>(row) * d, d, lane, cur);
+  for (; row < M; row += nw) {
+    const int nrow = row + nw;
+    if (nrow < M) ln_load_row<MAXV>(x + static_cast<size_t>(nrow) * d, d, lane, nxt);
+    if constexpr (Q8)
+      ln_finish_row<MAXV, true>(cur, d, g, b, nullptr, lane, q8 + static_cast<size_t>(row) * ldh, qscale + row);
+    else
+      ln_finish_row<MAXV>(cur, d, g, b, h + static_cast<size_t>(row) * ldh, lane);
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) cur[i] = nxt[i];
+  }
 }
 
 // Bandwidth-oriented LayerNorm: persistent CTAs, a producer warp streams groups of 8 consecutive x
@@ -193,7 +241,7 @@ __global__ void __launch_bounds__(288) ln_bulk_kernel(const float* __restrict__ 
 // One warp per row. CH > 0: the row (cols = 256*CH, multiple of 8) stays in registers between the
 // amax and the code pass; CH == 0: generic two-pass version (any width).
 template <int CH>
-__global__ void __launch_bounds__(256) quant_rows_kernel(const __nv_bfloat16* __restrict__ src, int lds, int M,
+__global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const __nv_bfloat16* __restrict__ src, int lds, int M,
                                                          int cols, int8_t* __restrict__ dst, int ldd,
                                                          float* __restrict__ scale) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -995,12 +1043,33 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
                cudaStream_t st, int8_t* q8, float* qscale) {
   if (M <= 0) return;
   const int nv = (d / 4 + 31) / 32;
+  static int sms = 0;
+  if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  if (std::getenv("IOLM_LN_LEGACY") == nullptr && nv <= 10) {
+    const int grid_s = std::min<int>((M + 7) / 8, sms * 2);
+#define LNS(V)                                                                                             \
+  do {                                                                                                     \
+    if (q8) ln_stream_kernel<V, true><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);            \
+    else ln_stream_kernel<V, false><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);              \
+  } while (0)
+    switch (nv) {
+      case 1: LNS(1); break;
+      case 2: LNS(2); break;
+      case 3: LNS(3); break;
+      case 4: LNS(4); break;
+      case 5: LNS(5); break;
+      case 6: LNS(6); break;
+      case 8: LNS(8); break;
+      default: LNS(10); break;
+    }
+#undef LNS
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
   const size_t bsmem = 256 + static_cast<size_t>(LN_STAGES) * 8 * d * 4;
   // the bulk-streamed variant pays off for the int8 (W8A8) output; the bf16 output keeps the
   // register-resident one-warp-per-row kernel (measured faster at d = 1280)
   if (q8 && d % 128 == 0 && (nv == 10 || nv == 16 || nv == 8 || nv == 4) && bsmem <= 200 * 1024) {
-    static int sms = 0;
-    if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const int per_sm = bsmem <= 100 * 1024 ? 2 : 1;
     const int grid_b = std::min<int>((M + 7) / 8, sms * per_sm);
 #define LNB(V)                                                                                          \
@@ -1059,11 +1128,9 @@ void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_
   const unsigned grid = blocks_for(M, 8);
   const int ch = (cols + 255) / 256;
   if (cols % 8 != 0) quant_rows_kernel<0><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  // register-resident rows up to 1024 columns; wider rows take the two-pass kernel (its second
+  // read hits L2) at 8 CTAs per SM: these launches are bound by load latency, not bytes
   else if (ch <= 4) quant_rows_kernel<4><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
-  else if (ch <= 8) quant_rows_kernel<8><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
-  else if (ch <= 12) quant_rows_kernel<12><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
-  else if (ch <= 16) quant_rows_kernel<16><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
-  else if (ch <= 20) quant_rows_kernel<20><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
   else quant_rows_kernel<0><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
   CUDA_OK(cudaGetLastError());
 }

@@ -184,6 +184,9 @@ class ModelRuntime:
         _check(self._lib.iolm_cuda_last_stats(self._h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in _lib.Stats._fields_}
 
+    def set_kernel_timing(self, on: bool) -> None:
+        _check(self._lib.iolm_cuda_set_kernel_timing(self._h, 1 if on else 0))
+
     def kernel_times(self) -> dict:
         """Per kernel class of the last call: {name: (ms, algorithmic work, launches)}."""
         n = len(_lib.KCLASSES)
