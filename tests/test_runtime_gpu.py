@@ -155,3 +155,25 @@ def test_errors_and_edges(model):
     got = rt.batch_decode([p], 8, c)
     assert ol[0] == 2 and got[0] == O.render(oi[0], ol[0])
     assert c.total() == om_madds
+
+
+@pytest.mark.parametrize("cfg,row_chars,n_rows", [
+    ((1280, 2, 20, 5120, 128), 64, 8),   # C1 layer shapes (hd 64), two layers
+    ((256, 2, 2, 1024, 576), 512, 4),    # C4 attention shapes: hd 128, 544-token prompts, S = 576
+], ids=["c1-hd64", "c4-hd128-long"])
+def test_parity_production_head_dims(cfg, row_chars, n_rows):
+    """The head dims and row lengths of the benchmark configs (BASELINE.json configs[1] and [4]) at
+    two layers, so the f32 restatement stays cheap: logits rel-L2 per row and greedy agreement."""
+    b = synth.toy_bundle(*cfg, seed=42)
+    rt, om = R.ModelRuntime(b), O.OracleModel(b)
+    ids, offs = synth.rows(3000, n_rows, row_chars)
+    for r in range(min(2, n_rows)):
+        row = ids[offs[r]:offs[r + 1]]
+        got, ref = rt.forward(row), om.forward(row)[0]
+        rel = np.linalg.norm(got - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-30)
+        assert rel.max() <= LOGIT_REL_TOL, rel.max()
+    gi, gl, gm = rt.decode_token_rows(ids, offs, 8)
+    oi, ol, omm = om.decode_ids(ids, offs, 8, threads=8)
+    assert gm == omm
+    same = sum(gl[i] == ol[i] and np.array_equal(gi[i, :gl[i]], oi[i, :ol[i]]) for i in range(n_rows))
+    assert same >= n_rows - 1, (same, n_rows)

@@ -113,3 +113,23 @@ def test_engine_sparse_batch_invariance():
     full = rt.batch_decode(prompts, 8)
     for i in [0, 7, 15]:
         assert rt.batch_decode([prompts[i]], 8) == [full[i]]
+
+
+def test_engine_sparse_long_rows_hd128():
+    """C4 attention shapes (hd 128, 544-token prompts) with 2:4 W8A8 weights: sparse MMAs are bitwise
+    equal to the dense-int8 engine, and track the W8A8 restatement (oracle) within tolerance."""
+    from oracle import oracle as O
+    cfg = (256, 2, 2, 1024, 576)
+    b = synth.toy_bundle(*cfg, seed=42, quant="sparse24", heads=[1, 2], ffn=[512, 516])
+    sp = R.ModelRuntime(b, act_quant=True)
+    dn = R.ModelRuntime(b, act_quant=True, sparse_mma=False)
+    ids, offs = synth.rows(4000, 3, 512)
+    row = ids[offs[0]:offs[1]]
+    got = sp.forward(row)
+    assert np.array_equal(got, dn.forward(row))
+    ref = O.OracleModel(b, act_quant=True).forward(row)[0]
+    rel = np.linalg.norm(got - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-30)
+    assert rel.max() <= 2.5e-2, rel.max()
+    gi, gl, _ = sp.decode_token_rows(ids, offs, 8)
+    di, dl, _ = dn.decode_token_rows(ids, offs, 8)
+    assert np.array_equal(gl, dl) and np.array_equal(gi, di)
