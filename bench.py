@@ -379,7 +379,7 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(name)
+            traffic = json.loads(prof.read_text()).get(args.config, {}).get(name)
         except Exception:
             traffic = None
     kernels = {}

@@ -1,10 +1,10 @@
-"""Driver for ncu captures (never a bench number): builds the C1 engine and runs `--calls` decode
-calls of `--rows` synthetic rows with device-resident ids.
+"""Driver for ncu captures (never a bench number): builds the engine of one bench.py config and runs
+`--calls` decode calls of `--rows` synthetic rows with device-resident ids.
 
-  ncu --metrics gpu__time_duration.sum --clock-control none -s 4000 -c 600 --csv \
-      --log-file gpurun_out/launches.csv python profiles/profile_run.py
-  ncu --set full --clock-control none --import-source on -k regex:gemm_bf16 -s 300 -c 2 \
-      -o gpurun_out/gemm python profiles/profile_run.py
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      -s 3000 -c 400 --csv --log-file gpurun_out/c1_launches.csv python profiles/profile_run.py --config c1
+  ncu --set full --clock-control none --import-source on -k regex:gemm_tn -s 300 -c 2 \
+      -o gpurun_out/gemm python profiles/profile_run.py --config c1
 """
 import argparse
 import sys
@@ -15,22 +15,21 @@ sys.path.insert(0, str(ROOT))
 
 import torch  # noqa: E402
 
+from bench import CONFIGS  # noqa: E402
 from paper_2507_04967_b200 import runtime as R  # noqa: E402
 from paper_2507_04967_b200 import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--rows", type=int, default=4096)
-ap.add_argument("--calls", type=int, default=2)
-ap.add_argument("--dims", default="1280,24,20,5120,128")
-ap.add_argument("--quant", default="dense")
-ap.add_argument("--act-quant", action="store_true")
+ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+ap.add_argument("--rows", type=int, default=16384)
+ap.add_argument("--calls", type=int, default=1)
 args = ap.parse_args()
-dims = tuple(int(x) for x in args.dims.split(","))
-b = synth.toy_bundle(*dims, seed=42, quant=args.quant)
-rt = R.ModelRuntime(b, act_quant=args.act_quant)
-ids, offs = synth.rows(0, args.rows, 64)
+cfg = CONFIGS[args.config]
+b = synth.toy_bundle(*cfg["dims"], seed=42, quant=cfg["quant"], heads=cfg.get("heads"), ffn=cfg.get("ffn"))
+rt = R.ModelRuntime(b, act_quant=cfg.get("act_quant", False))
+ids, offs = synth.rows(0, args.rows, cfg["row_chars"])
 d = torch.from_numpy(ids).cuda()
 torch.cuda.synchronize()
 for _ in range(args.calls):
     o, ln, _ = rt.decode_token_rows(None, offs, 8, device_ids=d.data_ptr())
-print("rows", args.rows, "stats", rt.last_stats())
+print("config", args.config, "rows", args.rows, "stats", rt.last_stats())
