@@ -51,7 +51,8 @@ struct SpCfg {
   static constexpr int WTOK = BN / (EPI_WARPS / 4);  // 56 tokens per epilogue warp
   static constexpr int CHUNK = 16;                   // tokens per tcgen05.ld
   static constexpr int NCH = (WTOK + CHUNK - 1) / CHUNK;
-  static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + 256 + EPI_WARPS * WTOK * sizeof(QkvRow);
+  static constexpr size_t SMEM =
+      1024 + STAGES * STAGE_BYTES + 256 + EPI_WARPS * WTOK * sizeof(QkvRow) + EPI_WARPS * 64 * sizeof(float);
   static_assert(E_COL0 + 8 * STAGES <= TMEM_COLS, "TMEM budget");
 };
 
@@ -224,6 +225,10 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
     constexpr int NCH = C::NCH;
     const uint32_t leader_tempty0 = mapa_shared(tempty_bar(0), 0);
     QkvRow* s_rows = reinterpret_cast<QkvRow*>(smem_raw + (bars + 256 - raw)) + e * C::WTOK;
+    // the warp's 56 per-token activation scales (+ padding to 64): read back as warp-uniform
+    // float4 broadcasts (4 LDS per 16 tokens instead of 16 shuffles)
+    float* s_as = reinterpret_cast<float*>(smem_raw + (bars + 256 - raw) + C::EPI_WARPS * C::WTOK * sizeof(QkvRow)) +
+                  e * 64;
     const bool has_ws = ep.w_scale != nullptr;
     const size_t head_stride = static_cast<size_t>(ep.page_size) << ep.hd_shift;
     int acc = 0;
@@ -238,12 +243,12 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
       // latency overlaps the mainloop instead of stalling every chunk: the channel's weight scale,
       // one activation scale per (chunk, lane & 15) token, and (QKV) the 112 token destinations.
       const float w_sc = has_ws && ch_ok ? ep.w_scale[ch] : 1.f;
-      float a_pre[NCH];
-#pragma unroll
-      for (int ci = 0; ci < NCH; ++ci) {
-        const int t = tw0 + ci * C::CHUNK + (lane & 15);
-        a_pre[ci] = ep.a_scale != nullptr ? (t < T && ci * C::CHUNK + (lane & 15) < C::WTOK ? ep.a_scale[t] : 0.f) : 1.f;
+      __syncwarp();  // the previous tile's readers of s_as are done
+      for (int i = lane; i < 64; i += 32) {
+        const int t = tw0 + i;
+        s_as[i] = ep.a_scale != nullptr ? (i < C::WTOK && t < T ? ep.a_scale[t] : 0.f) : 1.f;
       }
+      __syncwarp();
       int region = 0, off = ch;
       if constexpr (EPI == EPI_QKV) {
         if (ch >= ep.kh) {
@@ -294,12 +299,15 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
               if (j < jn && ch_ok && t0 + j < T) o[static_cast<size_t>(t0 + j) * ep.ldo + ch] = static_cast<int32_t>(rc[j]);
           } else {
             float v[16];
+            float as[16];
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+              *reinterpret_cast<float4*>(as + j) = *reinterpret_cast<const float4*>(s_as + ci * C::CHUNK + j);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               // same operations as the dense kind::i8 epilogue: (acc * s_a[token]) * s_w[ch], each
               // rounded (explicit _rn: no FMA contraction into the residual add below)
-              const float as = __shfl_sync(0xffffffffu, a_pre[ci], j);
-              v[j] = __fmul_rn(__fmul_rn(static_cast<float>(static_cast<int32_t>(rc[j])), as), w_sc);
+              v[j] = __fmul_rn(__fmul_rn(static_cast<float>(static_cast<int32_t>(rc[j])), as[j]), w_sc);
             }
             if constexpr (EPI == EPI_GELU_BF16) {
 #pragma unroll
@@ -319,6 +327,22 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
               // channel pair; even lanes write token j, odd lanes token j + 1
               const bool odd = lane & 1;
               const int c0 = ch & ~1;
+              if constexpr (EPI != EPI_QKV) {
+                if (jn == C::CHUNK && t0 + C::CHUNK <= T && c0 + 1 < N) {
+                  // whole chunk in range: one 4-byte store per token pair, pointer stepped by 2 rows
+                  uint32_t* dst = reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(ep.out) +
+                                                              static_cast<size_t>(t0 + (odd ? 1 : 0)) * ep.ldo + c0);
+                  const size_t step = static_cast<size_t>(ep.ldo);  // 2 rows of bf16 = ldo uint32
+#pragma unroll
+                  for (int j = 0; j < 16; j += 2) {
+                    const float send = odd ? v[j] : v[j + 1];
+                    const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+                    *dst = odd ? pack_bf16x2(recv, v[j + 1]) : pack_bf16x2(v[j], recv);
+                    dst += step;
+                  }
+                  continue;
+                }
+              }
 #pragma unroll
               for (int j = 0; j < 16; j += 2) {
                 const float send = odd ? v[j] : v[j + 1];
