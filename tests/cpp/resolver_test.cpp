@@ -22,6 +22,7 @@
 #include "iolm/sql.hpp"
 #include "iolm/table.hpp"
 #include "iolm/train.hpp"
+#include "iolm_cuda_join.hpp"
 #include "iolm_cuda_resolver.hpp"
 
 static int fails = 0;
@@ -180,6 +181,71 @@ int main() {
     EXPECT(!ref_msg.empty() && !got_msg.empty(), "SequenceTooLong raised by both");
     std::printf("SequenceTooLong: reference \"%s\" / resolver \"%s\"\n", ref_msg.c_str(), got_msg.c_str());
     EXPECT(tail(ref_msg) == tail(got_msg), "SequenceTooLong row suffix");
+  }
+
+  // SEMANTIC JOIN (exec.cpp:283-336) through iolm::cuda::semantic_join. A second model whose 'y' and
+  // 'n' embedding rows (tied head, runtime.cpp:213-215) are scaled up answers y or n on most pairs,
+  // so the match path is exercised too (the random-init one answers neither: all unparsable).
+  iolm::Rng yrng(21);
+  auto yn_params = iolm::ToyModelParams::init(iolm::ModelConfig::dense(32, 2, 2, 64, 96), yrng);
+  for (int c = 0; c < 32; ++c) {
+    yn_params.tok_embed.at('y', c) *= 40.f;
+    yn_params.tok_embed.at('n', c) *= -40.f;
+  }
+  const auto yn_bundle = yn_params.to_bundle();
+  const iolm::ModelRuntime cpu_yn(yn_bundle);
+#ifdef WITH_GPU
+  const iolm::cuda::ModelRuntime model_yn(yn_bundle);
+#else
+  const iolm::ModelRuntime& model_yn = cpu_yn;
+#endif
+  for (int which = 0; which < 2; ++which) {
+    const auto& cpu_j = which ? cpu_yn : cpu;
+    const auto& model_j = which ? model_yn : model;
+    const iolm::Table l = words_table(40, 11), r0 = words_table(40, 12);
+    iolm::Table r = r0;
+    r.name = "r";
+    r.columns[0].name = "v2";
+    iolm::Table lt = l;
+    lt.name = "l";
+    lt.columns[0].name = "v";
+    for (int batch : {1, 16})
+      for (size_t capacity : {size_t{0}, size_t{1024}}) {
+        iolm::PromptCache rcache(capacity);
+        iolm::ExecOptions opts;
+        opts.batch_size = batch;
+        opts.cache_capacity = capacity;
+        iolm::ExecStats rs;
+        iolm::FlopCounter f1;
+        const iolm::Table out = iolm::execute(iolm::parse_query("SELECT v, v2 FROM l SEMANTIC JOIN r ON v ~ v2"),
+                                              {{"l", lt}, {"r", r}}, cpu_j, rcache, opts, rs, f1);
+        iolm::cuda::PromptCache cache(capacity);
+        iolm::cuda::ResolverStats st;
+        iolm::cuda::JoinStats js;
+        iolm::FlopCounter f2;
+        const auto m = iolm::cuda::semantic_join(model_j, cache, batch, std::span<const std::string>(lt.columns[0].texts),
+                                                 std::span<const std::string>(r.columns[0].texts), st, js, f2, 64);
+        EXPECT(js.join_pairs_considered == rs.join_pairs_considered, "join pairs considered");
+        EXPECT(st.model_invocations == rs.model_invocations && st.cache_hits == rs.cache_hits &&
+                   st.cache_misses == rs.cache_misses,
+               "join resolver stats");
+#ifndef WITH_GPU
+        EXPECT(js.join_matches == rs.join_matches && js.unparsable_match_answers == rs.unparsable_match_answers,
+               "join match / unparsable counts");
+        bool same = m.size() == out.row_count;
+        for (size_t k = 0; same && k < m.size(); ++k)
+          same = lt.columns[0].texts[m[k].first] == out.columns[0].texts[k] &&
+                 r.columns[0].texts[m[k].second] == out.columns[1].texts[k];
+        EXPECT(same, "join output rows identical to iolm::execute");
+#endif
+        if (batch == 16 && capacity == 1024)
+          std::printf("semantic join: %llu pairs considered, %llu matches (reference %llu), %llu unparsable\n",
+                      static_cast<unsigned long long>(js.join_pairs_considered),
+                      static_cast<unsigned long long>(js.join_matches),
+                      static_cast<unsigned long long>(rs.join_matches),
+                      static_cast<unsigned long long>(js.unparsable_match_answers));
+        ++scenarios;
+      }
   }
 
 #ifdef WITH_GPU
