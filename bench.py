@@ -264,6 +264,8 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     import torch
     from paper_2507_04967_b200 import runtime as R
     from paper_2507_04967_b200 import synth
+    if os.environ.get("BENCH_SHARE_GPUS"):  # plumbing test only: N ranks on fewer GPUs
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     B, K, W = args.rows_per_step, args.steps, args.warmup
