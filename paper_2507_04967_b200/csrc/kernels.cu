@@ -181,6 +181,109 @@ __global__ void __launch_bounds__(256, 2) ln_stream_kernel(const float* __restri
   }
 }
 
+// Wide-row streaming LayerNorm (d = 2048-4096): a PAIR of warps owns each row (64 threads,
+// float4 index t + 64 i), so the per-thread row slice and its prefetched successor fit in registers
+// at 2 CTAs x 8 warps per SM. Partial sums are combined through shared memory under a 64-thread
+// named barrier per pair (ids 1-4); the arithmetic per element is the one-warp kernel's.
+template <int MAXV, bool Q8>
+__global__ void __launch_bounds__(256, 2) ln_stream2_kernel(const float* __restrict__ x, int M, int d,
+                                                            const float* __restrict__ g, const float* __restrict__ b,
+                                                            __nv_bfloat16* __restrict__ h, int ldh,
+                                                            int8_t* __restrict__ q8, float* __restrict__ qscale) {
+  __shared__ float red[4][2][3][2];  // [pair][row parity][reduction][half]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, half = warp & 1, t = half * 32 + lane;
+  const int nv = d >> 2;
+  const int np = gridDim.x * 4;
+  auto pair_sum = [&](float v, int par, int k, bool is_max) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? fmaxf(v, w) : v + w;
+    }
+    if (lane == 0) red[pair][par][k][half] = v;
+    asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+    const float a = red[pair][par][k][0], c = red[pair][par][k][1];
+    return is_max ? fmaxf(a, c) : a + c;  // same order in both warps: identical result
+  };
+  auto load = [&](int row, float4 (&v)[MAXV]) {
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(row) * d);
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int idx = t + 64 * i;
+      if (idx < nv) v[i] = xr[idx];
+    }
+  };
+  float4 cur[MAXV], nxt[MAXV];
+  int row = blockIdx.x * 4 + pair, par = 0;
+  if (row < M) load(row, cur);
+  for (; row < M; row += np, par ^= 1) {
+    if (row + np < M) load(row + np, nxt);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i)
+      if (t + 64 * i < nv) s += (cur[i].x + cur[i].y) + (cur[i].z + cur[i].w);
+    const float mean = pair_sum(s, par, 0, false) / static_cast<float>(d);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i)
+      if (t + 64 * i < nv) {
+        const float a = cur[i].x - mean, bb = cur[i].y - mean, c = cur[i].z - mean, e = cur[i].w - mean;
+        q += (a * a + bb * bb) + (c * c + e * e);
+      }
+    const float inv = 1.0f / sqrtf(pair_sum(q, par, 1, false) / static_cast<float>(d) + 1e-5f);
+    if constexpr (Q8) {
+      float amax = 0.f;
+#pragma unroll
+      for (int i = 0; i < MAXV; ++i) {
+        const int idx = t + 64 * i;
+        if (idx < nv) {
+          const float4 gg = reinterpret_cast<const float4*>(g)[idx];
+          const float4 bb = reinterpret_cast<const float4*>(b)[idx];
+          cur[i].x = (cur[i].x - mean) * inv * gg.x + bb.x;
+          cur[i].y = (cur[i].y - mean) * inv * gg.y + bb.y;
+          cur[i].z = (cur[i].z - mean) * inv * gg.z + bb.z;
+          cur[i].w = (cur[i].w - mean) * inv * gg.w + bb.w;
+          amax = fmaxf(fmaxf(amax, fmaxf(fabsf(cur[i].x), fabsf(cur[i].y))), fmaxf(fabsf(cur[i].z), fabsf(cur[i].w)));
+        }
+      }
+      amax = pair_sum(amax, par, 2, true);
+      const float sd = amax == 0.f ? 1.f : amax / 127.0f;
+      const float inv_sd = 1.0f / sd;
+      if (t == 0) qscale[row] = sd;
+      char4* qr = reinterpret_cast<char4*>(q8 + static_cast<size_t>(row) * ldh);
+#pragma unroll
+      for (int i = 0; i < MAXV; ++i) {
+        const int idx = t + 64 * i;
+        if (idx < nv) {
+          char4 c;
+          c.x = quant_one(cur[i].x, sd, inv_sd);
+          c.y = quant_one(cur[i].y, sd, inv_sd);
+          c.z = quant_one(cur[i].z, sd, inv_sd);
+          c.w = quant_one(cur[i].w, sd, inv_sd);
+          qr[idx] = c;
+        }
+      }
+    } else {
+      uint2* hr = reinterpret_cast<uint2*>(h + static_cast<size_t>(row) * ldh);
+#pragma unroll
+      for (int i = 0; i < MAXV; ++i) {
+        const int idx = t + 64 * i;
+        if (idx < nv) {
+          const float4 gg = reinterpret_cast<const float4*>(g)[idx];
+          const float4 bb = reinterpret_cast<const float4*>(b)[idx];
+          uint2 w;
+          w.x = pack_bf16x2((cur[i].x - mean) * inv * gg.x + bb.x, (cur[i].y - mean) * inv * gg.y + bb.y);
+          w.y = pack_bf16x2((cur[i].z - mean) * inv * gg.z + bb.z, (cur[i].w - mean) * inv * gg.w + bb.w);
+          hr[idx] = w;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) cur[i] = nxt[i];
+  }
+}
+
 // Bandwidth-oriented LayerNorm: persistent CTAs, a producer warp streams groups of 8 consecutive x
 // rows (one contiguous block) with cp.async.bulk into an LN_STAGES-deep smem ring; each of the 8
 // compute warps normalises one row of the group from smem (same arithmetic as ln_row_warp).
@@ -1045,6 +1148,19 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
   const int nv = (d / 4 + 31) / 32;
   static int sms = 0;
   if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  if (std::getenv("IOLM_LN_LEGACY") == nullptr && nv > 10 && nv <= 32 && d % 4 == 0) {
+    const int grid_s = std::min<int>((M + 3) / 4, sms * 2);
+    const int v2 = (d / 4 + 63) / 64;  // float4 per thread with two warps per row
+    if (v2 <= 8) {
+      if (q8) ln_stream2_kernel<8, true><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);
+      else ln_stream2_kernel<8, false><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);
+    } else {
+      if (q8) ln_stream2_kernel<16, true><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);
+      else ln_stream2_kernel<16, false><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);
+    }
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
   if (std::getenv("IOLM_LN_LEGACY") == nullptr && nv <= 10) {
     const int grid_s = std::min<int>((M + 7) / 8, sms * 2);
 #define LNS(V)                                                                                             \

@@ -160,7 +160,8 @@ def test_errors_and_edges(model):
 @pytest.mark.parametrize("cfg,row_chars,n_rows", [
     ((1280, 2, 20, 5120, 128), 64, 8),   # C1 layer shapes (hd 64), two layers
     ((256, 2, 2, 1024, 576), 512, 4),    # C4 attention shapes: hd 128, 544-token prompts, S = 576
-], ids=["c1-hd64", "c4-hd128-long"])
+    ((2048, 1, 16, 2048, 160), 64, 4),   # C4 width: d 2048 (two-warp LayerNorm rows), hd 128
+], ids=["c1-hd64", "c4-hd128-long", "c4-d2048"])
 def test_parity_production_head_dims(cfg, row_chars, n_rows):
     """The head dims and row lengths of the benchmark configs (BASELINE.json configs[1] and [4]) at
     two layers, so the f32 restatement stays cheap: logits rel-L2 per row and greedy agreement."""
