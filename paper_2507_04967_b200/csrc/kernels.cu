@@ -419,6 +419,70 @@ __global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const 
   }
 }
 
+// Wide rows (1024 < cols <= 4096, cols % 8 == 0): a pair of warps per row, the row slice and the
+// next row's slice in registers (16-B chunks t + 64 i), amax combined under a 64-thread named barrier.
+// Same per-element rule as quant_rows_kernel.
+template <int CH>
+__global__ void __launch_bounds__(256, 2) quant_rows2_kernel(const __nv_bfloat16* __restrict__ src, int lds, int M,
+                                                             int cols, int8_t* __restrict__ dst, int ldd,
+                                                             float* __restrict__ scale) {
+  __shared__ float red[4][2][2];  // [pair][row parity][half]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, half = warp & 1, t = half * 32 + lane;
+  const int nch = cols >> 3;  // 16-byte chunks per row
+  const int np = gridDim.x * 4;
+  auto load = [&](int row, uint4 (&u)[CH]) {
+    const uint4* r = reinterpret_cast<const uint4*>(src + static_cast<size_t>(row) * lds);
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int c = t + 64 * i;
+      u[i] = c < nch ? r[c] : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint4 cur[CH], nxt[CH];
+  int row = blockIdx.x * 4 + pair, par = 0;
+  if (row < M) load(row, cur);
+  for (; row < M; row += np, par ^= 1) {
+    if (row + np < M) load(row + np, nxt);
+    float amax = 0.f;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&cur[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h2[j]);
+        amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+      }
+    }
+    amax = warp_max(amax);
+    if (lane == 0) red[pair][par][half] = amax;
+    asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+    amax = fmaxf(red[pair][par][0], red[pair][par][1]);
+    const float sd = amax == 0.f ? 1.f : amax / 127.0f;
+    const float inv_sd = 1.0f / sd;
+    if (t == 0) scale[row] = sd;
+    uint2* o = reinterpret_cast<uint2*>(dst + static_cast<size_t>(row) * ldd);
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int c = t + 64 * i;
+      if (c < nch) {
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&cur[i]);
+        uint2 w;
+        int8_t* wb = reinterpret_cast<int8_t*>(&w);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(h2[j]);
+          wb[2 * j] = quant_one(f.x, sd, inv_sd);
+          wb[2 * j + 1] = quant_one(f.y, sd, inv_sd);
+        }
+        o[c] = w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CH; ++i) cur[i] = nxt[i];
+  }
+}
+
 // token id of step row m: prompt tokens come from the id table, generated tokens from the
 // per-slot "last token" register written by head_argmax_kernel.
 template <int MAXV, bool Q8>
@@ -1247,7 +1311,12 @@ void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_
   // register-resident rows up to 1024 columns; wider rows take the two-pass kernel (its second
   // read hits L2) at 8 CTAs per SM: these launches are bound by load latency, not bytes
   else if (ch <= 4) quant_rows_kernel<4><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
-  else quant_rows_kernel<0><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  else if (cols > 3072 && cols <= 4096) {  // measured: two-warp rows win at 4096 (C4 FFN), lose at 2560
+    static int sms = 0;
+    if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int grid2 = std::min<int>((M + 3) / 4, sms * 2);
+    quant_rows2_kernel<8><<<grid2, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  } else quant_rows_kernel<0><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
   CUDA_OK(cudaGetLastError());
 }
 

@@ -96,7 +96,7 @@ def test_activation_quantizer_bitexact(engine_lib):
     assert np.array_equal(codes, rc)
 
 
-@pytest.mark.parametrize("d", [1280, 5120, 2500, 1024, 4096])
+@pytest.mark.parametrize("d", [640, 1280, 2048, 2560, 5120, 2500, 1024, 4096])
 def test_activation_quantizer_widths_and_near_ties(engine_lib, d):
     """Register-resident and generic quantizer variants; values placed exactly on and next to
     rounding boundaries exercise the fast-path tie check."""
