@@ -52,7 +52,8 @@ typedef struct iolm_cuda_opts {
   int32_t kernel_timing;       /* 1: time every kernel class with CUDA events (iolm_cuda_kernel_times) */
   int32_t sparse_mma;          /* -1: expand sparse24_q8 to dense int8; 0/1: 2:4 sparse tensor cores (W8A8) */
   int32_t int4_mma;            /* -1: expand q4 codes to bf16 in HBM; 0/1: int4 in HBM, expanded in smem (W4A16) */
-  int32_t reserved[7];
+  int32_t prefill_tc;          /* prefill attention: -1 mma.sync; 0 default (tcgen05 for hd 128); 1 tcgen05 for hd 64 too */
+  int32_t reserved[6];
 } iolm_cuda_opts;
 
 /* ModelConfig (proj/include/iolm/model.hpp:20-41); per-layer lists are queried separately. */

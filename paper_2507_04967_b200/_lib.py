@@ -38,7 +38,8 @@ class Opts(C.Structure):
         ("kernel_timing", C.c_int32),
         ("sparse_mma", C.c_int32),
         ("int4_mma", C.c_int32),
-        ("reserved", C.c_int32 * 7),
+        ("prefill_tc", C.c_int32),
+        ("reserved", C.c_int32 * 6),
     ]
 
 

@@ -50,6 +50,7 @@ void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_
 void launch_decode_codes(const void* payload, int enc, int rows, int cols, void* dst, bool int8, int ld,
                          float* scales, cudaStream_t st);
 void launch_attention(const AttnParams& prefill, const AttnParams& decode, int hd, cudaStream_t st);
+bool launch_prefill_tc(const AttnParams& prefill, int hd, cudaStream_t st);
 int decode_heads_per_cta(int heads, int hd);
 void launch_head(const float* x, int d, const int* rows, int n_rows, const float* g, const float* b,
                  const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
@@ -225,8 +226,8 @@ class Engine {
   void upload_weights(const BundleView& b);
   void alloc_runtime();
   void set_prefix_pages(int prefix_pages);
-  static void add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head,
-                          int64_t owner);
+  void add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head,
+                   int64_t owner) const;
   void launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits);
   void gemm(int epi, bool i8, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
   // one projection: dense (A = activations, B = weights) or 2:4 sparse (weights are the MMA's A)
@@ -248,6 +249,8 @@ class Engine {
   bool act_quant_ = false;
   bool sparse_mma_ = true;
   bool int4_mma_ = true;
+  bool prefill_tc_ = true;  // tcgen05 prefill attention (hd 128 by default, hd 64 on request)
+  bool prefill_tc_force_ = false;
   uint64_t madds_A_ = 0, madds_B_ = 0;  // sum_l (4*d*kh + 2*d*f), sum_l kh
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
@@ -296,6 +299,9 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
   if (d_ % 8 != 0) throw Unsupported("d_model must be a multiple of 8 for the GPU layout");
   if (hd_ != 16 && hd_ != 32 && hd_ != 64 && hd_ != 128)
     throw Unsupported("head_dim must be 16, 32, 64 or 128 on the GPU path");
+  // measured (bench C1 / C4): for hd 64 rows of 64 + 32 tokens the mma.sync kernel is faster (the
+  // 128-query tcgen05 tile is half empty and latency-bound); hd 128 / 544-token rows gain 14%
+  if (hd_ != 128 && !(hd_ == 64 && prefill_tc_force_)) prefill_tc_ = false;
   if (d_ > 4096) throw Unsupported("d_model > 4096");
   device_ = device;
   CUDA_OK(cudaSetDevice(device_));
@@ -312,6 +318,8 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
     ktime_ = opts->kernel_timing != 0;
     if (opts->sparse_mma < 0) sparse_mma_ = false;
     if (opts->int4_mma < 0) int4_mma_ = false;
+    if (opts->prefill_tc < 0) prefill_tc_ = false;
+    prefill_tc_force_ = opts->prefill_tc > 0;
   }
   // Default token budget: one 256-row GEMM M-tile per SM pair (74 x 256 = 18944 on a 148-SM B200),
   // so every projection's tile count is a whole number of waves of the persistent GEMM grid.
@@ -555,15 +563,16 @@ void Engine::set_prefix_pages(int prefix_pages) {
 }
 
 void Engine::add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head,
-                         int64_t owner) {
+                         int64_t owner) const {
   const int m0 = s.T();
   for (int p = p_begin; p < p_end; ++p) {
     s.tok_src.push_back(src_base + p);
     s.tok_slot.push_back(slot);
     s.tok_pos.push_back(p);
   }
-  for (int c = p_begin; c < p_end; c += QCHUNK)
-    s.pre.push_back(AttnGroup{slot, m0 + (c - p_begin), std::min(QCHUNK, p_end - c), c});
+  const int qc = prefill_tc_ ? 2 * QCHUNK : QCHUNK;  // tcgen05 kernel: 128-query tiles
+  for (int c = p_begin; c < p_end; c += qc)
+    s.pre.push_back(AttnGroup{slot, m0 + (c - p_begin), std::min(qc, p_end - c), c});
   if (want_head) {
     s.head_rows.push_back(m0 + (p_end - p_begin) - 1);
     s.head_slot.push_back(slot);
@@ -726,7 +735,10 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     dec.n_groups = static_cast<int>(s.dec.size());
     none.n_groups = 0;
     if (pre.n_groups) {
-      timed(2, 4.0 * hd_ * ly.heads * pre_keys, [&] { launch_attention(pre, none, hd_, stream_); });
+      timed(2, 4.0 * hd_ * ly.heads * pre_keys, [&] {
+        if (prefill_tc_) launch_prefill_tc(pre, hd_, stream_);
+        else launch_attention(pre, none, hd_, stream_);
+      });
       ++stats_.kernel_launches;
     }
     if (dec.n_groups) {

@@ -140,7 +140,7 @@ class ModelRuntime:
 
     def __init__(self, bundle: bytes, device: int = 0, max_tokens_per_step: int = 0, max_slots: int = 0,
                  prefix_sharing: bool = True, act_quant: bool = False, kernel_timing: bool = False,
-                 sparse_mma: bool = True, int4_mma: bool = True):
+                 sparse_mma: bool = True, int4_mma: bool = True, prefill_tc: bool | None = None):
         self._lib = _lib.load()
         opts = _lib.Opts()
         opts.max_tokens_per_step = max_tokens_per_step
@@ -150,6 +150,7 @@ class ModelRuntime:
         opts.kernel_timing = 1 if kernel_timing else 0
         opts.sparse_mma = 0 if sparse_mma else -1
         opts.int4_mma = 0 if int4_mma else -1
+        opts.prefill_tc = 0 if prefill_tc is None else (1 if prefill_tc else -1)
         h = C.c_void_p()
         buf = (C.c_char * len(bundle)).from_buffer_copy(bundle)
         _check(self._lib.iolm_cuda_create(buf, len(bundle), device, C.byref(opts), C.byref(h)))
