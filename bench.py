@@ -273,6 +273,7 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     bundle = synth.toy_bundle(*cfg["dims"], seed=42, quant=cfg["quant"], heads=cfg.get("heads"),
                               ffn=cfg.get("ffn"))
     rt = R.ModelRuntime(bundle, device=local, kernel_timing=True, max_tokens_per_step=args.tokens_per_step,
+                        prefill_tc={"auto": None, "on": True, "off": False}[args.prefill_tc],
                         act_quant=cfg.get("act_quant", False))
     # this rank's rows for every warmup + timed step, host (pinned) and device copies
     host_ids, dev_ids, offsets = [], [], []
@@ -448,6 +449,8 @@ def main() -> None:
     ap.add_argument("--rows-per-step", type=int, default=16384)
     ap.add_argument("--tokens-per-step", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prefill-tc", choices=["auto", "on", "off"], default="auto",
+                    help="prefill attention kernel: tcgen05 (on), mma.sync (off), engine default (auto)")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="no per-kernel CUDA events (A/B check of their overhead; no roofline)")
     args = ap.parse_args()

@@ -299,9 +299,7 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
   if (d_ % 8 != 0) throw Unsupported("d_model must be a multiple of 8 for the GPU layout");
   if (hd_ != 16 && hd_ != 32 && hd_ != 64 && hd_ != 128)
     throw Unsupported("head_dim must be 16, 32, 64 or 128 on the GPU path");
-  // measured (bench C1 / C4): for hd 64 rows of 64 + 32 tokens the mma.sync kernel is faster (the
-  // 128-query tcgen05 tile is half empty and latency-bound); hd 128 / 544-token rows gain 14%
-  if (hd_ != 128 && !(hd_ == 64 && prefill_tc_force_)) prefill_tc_ = false;
+
   if (d_ > 4096) throw Unsupported("d_model > 4096");
   device_ = device;
   CUDA_OK(cudaSetDevice(device_));
@@ -321,6 +319,9 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
     if (opts->prefill_tc < 0) prefill_tc_ = false;
     prefill_tc_force_ = opts->prefill_tc > 0;
   }
+  // measured (bench C1 / C4): for hd 64 rows of 64 + 32 tokens the mma.sync kernel is faster (the
+  // 128-query tcgen05 tile is half empty); hd 128 / 544-token rows gain 40% (C4 prefill 158 -> 225 TFLOP/s)
+  if (hd_ != 128 && !(hd_ == 64 && prefill_tc_force_)) prefill_tc_ = false;
   // Default token budget: one 256-row GEMM M-tile per SM pair (74 x 256 = 18944 on a 148-SM B200),
   // so every projection's tile count is a whole number of waves of the persistent GEMM grid.
   const bool auto_budget = T_max_ <= 0;
