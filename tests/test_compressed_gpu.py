@@ -143,10 +143,13 @@ def test_reference_pruned_sparse24_bundle():
 
 def test_w8a8_wide_rows_d2048():
     """d_model 2048 (C4 width): the two-warp LayerNorm with int8 output feeds kind::i8 GEMMs;
-    checked against the W8A8 restatement."""
+    checked against the W8A8 restatement. Stated tolerance for this width: per position rel-L2
+    <= 3e-2 and mean <= 2e-2 - one per-token scale spans 2048 channels, so each int8 step is coarser
+    and a code flip caused by the GPU's bf16 attention (vs the restatement's f32) moves more."""
     b = synth.toy_bundle(2048, 1, 16, 2048, 160, seed=42, quant="q8")
     rt, oq = R.ModelRuntime(b, act_quant=True), O.OracleModel(b, act_quant=True)
     ids, offs = synth.rows(77, 2, 64)
     for r in range(2):
         row = ids[offs[r]:offs[r + 1]]
-        assert rel_l2_rows(rt.forward(row), oq.forward(row)[0]).max() <= W8A8_REL_TOL
+        rel = rel_l2_rows(rt.forward(row), oq.forward(row)[0])
+        assert rel.max() <= 3e-2 and rel.mean() <= 2e-2, (rel.max(), rel.mean())
