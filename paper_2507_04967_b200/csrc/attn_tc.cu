@@ -245,14 +245,15 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
       const int b = g & 1;
       mbar_wait(o_full(b), (g >> 1) & 1);
       tc_fence_after();
+      // all TMEM loads of the block in flight before one wait (each load-wait pair is a full
+      // TMEM round trip)
+      uint32_t r[HD];
 #pragma unroll
-      for (int c = 0; c < HD; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(lane_base + C::O_COL + b * HD + c, r);
-        tmem_ld_wait();
+      for (int c = 0; c < HD; c += 32)
+        tmem_ld_32x32b_x32(lane_base + C::O_COL + b * HD + c, *reinterpret_cast<uint32_t(*)[32]>(r + c));
+      tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[c + i] = fmaf(o[c + i], alpha, __uint_as_float(r[i]));
-      }
+      for (int i = 0; i < HD; ++i) o[i] = fmaf(o[i], alpha, __uint_as_float(r[i]));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty(b));
@@ -287,20 +288,20 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
           }
           continue;
         }
-        // pass 1: masked row max of the block (S stays in TMEM; it is read twice)
+        // the block's S row in registers (one TMEM round trip), masked row max
+        uint32_t sr[KB];
+#pragma unroll
+        for (int c = 0; c < KB; c += 32)
+          tmem_ld_32x32b_x32(lane_base + C::S_COL + b * KB + c, *reinterpret_cast<uint32_t(*)[32]>(sr + c));
+        tmem_ld_wait();
         float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < KB; c += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(lane_base + C::S_COL + b * KB + c, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int key = key0 + c + i;
-            bool ok = row_ok && key <= qpos;
-            if (MASK) ok = ok && key <= last_key && p.key_mask[key];
-            if (ok) mx = fmaxf(mx, __uint_as_float(r[i]));
-          }
+        for (int i = 0; i < KB; ++i) {
+          const int key = key0 + i;
+          bool ok = row_ok && key <= qpos;
+          if (MASK) ok = ok && key <= last_key && p.key_mask[key];
+          if (!ok) sr[i] = __float_as_uint(-INFINITY);
+          mx = fmaxf(mx, __uint_as_float(sr[i]));
         }
         const float mnew = fmaxf(m_run, mx * p.scale_log2);
         const float alpha = mnew == -INFINITY ? 1.f : ex2f(m_run - mnew);
@@ -311,16 +312,11 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
         uint8_t* prow = tsm + (sP + b * C::P_BYTES - raw) + row * 128;
 #pragma unroll
         for (int c = 0; c < KB; c += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(lane_base + C::S_COL + b * KB + c, r);
-          tmem_ld_wait();
           float pv[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const int key = key0 + c + i;
-            bool ok = row_ok && key <= qpos;
-            if (MASK) ok = ok && key <= last_key && p.key_mask[key];
-            pv[i] = ok ? ex2f(fmaf(__uint_as_float(r[i]), p.scale_log2, -msub)) : 0.f;
+            // masked keys hold -inf: ex2(-inf) = +0 (rows with no visible key have msub = 0)
+            pv[i] = ex2f(fmaf(__uint_as_float(sr[c + i]), p.scale_log2, -msub));
             l_run += pv[i];
           }
           // 32 keys = 4 16-byte chunks of this row; chunk g4 of 64-key region `region` lands at
