@@ -1311,11 +1311,12 @@ void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_
   // register-resident rows up to 1024 columns; wider rows take the two-pass kernel (its second
   // read hits L2) at 8 CTAs per SM: these launches are bound by load latency, not bytes
   else if (ch <= 4) quant_rows_kernel<4><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
-  else if (cols > 3072 && cols <= 4096) {  // measured: two-warp rows win at 4096 (C4 FFN), lose at 2560
+  else if (cols > 3072 && cols <= 5120) {  // measured: two-warp rows win at 4096 (C4 FFN), lose at 2560
     static int sms = 0;
     if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const int grid2 = std::min<int>((M + 3) / 4, sms * 2);
-    quant_rows2_kernel<8><<<grid2, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+    if (cols <= 4096) quant_rows2_kernel<8><<<grid2, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+    else quant_rows2_kernel<10><<<grid2, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
   } else quant_rows_kernel<0><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
   CUDA_OK(cudaGetLastError());
 }
