@@ -1,5 +1,7 @@
 // Kernel-level C entry points used by the parity tests: they run the production kernels on
 // host-provided operands (device allocation, H2D, launch, D2H inside).
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "capi_util.hpp"
@@ -37,6 +39,8 @@ int sm_count() {
 extern "C" int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, float* C,
                                          int32_t M, int32_t N, int32_t K, int32_t bn,
                                          int32_t epi) {
+  static const bool use_tma_epi =
+      std::getenv("IOLM_GEMM_TMA_EPI") == nullptr || std::string(std::getenv("IOLM_GEMM_TMA_EPI")) != "0";
   return guarded([&] {
     if (M <= 0 || N <= 0 || K <= 0 || (K % 8) != 0)
       throw ContractViolation("debug_gemm: need positive M,N and K % 8 == 0");
@@ -64,7 +68,14 @@ extern "C" int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, f
     } else {
       throw ContractViolation("debug_gemm: unsupported epilogue");
     }
-    launch_gemm(bn == 256, false, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
+    // the TMA store / reduce-add epilogue, as the engine runs it (N multiple of 8 keeps rows 16-B aligned)
+    CUtensorMap tc;
+    const CUtensorMap* out_map = nullptr;
+    if (use_tma_epi && N % 8 == 0 && (epi == iolmk::EPI_RESID_F32 || epi == iolmk::EPI_GELU_BF16 || epi == iolmk::EPI_BF16)) {
+      tc = epi == iolmk::EPI_RESID_F32 ? make_out_map(dC.p, true, N, M, 4ull * N) : make_out_map(dG.p, false, N, M, 2ull * N);
+      out_map = &tc;
+    }
+    launch_gemm(bn == 256, false, epi, ta, tb, M, N, K, ep, nullptr, sm_count(), out_map);
     CUDA_OK(cudaDeviceSynchronize());
     if (epi == iolmk::EPI_GELU_BF16 || epi == iolmk::EPI_BF16) {
       std::vector<__nv_bfloat16> h(static_cast<size_t>(M) * N);
@@ -146,9 +157,17 @@ extern "C" int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_
     cudaEvent_t e0, e1;
     CUDA_OK(cudaEventCreate(&e0));
     CUDA_OK(cudaEventCreate(&e1));
+    static const bool use_tma_epi =
+        std::getenv("IOLM_GEMM_TMA_EPI") == nullptr || std::string(std::getenv("IOLM_GEMM_TMA_EPI")) != "0";
+    CUtensorMap tc;
+    const CUtensorMap* out_map = nullptr;
+    if (use_tma_epi && N % 8 == 0 && (epi == iolmk::EPI_RESID_F32 || epi == iolmk::EPI_GELU_BF16 || epi == iolmk::EPI_BF16)) {
+      tc = make_out_map(dC.p, epi == iolmk::EPI_RESID_F32, N, M, (epi == iolmk::EPI_RESID_F32 ? 4ull : 2ull) * N);
+      out_map = &tc;
+    }
     auto go = [&] {
-      if (w4) launch_gemm_w4(pair != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
-      else launch_gemm(pair != 0, i8 != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count());
+      if (w4) launch_gemm_w4(pair != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count(), out_map);
+      else launch_gemm(pair != 0, i8 != 0, epi, ta, tb, M, N, K, ep, nullptr, sm_count(), out_map);
     };
     go();
     CUDA_OK(cudaEventRecord(e0));

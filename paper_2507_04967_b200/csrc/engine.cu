@@ -142,6 +142,7 @@ struct Layer {
   CUtensorMap tm_z, tm_g;    // bf16 A operands with this layer's K extent
   CUtensorMap tm_z8, tm_g8;  // int8 A operands (W8A8)
   CUtensorMap tm_z8s, tm_g8s;  // the same in the sparse kernel's 112-row boxes
+  CUtensorMap tm_g_out;        // g as the W_in GEMM's TMA store target (bf16 32 x 32 boxes)
   DevArray<__nv_bfloat16> kv;  // paged pool [pages][K|V][heads][PAGE][hd]
   CUtensorMap tm_kv, tm_kvg;     // the pool as rows of hd (prefill / decode attention TMA boxes)
 };
@@ -232,7 +233,7 @@ class Engine {
   void gemm(int epi, bool i8, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep);
   // one projection: dense (A = activations, B = weights) or 2:4 sparse (weights are the MMA's A)
   void gemm_w(int epi, const GemmW& w, const CUtensorMap& act, const CUtensorMap& act_sp, int M, int N, int K,
-              const GemmEpi& ep);
+              const GemmEpi& ep, const CUtensorMap* out_map = nullptr);
   void load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<std::string>& names, int K, int ld);
   uint64_t ref_madds_row(int s0, int advances) const;
   template <typename F>
@@ -251,6 +252,9 @@ class Engine {
   bool int4_mma_ = true;
   bool prefill_tc_ = true;  // tcgen05 prefill attention (hd 128 by default, hd 64 on request)
   bool prefill_tc_force_ = false;
+  // TMA-store epilogue of the W_in GEMM (IOLM_GEMM_TMA_EPI=0 disables, for A/B measurements):
+  // measured 3% faster than the warp's coalesced stores at the C1 shape
+  bool tma_epi_ = std::getenv("IOLM_GEMM_TMA_EPI") == nullptr || std::string(std::getenv("IOLM_GEMM_TMA_EPI")) != "0";
   uint64_t madds_A_ = 0, madds_B_ = 0;  // sum_l (4*d*kh + 2*d*f), sum_l kh
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
@@ -273,6 +277,8 @@ class Engine {
   DevArray<float> x_;
   DevArray<__nv_bfloat16> h_, q_, z_, g_;
   CUtensorMap tm_h_, tm_q_;
+  // (the TMA reduce-add epilogue for the residual GEMMs exists - GemmEpi::tma_out with an fp32 map -
+  // but measured 2% slower than the coalesced read-modify-write at the C1 shapes, so it is unused)
   DevArray<int8_t> h8_, z8_, g8_;  // W8A8 operands + per-token scales
   DevArray<float> hs_, zs_, gs_;
   CUtensorMap tm_h8_, tm_h8s_;
@@ -491,6 +497,7 @@ void Engine::alloc_runtime() {
   for (auto& ly : layers_) {
     ly->tm_z = make_kmajor_map(z_.p, BF, 2, ly->kh, T, 2ull * kh_max_, 128);
     ly->tm_g = make_kmajor_map(g_.p, BF, 2, ly->f, T, 2ull * f_ld_max_, 128);
+    ly->tm_g_out = make_out_map(g_.p, false, ly->f, T, 2ull * f_ld_max_);
   }
   if (any_int8_) {
     const auto U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
@@ -588,15 +595,16 @@ void Engine::gemm(int epi, bool i8, const CUtensorMap& A, const CUtensorMap& B, 
 }
 
 void Engine::gemm_w(int epi, const GemmW& w, const CUtensorMap& act, const CUtensorMap& act_sp, int M, int N, int K,
-                    const GemmEpi& ep) {
+                    const GemmEpi& ep, const CUtensorMap* out_map) {
   if (w.mode == W_SP24) {
     launch_gemm_sp(epi, w.tm, act_sp, w.tm_e, K, w.sl.katoms_pad, ep, stream_, sms_);
     ++stats_.kernel_launches;
   } else if (w.mode == W_INT4) {
-    launch_gemm_w4(use_pair(M, N), epi, act, w.tm, M, N, K, ep, stream_, sms_);
+    launch_gemm_w4(use_pair(M, N), epi, act, w.tm, M, N, K, ep, stream_, sms_, out_map);
     ++stats_.kernel_launches;
   } else {
-    gemm(epi, w.mode == W_INT8, act, w.tm, M, N, K, ep);
+    launch_gemm(use_pair(M, N), w.mode == W_INT8, epi, act, w.tm, M, N, K, ep, stream_, sms_, out_map);
+    ++stats_.kernel_launches;
   }
 }
 
@@ -773,7 +781,8 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     ei.ldo = f_ld_max_;
     scales(ei, ly.in, hs_.p);
     timed(6, 2.0 * dT * ly.f * d_, [&] {
-      gemm_w(iolmk::EPI_GELU_BF16, ly.in, i8_in ? tm_h8_ : tm_h_, tm_h8s_, T, ly.f, d_, ei);
+      gemm_w(iolmk::EPI_GELU_BF16, ly.in, i8_in ? tm_h8_ : tm_h_, tm_h8s_, T, ly.f, d_, ei,
+             tma_epi_ ? &ly.tm_g_out : nullptr);
     });
     // x += g * Wout^T
     if (i8_out) {

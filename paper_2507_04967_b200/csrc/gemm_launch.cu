@@ -9,6 +9,9 @@ namespace iolmh {
 
 using namespace iolmk;
 
+// Output tensor map of the launch in flight (ep.tma_out): set by launch_gemm / launch_gemm_w4.
+static thread_local const CUtensorMap* g_out_map = nullptr;
+
 template <int BN, int EPI, int CG, bool I8, bool W4 = false>
 static void launch_one(const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep,
                        cudaStream_t st, int grid_cap) {
@@ -34,7 +37,7 @@ static void launch_one(const CUtensorMap& A, const CUtensorMap& B, int M, int N,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_OK(cudaLaunchKernelEx(&cfg, kern, A, B, M, N, K, ep));
+  CUDA_OK(cudaLaunchKernelEx(&cfg, kern, A, B, ep.tma_out ? *g_out_map : A, M, N, K, ep));
 }
 
 template <int BN, int CG, bool I8>
@@ -74,8 +77,11 @@ static void dispatch_w4(int epi, const CUtensorMap& A, const CUtensorMap& B, int
 }
 
 void launch_gemm_w4(bool pair, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
-                    const GemmEpi& ep, cudaStream_t st, int grid_cap) {
+                    const GemmEpi& ep_in, cudaStream_t st, int grid_cap, const CUtensorMap* out_map) {
   if (M <= 0 || N <= 0) return;
+  GemmEpi ep = ep_in;
+  ep.tma_out = out_map != nullptr && (epi == EPI_RESID_F32 || epi == EPI_BF16 || epi == EPI_GELU_BF16);
+  g_out_map = out_map;
   if (pair) dispatch_w4<256, 2>(epi, A, B, M, N, K, ep, st, grid_cap);
   else dispatch_w4<128, 1>(epi, A, B, M, N, K, ep, st, grid_cap);
   CUDA_OK(cudaGetLastError());
@@ -83,8 +89,11 @@ void launch_gemm_w4(bool pair, int epi, const CUtensorMap& A, const CUtensorMap&
 
 // pair = true: 2-SM 256x256 tiles; false: single-CTA 128x128 tiles.
 void launch_gemm(bool pair, bool i8, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
-                 const GemmEpi& ep, cudaStream_t st, int grid_cap) {
+                 const GemmEpi& ep_in, cudaStream_t st, int grid_cap, const CUtensorMap* out_map) {
   if (M <= 0 || N <= 0) return;
+  GemmEpi ep = ep_in;
+  ep.tma_out = out_map != nullptr && (epi == EPI_RESID_F32 || epi == EPI_BF16 || epi == EPI_GELU_BF16);
+  g_out_map = out_map;
   if (pair) {
     if (i8) dispatch_epi<256, 2, true>(epi, A, B, M, N, K, ep, st, grid_cap);
     else dispatch_epi<256, 2, false>(epi, A, B, M, N, K, ep, st, grid_cap);

@@ -45,6 +45,9 @@ struct GemmEpi {
   // W8A8 dequant epilogue: acc_i32 * a_scale[row] * w_scale[col]
   const float* a_scale = nullptr;
   const float* w_scale = nullptr;
+  // RESID / BF16 / GELU: write full 32 x 32 chunks with TMA (store, or reduce-add into x) from the
+  // warp's staging tile instead of per-thread global stores (the kernel's tmC describes `out`)
+  int tma_out = 0;
 };
 
 // Tile configuration. CG = 2 runs the 2-SM UMMA: a CTA pair computes a 256 x BN tile, each CTA
@@ -71,8 +74,8 @@ struct GemmCfg {
   static constexpr int CONV_WARPS = W4 ? 4 : 0;
   static constexpr uint32_t RAW_BYTES = W4 ? BN_CTA * 32 : 0;  // packed int4 per stage
   static constexpr int THREADS = 64 + 32 * EPI_WARPS + 32 * CONV_WARPS;
-  static constexpr size_t SMEM = 1024 + STAGES * (STAGE_BYTES + RAW_BYTES) + 512 + BN * 4 +
-                                 EPI_WARPS * 5120;  // rings, barriers, scales, tiles
+  static constexpr size_t SMEM = 1024 + STAGES * (STAGE_BYTES + RAW_BYTES) + 2048 +
+                                 EPI_WARPS * 5120;  // rings, barriers + scales, 1 KB-aligned warp tiles
   static_assert(!W4 || BN_CTA == 128, "W4 converter maps one thread per staged weight row");
 };
 
@@ -214,11 +217,46 @@ __device__ __forceinline__ int swz(int r, int g) { return r * 32 + ((g ^ (r & 7)
 
 template <int EPI>
 __device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* tile, int m_base, int n0, float (&v)[32],
-                                                   int lane, const QkvRow* rows = nullptr) {
+                                                   int lane, const QkvRow* rows = nullptr,
+                                                   const CUtensorMap* tmC = nullptr) {
   const int rr = lane >> 3, gg = lane & 7;  // coalesced phase: row rr + 4i, column group gg
   if constexpr (EPI == EPI_GELU_BF16) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+  }
+  if constexpr (EPI == EPI_RESID_F32 || EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
+    if (ep.tma_out) {
+      // the tile may still be the source of this warp's previous bulk store
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+      if constexpr (EPI == EPI_RESID_F32) {
+        // fp32 32 x 32 box in the SWIZZLE_128B layout (16-byte chunk g of row r at g ^ (r & 7)):
+        // exactly swz(); TMA adds it into x in L2 - no read of x on the SM
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          *reinterpret_cast<float4*>(tile + swz(lane, g)) = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+      } else {
+        // bf16 32 x 32 box, SWIZZLE_64B: 16-byte chunk k of 64-byte row r at k ^ ((r >> 1) & 3)
+        uint8_t* trow = reinterpret_cast<uint8_t*>(tile) + lane * 64;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint4 w;
+          w.x = pack_bf16x2(v[8 * k + 0], v[8 * k + 1]);
+          w.y = pack_bf16x2(v[8 * k + 2], v[8 * k + 3]);
+          w.z = pack_bf16x2(v[8 * k + 4], v[8 * k + 5]);
+          w.w = pack_bf16x2(v[8 * k + 6], v[8 * k + 7]);
+          *reinterpret_cast<uint4*>(trow + ((k ^ ((lane >> 1) & 3)) << 4)) = w;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (EPI == EPI_RESID_F32) tma_reduce_add_2d(tmC, smem_u32(tile), n0, m_base);
+        else tma_store_2d(tmC, smem_u32(tile), n0, m_base);
+        bulk_commit();
+      }
+      return;
+    }
   }
 #pragma unroll
   for (int g = 0; g < 8; ++g)
@@ -294,8 +332,8 @@ __device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* til
 
 template <int BN, int EPI, int CG, bool I8, bool W4 = false>
 __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
-    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, GemmEpi ep) {
+    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, GemmEpi ep) {
   using C = GemmCfg<BN, CG, W4>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -487,7 +525,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
     constexpr int NCH = WCOLS / 32;              // 32-column chunks per warp per tile
     const uint32_t leader_tempty0 = CG == 2 ? mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
     float* s_scale = reinterpret_cast<float*>(smem_raw + (bars + 512 - raw));  // [BN] per tile
-    uint8_t* s_warp = smem_raw + (bars + 512 + BN * 4 - raw) + e * 5120;
+    uint8_t* s_warp = smem_raw + (bars + 2048 - raw) + e * 5120;  // 1024-byte aligned (TMA swizzle)
     float* s_tile = reinterpret_cast<float*>(s_warp);                 // 32 x 32 fp32 (4 KB)
     QkvRow* s_rows = reinterpret_cast<QkvRow*>(s_warp + 4096);        // the warp's 32 row destinations
     const bool has_ws = ep.w_scale != nullptr;
@@ -556,7 +594,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rc[j]);
             }
-            warp_tile_epilogue<EPI>(ep, s_tile, m_base, n0, v, lane, s_rows);
+            warp_tile_epilogue<EPI>(ep, s_tile, m_base, n0, v, lane, s_rows, &tmC);
             continue;
           }
         }
@@ -597,6 +635,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1u;
     }
+    if (ep.tma_out && lane == 0) bulk_wait0();  // this warp's bulk stores / reductions are complete
   }
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync();

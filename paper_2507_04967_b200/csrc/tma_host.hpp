@@ -93,4 +93,22 @@ inline CUtensorMap make_w4_map(const void* ptr, uint64_t K, uint64_t rows, uint6
   return m;
 }
 
+// GEMM output boxes of 32 x 32 for the TMA epilogue: fp32 [rows x cols] with SWIZZLE_128B (the
+// epilogue's swz() staging layout), bf16 [rows x cols] with SWIZZLE_64B.
+inline CUtensorMap make_out_map(const void* ptr, bool f32, uint64_t cols, uint64_t rows, uint64_t row_stride_bytes) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  if ((row_stride_bytes % 16) != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
+    throw std::runtime_error("output map must be 16-byte aligned with a 16-byte row stride");
+  CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (GEMM output) failed: " + std::to_string(r));
+  return m;
+}
+
 }  // namespace iolmh
