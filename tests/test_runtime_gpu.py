@@ -200,3 +200,26 @@ def test_prefill_tc_matches_mma_sync(cfg, row_chars):
     assert same >= 5
     one, ol, _ = tc.decode_token_rows(ids[offs[3]:offs[4]], np.array([0, offs[4] - offs[3]]), 8)
     assert ol[0] == gl[3] and np.array_equal(one[0, :ol[0]], gi[3, :gl[3]])
+
+
+@pytest.mark.parametrize("max_new", [1, 3, 8])
+def test_ragged_rows_and_budgets(model, max_new):
+    """Rows of mixed lengths (BOS only, 1 char, ... up to near max_seq_len) in one call, with the
+    join's 1-token budget and others: identical to the oracle except fp near-ties, madds exact,
+    and every row equal to its own single-row call (batch invariance with ragged neighbours)."""
+    cfg, b, rt = model
+    S = cfg[4]
+    rng = np.random.default_rng(max_new)
+    lens = [0, 1, 2, 15, 16, 17, 31, 33, 63, 64, 65, S - 2 - max_new, S - 2] + list(rng.integers(0, S - 1, 19))
+    rows = ["".join(chr(32 + int(c)) for c in rng.integers(0, 95, n)) for n in lens]
+    ids = np.concatenate([np.array([R.BOS] + R.encode(r), np.int32) for r in rows])
+    offs = np.concatenate([[0], np.cumsum([len(r) + 1 for r in rows])]).astype(np.int64)
+    om = O.OracleModel(b)
+    gi, gl, gm = rt.decode_token_rows(ids, offs, max_new)
+    oi, ol, omm = om.decode_ids(ids, offs, max_new, threads=8)
+    assert gm == omm
+    bad = [i for i in range(len(rows)) if gl[i] != ol[i] or not np.array_equal(gi[i, :gl[i]], oi[i, :ol[i]])]
+    assert len(bad) <= 1, bad
+    for i in [0, 1, 12, 20]:
+        one, l1, _ = rt.decode_token_rows(ids[offs[i]:offs[i + 1]], np.array([0, offs[i + 1] - offs[i]]), max_new)
+        assert l1[0] == gl[i] and np.array_equal(one[0, :l1[0]], gi[i, :gl[i]])
