@@ -48,6 +48,10 @@ CONFIGS = {
                heads=[10] * 24, ffn=[2560] * 24,
                desc="C3: C1 model pruned 50% (10 of 20 heads, FFN 2560) + 2:4 magnitude + q8 (sparse24_q8), "
                     "W8A8, 32+64, 8 new"),
+    "c3b": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="sparse24", act_quant=True,
+                heads=[7 + l % 6 for l in range(24)], ffn=[2500 + 12 * l for l in range(24)],
+                desc="C3b: C1 model with irregular per-layer pruning (7-12 of 20 heads, FFN 2500 + 12 l) + 2:4 + q8 "
+                     "(sparse24_q8), W8A8, 32+64, 8 new"),
     "c4": dict(dims=(2048, 28, 16, 8192, 576), row_chars=512, quant="sparse24", act_quant=True,
                heads=[8] * 28, ffn=[4096] * 28,
                desc="C4: 1.5B-class (2048,28,16,8192,576) pruned 50% + 2:4 + q8, W8A8, 32-token prefix + "
