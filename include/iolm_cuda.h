@@ -118,6 +118,19 @@ int iolm_cuda_decode_device_ids(iolm_cuda_ctx* ctx, const int32_t* d_ids,
 int iolm_cuda_forward_logits(iolm_cuda_ctx* ctx, const int32_t* ids, const uint8_t* mask,
                              int32_t n, float* logits, uint64_t* madds);
 
+/*
+ * forward with calibration capture (ModelRuntime::forward(ids, mask, counter, CaptureSink*),
+ * runtime.hpp:22-28 / :48-49, used by capture_calibration, proj/src/calib.cpp:20-62): logits as in
+ * iolm_cuda_forward_logits, plus the inputs every linear weight saw, as bf16 bit patterns, for ALL n
+ * positions (the caller drops masked rows, as the reference records non-pad positions only).
+ * Layout, layer by layer: [attn_in n x d][attn_out_in n x kh_l][ffn_in n x d][ffn_mid n x f_l]
+ * (capture points "layers.<l>.attn_in" = LN1 output, "attn_out_in" = attention output, "ffn_in" =
+ * LN2 output, "ffn_mid" = GELU output). capture holds n * sum_l (2 d + kh_l + f_l) elements.
+ * Not available with opts.act_quant (the reference calibrates the baseline model).
+ */
+int iolm_cuda_forward_capture(iolm_cuda_ctx* ctx, const int32_t* ids, const uint8_t* mask, int32_t n,
+                              float* logits, uint16_t* capture, uint64_t* madds);
+
 /* Counters of the last decode/forward call on this context. */
 int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* out);
 

@@ -15,6 +15,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -27,6 +28,7 @@
 #include "iolm/common.hpp"
 #include "iolm/matrix.hpp"
 #include "iolm/model.hpp"
+#include "iolm/runtime.hpp"  // iolm::CaptureSink
 #endif
 
 namespace iolm::cuda {
@@ -127,6 +129,58 @@ class ModelRuntime {
     counter.add(madds);
     return out;
   }
+
+#ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
+  // forward(ids, mask, counter, CaptureSink*) (runtime.hpp:48-49): the calibration capture of
+  // capture_calibration (calib.cpp:44-51) - every linear weight's input rows for the non-pad
+  // positions, under the reference's capture-point names, captured on the GPU (bf16 -> f32).
+  std::vector<float> forward(std::span<const int> ids, std::span<const uint8_t> mask, FlopCounter& counter,
+                             iolm::CaptureSink* capture) const {
+    if (!capture) return forward(ids, mask, counter);
+    if (ids.empty()) throw ContractViolation("forward: empty sequence");
+    if (!mask.empty() && mask.size() != ids.size()) throw ContractViolation("forward: mask length mismatch");
+    const int n = static_cast<int>(ids.size());
+    std::vector<int> kh(cfg_.n_layers), f(cfg_.n_layers);
+    size_t total = 0;
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+      int32_t heads = 0, ffn = 0;
+      check(iolm_cuda_layer_shape(ctx_, l, &heads, &ffn));
+      kh[l] = heads * cfg_.head_dim;
+      f[l] = ffn;
+      total += static_cast<size_t>(n) * (2 * cfg_.d_model + kh[l] + f[l]);
+    }
+    std::vector<int32_t> v(ids.begin(), ids.end());
+    std::vector<float> out(static_cast<size_t>(n) * cfg_.vocab_size);
+    std::vector<uint16_t> cap(total);
+    uint64_t madds = 0;
+    check(iolm_cuda_forward_capture(ctx_, v.data(), mask.empty() ? nullptr : mask.data(), n, out.data(), cap.data(),
+                                    &madds));
+    counter.add(madds);
+    size_t off = 0;
+    std::vector<float> row;
+    auto take = [&](const std::string& point, int cols) {
+      for (int t = 0; t < n; ++t) {
+        if (mask.empty() || mask[t]) {
+          row.resize(cols);
+          for (int c = 0; c < cols; ++c) {
+            const uint32_t bits = static_cast<uint32_t>(cap[off + static_cast<size_t>(t) * cols + c]) << 16;
+            std::memcpy(&row[c], &bits, 4);
+          }
+          capture->add_row(point, row);
+        }
+      }
+      off += static_cast<size_t>(n) * cols;
+    };
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+      const std::string p = "layers." + std::to_string(l) + ".";
+      take(p + "attn_in", cfg_.d_model);
+      take(p + "attn_out_in", kh[l]);
+      take(p + "ffn_in", cfg_.d_model);
+      take(p + "ffn_mid", f[l]);
+    }
+    return out;
+  }
+#endif
 
   std::string greedy_decode(std::string_view prompt, int max_new_tokens, FlopCounter& counter) const {
     const std::string p(prompt);

@@ -215,7 +215,8 @@ class Engine {
 
   void decode(const int32_t* ids, bool ids_on_device, const int64_t* offsets, int64_t n_rows, int max_new,
               int32_t* out_ids, int32_t* out_len, uint64_t* madds, int64_t* bad_row);
-  void forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds);
+  void forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds,
+               uint16_t* capture = nullptr);
 
   std::mutex mu;
   void set_kernel_timing(bool on) { ktime_ = on; }
@@ -290,6 +291,12 @@ class Engine {
   DevArray<int> d_scalar_;
   DevArray<float> d_logits_;
   DevArray<uint8_t> d_mask_;
+  // calibration capture (forward with a CaptureSink, runtime.hpp:22-28): per layer the four linear
+  // inputs [attn_in n x d][attn_out_in n x kh][ffn_in n x d][ffn_mid n x f] as bf16, back to back
+  DevArray<__nv_bfloat16> d_cap_;
+  __nv_bfloat16* cap_ = nullptr;  // non-null while a capturing forward is being launched
+  size_t cap_off_ = 0;
+  void capture_rows(const __nv_bfloat16* src, int ld, int T, int cols);
 };
 
 Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opts* opts) {
@@ -685,6 +692,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
                     hs_.p);
   });
   ++stats_.kernel_launches;
+  capture_rows(h_.p, d_, T, d_);  // layers.0.attn_in
   // algorithmic attention work of this step (per head): prefill FLOPs 4*hd*sum(pos+1),
   // decode K+V bytes 2*2*hd*(pos+1)
   double pre_keys = 0, dec_keys = 0;
@@ -754,6 +762,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       timed(3, 4.0 * hd_ * ly.heads * dec_keys, [&] { launch_attention(none, dec, hd_, stream_); });
       ++stats_.kernel_launches;
     }
+    capture_rows(z_.p, kh_max_, T, ly.kh);  // layers.l.attn_out_in
     // x += z * Wo^T
     if (i8_o) {
       timed(9, dT * ly.kh * 3.0, [&] { launch_quant_rows(z_.p, kh_max_, T, ly.kh, z8_.p, kh_max_, zs_.p, stream_); });
@@ -773,6 +782,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       launch_ln(x_.p, T, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_, i8_in ? h8_.p : nullptr, hs_.p);
     });
     ++stats_.kernel_launches;
+    capture_rows(h_.p, d_, T, d_);  // layers.l.ffn_in
     // g = gelu(h * Win^T)
     GemmEpi ei;
     ei.M = T;
@@ -784,6 +794,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       gemm_w(iolmk::EPI_GELU_BF16, ly.in, i8_in ? tm_h8_ : tm_h_, tm_h8s_, T, ly.f, d_, ei,
              tma_epi_ ? &ly.tm_g_out : nullptr);
     });
+    capture_rows(g_.p, f_ld_max_, T, ly.f);  // layers.l.ffn_mid (post-GELU)
     // x += g * Wout^T
     if (i8_out) {
       timed(9, dT * ly.f * 3.0, [&] { launch_quant_rows(g_.p, f_ld_max_, T, ly.f, g8_.p, f_ld_max_, gs_.p, stream_); });
@@ -801,6 +812,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
                   q8_next ? h8_.p : nullptr, hs_.p);
       });
       ++stats_.kernel_launches;
+      capture_rows(h_.p, d_, T, d_);  // layers.l+1.attn_in
     }
   }
   if (R > 0) {
@@ -1002,7 +1014,15 @@ void Engine::decode(const int32_t* ids, bool ids_on_device, const int64_t* offse
   stats_.device_ms = ms;
 }
 
-void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds) {
+void Engine::capture_rows(const __nv_bfloat16* src, int ld, int T, int cols) {
+  if (!cap_) return;
+  CUDA_OK(cudaMemcpy2DAsync(cap_ + cap_off_, static_cast<size_t>(cols) * 2, src, static_cast<size_t>(ld) * 2,
+                            static_cast<size_t>(cols) * 2, T, cudaMemcpyDeviceToDevice, stream_));
+  cap_off_ += static_cast<size_t>(T) * cols;
+}
+
+void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds,
+                     uint16_t* capture) {
   CUDA_OK(cudaSetDevice(device_));
   reset_counters();
   if (n <= 0 || !ids) throw ContractViolation("forward: empty sequence");
@@ -1028,7 +1048,23 @@ void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logi
     sb.step.head_slot.push_back(0);
     sb.step.head_owner.push_back(0);
   }
-  launch_step(sb, d_ids_.p, dmask, d_logits_.p);
+  size_t cap_elems = 0;
+  if (capture) {
+    if (act_quant_) throw Unsupported("forward capture: not available with act_quant (capture the baseline model)");
+    for (const auto& ly : layers_) cap_elems += static_cast<size_t>(n) * (2 * d_ + ly->kh + ly->f);
+    d_cap_.ensure(cap_elems);
+    cap_ = d_cap_.p;
+    cap_off_ = 0;
+  }
+  try {
+    launch_step(sb, d_ids_.p, dmask, d_logits_.p);
+  } catch (...) {
+    cap_ = nullptr;
+    throw;
+  }
+  cap_ = nullptr;
+  if (capture)
+    CUDA_OK(cudaMemcpyAsync(capture, d_cap_.p, cap_elems * sizeof(__nv_bfloat16), cudaMemcpyDeviceToHost, stream_));
   CUDA_OK(cudaMemcpyAsync(logits, d_logits_.p, sizeof(float) * n * V_, cudaMemcpyDeviceToHost, stream_));
   CUDA_OK(cudaEventRecord(ev1_, stream_));
   CUDA_OK(cudaEventSynchronize(ev1_));
@@ -1139,6 +1175,15 @@ extern "C" int iolm_cuda_set_kernel_timing(iolm_cuda_ctx* ctx, int32_t on) {
     if (!ctx) throw iolmh::ContractViolation("null argument");
     std::lock_guard<std::mutex> lk(ctx->eng->mu);
     ctx->eng->set_kernel_timing(on != 0);
+  });
+}
+
+extern "C" int iolm_cuda_forward_capture(iolm_cuda_ctx* ctx, const int32_t* ids, const uint8_t* mask, int32_t n,
+                                         float* logits, uint16_t* capture, uint64_t* madds) {
+  return guarded([&] {
+    if (!ctx || !logits || !capture) throw iolmh::ContractViolation("null argument");
+    std::lock_guard<std::mutex> lock(ctx->eng->mu);
+    ctx->eng->forward(ids, mask, n, logits, madds, capture);
   });
 }
 

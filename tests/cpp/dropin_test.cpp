@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "iolm/calib.hpp"
 #include "iolm/runtime.hpp"
 #include "iolm/tokenizer.hpp"
 #include "iolm/train.hpp"
@@ -81,6 +82,36 @@ int main() {
     threw = true;
   }
   EXPECT(threw, "ContractViolation");
+  // calibration capture (capture_calibration, calib.cpp:20-62) on the GPU: same capture points,
+  // shapes, and rows (bf16 capture of the f32 activations: rel-L2 per point <= 1e-2)
+  {
+    std::vector<std::string> cal(prompts.begin(), prompts.begin() + 4);
+    cal[1].resize(20);
+    iolm::Rng crng(3);
+    const iolm::CalibrationSet ref = iolm::capture_calibration(cpu, cal, 8, crng);
+    iolm::CaptureSink sink;
+    iolm::FlopCounter fc;
+    for (const auto& pr : cal) {
+      std::vector<int> cids{iolm::Tokenizer::kBos};
+      for (int id : iolm::Tokenizer::encode(pr)) cids.push_back(id);
+      gpu.forward(cids, {}, fc, &sink);
+    }
+    EXPECT(sink.points.size() == ref.inputs.size(), "capture point count");
+    double worst_cap = 0;
+    for (const auto& [point, m] : ref.inputs) {
+      const iolm::Matrix g = sink.matrix(point);
+      EXPECT(g.rows == m.rows && g.cols == m.cols, "capture shape");
+      if (g.rows != m.rows || g.cols != m.cols) continue;
+      double num = 0, den = 0;
+      for (size_t i = 0; i < m.data.size(); ++i) {
+        num += (m.data[i] - g.data[i]) * (m.data[i] - g.data[i]);
+        den += static_cast<double>(m.data[i]) * m.data[i];
+      }
+      worst_cap = std::max(worst_cap, std::sqrt(num / std::max(den, 1e-30)));
+    }
+    EXPECT(worst_cap <= 1e-2, "capture rel-L2");
+    std::printf("calibration capture: %zu points, worst rel-L2 %.3e\n", ref.inputs.size(), worst_cap);
+  }
   std::printf(fails ? "DROPIN FAIL\n" : "DROPIN OK\n");
   return fails ? 1 : 0;
 }
