@@ -223,3 +223,36 @@ def test_ragged_rows_and_budgets(model, max_new):
     for i in [0, 1, 12, 20]:
         one, l1, _ = rt.decode_token_rows(ids[offs[i]:offs[i + 1]], np.array([0, offs[i + 1] - offs[i]]), max_new)
         assert l1[0] == gl[i] and np.array_equal(one[0, :l1[0]], gi[i, :gl[i]])
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_c1_full_model_against_compiled_reference():
+    """The benchmark model itself (BASELINE configs[1]: 0.5B-class, 24 layers, seed-42 weights) on
+    the benchmark rows: GPU greedy outputs against the reference's own batch_decode (compiled
+    unmodified) on 8 rows, madds exact, and last-position logits within the stated tolerance."""
+    b = synth.toy_bundle(1280, 24, 20, 5120, 128, seed=42)
+    rt, ref = R.ModelRuntime(b), O.RefRuntime(b)
+    prompts = synth.row_strings(0, 8, 64)
+    want, rm = ref.batch_decode(prompts, 8, threads=8)
+    c = R.FlopCounter()
+    got = rt.batch_decode(prompts, 8, c)
+    assert c.total() == rm
+    assert sum(a == b2 for a, b2 in zip(got, want)) >= 7, (got, want)
+    ids, offs = synth.rows(0, 1, 64)
+    row = ids[offs[0]:offs[1]]
+    g, r = rt.forward(row)[-1], ref.forward(row)[0][-1]
+    assert np.linalg.norm(g - r) / np.linalg.norm(r) <= LOGIT_REL_TOL
+    threads_out = []
+
+    import threading
+
+    def worker():
+        threads_out.append(rt.batch_decode(prompts[:4], 8))
+
+    ts = [threading.Thread(target=worker) for _ in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    # concurrent calls on one runtime are serialized by the engine and give identical results
+    assert all(o == got[:4] for o in threads_out)
