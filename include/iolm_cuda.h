@@ -32,6 +32,7 @@ extern "C" {
 #define IOLM_E_CORRUPT_HEADER 6    /* iolm::CorruptHeader */
 #define IOLM_E_TRUNCATED_BLOB 7    /* iolm::TruncatedBlob */
 #define IOLM_E_UNKNOWN_ENCODING 8  /* iolm::UnknownEncoding */
+#define IOLM_E_STALE 9             /* device-layout image does not match the bundle hash / weight options */
 
 /* Tokenizer constants (proj/include/iolm/tokenizer.hpp:17-20). */
 #define IOLM_VOCAB 131
@@ -130,6 +131,31 @@ int iolm_cuda_forward_logits(iolm_cuda_ctx* ctx, const int32_t* ids, const uint8
  */
 int iolm_cuda_forward_capture(iolm_cuda_ctx* ctx, const int32_t* ids, const uint8_t* mask, int32_t n,
                               float* logits, uint16_t* capture, uint64_t* madds);
+
+/*
+ * Device-layout image: the pre-tiled cache a registry keeps next to a bundle.
+ * The reference rebuilds its runtime from the bundle on every load - deserialize, FNV-1a over the
+ * whole serialized bundle, decode every tensor (ModelRegistry::lookup, proj/src/optimize.cpp:
+ * 139-151; deserialize_bundle / ModelBundle::hash, proj/src/model.cpp:348-411; ModelRuntime ctor,
+ * proj/src/runtime.cpp:60-89). An image holds the weights exactly as this engine keeps them in HBM
+ * (bf16 / int8 / 2:4-compressed codes + pre-tiled metadata / packed int4, per-row scales), the model
+ * config and the bundle hash, so loading is a streamed file read + H2D copy: no hashing, no decode,
+ * no host repack, and half the bytes of the f32 bundle for dense models.
+ *
+ * save_image: writes the context's device layout to `path` (atomically: path.tmp + rename).
+ * create_from_image: builds a context from an image. expected_hash != 0 must equal the image's
+ * bundle hash (the registry index entry's hash), and the weight-shaping options (act_quant,
+ * sparse_mma, int4_mma) must resolve as they did for the saved context; otherwise IOLM_E_STALE and
+ * the caller falls back to iolm_cuda_create on the bundle. Engine-only options (token budget,
+ * slots, prefix sharing, timing, prefill kernel) may differ. Bad magic / malformed header:
+ * IOLM_E_CORRUPT_HEADER; short file: IOLM_E_TRUNCATED_BLOB; checksum mismatch: IOLM_E_CORRUPT_HEADER.
+ * The context then behaves bit-for-bit like the one that was saved.
+ * image_info: header only (no device work): the image's bundle hash and model config.
+ */
+int iolm_cuda_save_image(iolm_cuda_ctx* ctx, const char* path);
+int iolm_cuda_create_from_image(const char* path, uint64_t expected_hash, int device,
+                                const iolm_cuda_opts* opts, iolm_cuda_ctx** out);
+int iolm_cuda_image_info(const char* path, uint64_t* bundle_hash, iolm_cuda_model_config* cfg);
 
 /* Counters of the last decode/forward call on this context. */
 int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* out);

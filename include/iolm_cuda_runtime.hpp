@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -74,6 +75,11 @@ class FlopCounter {
 struct GpuError : Error {
   explicit GpuError(const std::string& w) : Error(w) {}
 };
+// A device-layout image that no longer matches its bundle / the requested weight options: the
+// caller rebuilds from the bundle (what ModelRegistry::lookup does for a stale entry, optimize.cpp:145).
+struct StaleImage : Error {
+  explicit StaleImage(const std::string& w) : Error(w) {}
+};
 
 inline void check(int st) {
   if (st == IOLM_OK) return;
@@ -84,6 +90,7 @@ inline void check(int st) {
     case IOLM_E_CORRUPT_HEADER: throw CorruptHeader(msg);
     case IOLM_E_TRUNCATED_BLOB: throw TruncatedBlob(msg);
     case IOLM_E_UNKNOWN_ENCODING: throw UnknownEncoding(msg);
+    case IOLM_E_STALE: throw StaleImage(msg);
     default: throw GpuError(msg);
   }
 }
@@ -109,6 +116,17 @@ class ModelRuntime {
   ModelRuntime(const ModelRuntime&) = delete;
   ModelRuntime& operator=(const ModelRuntime&) = delete;
   ~ModelRuntime() { iolm_cuda_destroy(ctx_); }
+
+  // From a device-layout image (iolm_cuda_create_from_image); expected_hash = the registry entry's
+  // bundle hash (0: unchecked). Throws StaleImage when the image must be rebuilt from the bundle.
+  static std::unique_ptr<ModelRuntime> from_image(const std::string& path, uint64_t expected_hash, int device = 0,
+                                                  const iolm_cuda_opts* opts = nullptr) {
+    iolm_cuda_ctx* ctx = nullptr;
+    check(iolm_cuda_create_from_image(path.c_str(), expected_hash, device, opts, &ctx));
+    return std::unique_ptr<ModelRuntime>(new ModelRuntime(ctx));
+  }
+  // Writes this runtime's device layout next to its bundle (iolm_cuda_save_image).
+  void save_image(const std::string& path) const { check(iolm_cuda_save_image(ctx_, path.c_str())); }
 
   const Config& config() const { return cfg_; }
   uint64_t bundle_hash() const {
@@ -227,6 +245,13 @@ class ModelRuntime {
   iolm_cuda_ctx* handle() const { return ctx_; }
 
  private:
+  explicit ModelRuntime(iolm_cuda_ctx* ctx) : ctx_(ctx) {
+    iolm_cuda_model_config c{};
+    const int st = iolm_cuda_config(ctx_, &c);
+    if (st != IOLM_OK) iolm_cuda_destroy(ctx_);
+    check(st);
+    cfg_ = {c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.d_ff, c.max_seq_len, c.head_dim};
+  }
   iolm_cuda_ctx* ctx_ = nullptr;
   Config cfg_{};
 };

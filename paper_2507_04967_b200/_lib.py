@@ -21,6 +21,7 @@ IOLM_E_OOM = 5
 IOLM_E_CORRUPT_HEADER = 6
 IOLM_E_TRUNCATED_BLOB = 7
 IOLM_E_UNKNOWN_ENCODING = 8
+IOLM_E_STALE = 9
 
 VOCAB, PAD, BOS, EOS = 131, 128, 129, 130
 KCLASSES = ["embed_ln", "gemm_qkv", "attn_prefill", "attn_decode", "gemm_o", "ln", "gemm_in",
@@ -64,6 +65,10 @@ class Stats(C.Structure):
 SIGNATURES = {
     "iolm_cuda_create": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.POINTER(Opts), C.POINTER(C.c_void_p)]),
     "iolm_cuda_destroy": (None, [C.c_void_p]),
+    "iolm_cuda_save_image": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "iolm_cuda_create_from_image": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(Opts),
+                                              C.POINTER(C.c_void_p)]),
+    "iolm_cuda_image_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(ModelConfigC)]),
     "iolm_cuda_bundle_hash": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "iolm_cuda_config": (C.c_int, [C.c_void_p, C.POINTER(ModelConfigC)]),
     "iolm_cuda_layer_shape": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),

@@ -18,12 +18,14 @@
 // contribution is the reference's closed form (runtime.cpp:311-345).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "bundle.hpp"
@@ -135,6 +137,26 @@ struct GemmW {
   bool int8() const { return mode == W_INT8 || mode == W_SP24; }
 };
 
+size_t w4_pitch(int K) { return (static_cast<size_t>(K + 1) / 2 + 15) / 16 * 16; }
+
+// TMA descriptors of one weight group once its arrays are resident (bundle or image load).
+void weight_maps(GemmW& w, int N, int K, int ld) {
+  switch (w.mode) {
+    case W_SP24:
+      w.tm = sp24_codes_map(w.sl, w.w8.p);
+      w.tm_e = sp24_meta_map(w.sl, w.meta.p);
+      break;
+    case W_INT4:
+      w.tm = make_w4_map(w.w4.p, static_cast<uint64_t>(K), static_cast<uint64_t>(N), w4_pitch(K));
+      break;
+    case W_INT8:
+      w.tm = make_kmajor_map(w.w8.p, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, N, static_cast<uint64_t>(ld), 128);
+      break;
+    default:
+      w.tm = make_kmajor_map(w.wb.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, N, 2ull * ld, 128);
+  }
+}
+
 struct Layer {
   int heads = 0, kh = 0, f = 0;
   DevArray<float> ln1_g, ln1_b, ln2_g, ln2_b;
@@ -146,6 +168,8 @@ struct Layer {
   DevArray<__nv_bfloat16> kv;  // paged pool [pages][K|V][heads][PAGE][hd]
   CUtensorMap tm_kv, tm_kvg;     // the pool as rows of hd (prefill / decode attention TMA boxes)
 };
+
+GemmW& weight_group(Layer& ly, int g) { return g == 0 ? ly.qkv : g == 1 ? ly.o : g == 2 ? ly.in : ly.out; }
 
 // 2-SM 256x256 tiles once both M and N fill at least one pair tile. IOLM_GEMM_TILES=single|pair
 // overrides (A/B measurements).
@@ -197,11 +221,165 @@ struct StepBuffers {
   }
 };
 
+// ------------------------------------------------ device-layout image I/O (iolm_cuda_save_image)
+// File: "IOLMDL01" | u64 header words | int64 header words | per weight array: u64 bytes + bytes |
+// u64 checksum. The checksum combines one ImageSum per section (header, each array).
+constexpr char kImageMagic[8] = {'I', 'O', 'L', 'M', 'D', 'L', '0', '1'};
+constexpr size_t kImageChunk = 32ull << 20;  // pinned staging chunk (2 in flight)
+constexpr uint64_t kSumPrime = 0x100000001B3ull;
+
+// 4-lane multiplicative word hash: (h ^ w) * odd is a bijection of h, so any single corrupted word
+// changes the result; 4 independent lanes run at memory speed. Restartable across chunks whose
+// sizes are multiples of 32 bytes.
+struct ImageSum {
+  uint64_t h[4] = {0x9E3779B97F4A7C15ull, 0xC2B2AE3D27D4EB4Full, 0x165667B19E3779F9ull, 0x27D4EB2F165667C5ull};
+  uint64_t n = 0;
+  void add(const uint8_t* p, size_t len) {
+    size_t i = 0;
+    for (; i + 32 <= len; i += 32) {
+      uint64_t w[4];
+      std::memcpy(w, p + i, 32);
+      for (int k = 0; k < 4; ++k) h[k] = (h[k] ^ w[k]) * kSumPrime;
+    }
+    for (; i < len; ++i) h[0] = (h[0] ^ p[i]) * kSumPrime;
+    n += len;
+  }
+  uint64_t value() const {
+    uint64_t r = n * 0x9E3779B97F4A7C15ull;
+    for (int k = 0; k < 4; ++k) r = (r ^ h[k]) * kSumPrime;
+    return r;
+  }
+  void combine(uint64_t section) { h[0] = (h[0] ^ section) * kSumPrime, ++n; }
+};
+
+struct ImageHeader {
+  uint64_t hash = 0;
+  ModelConfig cfg;
+  int act_quant = 0, sparse_mma = 0, int4_mma = 0;
+  std::vector<int> modes;  // 4 per layer: qkv, o, in, out
+};
+
+struct ImageFile {
+  FILE* f = nullptr;
+  ImageFile(const std::string& path, const char* mode) : f(std::fopen(path.c_str(), mode)) {
+    if (!f) throw ContractViolation("device-layout image: cannot open " + path);
+  }
+  ~ImageFile() {
+    if (f) std::fclose(f);
+  }
+  void read(void* p, size_t n) const {
+    if (std::fread(p, 1, n, f) != n) throw TruncatedBlob("device-layout image: file ends early");
+  }
+  void write(const void* p, size_t n) const {
+    if (std::fwrite(p, 1, n, f) != n) throw ContractViolation("device-layout image: write failed");
+  }
+};
+
+ImageHeader read_image_header(const ImageFile& f, ImageSum& total) {
+  char magic[8];
+  f.read(magic, 8);
+  if (std::memcmp(magic, kImageMagic, 8) != 0) throw CorruptHeader("device-layout image: bad magic");
+  uint64_t nw = 0;
+  f.read(&nw, 8);
+  if (nw < 10 || nw > (1u << 24)) throw CorruptHeader("device-layout image: bad header length");
+  std::vector<int64_t> w(nw);
+  f.read(w.data(), nw * 8);
+  ImageSum hs;
+  hs.add(reinterpret_cast<const uint8_t*>(w.data()), nw * 8);
+  total.combine(hs.value());
+  size_t at = 0;
+  auto next = [&]() -> int64_t {
+    if (at >= w.size()) throw CorruptHeader("device-layout image: header too short");
+    return w[at++];
+  };
+  auto next_int = [&](int64_t lo, int64_t hi) -> int {
+    const int64_t v = next();
+    if (v < lo || v > hi) throw CorruptHeader("device-layout image: header field out of range");
+    return static_cast<int>(v);
+  };
+  ImageHeader h;
+  h.hash = static_cast<uint64_t>(next());
+  h.cfg.vocab_size = next_int(1, 1 << 20);
+  h.cfg.d_model = next_int(1, 1 << 16);
+  h.cfg.n_layers = next_int(1, 1 << 12);
+  h.cfg.n_heads = next_int(1, 1 << 12);
+  h.cfg.d_ff = next_int(1, 1 << 20);
+  h.cfg.max_seq_len = next_int(1, 1 << 20);
+  h.act_quant = next_int(0, 1);
+  h.sparse_mma = next_int(0, 1);
+  h.int4_mma = next_int(0, 1);
+  for (int l = 0; l < h.cfg.n_layers; ++l) {
+    std::vector<int> heads(next_int(1, h.cfg.n_heads));
+    for (int& x : heads) x = next_int(0, h.cfg.n_heads - 1);
+    h.cfg.active_heads.push_back(std::move(heads));
+  }
+  for (int l = 0; l < h.cfg.n_layers; ++l) h.cfg.active_ffn.push_back(next_int(1, h.cfg.d_ff));
+  for (int i = 0; i < 4 * h.cfg.n_layers; ++i) h.modes.push_back(next_int(W_VALUES, W_INT4));
+  if (at != w.size()) throw CorruptHeader("device-layout image: trailing header words");
+  try {
+    h.cfg.validate();
+  } catch (const EngineError& e) {
+    throw CorruptHeader(std::string("device-layout image: ") + e.what());
+  }
+  return h;
+}
+
+// Pinned double-buffered staging between the image file and HBM.
+class ImageStager {
+ public:
+  ~ImageStager() {
+    for (auto e : ev_)
+      if (e) {
+        cudaEventSynchronize(e);
+        cudaEventDestroy(e);
+      }
+  }
+  // file -> device: the read of chunk i+1 overlaps the H2D copy of chunk i
+  void to_device(const ImageFile& f, void* dst, size_t n, cudaStream_t st, ImageSum& sum) {
+    for (size_t off = 0; off < n; off += kImageChunk) {
+      const size_t c = std::min(kImageChunk, n - off);
+      uint8_t* b = slot();
+      f.read(b, c);
+      sum.add(b, c);
+      CUDA_OK(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, b, c, cudaMemcpyHostToDevice, st));
+      CUDA_OK(cudaEventRecord(ev_[k_], st));
+      k_ ^= 1;
+    }
+  }
+  void from_device(const ImageFile& f, const void* src, size_t n, cudaStream_t st, ImageSum& sum) {
+    for (size_t off = 0; off < n; off += kImageChunk) {
+      const size_t c = std::min(kImageChunk, n - off);
+      uint8_t* b = slot();
+      CUDA_OK(cudaMemcpyAsync(b, static_cast<const uint8_t*>(src) + off, c, cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaStreamSynchronize(st));
+      sum.add(b, c);
+      f.write(b, c);
+    }
+  }
+
+ private:
+  uint8_t* slot() {
+    if (!ev_[k_]) {
+      buf_[k_].ensure(kImageChunk);
+      CUDA_OK(cudaEventCreateWithFlags(&ev_[k_], cudaEventDisableTiming));
+    } else {
+      CUDA_OK(cudaEventSynchronize(ev_[k_]));  // the copy that last used this buffer is done
+    }
+    return buf_[k_].p;
+  }
+  PinnedArray<uint8_t> buf_[2];
+  cudaEvent_t ev_[2] = {nullptr, nullptr};
+  int k_ = 0;
+};
+
 }  // namespace
 
 class Engine {
  public:
   Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opts* opts);
+  // From a device-layout image written by save_image (iolm_cuda_create_from_image).
+  Engine(const std::string& image_path, uint64_t expected_hash, int device, const iolm_cuda_opts* opts);
+  void save_image(const std::string& path);
   ~Engine() {
     for (auto e : kev_) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
@@ -225,6 +403,12 @@ class Engine {
 
  private:
   void reset_counters();
+  void setup(int device, const iolm_cuda_opts* opts);
+  void finish_setup();
+  // [N x K] (row pitch ld elements) of weight group g (0 qkv, 1 o, 2 in, 3 out) of a layer
+  void group_dims(const Layer& ly, int g, int& N, int& K, int& ld) const;
+  template <typename F>
+  void visit_weights(F&& f);
   void upload_weights(const BundleView& b);
   void alloc_runtime();
   void set_prefix_pages(int prefix_pages);
@@ -247,6 +431,7 @@ class Engine {
   int d_ = 0, L_ = 0, V_ = 0, S_ = 0, hd_ = 0, kh_max_ = 0, f_ld_max_ = 0;
   int T_max_ = 0, max_slots_ = 0, pps_ = 0, prefix_slot_ = 0;
   int cur_prefix_pages_ = -1;
+  bool auto_budget_ = false;
   bool prefix_sharing_ = true;
   bool act_quant_ = false;
   bool sparse_mma_ = true;
@@ -303,6 +488,22 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
   if (!bytes || len == 0) throw ContractViolation("iolm_cuda_create: empty bundle");
   BundleView b = parse_bundle(bytes, len);
   cfg_ = b.config;
+  setup(device, opts);
+  // The FNV-1a hash of the serialized bundle is inherently sequential; overlap it with the upload.
+  std::thread hasher([&] { hash_ = fnv1a64(bytes, len); });
+  try {
+    upload_weights(b);
+    finish_setup();
+  } catch (...) {
+    hasher.join();
+    throw;
+  }
+  hasher.join();
+}
+
+// Everything that depends on the model config and the options only (shared by the bundle and the
+// device-layout image constructors).
+void Engine::setup(int device, const iolm_cuda_opts* opts) {
   d_ = cfg_.d_model;
   L_ = cfg_.n_layers;
   V_ = cfg_.vocab_size;
@@ -337,30 +538,175 @@ Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opt
   if (hd_ != 128 && !(hd_ == 64 && prefill_tc_force_)) prefill_tc_ = false;
   // Default token budget: one 256-row GEMM M-tile per SM pair (74 x 256 = 18944 on a 148-SM B200),
   // so every projection's tile count is a whole number of waves of the persistent GEMM grid.
-  const bool auto_budget = T_max_ <= 0;
-  if (auto_budget) T_max_ = std::max(1, sms_ / 2) * 256;
+  auto_budget_ = T_max_ <= 0;
+  if (auto_budget_) T_max_ = std::max(1, sms_ / 2) * 256;
   T_max_ = std::max(round_up(T_max_, 128), round_up(S_, 128));
   for (int l = 0; l < L_; ++l) {
     const uint64_t kh = static_cast<uint64_t>(cfg_.layer_heads(l)) * hd_;
     madds_A_ += 4ull * d_ * kh + 2ull * d_ * cfg_.layer_ffn(l);
     madds_B_ += kh;
   }
-  // The FNV-1a hash of the serialized bundle is inherently sequential; overlap it with the upload.
-  std::thread hasher([&] { hash_ = fnv1a64(bytes, len); });
+}
+
+void Engine::finish_setup() {
+  // All projections on the 2:4 sparse kernel (224-token pair tiles): whole waves of that grid.
+  bool all_sp = true;
+  for (const auto& ly : layers_)
+    all_sp = all_sp && ly->qkv.mode == W_SP24 && ly->o.mode == W_SP24 && ly->in.mode == W_SP24 &&
+             ly->out.mode == W_SP24;
+  if (auto_budget_ && all_sp) T_max_ = std::max(std::max(1, sms_ / 2) * 224, round_up(S_, 32));
+  alloc_runtime();
+}
+
+void Engine::group_dims(const Layer& ly, int g, int& N, int& K, int& ld) const {
+  switch (g) {
+    case 0: N = 3 * ly.kh, K = d_, ld = d_; break;          // wq | wk | wv  [3 kh x d]
+    case 1: N = d_, K = ly.kh, ld = ly.kh; break;           // wo            [d x kh]
+    case 2: N = ly.f, K = d_, ld = d_; break;               // w_in          [f x d]
+    default: N = d_, K = ly.f, ld = round_up(ly.f, 16);     // w_out         [d x f]
+  }
+}
+
+// Every resident weight array, in image order, with the element count its weight form implies
+// (derived from config + form, so the image loader validates sizes before allocating).
+template <typename F>
+void Engine::visit_weights(F&& f) {
+  const size_t d = static_cast<size_t>(d_);
+  f(tok_embed_, static_cast<size_t>(V_) * d);
+  f(pos_embed_, static_cast<size_t>(S_) * d);
+  f(lnf_g_, d);
+  f(lnf_b_, d);
+  for (auto& ly : layers_) {
+    f(ly->ln1_g, d);
+    f(ly->ln1_b, d);
+    f(ly->ln2_g, d);
+    f(ly->ln2_b, d);
+    for (int g = 0; g < 4; ++g) {
+      GemmW& w = weight_group(*ly, g);
+      int N, K, ld;
+      group_dims(*ly, g, N, K, ld);
+      const size_t nl = static_cast<size_t>(N) * ld;
+      switch (w.mode) {
+        case W_VALUES: f(w.wb, nl); break;
+        case W_CODES: f(w.wb, nl), f(w.scale, static_cast<size_t>(N)); break;
+        case W_INT8: f(w.w8, nl), f(w.scale, static_cast<size_t>(N)); break;
+        case W_SP24:
+          f(w.w8, w.sl.code_bytes()), f(w.meta, w.sl.meta_bytes()), f(w.scale, static_cast<size_t>(N));
+          break;
+        case W_INT4: f(w.w4, static_cast<size_t>(N) * w4_pitch(K)), f(w.scale, static_cast<size_t>(N)); break;
+      }
+    }
+  }
+}
+
+void Engine::save_image(const std::string& path) {
+  CUDA_OK(cudaSetDevice(device_));
+  CUDA_OK(cudaStreamSynchronize(stream_));
+  std::vector<int64_t> hw = {static_cast<int64_t>(hash_), cfg_.vocab_size, cfg_.d_model, cfg_.n_layers,
+                             cfg_.n_heads, cfg_.d_ff, cfg_.max_seq_len, act_quant_, sparse_mma_, int4_mma_};
+  for (const auto& heads : cfg_.active_heads) {
+    hw.push_back(static_cast<int64_t>(heads.size()));
+    hw.insert(hw.end(), heads.begin(), heads.end());
+  }
+  hw.insert(hw.end(), cfg_.active_ffn.begin(), cfg_.active_ffn.end());
+  for (auto& ly : layers_)
+    for (int g = 0; g < 4; ++g) hw.push_back(weight_group(*ly, g).mode);
+  const std::string tmp = path + ".tmp";
   try {
-    upload_weights(b);
-    // All projections on the 2:4 sparse kernel (224-token pair tiles): whole waves of that grid.
-    bool all_sp = true;
-    for (const auto& ly : layers_)
-      all_sp = all_sp && ly->qkv.mode == W_SP24 && ly->o.mode == W_SP24 && ly->in.mode == W_SP24 &&
-               ly->out.mode == W_SP24;
-    if (auto_budget && all_sp) T_max_ = std::max(std::max(1, sms_ / 2) * 224, round_up(S_, 32));
-    alloc_runtime();
+    ImageFile f(tmp, "wb");
+    ImageSum total, hs;
+    f.write(kImageMagic, 8);
+    const uint64_t nw = hw.size();
+    f.write(&nw, 8);
+    f.write(hw.data(), nw * 8);
+    hs.add(reinterpret_cast<const uint8_t*>(hw.data()), nw * 8);
+    total.combine(hs.value());
+    ImageStager stager;
+    visit_weights([&](auto& arr, size_t count) {
+      using T = std::remove_pointer_t<decltype(arr.p)>;
+      if (arr.n != count) throw ContractViolation("save_image: internal size mismatch");
+      const uint64_t nb = count * sizeof(T);
+      f.write(&nb, 8);
+      ImageSum s;
+      stager.from_device(f, arr.p, nb, stream_, s);
+      total.combine(s.value());
+    });
+    const uint64_t sum = total.value();
+    f.write(&sum, 8);
+    if (std::fflush(f.f) != 0) throw ContractViolation("save_image: write failed");
   } catch (...) {
-    hasher.join();
+    std::remove(tmp.c_str());
     throw;
   }
-  hasher.join();
+  if (std::rename(tmp.c_str(), path.c_str()) != 0) {
+    std::remove(tmp.c_str());
+    throw ContractViolation("save_image: cannot rename " + tmp + " to " + path);
+  }
+}
+
+Engine::Engine(const std::string& image_path, uint64_t expected_hash, int device, const iolm_cuda_opts* opts) {
+  ImageFile f(image_path, "rb");
+  ImageSum total;
+  const ImageHeader h = read_image_header(f, total);
+  if (expected_hash != 0 && h.hash != expected_hash)
+    throw StaleImage("device-layout image was built from another bundle (hash mismatch)");
+  cfg_ = h.cfg;
+  setup(device, opts);
+  if (act_quant_ != (h.act_quant != 0) || sparse_mma_ != (h.sparse_mma != 0) || int4_mma_ != (h.int4_mma != 0))
+    throw StaleImage("device-layout image was built with other weight options (act_quant/sparse_mma/int4_mma)");
+  hash_ = h.hash;
+  for (int l = 0; l < L_; ++l) {
+    auto ly = std::make_unique<Layer>();
+    ly->heads = cfg_.layer_heads(l);
+    ly->kh = ly->heads * hd_;
+    ly->f = cfg_.layer_ffn(l);
+    for (int g = 0; g < 4; ++g) {
+      GemmW& w = weight_group(*ly, g);
+      w.mode = h.modes[4 * l + g];
+      // the forms the bundle loader can produce under these options
+      const bool ok = act_quant_ ? (w.mode == W_INT8 || (w.mode == W_SP24 && sparse_mma_))
+                                 : (w.mode == W_VALUES || w.mode == W_CODES || (w.mode == W_INT4 && int4_mma_));
+      if (!ok) throw CorruptHeader("device-layout image: weight form inconsistent with its options");
+      int N, K, ld;
+      group_dims(*ly, g, N, K, ld);
+      if (w.mode == W_SP24) {
+        if (K % 4 != 0) throw CorruptHeader("device-layout image: 2:4 form needs K % 4 == 0");
+        w.sl = sp24_layout(N, K);
+      }
+    }
+    any_int8_ = any_int8_ || ly->qkv.int8() || ly->o.int8() || ly->in.int8() || ly->out.int8();
+    kh_max_ = std::max(kh_max_, ly->kh);
+    f_ld_max_ = std::max(f_ld_max_, round_up(ly->f, 16));
+    layers_.push_back(std::move(ly));
+  }
+  {
+    ImageStager stager;
+    visit_weights([&](auto& arr, size_t count) {
+      using T = std::remove_pointer_t<decltype(arr.p)>;
+      uint64_t nb = 0;
+      f.read(&nb, 8);
+      if (nb != count * sizeof(T)) throw CorruptHeader("device-layout image: array size does not match the config");
+      arr.alloc(count);
+      ImageSum s;
+      stager.to_device(f, arr.p, nb, stream_, s);
+      total.combine(s.value());
+    });
+    CUDA_OK(cudaStreamSynchronize(stream_));
+  }
+  uint64_t sum = 0;
+  f.read(&sum, 8);
+  if (sum != total.value()) throw CorruptHeader("device-layout image: checksum mismatch");
+  if (std::fgetc(f.f) != EOF) throw CorruptHeader("device-layout image: trailing bytes");
+  tok_embed_t_.alloc(static_cast<size_t>(V_) * d_);
+  launch_transpose(tok_embed_.p, V_, d_, tok_embed_t_.p, stream_);
+  for (auto& ly : layers_)
+    for (int g = 0; g < 4; ++g) {
+      int N, K, ld;
+      group_dims(*ly, g, N, K, ld);
+      weight_maps(weight_group(*ly, g), N, K, ld);
+    }
+  CUDA_OK(cudaStreamSynchronize(stream_));
+  finish_setup();
 }
 
 void Engine::upload_weights(const BundleView& b) {
@@ -435,15 +781,13 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
     CUDA_OK(cudaMemcpy(w.w8.p, codes.data(), codes.size(), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(w.meta.p, meta.data(), meta.size(), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(w.scale.p, scales.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
-    w.tm = sp24_codes_map(w.sl, w.w8.p);
-    w.tm_e = sp24_meta_map(w.sl, w.meta.p);
-    (void)ld;
+    weight_maps(w, N, K, ld);
     return;
   }
   if (w.mode == W_CODES && q4_ok) {
     // W4A16: the bundle's nibble rows (ceil(K/2) bytes, low nibble = even column) re-pitched to 16 B
     w.mode = W_INT4;
-    const size_t rb = static_cast<size_t>(K + 1) / 2, ld4 = (rb + 15) / 16 * 16;
+    const size_t rb = static_cast<size_t>(K + 1) / 2, ld4 = w4_pitch(K);
     w.w4.alloc(static_cast<size_t>(N) * ld4);
     w.scale.alloc(N);
     CUDA_OK(cudaMemset(w.w4.p, 0x88, static_cast<size_t>(N) * ld4));  // pad bytes: codes 0
@@ -455,8 +799,7 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
                          cudaMemcpyHostToDevice));
       row0 += t->rows;
     }
-    w.tm = make_w4_map(w.w4.p, static_cast<uint64_t>(K), static_cast<uint64_t>(N), ld4);
-    (void)ld;
+    weight_maps(w, N, K, ld);
     return;
   }
   if (act_quant_ && w.mode != W_INT8)
@@ -484,10 +827,7 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
     CUDA_OK(cudaStreamSynchronize(stream_));  // scratch is reused by the next tensor
     row0 += t->rows;
   }
-  if (w.mode == W_INT8)
-    w.tm = make_kmajor_map(w.w8.p, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, N, static_cast<uint64_t>(ld), 128);
-  else
-    w.tm = make_kmajor_map(w.wb.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, N, 2ull * ld, 128);
+  weight_maps(w, N, K, ld);
 }
 
 void Engine::alloc_runtime() {
@@ -1107,6 +1447,38 @@ extern "C" int iolm_cuda_create(const uint8_t* bundle_bytes, size_t len, int dev
 }
 
 extern "C" void iolm_cuda_destroy(iolm_cuda_ctx* ctx) { delete ctx; }
+
+extern "C" int iolm_cuda_save_image(iolm_cuda_ctx* ctx, const char* path) {
+  return guarded([&] {
+    if (!ctx || !path) throw iolmh::ContractViolation("null argument");
+    std::lock_guard<std::mutex> lock(ctx->eng->mu);
+    ctx->eng->save_image(path);
+  });
+}
+
+extern "C" int iolm_cuda_create_from_image(const char* path, uint64_t expected_hash, int device,
+                                           const iolm_cuda_opts* opts, iolm_cuda_ctx** out) {
+  return guarded([&] {
+    if (!out || !path) throw iolmh::ContractViolation("iolm_cuda_create_from_image: null argument");
+    *out = nullptr;
+    auto ctx = std::make_unique<iolm_cuda_ctx>();
+    ctx->eng = std::make_unique<Engine>(std::string(path), expected_hash, device, opts);
+    *out = ctx.release();
+  });
+}
+
+extern "C" int iolm_cuda_image_info(const char* path, uint64_t* bundle_hash, iolm_cuda_model_config* cfg) {
+  return guarded([&] {
+    if (!path || !bundle_hash || !cfg) throw iolmh::ContractViolation("null argument");
+    iolmh::ImageFile f(path, "rb");
+    iolmh::ImageSum total;
+    const iolmh::ImageHeader h = iolmh::read_image_header(f, total);
+    *bundle_hash = h.hash;
+    const auto& c = h.cfg;
+    *cfg = iolm_cuda_model_config{c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.d_ff, c.max_seq_len,
+                                  c.head_dim()};
+  });
+}
 
 extern "C" int iolm_cuda_bundle_hash(const iolm_cuda_ctx* ctx, uint64_t* out) {
   return guarded([&] {

@@ -42,6 +42,9 @@ struct TruncatedBlob : EngineError {
 struct UnknownEncoding : EngineError {
   explicit UnknownEncoding(const std::string& w) : EngineError(IOLM_E_UNKNOWN_ENCODING, w) {}
 };
+struct StaleImage : EngineError {
+  explicit StaleImage(const std::string& w) : EngineError(IOLM_E_STALE, w) {}
+};
 
 inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e == cudaSuccess) return;

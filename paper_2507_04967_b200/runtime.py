@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -52,6 +53,10 @@ class CudaError(Error):
     pass
 
 
+class StaleImage(Error):
+    """A device-layout image built from another bundle or with other weight options."""
+
+
 class DeviceOutOfMemory(CudaError):
     pass
 
@@ -65,6 +70,7 @@ _STATUS = {
     _lib.IOLM_E_CORRUPT_HEADER: CorruptHeader,
     _lib.IOLM_E_TRUNCATED_BLOB: TruncatedBlob,
     _lib.IOLM_E_UNKNOWN_ENCODING: UnknownEncoding,
+    _lib.IOLM_E_STALE: StaleImage,
 }
 
 
@@ -134,6 +140,30 @@ def bundle_config(bundle: bytes) -> ModelConfig:
     return ModelConfig(**c)
 
 
+def image_header(path) -> dict:
+    """Header of a device-layout image (format: iolm_cuda.h, iolm_cuda_save_image): bundle hash,
+    model config (with the active head ids), the weight options and per-layer weight forms."""
+    with open(path, "rb") as f:
+        if f.read(8) != b"IOLMDL01":
+            raise CorruptHeader("device-layout image: bad magic")
+        nw = int.from_bytes(f.read(8), "little")
+        w = np.frombuffer(f.read(8 * nw), dtype="<i8").tolist()
+    if len(w) != nw or nw < 10:
+        raise TruncatedBlob("device-layout image: file ends early")
+    cfg = ModelConfig(*w[1:7])
+    at = 10
+    for _ in range(cfg.n_layers):
+        n = w[at]
+        cfg.active_heads.append(w[at + 1:at + 1 + n])
+        at += 1 + n
+    cfg.active_ffn = w[at:at + cfg.n_layers]
+    at += cfg.n_layers
+    forms = ["values", "codes", "int8", "sp24", "int4"]
+    return {"bundle_hash": w[0] & (2**64 - 1), "config": cfg,
+            "act_quant": bool(w[7]), "sparse_mma": bool(w[8]), "int4_mma": bool(w[9]),
+            "weight_forms": [forms[m] for m in w[at:at + 4 * cfg.n_layers]]}
+
+
 # --------------------------------------------------------------------------- runtime
 class ModelRuntime:
     """iolm::ModelRuntime on a B200. `bundle` is the serialize_bundle byte stream."""
@@ -142,6 +172,18 @@ class ModelRuntime:
                  prefix_sharing: bool = True, act_quant: bool = False, kernel_timing: bool = False,
                  sparse_mma: bool = True, int4_mma: bool = True, prefill_tc: bool | None = None):
         self._lib = _lib.load()
+        opts = self._opts(max_tokens_per_step, max_slots, prefix_sharing, act_quant, kernel_timing, sparse_mma,
+                          int4_mma, prefill_tc)
+        h = C.c_void_p()
+        buf = (C.c_char * len(bundle)).from_buffer_copy(bundle)
+        _check(self._lib.iolm_cuda_create(buf, len(bundle), device, C.byref(opts), C.byref(h)))
+        self._h = h
+        hl = int.from_bytes(bundle[6:10], "little")
+        self._config = ModelConfig(**json.loads(bundle[10:10 + hl].decode())["config"])
+
+    @staticmethod
+    def _opts(max_tokens_per_step=0, max_slots=0, prefix_sharing=True, act_quant=False, kernel_timing=False,
+              sparse_mma=True, int4_mma=True, prefill_tc=None) -> _lib.Opts:
         opts = _lib.Opts()
         opts.max_tokens_per_step = max_tokens_per_step
         opts.max_slots = max_slots
@@ -151,12 +193,25 @@ class ModelRuntime:
         opts.sparse_mma = 0 if sparse_mma else -1
         opts.int4_mma = 0 if int4_mma else -1
         opts.prefill_tc = 0 if prefill_tc is None else (1 if prefill_tc else -1)
+        return opts
+
+    @classmethod
+    def from_image(cls, path, expected_hash: int = 0, device: int = 0, **options) -> "ModelRuntime":
+        """A runtime from a device-layout image (iolm_cuda_create_from_image): `options` take the
+        constructor's keywords; the weight-shaping ones must match the saved runtime's (StaleImage)."""
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        opts = cls._opts(**options)
         h = C.c_void_p()
-        buf = (C.c_char * len(bundle)).from_buffer_copy(bundle)
-        _check(self._lib.iolm_cuda_create(buf, len(bundle), device, C.byref(opts), C.byref(h)))
+        _check(self._lib.iolm_cuda_create_from_image(os.fsencode(path), expected_hash, device, C.byref(opts),
+                                                     C.byref(h)))
         self._h = h
-        hl = int.from_bytes(bundle[6:10], "little")
-        self._config = ModelConfig(**json.loads(bundle[10:10 + hl].decode())["config"])
+        self._config = image_header(path)["config"]
+        return self
+
+    def save_image(self, path) -> None:
+        """Writes this runtime's device layout (iolm_cuda_save_image)."""
+        _check(self._lib.iolm_cuda_save_image(self._h, os.fsencode(path)))
 
     def close(self) -> None:
         if getattr(self, "_h", None):

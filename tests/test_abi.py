@@ -127,3 +127,51 @@ def test_cpp_shim_compiles(with_ref, tmp_path):
         cmd += ["-DIOLM_CUDA_WITH_REFERENCE_TYPES", f"-I{ref_inc}", f"-I{json_dir}"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
+
+
+def _image_bytes(words, arrays=b""):
+    w = np.asarray(words, dtype="<i8")
+    return b"IOLMDL01" + len(w).to_bytes(8, "little") + w.tobytes() + arrays
+
+
+def _image_info(path):
+    lib = _lib.load()
+    h, cfg = C.c_uint64(), _lib.ModelConfigC()
+    st = lib.iolm_cuda_image_info(str(path).encode(), C.byref(h), C.byref(cfg))
+    return st, h.value, cfg
+
+
+def test_device_image_header_validation(tmp_path):
+    """iolm_cuda_image_info parses and validates a device-layout image header without device work
+    (the registry can check an image's bundle hash before loading it)."""
+    # hash, vocab, d, L, n_heads, d_ff, S, act_quant, sparse_mma, int4_mma | heads | ffn | forms
+    words = [-7, 131, 64, 2, 4, 256, 128, 0, 1, 1, 2, 0, 1, 4, 0, 1, 2, 3, 256, 128, 0, 0, 0, 0, 1, 1, 1, 1]
+    p = tmp_path / "ok.iolmdev"
+    p.write_bytes(_image_bytes(words))
+    st, h, cfg = _image_info(p)
+    assert st == _lib.IOLM_OK, _lib.last_error()
+    assert h == 2**64 - 7 and (cfg.d_model, cfg.n_layers, cfg.head_dim, cfg.max_seq_len) == (64, 2, 16, 128)
+    hdr = R.image_header(p)
+    assert hdr["bundle_hash"] == h and hdr["config"].active_heads == [[0, 1], [0, 1, 2, 3]]
+    assert hdr["config"].active_ffn == [256, 128] and hdr["weight_forms"] == ["values"] * 4 + ["codes"] * 4
+
+    def status(data):
+        q = tmp_path / "x.iolmdev"
+        q.write_bytes(data)
+        return _image_info(q)[0]
+
+    assert status(b"IOLMDL02" + _image_bytes(words)[8:]) == _lib.IOLM_E_CORRUPT_HEADER      # magic
+    assert status(_image_bytes(words)[:40]) == _lib.IOLM_E_TRUNCATED_BLOB                   # short
+    assert status(_image_bytes(words[:-1])) == _lib.IOLM_E_CORRUPT_HEADER                   # words
+    assert status(_image_bytes(words + [0])) == _lib.IOLM_E_CORRUPT_HEADER                  # trailing
+    bad_heads = list(words)
+    bad_heads[11], bad_heads[12] = 1, 0                                                     # descending
+    assert status(_image_bytes(bad_heads)) == _lib.IOLM_E_CORRUPT_HEADER
+    bad_form = list(words)
+    bad_form[-1] = 9                                                                        # form tag
+    assert status(_image_bytes(bad_form)) == _lib.IOLM_E_CORRUPT_HEADER
+    bad_ffn = list(words)
+    bad_ffn[18] = 512                                                                       # > d_ff
+    assert status(_image_bytes(bad_ffn)) == _lib.IOLM_E_CORRUPT_HEADER
+    st, _, _ = _image_info(tmp_path / "missing.iolmdev")
+    assert st == _lib.IOLM_E_CONTRACT
