@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<const uint32_t*>(tsm + (tmem_slot - raw));
+  pdl_sync();
 
   if (warp == 0) {  // ------------------------------------------------------------------ producer
     if (lane == 0) {
@@ -392,8 +393,8 @@ static void launch_tc(const AttnParams& p, cudaStream_t st) {
   if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int items = p.n_groups * p.heads;
   const int grid = std::min(items, sms * (HD == 64 ? 2 : 1));  // persistent: every CTA walks items
-  if (p.key_mask) attn_prefill_tc_kernel<HD, true><<<grid, 192, smem, st>>>(p);
-  else attn_prefill_tc_kernel<HD, false><<<grid, 192, smem, st>>>(p);
+  if (p.key_mask) launch_k(attn_prefill_tc_kernel<HD, true>, grid, 192, smem, st, p);
+  else launch_k(attn_prefill_tc_kernel<HD, false>, grid, 192, smem, st, p);
 }
 
 // Groups must hold <= 128 queries. Returns false when hd has no tcgen05 variant (caller falls back).

@@ -30,13 +30,13 @@ static void launch_one(const CUtensorMap& A, const CUtensorMap& B, int M, int N,
   cfg.blockDim = dim3(Cfg::THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1 + pdl_attr(&attr[1]);  // the kernel calls pdl_sync() after its prologue
   CUDA_OK(cudaLaunchKernelEx(&cfg, kern, A, B, ep.tma_out ? *g_out_map : A, M, N, K, ep));
 }
 

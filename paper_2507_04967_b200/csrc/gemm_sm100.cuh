@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+  pdl_sync();
 
   const int m_tiles = (M + C::TILE_M - 1) / C::TILE_M;
   const int n_tiles = (N + BN - 1) / BN;

@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+  pdl_sync();
 
   const int T = ep.M, N = ep.N;
   const int w_tiles = (N + C::TILE_M - 1) / C::TILE_M;

@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(256, MAXV <= 10 ? 4 : 2) ln_kernel(const float
                                                  const float* __restrict__ g, const float* __restrict__ b,
                                                  __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
                                                  float* __restrict__ qscale) {
+  pdl_sync();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= M) return;
   if constexpr (Q8)
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(256, 2) ln_stream_kernel(const float* __restri
                                                            const float* __restrict__ g, const float* __restrict__ b,
                                                            __nv_bfloat16* __restrict__ h, int ldh,
                                                            int8_t* __restrict__ q8, float* __restrict__ qscale) {
+  pdl_sync();
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * 8;
   int row = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(256, 2) ln_stream2_kernel(const float* __restr
                                                             const float* __restrict__ g, const float* __restrict__ b,
                                                             __nv_bfloat16* __restrict__ h, int ldh,
                                                             int8_t* __restrict__ q8, float* __restrict__ qscale) {
+  pdl_sync();
   __shared__ float red[4][2][3][2];  // [pair][row parity][reduction][half]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, half = warp & 1, t = half * 32 + lane;
@@ -293,6 +296,7 @@ __global__ void __launch_bounds__(288) ln_bulk_kernel(const float* __restrict__ 
                                                       const float* __restrict__ g, const float* __restrict__ b,
                                                       __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
                                                       float* __restrict__ qscale) {
+  pdl_sync();
   extern __shared__ __align__(128) uint8_t lsm[];
   const uint32_t sbase = (smem_u32(lsm) + 127u) & ~127u;
   float* ring = reinterpret_cast<float*>(lsm + (sbase - smem_u32(lsm)));
@@ -347,6 +351,7 @@ template <int CH>
 __global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const __nv_bfloat16* __restrict__ src, int lds, int M,
                                                          int cols, int8_t* __restrict__ dst, int ldd,
                                                          float* __restrict__ scale) {
+  pdl_sync();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= M) return;
   const int lane = threadIdx.x & 31;
@@ -426,6 +431,7 @@ template <int CH>
 __global__ void __launch_bounds__(256, 2) quant_rows2_kernel(const __nv_bfloat16* __restrict__ src, int lds, int M,
                                                              int cols, int8_t* __restrict__ dst, int ldd,
                                                              float* __restrict__ scale) {
+  pdl_sync();
   __shared__ float red[4][2][2];  // [pair][row parity][half]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, half = warp & 1, t = half * 32 + lane;
@@ -493,6 +499,7 @@ __global__ void __launch_bounds__(256)
                     const float* __restrict__ pos_embed, float* __restrict__ x, const float* __restrict__ g,
                     const float* __restrict__ b, __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
                     float* __restrict__ qscale) {
+  pdl_sync();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= M) return;
   const int lane = threadIdx.x & 31;
@@ -580,6 +587,7 @@ __device__ __forceinline__ uint32_t pf_off(int R, int r, int c) {
 
 template <int HD, bool MASK>
 __global__ void __launch_bounds__(128, PfCfg<HD>::MINB) attn_prefill_kernel(const __grid_constant__ AttnParams p) {
+  pdl_sync();
   using C = PfCfg<HD>;
   constexpr int ST = C::ST;
   extern __shared__ __align__(1024) uint8_t pf_smem[];
@@ -812,6 +820,7 @@ struct DecCfg {
 template <int HD>
 __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_constant__ AttnParams p, int hg,
                                                               int n_hgroups, int nst) {
+  pdl_sync();
   using C = PfCfg<HD>;
   extern __shared__ __align__(1024) uint8_t dsm[];
   const uint32_t sraw = smem_u32(dsm);
@@ -963,6 +972,7 @@ __global__ void __launch_bounds__(256)
                        const float* __restrict__ embed_t, int V, const int* __restrict__ row_slot,
                        int32_t* __restrict__ next_tok, int32_t* __restrict__ last_tok,
                        float* __restrict__ logits_out) {
+  pdl_sync();
   extern __shared__ float sy[];  // [HEAD_ROWS][d] then [HEAD_ROWS][V]
   float* slog = sy + HEAD_ROWS * d;
   const int r0 = blockIdx.x * HEAD_ROWS;
@@ -1186,6 +1196,14 @@ __global__ void transpose_f32_kernel(const float* __restrict__ src, int rows, in
 
 // ====================================================================== host launchers
 namespace iolmh {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("IOLM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 using namespace iolmk;
 
 static int env_int(const char* name, int dflt) {
@@ -1218,11 +1236,11 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
     const int grid_s = std::min<int>((M + 3) / 4, sms * 2);
     const int v2 = (d / 4 + 63) / 64;  // float4 per thread with two warps per row
     if (v2 <= 8) {
-      if (q8) ln_stream2_kernel<8, true><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);
-      else ln_stream2_kernel<8, false><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);
+      if (q8) launch_k<false>(ln_stream2_kernel<8, true>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);
+      else launch_k<false>(ln_stream2_kernel<8, false>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);
     } else {
-      if (q8) ln_stream2_kernel<16, true><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);
-      else ln_stream2_kernel<16, false><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);
+      if (q8) launch_k<false>(ln_stream2_kernel<16, true>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);
+      else launch_k<false>(ln_stream2_kernel<16, false>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);
     }
     CUDA_OK(cudaGetLastError());
     return;
@@ -1231,8 +1249,8 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
     const int grid_s = std::min<int>((M + 7) / 8, sms * 2);
 #define LNS(V)                                                                                             \
   do {                                                                                                     \
-    if (q8) ln_stream_kernel<V, true><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);            \
-    else ln_stream_kernel<V, false><<<grid_s, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);              \
+    if (q8) launch_k<false>(ln_stream_kernel<V, true>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);            \
+    else launch_k<false>(ln_stream_kernel<V, false>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);              \
   } while (0)
     switch (nv) {
       case 1: LNS(1); break;
@@ -1264,8 +1282,8 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
                                    200 * 1024));                                                        \
       cfg = true;                                                                                       \
     }                                                                                                   \
-    if (q8) ln_bulk_kernel<V, true><<<grid_b, 288, bsmem, st>>>(x, M, d, g, b, h, ldh, q8, qscale);      \
-    else ln_bulk_kernel<V, false><<<grid_b, 288, bsmem, st>>>(x, M, d, g, b, h, ldh, q8, qscale);        \
+    if (q8) launch_k<false>(ln_bulk_kernel<V, true>, grid_b, 288, bsmem, st, x, M, d, g, b, h, ldh, q8, qscale);      \
+    else launch_k<false>(ln_bulk_kernel<V, false>, grid_b, 288, bsmem, st, x, M, d, g, b, h, ldh, q8, qscale);        \
   } while (0)
     switch (nv) {
       case 4: LNB(4); break;
@@ -1280,8 +1298,8 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
   const unsigned grid = blocks_for(M, 8);
 #define LNK(V)                                                                     \
   do {                                                                             \
-    if (q8) ln_kernel<V, true><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale); \
-    else ln_kernel<V, false><<<grid, 256, 0, st>>>(x, M, d, g, b, h, ldh, q8, qscale);   \
+    if (q8) launch_k(ln_kernel<V, true>, grid, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale); \
+    else launch_k(ln_kernel<V, false>, grid, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);   \
   } while (0)
   switch (nv) {
     case 1: LNK(1); break;
@@ -1309,17 +1327,17 @@ void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_
   if (lds % 8 != 0 || ldd % 8 != 0) throw Unsupported("quant_rows: leading dimensions must be multiples of 8");
   const unsigned grid = blocks_for(M, 8);
   const int ch = (cols + 255) / 256;
-  if (cols % 8 != 0) quant_rows_kernel<0><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  if (cols % 8 != 0) launch_k(quant_rows_kernel<0>, grid, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
   // register-resident rows up to 1024 columns; wider rows take the two-pass kernel (its second
   // read hits L2) at 8 CTAs per SM: these launches are bound by load latency, not bytes
-  else if (ch <= 4) quant_rows_kernel<4><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+  else if (ch <= 4) launch_k(quant_rows_kernel<4>, grid, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
   else if (cols > 3072 && cols <= 5120) {  // measured: two-warp rows win at 4096 (C4 FFN), lose at 2560
     static int sms = 0;
     if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const int grid2 = std::min<int>((M + 3) / 4, sms * 2);
-    if (cols <= 4096) quant_rows2_kernel<8><<<grid2, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
-    else quant_rows2_kernel<10><<<grid2, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
-  } else quant_rows_kernel<0><<<grid, 256, 0, st>>>(src, lds, M, cols, dst, ldd, scale);
+    if (cols <= 4096) launch_k<false>(quant_rows2_kernel<8>, grid2, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
+    else launch_k<false>(quant_rows2_kernel<10>, grid2, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
+  } else launch_k(quant_rows_kernel<0>, grid, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -1333,10 +1351,10 @@ void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_
 #define EMB(V)                                                                                        \
   do {                                                                                                \
     if (q8)                                                                                           \
-      embed_ln_kernel<V, true><<<grid, 256, 0, st>>>(ids, tok_src, tok_slot, tok_pos, last_tok, M, d, \
+      launch_k(embed_ln_kernel<V, true>, grid, 256, 0, st, ids, tok_src, tok_slot, tok_pos, last_tok, M, d, \
                                                      tok_embed, pos_embed, x, g, b, h, ldh, q8, qscale); \
     else                                                                                              \
-      embed_ln_kernel<V, false><<<grid, 256, 0, st>>>(ids, tok_src, tok_slot, tok_pos, last_tok, M, d, \
+      launch_k(embed_ln_kernel<V, false>, grid, 256, 0, st, ids, tok_src, tok_slot, tok_pos, last_tok, M, d, \
                                                       tok_embed, pos_embed, x, g, b, h, ldh, q8, qscale); \
   } while (0)
   switch (nv) {
@@ -1372,9 +1390,9 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
     if (prefill.n_groups > 0) {                                                                     \
       const dim3 grid(prefill.n_groups, prefill.heads);                                             \
       if (prefill.key_mask)                                                                         \
-        attn_prefill_kernel<HD, true><<<grid, 128, smem, st>>>(prefill);                            \
+        launch_k(attn_prefill_kernel<HD, true>, grid, 128, smem, st, prefill);                            \
       else                                                                                          \
-        attn_prefill_kernel<HD, false><<<grid, 128, smem, st>>>(prefill);                           \
+        launch_k(attn_prefill_kernel<HD, false>, grid, 128, smem, st, prefill);                           \
     }                                                                                               \
     if (decode.n_groups > 0) {                                                                      \
       const int hg = decode_heads_per_cta(decode.heads, HD);                                        \
@@ -1389,7 +1407,7 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));         \
         dcfg = sm;                                                                                  \
       }                                                                                             \
-      attn_decode_kernel<HD><<<decode.n_groups * ngrp, 32 * (hg + 1), sm, st>>>(decode, hg, ngrp, nst); \
+      launch_k(attn_decode_kernel<HD>, decode.n_groups * ngrp, 32 * (hg + 1), sm, st, decode, hg, ngrp, nst); \
     }                                                                                               \
   } while (0)
   switch (hd) {
@@ -1416,7 +1434,7 @@ void launch_head(const float* x, int d, const int* rows, int n_rows, const float
                                  static_cast<int>(smem)));
     configured = smem;
   }
-  head_argmax_kernel<<<blocks_for(n_rows, HEAD_ROWS), 256, smem, st>>>(x, d, rows, n_rows, g, b, embed_t, V,
+  launch_k(head_argmax_kernel, blocks_for(n_rows, HEAD_ROWS), 256, smem, st, x, d, rows, n_rows, g, b, embed_t, V,
                                                                        row_slot, next_tok, last_tok, logits_out);
   CUDA_OK(cudaGetLastError());
 }

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "gemm_sm100.cuh"
 #include "../../include/iolm_cuda.h"
@@ -54,6 +55,32 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
   throw CudaError(msg);
 }
 #define CUDA_OK(x) ::iolmh::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Programmatic dependent launch (ptx.cuh pdl_sync): on unless IOLM_PDL=0 (A/B measurements).
+bool pdl_enabled();
+inline int pdl_attr(cudaLaunchAttribute* at) {
+  if (!pdl_enabled()) return 0;
+  at->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at->val.programmaticStreamSerializationAllowed = 1;
+  return 1;
+}
+// kern<<<grid, block, smem, st>>>(args...) with the PDL attribute. Only for kernels that call
+// pdl_sync() before touching global memory. PDL = false for persistent grids of small CTAs (LN,
+// row quantization): launched early, their CTAs would be packed onto the SMs the predecessor frees
+// first instead of spread evenly, and a persistent grid with a static row split then runs at the
+// pace of its most crowded SM (measured: C4 -3% with PDL on every kernel).
+template <bool PDL = true, typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  cfg.attrs = at;
+  cfg.numAttrs = PDL ? pdl_attr(at) : 0;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // ---- launchers (gemm_launch.cu, kernels.cu)
 // pair: 2-SM 256x256 tiles (clusters of 2) vs single-CTA 128x128 tiles; i8: W8A8 kind::i8.

@@ -41,6 +41,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every hot kernel is launched with programmatic stream serialization (launch_k / the GEMM
+// launchers), so its CTAs may be scheduled while the previous kernel in the stream drains. Each such
+// kernel calls pdl_sync() before its first global-memory access: griddepcontrol.wait blocks until
+// the predecessor grid has completed and its writes are visible (a no-op without the attribute),
+// then launch_dependents lets the NEXT kernel's CTAs start their prologue (barrier init, TMEM
+// alloc, descriptor prefetch) on SMs this grid leaves free.
+__device__ __forceinline__ void pdl_sync() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

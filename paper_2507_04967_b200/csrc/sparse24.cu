@@ -106,13 +106,13 @@ static void launch_sp_one(const CUtensorMap& A, const CUtensorMap& B, const CUte
   cfg.blockDim = dim3(SpCfg::THREADS);
   cfg.dynamicSmemBytes = SpCfg::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1 + pdl_attr(&attr[1]);  // the kernel calls pdl_sync() after its prologue
   CUDA_OK(cudaLaunchKernelEx(&cfg, kern, A, B, E, K, katoms_pad, ep));
 }
 
