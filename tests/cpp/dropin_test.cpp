@@ -112,6 +112,24 @@ int main() {
     EXPECT(worst_cap <= 1e-2, "capture rel-L2");
     std::printf("calibration capture: %zu points, worst rel-L2 %.3e\n", ref.inputs.size(), worst_cap);
   }
+  {  // device-layout image next to the bundle: bit-identical runtime, stale on another hash
+    const std::string img = "/tmp/iolm_dropin_test.iolmdev";
+    gpu.save_image(img);
+    auto im = iolm::cuda::ModelRuntime::from_image(img, bundle.hash());
+    iolm::FlopCounter c3;
+    EXPECT(im->bundle_hash() == gpu.bundle_hash(), "image bundle_hash");
+    EXPECT(im->batch_decode(prompts, 8, c3) == b, "image batch_decode identical");
+    EXPECT(c3.total() == c2.total(), "image FlopCounter madds");
+    bool stale = false;
+    try {
+      iolm::cuda::ModelRuntime::from_image(img, bundle.hash() ^ 1);
+    } catch (const iolm::cuda::StaleImage&) {
+      stale = true;
+    }
+    EXPECT(stale, "image with another bundle hash -> StaleImage");
+    std::remove(img.c_str());
+    std::printf("device-layout image: identical decode, stale check ok\n");
+  }
   std::printf(fails ? "DROPIN FAIL\n" : "DROPIN OK\n");
   return fails ? 1 : 0;
 }
