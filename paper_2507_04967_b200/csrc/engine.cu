@@ -380,12 +380,6 @@ class Engine {
   // From a device-layout image written by save_image (iolm_cuda_create_from_image).
   Engine(const std::string& image_path, uint64_t expected_hash, int device, const iolm_cuda_opts* opts);
   void save_image(const std::string& path);
-  ~Engine() {
-    for (auto e : kev_) cudaEventDestroy(e);
-    if (stream_) cudaStreamDestroy(stream_);
-    if (ev0_) cudaEventDestroy(ev0_);
-    if (ev1_) cudaEventDestroy(ev1_);
-  }
 
   const ModelConfig& config() const { return cfg_; }
   uint64_t bundle_hash() const { return hash_; }
@@ -450,6 +444,17 @@ class Engine {
   // kernel-class timing (opts.kernel_timing)
   bool ktime_ = false;
   std::vector<cudaEvent_t> kev_;
+  // Destroys the raw stream / event handles above, also when a constructor throws after creating
+  // them (members are unwound then, the destructor body is not run).
+  struct HandleGuard {
+    Engine* e;
+    ~HandleGuard() {
+      for (auto ev : e->kev_) cudaEventDestroy(ev);
+      if (e->stream_) cudaStreamDestroy(e->stream_);
+      if (e->ev0_) cudaEventDestroy(e->ev0_);
+      if (e->ev1_) cudaEventDestroy(e->ev1_);
+    }
+  } handle_guard_{this};
   std::vector<int> kev_free_;
   struct KPending {
     int cat, ev0, ev1;
