@@ -153,3 +153,11 @@ def test_w8a8_wide_rows_d2048():
         row = ids[offs[r]:offs[r + 1]]
         rel = rel_l2_rows(rt.forward(row), oq.forward(row)[0])
         assert rel.max() <= 3e-2 and rel.mean() <= 2e-2, (rel.max(), rel.mean())
+
+
+def test_decode_head_groupings():
+    """Head counts whose decode-attention CTA grouping differs (kernels.cu decode_heads_per_cta):
+    10 -> 5 CTAs of 2 heads, 14 -> 7 x 2, 7 -> 4 + 3 (partial last group), 16 -> 4 x 4."""
+    b = synth.toy_bundle(1024, 4, 16, 1024, 160, seed=5, quant="dense", heads=[10, 14, 7, 16], ffn=[1024] * 4)
+    rt, om = R.ModelRuntime(b), O.OracleModel(b)
+    assert check_decode(rt, om, n=16) >= 15
