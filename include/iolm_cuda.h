@@ -133,6 +133,16 @@ int iolm_cuda_forward_capture(iolm_cuda_ctx* ctx, const int32_t* ids, const uint
                               float* logits, uint16_t* capture, uint64_t* madds);
 
 /*
+ * W8A8 parity (opts.act_quant): forward logits plus the int8 operand codes every linear layer consumed,
+ * per layer [attn_in n x d][attn_out_in n x kh_l][ffn_in n x d][ffn_mid n x f_l] (the capture points of
+ * iolm_cuda_forward_capture, as the per-token int8 codes of DESIGN.md's W8A8 rule), and their per-token
+ * scales, per layer [4 x n] f32. Checked against the W8A8 restatement's codes (oracle/iolm_oracle.c
+ * orc_forward_codes). Every projection must run W8A8, else IOLM_E_UNSUPPORTED.
+ */
+int iolm_cuda_forward_codes(iolm_cuda_ctx* ctx, const int32_t* ids, int32_t n, float* logits, int8_t* codes,
+                            float* scales, uint64_t* madds);
+
+/*
  * Device-layout image: the pre-tiled cache a registry keeps next to a bundle.
  * The reference rebuilds its runtime from the bundle on every load - deserialize, FNV-1a over the
  * whole serialized bundle, decode every tensor (ModelRegistry::lookup, proj/src/optimize.cpp:

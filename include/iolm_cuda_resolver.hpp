@@ -19,7 +19,17 @@
 //     kept bitwise by the GPU runtime), so merging windows cannot change any output.
 //
 // Streaming: push() takes rows one at a time (no need to materialise the table's prompts), and
-// take_ready() hands back the finished prefix of the output column in row order.
+// take_ready() hands back the finished prefix of the output column in row order; rows and decoded
+// slots are released once handed back, so host memory is bounded by the rows in flight (about
+// device_batch x batch_size), not by the table.
+//
+// Errors: everything since the last completed device call is one transaction. If a device call
+// throws (SequenceTooLong, ContractViolation, GpuError, ...), the cache (contents, LRU order, hit /
+// miss counters) and the stats are rolled back to the transaction start and the transaction's rows
+// are replayed exactly as the reference executes them - lookup, window, synchronous batch_decode per
+// flush window - so the exception, its " (row N)" suffix, the cache and the stats are the reference's
+// at its failure point (exec.cpp:95-146): earlier windows decoded and cached, the failing window
+// neither counted nor cached, later rows never looked up. No pending entry survives a failure.
 //
 // `Model` is any type with the reference ModelRuntime's `batch_decode(span<const string>, int,
 // FlopCounter&) const` and `bundle_hash() const` - iolm::cuda::ModelRuntime (the B200 runtime) or
@@ -27,6 +37,7 @@
 #pragma once
 
 #include <cstdint>
+#include <deque>
 #include <list>
 #include <map>
 #include <memory>
@@ -51,7 +62,8 @@ struct ResolverStats {
 
 // LRU prompt cache with the semantics of iolm::PromptCache (exec.cpp:14-46): exact-key lookups
 // refresh recency, inserts of an existing key overwrite and refresh, capacity 0 disables caching.
-// Values may be pending (bound to a slot of an in-flight device batch).
+// Values may be pending (bound to a slot of an in-flight device batch of one resolver). Mutations can
+// be journaled (begin / commit / rollback) so a failed device batch leaves no trace.
 class PromptCache {
  public:
   struct Key {
@@ -62,10 +74,13 @@ class PromptCache {
   };
   struct Value {
     std::string text;
-    int64_t slot = -1;  // >= 0: pending, the value is the output of resolver slot `slot`
+    int64_t slot = -1;            // >= 0: pending, the value is the output of resolver slot `slot`
+    const void* owner = nullptr;  // the resolver whose slot it is
   };
 
   explicit PromptCache(size_t capacity) : capacity_(capacity) {}
+  PromptCache(const PromptCache&) = delete;
+  PromptCache& operator=(const PromptCache&) = delete;
   bool enabled() const { return capacity_ > 0; }
   size_t size() const { return lru_.size(); }
   uint64_t hits() const { return hits_; }
@@ -78,28 +93,71 @@ class PromptCache {
       return nullptr;
     }
     ++hits_;
-    lru_.splice(lru_.begin(), lru_, it->second);
+    to_front(it->second);
     return &it->second->value;
   }
   void insert(const Key& key, Value value) {
     if (capacity_ == 0) return;
     auto it = index_.find(key);
     if (it != index_.end()) {
+      if (journaling_) log_.push_back(Op{Op::SET, it->second, it->second->value});
       it->second->value = std::move(value);
-      lru_.splice(lru_.begin(), lru_, it->second);
+      to_front(it->second);
       return;
     }
     lru_.push_front(Entry{key, std::move(value)});
     index_[key] = lru_.begin();
+    if (journaling_) log_.push_back(Op{Op::INSERT, lru_.begin(), {}});
     if (lru_.size() > capacity_) {
-      index_.erase(lru_.back().key);
-      lru_.pop_back();
+      auto last = std::prev(lru_.end());
+      index_.erase(last->key);
+      if (journaling_) {  // keep the node itself so a rollback restores it in place
+        graveyard_.splice(graveyard_.end(), lru_, last);
+        log_.push_back(Op{Op::EVICT, last, {}});
+      } else {
+        lru_.pop_back();
+      }
     }
   }
   // Fills a pending entry (no recency change: the reference inserted the value at window close).
-  void resolve_pending(const Key& key, int64_t slot, const std::string& text) {
+  void resolve_pending(const Key& key, const void* owner, int64_t slot, const std::string& text) {
     auto it = index_.find(key);
-    if (it != index_.end() && it->second->value.slot == slot) it->second->value = Value{text, -1};
+    if (it == index_.end() || it->second->value.slot != slot || it->second->value.owner != owner) return;
+    if (journaling_) log_.push_back(Op{Op::SET, it->second, it->second->value});
+    it->second->value = Value{text, -1, nullptr};
+  }
+
+  // Journal of every mutation (and the counters) from begin() until commit() / rollback().
+  void begin() {
+    log_.clear();
+    graveyard_.clear();
+    journaling_ = true;
+    saved_hits_ = hits_;
+    saved_misses_ = misses_;
+  }
+  void commit() {
+    log_.clear();
+    graveyard_.clear();
+    journaling_ = false;
+  }
+  void rollback() {
+    for (auto op = log_.rbegin(); op != log_.rend(); ++op) {
+      switch (op->kind) {
+        case Op::MOVE: lru_.splice(op->next, lru_, op->it); break;
+        case Op::SET: op->it->value = op->old; break;
+        case Op::INSERT:
+          index_.erase(op->it->key);
+          lru_.erase(op->it);
+          break;
+        case Op::EVICT:
+          lru_.splice(lru_.end(), graveyard_, op->it);
+          index_[op->it->key] = op->it;
+          break;
+      }
+    }
+    hits_ = saved_hits_;
+    misses_ = saved_misses_;
+    commit();
   }
 
  private:
@@ -107,6 +165,18 @@ class PromptCache {
     Key key;
     Value value;
   };
+  using Iter = typename std::list<Entry>::iterator;
+  struct Op {
+    enum Kind { MOVE, SET, INSERT, EVICT } kind;
+    Iter it;
+    Value old;
+    Iter next{};  // MOVE: the node that followed `it` before it moved to the front
+  };
+  void to_front(Iter it) {
+    if (it == lru_.begin()) return;
+    if (journaling_) log_.push_back(Op{Op::MOVE, it, {}, std::next(it)});
+    lru_.splice(lru_.begin(), lru_, it);
+  }
   struct KeyHash {
     size_t operator()(const Key& k) const {
       uint64_t h = 1469598103934665603ull;  // FNV-1a (the reference hashes the same fields)
@@ -122,8 +192,12 @@ class PromptCache {
   };
   size_t capacity_;
   std::list<Entry> lru_;
-  std::unordered_map<Key, typename std::list<Entry>::iterator, KeyHash> index_;
+  std::unordered_map<Key, Iter, KeyHash> index_;
   uint64_t hits_ = 0, misses_ = 0;
+  bool journaling_ = false;
+  std::vector<Op> log_;
+  std::list<Entry> graveyard_;
+  uint64_t saved_hits_ = 0, saved_misses_ = 0;
 };
 
 template <typename Model, typename Counter>
@@ -136,50 +210,51 @@ class StreamingPromptResolver {
       : model_(model), cache_(cache), batch_size_(batch_size < 1 ? 1 : batch_size), max_new_(max_new_tokens),
         stats_(stats), counter_(counter), device_batch_(device_batch < 1 ? 1 : device_batch),
         hash_(model.bundle_hash()) {}
+  StreamingPromptResolver(const StreamingPromptResolver&) = delete;
+  StreamingPromptResolver& operator=(const StreamingPromptResolver&) = delete;
+  ~StreamingPromptResolver() {
+    if (in_txn_) cache_.rollback();  // abandoned mid-transaction: no pending entry may outlive us
+  }
 
   // Next table row's rendered prompt.
   void push(std::string_view prompt_sv) {
-    std::string prompt(prompt_sv);
-    const int64_t row = static_cast<int64_t>(row_slot_.size());
-    if (cache_.enabled()) {
-      if (const PromptCache::Value* hit = cache_.lookup(key(prompt))) {
-        ++stats_.cache_hits;
-        if (hit->slot >= 0) {
-          row_slot_.push_back(hit->slot);
-        } else {
-          row_slot_.push_back(static_cast<int64_t>(slots_.size()));
-          slots_.push_back(Slot{std::string(), hit->text, true, row});
-        }
-        return;
-      }
-      ++stats_.cache_misses;
-    }
-    auto it = window_index_.find(prompt);
-    if (it != window_index_.end()) {
-      row_slot_.push_back(it->second);
-      return;
-    }
-    const int64_t slot = static_cast<int64_t>(slots_.size());
-    if (window_first_row_ < 0) window_first_row_ = row;
-    slots_.push_back(Slot{prompt, std::string(), false, window_first_row_});
-    window_index_.emplace(std::move(prompt), slot);
-    window_.push_back(slot);
-    row_slot_.push_back(slot);
-    if (static_cast<int>(window_.size()) == batch_size_) close_window();
+    if (failed_) throw ContractViolation("StreamingPromptResolver: a previous device batch failed");
+    if (!in_txn_) begin_txn();
+    txn_prompts_.emplace_back(prompt_sv);
+    process_row(txn_prompts_.back());
+    if (window_.empty() && queue_.empty()) commit_txn();  // nothing in flight: rows are final
   }
 
   // End of input: closes the last window and decodes everything still queued.
   void finish() {
+    if (failed_) throw ContractViolation("StreamingPromptResolver: a previous device batch failed");
+    if (!in_txn_) return;
     close_window();
     run_device();
   }
 
-  // Output column entries for rows [taken, first unfinished row), in row order.
+  // Output column entries for rows [taken, first unfinished row), in row order (rows of completed
+  // transactions only), released from the resolver as they are handed back.
   std::vector<std::string> take_ready() {
     std::vector<std::string> out;
-    while (taken_ < row_slot_.size() && slots_[row_slot_[taken_]].done) {
-      out.push_back(slots_[row_slot_[taken_]].text);
-      ++taken_;
+    const int64_t limit = in_txn_ ? txn_row0_ : n_rows_;
+    while (row_base_ < limit) {
+      Row& r = rows_.front();
+      if (r.slot >= 0) {
+        const Slot& s = slot(r.slot);
+        if (!s.done) break;
+        out.push_back(s.text);
+      } else {
+        out.push_back(std::move(r.text));
+      }
+      rows_.pop_front();
+      ++row_base_;
+    }
+    // a slot is referenced only by rows up to its last binding; once those are handed back and the
+    // slot is decoded (its cache entry resolved), nothing refers to it any more
+    while (!slots_.empty() && slots_.front().done && slots_.front().last_row < row_base_) {
+      slots_.pop_front();
+      ++slot_base_;
     }
     return out;
   }
@@ -191,15 +266,57 @@ class StreamingPromptResolver {
     return take_ready();
   }
 
+  // Rows / decoded slots currently held (memory accounting for the streaming tests).
+  size_t rows_held() const { return rows_.size(); }
+  size_t slots_held() const { return slots_.size(); }
+
  private:
   struct Slot {
     std::string prompt;
     std::string text;
     bool done = false;
     int64_t first_row = -1;  // first row of the reference flush window (error messages)
+    int64_t last_row = -1;   // last row bound to this slot
+  };
+  struct Row {
+    int64_t slot = -1;  // >= 0: the row's output is that slot's; < 0: `text` is final (cache hit)
+    std::string text;
   };
 
   PromptCache::Key key(const std::string& p) const { return {hash_, max_new_, p}; }
+  Slot& slot(int64_t id) { return slots_[static_cast<size_t>(id - slot_base_)]; }
+  int64_t next_slot_id() const { return slot_base_ + static_cast<int64_t>(slots_.size()); }
+
+  void process_row(const std::string& prompt) {
+    const int64_t row = n_rows_++;
+    if (cache_.enabled()) {
+      if (const PromptCache::Value* hit = cache_.lookup(key(prompt))) {
+        ++stats_.cache_hits;
+        if (hit->slot >= 0) {
+          if (hit->owner != this) throw ContractViolation("PromptCache: entry pending in another resolver");
+          slot(hit->slot).last_row = row;
+          rows_.push_back(Row{hit->slot, {}});
+        } else {
+          rows_.push_back(Row{-1, hit->text});
+        }
+        return;
+      }
+      ++stats_.cache_misses;
+    }
+    auto it = window_index_.find(prompt);
+    if (it != window_index_.end()) {
+      slot(it->second).last_row = row;
+      rows_.push_back(Row{it->second, {}});
+      return;
+    }
+    const int64_t s = next_slot_id();
+    if (window_first_row_ < 0) window_first_row_ = row;
+    slots_.push_back(Slot{prompt, std::string(), false, window_first_row_, row});
+    window_index_.emplace(prompt, s);
+    window_.push_back(s);
+    rows_.push_back(Row{s, {}});
+    if (static_cast<int>(window_.size()) == batch_size_) close_window();
+  }
 
   // The reference's flush(): the window's distinct prompts count as model invocations and enter the
   // cache (pending) in window order; the prompts join the device queue.
@@ -207,7 +324,7 @@ class StreamingPromptResolver {
     if (window_.empty()) return;
     stats_.model_invocations += window_.size();
     for (int64_t s : window_) {
-      cache_.insert(key(slots_[s].prompt), PromptCache::Value{std::string(), s});
+      cache_.insert(key(slot(s).prompt), PromptCache::Value{std::string(), s, this});
       queue_.push_back(s);
     }
     window_.clear();
@@ -217,55 +334,110 @@ class StreamingPromptResolver {
   }
 
   void run_device() {
-    size_t i = 0;
-    while (i < queue_.size()) {
-      const size_t n = std::min(device_batch_, queue_.size() - i);
-      std::vector<std::string> prompts;
-      prompts.reserve(n);
-      for (size_t j = 0; j < n; ++j) prompts.push_back(slots_[queue_[i + j]].prompt);
-      std::vector<std::string> decoded;
-      try {
-        decoded = model_.batch_decode(std::span<const std::string>(prompts), max_new_, counter_);
-      } catch (const SequenceTooLong&) {
-        replay_windows(i, n);  // reproduces the reference's failure point exactly, then throws
+    try {
+      size_t i = 0;
+      while (i < queue_.size()) {
+        const size_t n = std::min(device_batch_, queue_.size() - i);
+        std::vector<std::string> prompts;
+        prompts.reserve(n);
+        for (size_t j = 0; j < n; ++j) prompts.push_back(slot(queue_[i + j]).prompt);
+        std::vector<std::string> decoded = model_.batch_decode(std::span<const std::string>(prompts), max_new_, counter_);
+        ++stats_.device_calls;
+        for (size_t j = 0; j < n; ++j) {
+          Slot& s = slot(queue_[i + j]);
+          s.text = std::move(decoded[j]);
+          s.done = true;
+          cache_.resolve_pending(key(s.prompt), this, queue_[i + j], s.text);
+          std::string().swap(s.prompt);  // only the pending cache key needed it
+        }
+        i += n;
       }
-      ++stats_.device_calls;
-      fill(i, n, decoded);
-      i += n;
+    } catch (...) {
+      rollback_and_replay();  // throws the reference's exception (or returns after a transient error)
+      return;
     }
     queue_.clear();
+    commit_txn();
   }
 
-  void fill(size_t i, size_t n, std::vector<std::string>& decoded) {
-    for (size_t j = 0; j < n; ++j) {
-      Slot& s = slots_[queue_[i + j]];
-      s.text = std::move(decoded[j]);
-      s.done = true;
-      cache_.resolve_pending(key(s.prompt), queue_[i + j], s.text);
-    }
+  void begin_txn() {
+    cache_.begin();
+    in_txn_ = true;
+    txn_stats_ = stats_;
+    txn_row0_ = n_rows_;
+    txn_slot0_ = next_slot_id();
+    txn_prompts_.clear();
+  }
+  void commit_txn() {
+    cache_.commit();
+    in_txn_ = false;
+    txn_prompts_.clear();
   }
 
-  // Error path: decode the device batch window by window, as the reference would have, so the
-  // windows before the failing one complete (and stay cached) and SequenceTooLong carries the
-  // reference's " (row N)" suffix, N = first row of the failing flush window (exec.cpp:134-137).
-  [[noreturn]] void replay_windows(size_t i, size_t n) {
-    size_t a = i;
-    while (a < i + n) {
-      size_t b = a;
-      while (b < i + n && slots_[queue_[b]].first_row == slots_[queue_[a]].first_row) ++b;
-      std::vector<std::string> prompts;
-      for (size_t j = a; j < b; ++j) prompts.push_back(slots_[queue_[j]].prompt);
+  // Undo the transaction and run its rows as the reference does: lookup per row, synchronous
+  // batch_decode per flush window, cache inserts after each successful window (exec.cpp:95-146).
+  void rollback_and_replay() {
+    cache_.rollback();
+    in_txn_ = false;
+    stats_ = txn_stats_;
+    rows_.resize(static_cast<size_t>(txn_row0_ - row_base_));
+    slots_.resize(static_cast<size_t>(txn_slot0_ - slot_base_));
+    n_rows_ = txn_row0_;
+    window_.clear();
+    window_index_.clear();
+    window_first_row_ = -1;
+    queue_.clear();
+    std::vector<std::string> prompts = std::move(txn_prompts_);
+    txn_prompts_.clear();
+    failed_ = true;  // until the replay completes
+    std::vector<int64_t> win;
+    std::map<std::string, int64_t> win_index;
+    auto flush = [&] {
+      if (win.empty()) return;
+      std::vector<std::string> ps;
+      for (int64_t s : win) ps.push_back(slot(s).prompt);
       std::vector<std::string> decoded;
       try {
-        decoded = model_.batch_decode(std::span<const std::string>(prompts), max_new_, counter_);
+        decoded = model_.batch_decode(std::span<const std::string>(ps), max_new_, counter_);
       } catch (const SequenceTooLong& e) {
-        throw SequenceTooLong(std::string(e.what()) + " (row " + std::to_string(slots_[queue_[a]].first_row) + ")");
+        throw SequenceTooLong(std::string(e.what()) + " (row " + std::to_string(slot(win.front()).first_row) + ")");
       }
       ++stats_.device_calls;
-      fill(a, b - a, decoded);
-      a = b;
+      stats_.model_invocations += win.size();
+      for (size_t j = 0; j < win.size(); ++j) {
+        Slot& s = slot(win[j]);
+        s.text = std::move(decoded[j]);
+        s.done = true;
+        cache_.insert(key(s.prompt), PromptCache::Value{s.text, -1, nullptr});
+      }
+      win.clear();
+      win_index.clear();
+    };
+    for (const std::string& prompt : prompts) {
+      const int64_t row = n_rows_++;
+      if (cache_.enabled()) {
+        if (const PromptCache::Value* hit = cache_.lookup(key(prompt))) {
+          ++stats_.cache_hits;
+          rows_.push_back(Row{-1, hit->text});
+          continue;
+        }
+        ++stats_.cache_misses;
+      }
+      auto it = win_index.find(prompt);
+      if (it != win_index.end()) {
+        slot(it->second).last_row = row;
+        rows_.push_back(Row{it->second, {}});
+        continue;
+      }
+      const int64_t s = next_slot_id();
+      slots_.push_back(Slot{prompt, std::string(), false, win.empty() ? row : slot(win.front()).first_row, row});
+      win_index.emplace(prompt, s);
+      win.push_back(s);
+      rows_.push_back(Row{s, {}});
+      if (static_cast<int>(win.size()) == batch_size_) flush();
     }
-    throw SequenceTooLong("StreamingPromptResolver: device batch failed but no flush window did");
+    flush();
+    failed_ = false;  // the failure did not reproduce (transient): the rows are decoded and final
   }
 
   const Model& model_;
@@ -276,13 +448,20 @@ class StreamingPromptResolver {
   Counter& counter_;
   size_t device_batch_;
   uint64_t hash_;
-  std::vector<Slot> slots_;
-  std::vector<int64_t> row_slot_;
-  size_t taken_ = 0;
+  std::deque<Slot> slots_;
+  int64_t slot_base_ = 0;  // id of slots_.front()
+  std::deque<Row> rows_;
+  int64_t row_base_ = 0;  // index of rows_.front() = rows handed back so far
+  int64_t n_rows_ = 0;
   std::vector<int64_t> window_;
   std::map<std::string, int64_t> window_index_;
   int64_t window_first_row_ = -1;
   std::vector<int64_t> queue_;
+  // transaction: everything since the last completed device call
+  bool in_txn_ = false, failed_ = false;
+  ResolverStats txn_stats_{};
+  int64_t txn_row0_ = 0, txn_slot0_ = 0;
+  std::vector<std::string> txn_prompts_;
 };
 
 }  // namespace iolm::cuda

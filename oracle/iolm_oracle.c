@@ -196,7 +196,31 @@ typedef struct {
   int act_quant;
   const int8_t* const* wcodes_t;
   const float* const* wscale;
+  /* act_quant only: 1 = the GPU W8A8 engine's rounding points - q/k/v leave the QKV GEMM epilogue
+   * as bf16 (KV pages, q operand), the attention output z and the GELU output g are bf16 before
+   * they are quantized (engine.cu launch_step; kernels.cu quant_rows_kernel). bf16 = RNE of f32. */
+  int gpu_points;
 } orc_model;
+
+/* f32 -> bf16 -> f32, round to nearest even (cvt.rn.bf16.f32 / __float2bfloat16_rn). */
+static float bf16r(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
+  u &= 0xffff0000u;
+  memcpy(&x, &u, 4);
+  return x;
+}
+static void bf16r_rows(float* p, size_t n) {
+  for (size_t i = 0; i < n; ++i) p[i] = bf16r(p[i]);
+}
+
+/* Capture of the int8 GEMM operands of one W8A8 forward (orc_forward_codes): per layer the codes of
+ * [attn_in n x d][attn_out_in n x kh][ffn_in n x d][ffn_mid n x f] and their per-token scales
+ * [4 x n]. Thread-local so concurrent decodes on one model are unaffected. */
+static __thread int8_t* tl_cap_codes;
+static __thread float* tl_cap_scales;
+static __thread size_t tl_cap_off, tl_cap_soff;
 
 void orc_quant_rows_s8(const float* x, int n, int d, int8_t* codes, float* scales);
 
@@ -207,6 +231,12 @@ static void linear_w8a8(const orc_model* m, int li, const float* x, int n, int K
   float* xs = (float*)malloc(sizeof(float) * n);
   int32_t* acc = (int32_t*)malloc(sizeof(int32_t) * N);
   orc_quant_rows_s8(x, n, K, xc, xs);
+  if (tl_cap_codes && li % 6 != 1 && li % 6 != 2) { /* wk / wv share wq's input */
+    memcpy(tl_cap_codes + tl_cap_off, xc, (size_t)n * K);
+    memcpy(tl_cap_scales + tl_cap_soff, xs, sizeof(float) * n);
+    tl_cap_off += (size_t)n * K;
+    tl_cap_soff += (size_t)n;
+  }
   const int8_t* w = m->wcodes_t[li];
   const float* ws = m->wscale[li];
   for (int i = 0; i < n; ++i) {
@@ -283,6 +313,11 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
       matmul_wt(h, n, d, m->wk[l], kh, kn);
       matmul_wt(h, n, d, m->wv[l], kh, vn);
     }
+    if (m->act_quant && m->gpu_points) {
+      bf16r_rows(q, (size_t)n * kh);
+      bf16r_rows(kn, (size_t)n * kh);
+      bf16r_rows(vn, (size_t)n * kh);
+    }
     *madds += 3ull * n * d * kh;
     for (int i = 0; i < n; ++i) {
       memcpy(st->k[l] + (size_t)(p0 + i) * kh, kn + (size_t)i * kh, sizeof(float) * kh);
@@ -327,6 +362,7 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
         *madds += (uint64_t)span * hd;
       }
     }
+    if (m->act_quant && m->gpu_points) bf16r_rows(z, (size_t)n * kh);
     if (m->act_quant) linear_w8a8(m, l * 6 + 3, z, n, kh, d, ao);
     else matmul_wt(z, n, kh, m->wo[l], d, ao);
     *madds += (uint64_t)n * kh * d;
@@ -336,6 +372,7 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
     else matmul_wt(h, n, d, m->w_in[l], f, g);
     *madds += (uint64_t)n * d * f;
     for (size_t t = 0; t < (size_t)n * f; ++t) g[t] = gelu(g[t]);
+    if (m->act_quant && m->gpu_points) bf16r_rows(g, (size_t)n * f);
     if (m->act_quant) linear_w8a8(m, l * 6 + 5, g, n, f, d, ao);
     else matmul_wt(g, n, f, m->w_out[l], d, ao);
     *madds += (uint64_t)n * f * d;
@@ -380,11 +417,42 @@ int orc_forward(const orc_model* m, const int* ids, const uint8_t* mask, int n, 
   return 0;
 }
 
+/* W8A8 forward that also returns the int8 operand codes and scales of every linear input (layout
+ * at tl_cap_codes above). Requires act_quant. */
+int orc_forward_codes(const orc_model* m, const int* ids, int n, float* logits, int8_t* codes,
+                      float* scales) {
+  if (!m->act_quant) return 1;
+  tl_cap_codes = codes;
+  tl_cap_scales = scales;
+  tl_cap_off = tl_cap_soff = 0;
+  const int st = orc_forward(m, ids, NULL, n, logits, NULL);
+  tl_cap_codes = NULL;
+  tl_cap_scales = NULL;
+  return st;
+}
+
 /* Greedy decode of ONE prompt (ids already [BOS]+bytes): the per-item state machine of
  * batch_decode (runtime.cpp:261-307). batch_decode(P)[i] == this(P[i]) bit-for-bit, which is the
  * reference's own batch-invariance contract (test_model.cpp:240-267). */
-int orc_decode_row(const orc_model* m, const int* ids, int n, int max_new, int* out_ids,
-                   int* out_len, uint64_t* madds) {
+static void top2(const float* x, int n, float* gap, float* amax) {
+  float a = -INFINITY, b = -INFINITY, mx = 0.0f;
+  for (int i = 0; i < n; ++i) {
+    if (x[i] > a) {
+      b = a;
+      a = x[i];
+    } else if (x[i] > b) {
+      b = x[i];
+    }
+    mx = fmaxf(mx, fabsf(x[i]));
+  }
+  *gap = a - b;
+  *amax = mx;
+}
+
+/* gap / amax (optional, max_new + 1 entries each): the CPU logits' top-1 minus top-2 and max |logit| at
+ * every prediction of the row - what a GPU divergence at that step is traced against (tests/parity.py). */
+static int decode_row_gaps(const orc_model* m, const int* ids, int n, int max_new, int* out_ids,
+                           int* out_len, uint64_t* madds, float* gap, float* amax) {
   *out_len = 0;
   if (max_new == 0) return 0;
   if (n > m->S) return 2;
@@ -399,6 +467,7 @@ int orc_decode_row(const orc_model* m, const int* ids, int n, int max_new, int* 
   logits_for(m, y + (size_t)(n - 1) * m->d, 1, logits, &c);
   int emitted = 0;
   for (;;) {
+    if (gap) top2(logits, m->V, gap + emitted, amax + emitted);
     const int next = argmax_row(logits, m->V);
     if (next == 130 || emitted == max_new) break;
     out_ids[emitted++] = next;
@@ -414,8 +483,15 @@ int orc_decode_row(const orc_model* m, const int* ids, int n, int max_new, int* 
   return 0;
 }
 
+int orc_decode_row(const orc_model* m, const int* ids, int n, int max_new, int* out_ids,
+                   int* out_len, uint64_t* madds) {
+  return decode_row_gaps(m, ids, n, max_new, out_ids, out_len, madds, NULL, NULL);
+}
+
 typedef struct {
   const orc_model* m;
+  float* gap;
+  float* amax;
   const int* ids;
   const int64_t* offsets;
   int n_rows, max_new;
@@ -435,8 +511,10 @@ static void* decode_worker(void* arg) {
     pthread_mutex_unlock(j->mu);
     if (r >= j->n_rows) break;
     uint64_t c = 0;
-    const int st = orc_decode_row(j->m, j->ids + j->offsets[r], (int)(j->offsets[r + 1] - j->offsets[r]),
-                                  j->max_new, j->out_ids + (size_t)r * j->max_new, j->out_len + r, &c);
+    const size_t g = (size_t)r * (j->max_new + 1);
+    const int st = decode_row_gaps(j->m, j->ids + j->offsets[r], (int)(j->offsets[r + 1] - j->offsets[r]),
+                                   j->max_new, j->out_ids + (size_t)r * j->max_new, j->out_len + r, &c,
+                                   j->gap ? j->gap + g : NULL, j->amax ? j->amax + g : NULL);
     if (st && !j->status) j->status = st;
     j->madds += c;
   }
@@ -444,8 +522,9 @@ static void* decode_worker(void* arg) {
 }
 
 /* Rows spread over `threads` workers. */
-int orc_decode_rows(const orc_model* m, const int* ids, const int64_t* offsets, int n_rows,
-                    int max_new, int* out_ids, int* out_len, uint64_t* madds, int threads) {
+int orc_decode_rows_gaps(const orc_model* m, const int* ids, const int64_t* offsets, int n_rows,
+                         int max_new, int* out_ids, int* out_len, uint64_t* madds, int threads,
+                         float* gap, float* amax) {
   if (threads < 1) threads = 1;
   int next = 0;
   pthread_mutex_t mu;
@@ -453,7 +532,7 @@ int orc_decode_rows(const orc_model* m, const int* ids, const int64_t* offsets, 
   decode_job* jobs = (decode_job*)calloc((size_t)threads, sizeof(decode_job));
   pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
   for (int t = 0; t < threads; ++t) {
-    jobs[t] = (decode_job){m, ids, offsets, n_rows, max_new, out_ids, out_len, 0, 0, &next, &mu};
+    jobs[t] = (decode_job){m, gap, amax, ids, offsets, n_rows, max_new, out_ids, out_len, 0, 0, &next, &mu};
     if (t) pthread_create(&th[t], NULL, decode_worker, &jobs[t]);
   }
   decode_worker(&jobs[0]);
@@ -469,6 +548,11 @@ int orc_decode_rows(const orc_model* m, const int* ids, const int64_t* offsets, 
   free(th);
   pthread_mutex_destroy(&mu);
   return status;
+}
+
+int orc_decode_rows(const orc_model* m, const int* ids, const int64_t* offsets, int n_rows,
+                    int max_new, int* out_ids, int* out_len, uint64_t* madds, int threads) {
+  return orc_decode_rows_gaps(m, ids, offsets, n_rows, max_new, out_ids, out_len, madds, threads, NULL, NULL);
 }
 
 /* ------------------------------------------------------------------ W8A8 restatement */

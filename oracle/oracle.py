@@ -108,6 +108,7 @@ class _OrcModel(C.Structure):
         ("wq", C.POINTER(C.c_void_p)), ("wk", C.POINTER(C.c_void_p)), ("wv", C.POINTER(C.c_void_p)),
         ("wo", C.POINTER(C.c_void_p)), ("w_in", C.POINTER(C.c_void_p)), ("w_out", C.POINTER(C.c_void_p)),
         ("act_quant", C.c_int), ("wcodes_t", C.POINTER(C.c_void_p)), ("wscale", C.POINTER(C.c_void_p)),
+        ("gpu_points", C.c_int),
     ]
 
 
@@ -126,6 +127,11 @@ def load_oracle() -> C.CDLL:
                                        C.c_void_p, C.POINTER(C.c_uint64)]
         lib.orc_decode_rows.argtypes = [C.POINTER(_OrcModel), C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                         C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_int]
+        lib.orc_decode_rows_gaps.argtypes = [C.POINTER(_OrcModel), C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                             C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_int,
+                                             C.c_void_p, C.c_void_p]
+        lib.orc_forward_codes.argtypes = [C.POINTER(_OrcModel), C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]
         lib.orc_init_dense_params.restype = C.c_size_t
         lib.orc_init_dense_params.argtypes = [C.c_int] * 6 + [C.c_uint64, C.c_void_p]
         lib.orc_quant_rows_s8.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
@@ -137,9 +143,11 @@ def load_oracle() -> C.CDLL:
 class OracleModel:
     """The C restatement over a decoded bundle."""
 
-    def __init__(self, bundle: bytes | dict, act_quant: bool = False):
+    def __init__(self, bundle: bytes | dict, act_quant: bool = False, gpu_points: bool = False):
         """act_quant: the W8A8 restatement (per-token int8 activations, int8 weight codes, exact
-        int32 accumulation) - requires q8 / sparse24_q8 encodings for every linear weight."""
+        int32 accumulation) - requires q8 / sparse24_q8 encodings for every linear weight.
+        gpu_points (W8A8 only): round q/k/v, the attention output and the GELU output to bf16 where
+        the GPU engine stores them, before they are quantized (W8A8 semantics)."""
         b = parse_bundle(bundle, with_codes=act_quant) if isinstance(bundle, (bytes, bytearray)) else bundle
         cfg, T = b["config"], b["tensors"]
         self.cfg = cfg
@@ -169,6 +177,7 @@ class OracleModel:
             self._keep.append(arr)
             setattr(m, fld, arr)
         m.act_quant = 1 if act_quant else 0
+        m.gpu_points = 1 if (act_quant and gpu_points) else 0
         if act_quant:
             names = ["attn.wq", "attn.wk", "attn.wv", "attn.wo", "ffn.w_in", "ffn.w_out"]
             cw, cs = [], []
@@ -198,18 +207,44 @@ class OracleModel:
             raise RuntimeError(f"oracle forward status {st}")
         return out, madds.value
 
-    def decode_ids(self, ids: np.ndarray, offsets: np.ndarray, max_new: int, threads: int = 1):
+    def decode_ids(self, ids: np.ndarray, offsets: np.ndarray, max_new: int, threads: int = 1,
+                   gaps: bool = False):
+        """Greedy ids [n x max_new], lengths, madds; with gaps=True also the CPU top-1 - top-2 logit
+        gap and max |logit| at every prediction ([n x (max_new + 1)] each, NaN past the row's end)."""
         ids = np.ascontiguousarray(ids, dtype=np.int32)
         offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         n = len(offsets) - 1
         out = np.zeros((n, max(max_new, 1)), np.int32)
         ln = np.zeros(n, np.int32)
         madds = C.c_uint64()
-        st = self.lib.orc_decode_rows(C.byref(self._m), ids.ctypes.data, offsets.ctypes.data, n, max_new,
-                                      out.ctypes.data, ln.ctypes.data, C.byref(madds), threads)
+        gap = np.full((n, max_new + 1), np.nan, np.float32) if gaps else None
+        amax = np.full((n, max_new + 1), np.nan, np.float32) if gaps else None
+        st = self.lib.orc_decode_rows_gaps(C.byref(self._m), ids.ctypes.data, offsets.ctypes.data, n, max_new,
+                                           out.ctypes.data, ln.ctypes.data, C.byref(madds), threads,
+                                           None if gap is None else gap.ctypes.data,
+                                           None if amax is None else amax.ctypes.data)
         if st:
             raise RuntimeError(f"oracle decode status {st}")
+        if gaps:
+            return out[:, :max_new], ln, madds.value, gap, amax
         return out[:, :max_new], ln, madds.value
+
+    def forward_codes(self, ids):
+        """W8A8 forward returning (logits, codes, scales): the int8 operand codes of every linear input,
+        per layer [attn_in n x d][attn_out_in n x kh][ffn_in n x d][ffn_mid n x f], and their
+        per-token scales, per layer [4 x n]."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        n, cfg = len(ids), self.cfg
+        tot = sum(n * (2 * cfg["d_model"] + len(h) * (cfg["d_model"] // cfg["n_heads"]) + f)
+                  for h, f in zip(cfg["active_heads"], cfg["active_ffn"]))
+        codes = np.zeros(tot, np.int8)
+        scales = np.zeros(4 * n * cfg["n_layers"], np.float32)
+        out = np.zeros((n, cfg["vocab_size"]), np.float32)
+        st = self.lib.orc_forward_codes(C.byref(self._m), ids.ctypes.data, n, out.ctypes.data, codes.ctypes.data,
+                                        scales.ctypes.data)
+        if st:
+            raise RuntimeError(f"oracle forward_codes status {st}")
+        return out, codes, scales
 
 
 def render(ids_row, n) -> str:

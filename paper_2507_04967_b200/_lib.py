@@ -81,6 +81,8 @@ SIGNATURES = {
                                            C.POINTER(C.c_uint64)]),
     "iolm_cuda_forward_capture": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                             C.POINTER(C.c_uint64)]),
+    "iolm_cuda_forward_codes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.POINTER(C.c_uint64)]),
     "iolm_cuda_last_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
     "iolm_cuda_last_error": (C.c_char_p, []),
     "iolm_cuda_set_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),

@@ -388,7 +388,7 @@ class Engine {
   void decode(const int32_t* ids, bool ids_on_device, const int64_t* offsets, int64_t n_rows, int max_new,
               int32_t* out_ids, int32_t* out_len, uint64_t* madds, int64_t* bad_row);
   void forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds,
-               uint16_t* capture = nullptr);
+               uint16_t* capture = nullptr, int8_t* codes = nullptr, float* code_scales = nullptr);
 
   std::mutex mu;
   void set_kernel_timing(bool on) { ktime_ = on; }
@@ -486,7 +486,15 @@ class Engine {
   DevArray<__nv_bfloat16> d_cap_;
   __nv_bfloat16* cap_ = nullptr;  // non-null while a capturing forward is being launched
   size_t cap_off_ = 0;
-  void capture_rows(const __nv_bfloat16* src, int ld, int T, int cols);
+  // W8A8 capture (iolm_cuda_forward_codes): the int8 operand codes of the same four points and their
+  // per-token scales [4 x n] per layer
+  DevArray<int8_t> d_cap8_;
+  DevArray<float> d_capsc_;
+  int8_t* cap8_ = nullptr;
+  float* capsc_ = nullptr;
+  size_t capsc_off_ = 0;
+  // point: 0 attn_in (LN1 out), 1 attn_out_in (attention out), 2 ffn_in (LN2 out), 3 ffn_mid (GELU out)
+  void capture_point(int point, int T, int cols);
 };
 
 Engine::Engine(const uint8_t* bytes, size_t len, int device, const iolm_cuda_opts* opts) {
@@ -1037,7 +1045,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
                     hs_.p);
   });
   ++stats_.kernel_launches;
-  capture_rows(h_.p, d_, T, d_);  // layers.0.attn_in
+  capture_point(0, T, d_);  // layers.0.attn_in
   // algorithmic attention work of this step (per head): prefill FLOPs 4*hd*sum(pos+1),
   // decode K+V bytes 2*2*hd*(pos+1)
   double pre_keys = 0, dec_keys = 0;
@@ -1107,12 +1115,12 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       timed(3, 4.0 * hd_ * ly.heads * dec_keys, [&] { launch_attention(none, dec, hd_, stream_); });
       ++stats_.kernel_launches;
     }
-    capture_rows(z_.p, kh_max_, T, ly.kh);  // layers.l.attn_out_in
     // x += z * Wo^T
     if (i8_o) {
       timed(9, dT * ly.kh * 3.0, [&] { launch_quant_rows(z_.p, kh_max_, T, ly.kh, z8_.p, kh_max_, zs_.p, stream_); });
       ++stats_.kernel_launches;
     }
+    capture_point(1, T, ly.kh);  // layers.l.attn_out_in
     GemmEpi eo;
     eo.M = T;
     eo.N = d_;
@@ -1127,7 +1135,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       launch_ln(x_.p, T, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_, i8_in ? h8_.p : nullptr, hs_.p);
     });
     ++stats_.kernel_launches;
-    capture_rows(h_.p, d_, T, d_);  // layers.l.ffn_in
+    capture_point(2, T, d_);  // layers.l.ffn_in
     // g = gelu(h * Win^T)
     GemmEpi ei;
     ei.M = T;
@@ -1139,12 +1147,12 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       gemm_w(iolmk::EPI_GELU_BF16, ly.in, i8_in ? tm_h8_ : tm_h_, tm_h8s_, T, ly.f, d_, ei,
              tma_epi_ ? &ly.tm_g_out : nullptr);
     });
-    capture_rows(g_.p, f_ld_max_, T, ly.f);  // layers.l.ffn_mid (post-GELU)
     // x += g * Wout^T
     if (i8_out) {
       timed(9, dT * ly.f * 3.0, [&] { launch_quant_rows(g_.p, f_ld_max_, T, ly.f, g8_.p, f_ld_max_, gs_.p, stream_); });
       ++stats_.kernel_launches;
     }
+    capture_point(3, T, ly.f);  // layers.l.ffn_mid (post-GELU)
     GemmEpi eo2 = eo;
     scales(eo2, ly.out, gs_.p);
     timed(7, 2.0 * dT * d_ * ly.f, [&] {
@@ -1157,7 +1165,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
                   q8_next ? h8_.p : nullptr, hs_.p);
       });
       ++stats_.kernel_launches;
-      capture_rows(h_.p, d_, T, d_);  // layers.l+1.attn_in
+      capture_point(0, T, d_);  // layers.l+1.attn_in
     }
   }
   if (R > 0) {
@@ -1359,15 +1367,28 @@ void Engine::decode(const int32_t* ids, bool ids_on_device, const int64_t* offse
   stats_.device_ms = ms;
 }
 
-void Engine::capture_rows(const __nv_bfloat16* src, int ld, int T, int cols) {
-  if (!cap_) return;
-  CUDA_OK(cudaMemcpy2DAsync(cap_ + cap_off_, static_cast<size_t>(cols) * 2, src, static_cast<size_t>(ld) * 2,
-                            static_cast<size_t>(cols) * 2, T, cudaMemcpyDeviceToDevice, stream_));
-  cap_off_ += static_cast<size_t>(T) * cols;
+void Engine::capture_point(int point, int T, int cols) {
+  if (cap_) {
+    const __nv_bfloat16* src = point == 1 ? z_.p : point == 3 ? g_.p : h_.p;
+    const int ld = point == 1 ? kh_max_ : point == 3 ? f_ld_max_ : d_;
+    CUDA_OK(cudaMemcpy2DAsync(cap_ + cap_off_, static_cast<size_t>(cols) * 2, src, static_cast<size_t>(ld) * 2,
+                              static_cast<size_t>(cols) * 2, T, cudaMemcpyDeviceToDevice, stream_));
+    cap_off_ += static_cast<size_t>(T) * cols;
+  }
+  if (cap8_) {
+    const int8_t* src = point == 1 ? z8_.p : point == 3 ? g8_.p : h8_.p;
+    const float* sc = point == 1 ? zs_.p : point == 3 ? gs_.p : hs_.p;
+    const int ld = point == 1 ? kh_max_ : point == 3 ? f_ld_max_ : d_;
+    CUDA_OK(cudaMemcpy2DAsync(cap8_ + cap_off_, static_cast<size_t>(cols), src, static_cast<size_t>(ld),
+                              static_cast<size_t>(cols), T, cudaMemcpyDeviceToDevice, stream_));
+    CUDA_OK(cudaMemcpyAsync(capsc_ + capsc_off_, sc, sizeof(float) * T, cudaMemcpyDeviceToDevice, stream_));
+    cap_off_ += static_cast<size_t>(T) * cols;
+    capsc_off_ += static_cast<size_t>(T);
+  }
 }
 
 void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logits, uint64_t* madds,
-                     uint16_t* capture) {
+                     uint16_t* capture, int8_t* codes, float* code_scales) {
   CUDA_OK(cudaSetDevice(device_));
   reset_counters();
   if (n <= 0 || !ids) throw ContractViolation("forward: empty sequence");
@@ -1401,15 +1422,36 @@ void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logi
     cap_ = d_cap_.p;
     cap_off_ = 0;
   }
+  if (codes) {
+    if (!act_quant_ || !any_int8_) throw Unsupported("forward_codes: needs act_quant (W8A8) weights");
+    for (const auto& ly : layers_) {
+      if (!(ly->qkv.int8() && ly->o.int8() && ly->in.int8() && ly->out.int8()))
+        throw Unsupported("forward_codes: every projection must run W8A8");
+      cap_elems += static_cast<size_t>(n) * (2 * d_ + ly->kh + ly->f);
+    }
+    d_cap8_.ensure(cap_elems);
+    d_capsc_.ensure(static_cast<size_t>(4) * n * L_);
+    cap8_ = d_cap8_.p;
+    capsc_ = d_capsc_.p;
+    cap_off_ = capsc_off_ = 0;
+  }
   try {
     launch_step(sb, d_ids_.p, dmask, d_logits_.p);
   } catch (...) {
     cap_ = nullptr;
+    cap8_ = nullptr;
+    capsc_ = nullptr;
     throw;
   }
   cap_ = nullptr;
+  cap8_ = nullptr;
+  capsc_ = nullptr;
   if (capture)
     CUDA_OK(cudaMemcpyAsync(capture, d_cap_.p, cap_elems * sizeof(__nv_bfloat16), cudaMemcpyDeviceToHost, stream_));
+  if (codes) {
+    CUDA_OK(cudaMemcpyAsync(codes, d_cap8_.p, cap_elems, cudaMemcpyDeviceToHost, stream_));
+    CUDA_OK(cudaMemcpyAsync(code_scales, d_capsc_.p, sizeof(float) * 4 * n * L_, cudaMemcpyDeviceToHost, stream_));
+  }
   CUDA_OK(cudaMemcpyAsync(logits, d_logits_.p, sizeof(float) * n * V_, cudaMemcpyDeviceToHost, stream_));
   CUDA_OK(cudaEventRecord(ev1_, stream_));
   CUDA_OK(cudaEventSynchronize(ev1_));
@@ -1561,6 +1603,15 @@ extern "C" int iolm_cuda_forward_capture(iolm_cuda_ctx* ctx, const int32_t* ids,
     if (!ctx || !logits || !capture) throw iolmh::ContractViolation("null argument");
     std::lock_guard<std::mutex> lock(ctx->eng->mu);
     ctx->eng->forward(ids, mask, n, logits, madds, capture);
+  });
+}
+
+extern "C" int iolm_cuda_forward_codes(iolm_cuda_ctx* ctx, const int32_t* ids, int32_t n, float* logits,
+                                       int8_t* codes, float* scales, uint64_t* madds) {
+  return guarded([&] {
+    if (!ctx || !logits || !codes || !scales) throw iolmh::ContractViolation("null argument");
+    std::lock_guard<std::mutex> lock(ctx->eng->mu);
+    ctx->eng->forward(ids, nullptr, n, logits, madds, nullptr, codes, scales);
   });
 }
 

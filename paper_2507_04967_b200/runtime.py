@@ -268,6 +268,21 @@ class ModelRuntime:
             counter.add(madds.value)
         return out
 
+    def forward_codes(self, ids):
+        """W8A8 runtimes (act_quant): (logits, int8 operand codes, per-token scales) of every linear
+        input - layout of iolm_cuda_forward_codes (include/iolm_cuda.h)."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        n, cfg = len(ids), self._config
+        hd = cfg.d_model // cfg.n_heads
+        tot = sum(n * (2 * cfg.d_model + cfg.layer_heads(l) * hd + cfg.layer_ffn(l)) for l in range(cfg.n_layers))
+        codes = np.zeros(tot, np.int8)
+        scales = np.zeros(4 * n * cfg.n_layers, np.float32)
+        out = np.empty((n, cfg.vocab_size), np.float32)
+        madds = C.c_uint64()
+        _check(self._lib.iolm_cuda_forward_codes(self._h, ids.ctypes.data, n, out.ctypes.data, codes.ctypes.data,
+                                                 scales.ctypes.data, C.byref(madds)))
+        return out, codes, scales
+
     # ---- token-level throughput API
     def decode_token_rows(self, ids: np.ndarray, offsets: np.ndarray, max_new_tokens: int,
                           device_ids: int | None = None):

@@ -70,3 +70,24 @@ def rows(first_row: int, n_rows: int, row_chars: int = 64, instruction: str = IN
 def row_strings(first_row: int, n_rows: int, row_chars: int = 64, instruction: str = INSTRUCTION) -> list[str]:
     ids, offs = rows(first_row, n_rows, row_chars, instruction)
     return ["".join(chr(c) for c in ids[offs[i] + 1:offs[i + 1]]) for i in range(n_rows)]
+
+
+def scale_token_embeddings(bundle: bytes, factors: dict[int, float]) -> bytes:
+    """A copy of a dense_f32 bundle with rows of `tok_embed` scaled (f32 multiply). The head is tied
+    (logits = y . tok_embed^T, /root/reference/proj/src/runtime.cpp:213-215), so scaling the EOS / PAD /
+    BOS rows makes a random-init model emit those ids at varied steps - the stop and no-render paths
+    of batch_decode (runtime.cpp:286-298) that plain random-init models never reach. Test harness."""
+    import json
+
+    hl = int.from_bytes(bundle[6:10], "little")
+    header = json.loads(bundle[10:10 + hl].decode())
+    rec = next(t for t in header["tensors"] if t["name"] == "tok_embed")
+    if rec["encoding"] != 0:
+        raise ValueError("tok_embed must be dense_f32")
+    base = 10 + hl + rec["offset"]
+    emb = np.frombuffer(bundle[base:base + rec["length"]], np.float32).reshape(rec["rows"], rec["cols"]).copy()
+    for tok, f in factors.items():
+        emb[tok] *= np.float32(f)
+    out = bytearray(bundle)
+    out[base:base + rec["length"]] = emb.tobytes()
+    return bytes(out)

@@ -74,6 +74,16 @@ RefRun run_reference(const iolm::ModelRuntime& cpu, const iolm::Table& t, int ba
   return r;
 }
 
+std::vector<std::string> run_reference_on(const iolm::ModelRuntime& cpu, const iolm::Table& t, int batch,
+                                          iolm::PromptCache& cache, iolm::ExecStats& stats, int max_new) {
+  const iolm::QueryPlan plan = iolm::parse_query("SELECT prompt('echo ' || w) AS r FROM t");
+  iolm::ExecOptions opts;
+  opts.batch_size = batch;
+  opts.max_new_tokens = max_new;
+  iolm::FlopCounter fc;
+  return iolm::execute(plan, {{"t", t}}, cpu, cache, opts, stats, fc).columns[0].texts;
+}
+
 }  // namespace
 
 int main() {
@@ -183,6 +193,91 @@ int main() {
     EXPECT(tail(ref_msg) == tail(got_msg), "SequenceTooLong row suffix");
   }
 
+  // A failing query on a SHARED cache (SequenceTooLong / non-ASCII ContractViolation at row 25):
+  // the cache contents, LRU order and counters and the ExecStats must be the reference's at its
+  // failure point (earlier flush windows decoded and cached, the failing one not, later rows never
+  // looked up), and the same cache must then serve the next query exactly like the reference's.
+  for (int kind = 0; kind < 2; ++kind)
+    for (int batch : {2, 16})
+      for (size_t capacity : {size_t{0}, size_t{5}, size_t{1024}})
+        for (size_t device_batch : {size_t{1}, size_t{7}, size_t{100000}}) {
+          iolm::Table bad = words_table(40, 9);
+          bad.columns[0].texts[25] = kind == 0 ? std::string(200, 'x') : std::string("caf\xe9");
+          std::vector<std::string> pb;
+          for (const auto& w : bad.columns[0].texts) pb.push_back("echo " + w);
+          iolm::PromptCache rcache(capacity);
+          iolm::ExecStats rs;
+          std::string rmsg = "none", gmsg = "none";
+          int rkind = -1, gkind = -1;
+          try {
+            run_reference_on(cpu, bad, batch, rcache, rs, 6);
+          } catch (const iolm::SequenceTooLong& e) {
+            rkind = 0, rmsg = e.what();
+          } catch (const iolm::ContractViolation& e) {
+            rkind = 1, rmsg = e.what();
+          }
+          iolm::cuda::PromptCache cache(capacity);
+          iolm::cuda::ResolverStats st;
+          iolm::FlopCounter fc;
+          {
+            Resolver res(model, cache, batch, 6, st, fc, device_batch);
+            try {
+              for (const auto& p : pb) {
+                res.push(p);
+                res.take_ready();
+              }
+              res.finish();
+            } catch (const iolm::SequenceTooLong& e) {
+              gkind = 0, gmsg = e.what();
+            } catch (const iolm::ContractViolation& e) {
+              gkind = 1, gmsg = e.what();
+            }
+          }
+          const auto tail = [](const std::string& m) { return m.substr(m.rfind(" (row ") == std::string::npos ? m.size() : m.rfind(" (row ")); };
+          EXPECT(rkind == kind && gkind == kind, "failing query raises the reference's exception class");
+          EXPECT(tail(rmsg) == tail(gmsg), "failing query: row suffix");
+          EXPECT(st.model_invocations == rs.model_invocations && st.cache_hits == rs.cache_hits &&
+                     st.cache_misses == rs.cache_misses,
+                 "failing query: stats at the failure point");
+          EXPECT(cache.size() == rcache.size() && cache.hits() == rcache.hits() && cache.misses() == rcache.misses(),
+                 "failing query: cache size and counters");
+          // the next query through the same cache: identical stats (LRU contents and order) and outputs
+          iolm::ExecStats rs2;
+          const auto rout = run_reference_on(cpu, t, batch, rcache, rs2, 6);
+          iolm::cuda::ResolverStats st2;
+          Resolver res2(model, cache, batch, 6, st2, fc, device_batch);
+          const auto gout = res2.resolve(prompts);
+          EXPECT(st2.model_invocations == rs2.model_invocations && st2.cache_hits == rs2.cache_hits &&
+                     st2.cache_misses == rs2.cache_misses,
+                 "query after a failure: stats");
+          EXPECT(cache.size() == rcache.size(), "query after a failure: cache size");
+#ifndef WITH_GPU
+          EXPECT(gout == rout, "query after a failure: outputs");
+#endif
+          ++scenarios;
+        }
+
+  // Bounded host memory while streaming: rows and decoded slots are released as they are handed back.
+  {
+    iolm::cuda::PromptCache cache(64);
+    iolm::cuda::ResolverStats st;
+    iolm::FlopCounter fc;
+    Resolver res(model, cache, 16, 2, st, fc, 64);
+    size_t max_rows = 0, max_slots = 0, got = 0;
+    for (int i = 0; i < 20000; ++i) {
+      res.push("echo " + std::to_string(i % 5000));
+      got += res.take_ready().size();
+      max_rows = std::max(max_rows, res.rows_held());
+      max_slots = std::max(max_slots, res.slots_held());
+    }
+    res.finish();
+    got += res.take_ready().size();
+    std::printf("streaming 20000 rows: at most %zu rows / %zu slots held\n", max_rows, max_slots);
+    EXPECT(got == 20000, "streaming memory test row count");
+    EXPECT(max_rows <= 2 * 64 + 16 && max_slots <= 2 * 64 + 16, "held rows / slots bounded by the device batch");
+    EXPECT(res.rows_held() == 0 && res.slots_held() == 0, "everything released after the last take_ready");
+  }
+
   // SEMANTIC JOIN (exec.cpp:283-336) through iolm::cuda::semantic_join. A second model whose 'y' and
   // 'n' embedding rows (tied head, runtime.cpp:213-215) are scaled up answers y or n on most pairs,
   // so the match path is exercised too (the random-init one answers neither: all unparsable).
@@ -229,7 +324,7 @@ int main() {
         EXPECT(st.model_invocations == rs.model_invocations && st.cache_hits == rs.cache_hits &&
                    st.cache_misses == rs.cache_misses,
                "join resolver stats");
-#ifndef WITH_GPU
+        // (on the GPU too: the y/n model's answers sit far from any fp tie - 40x embedding rows)
         EXPECT(js.join_matches == rs.join_matches && js.unparsable_match_answers == rs.unparsable_match_answers,
                "join match / unparsable counts");
         bool same = m.size() == out.row_count;
@@ -237,7 +332,6 @@ int main() {
           same = lt.columns[0].texts[m[k].first] == out.columns[0].texts[k] &&
                  r.columns[0].texts[m[k].second] == out.columns[1].texts[k];
         EXPECT(same, "join output rows identical to iolm::execute");
-#endif
         if (batch == 16 && capacity == 1024)
           std::printf("semantic join: %llu pairs considered, %llu matches (reference %llu), %llu unparsable\n",
                       static_cast<unsigned long long>(js.join_pairs_considered),
@@ -250,7 +344,7 @@ int main() {
 
 #ifdef WITH_GPU
   std::printf("gpu vs cpu reference agreement %zu/%zu rows\n", agree, total);
-  EXPECT(agree * 100 >= total * 95, "gpu vs cpu agreement >= 95%");
+  EXPECT(agree * 100 >= total * 99, "gpu vs cpu agreement >= 99%");
 #endif
   std::printf("%d scenarios, %d failures\n", scenarios, fails);
   if (fails == 0) std::printf("RESOLVER OK\n");

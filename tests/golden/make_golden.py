@@ -64,6 +64,39 @@ def fixture(name: str, bundle: bytes, n_rows: int, logit_rows: int, row_chars: i
     print(f"{name}: hash {meta['bundle_hash']}, {n_rows} rows, madds {madds}")
 
 
+# Stop-path fixtures: the tied head makes a scaled tok_embed row
+# win the argmax, so these bundles emit EOS (stop before emitting), PAD / BOS (emitted, fed back,
+# rendered as nothing) at varied steps. Per-row FlopCounter madds pin each row's number of advances.
+STOP_VARIANTS = {"eos": {130: 8.0}, "pad": {128: 8.0}, "bos": {129: 12.0}, "mix": {130: 6.0, 128: 6.0, 129: 6.0}}
+STOP_BUDGETS = (1, 3, 8)
+
+
+def stop_rows(max_seq: int) -> list[str]:
+    rng = np.random.default_rng(11)
+    lens = [0, 1, 2, 15, 16, 17, 31, 33, 63, max_seq - 4, max_seq - 3, max_seq - 2] + \
+        [int(x) for x in rng.integers(0, max_seq - 1, 4)]
+    ragged = ["".join(chr(32 + int(c)) for c in rng.integers(0, 95, n)) for n in lens]
+    return synth.row_strings(0, 32, 64) + ragged
+
+
+def stop_fixture(name: str, dims) -> None:
+    base = O.ref_toy_bundle(*dims, seed=42)
+    prompts = stop_rows(dims[4])
+    meta = {"name": name, "dims": dims, "seed": 42, "rows": prompts, "variants": {}}
+    for var, factors in STOP_VARIANTS.items():
+        b = synth.scale_token_embeddings(base, factors)
+        rt = O.RefRuntime(b)
+        entry = {"factors": {str(k): v for k, v in factors.items()}, "bundle_hash": f"{rt.bundle_hash():016x}"}
+        for n in STOP_BUDGETS:
+            outs, total = rt.batch_decode(prompts, n, threads=8)
+            per_row = [rt.batch_decode([p], n)[1] for p in prompts]
+            assert sum(per_row) == total
+            entry[str(n)] = {"outputs": outs, "row_madds": per_row, "madds": total}
+        meta["variants"][var] = entry
+    (HERE / f"{name}.json").write_text(json.dumps(meta, indent=1))
+    print(f"{name}: {len(prompts)} rows x {len(STOP_VARIANTS)} variants x budgets {STOP_BUDGETS}")
+
+
 def main() -> None:
     for name, c in CONFIGS.items():
         b = O.ref_toy_bundle(*c["dims"], seed=42)
@@ -74,6 +107,8 @@ def main() -> None:
         b = O.ref_compress(base, recipe, calib, seed=7)
         fixture(f"toy_{name}", b, 32, 1, extra={"dims": CONFIGS["toy"]["dims"], "recipe": recipe,
                                                 "calibration_rows": 8, "calibration_seed": 7})
+    stop_fixture("tiny_stops", CONFIGS["tiny"]["dims"])
+    stop_fixture("toy_stops", CONFIGS["toy"]["dims"])
     if "--c1" in sys.argv:
         b = O.ref_toy_bundle(1280, 24, 20, 5120, 128, seed=42)
         fixture("c1", b, 16, 2, extra={"dims": (1280, 24, 20, 5120, 128)})

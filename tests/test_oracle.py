@@ -138,3 +138,39 @@ def test_oracle_edge_semantics():
     oi0, ol0, m0 = om.decode_ids(ids, np.array([0, 15]), 0)
     assert ol0[0] == 0 and m0 == 0
     assert O.render([65, 128, 129, 66], 4) == "AB"
+
+
+def stop_case(name, var, budget):
+    meta = json.loads((GOLD / f"{name}.json").read_text())
+    e = meta["variants"][var]
+    b = synth.scale_token_embeddings(synth.toy_bundle(*meta["dims"], seed=meta["seed"]),
+                                     {int(k): v for k, v in e["factors"].items()})
+    assert f"{synth.fnv1a(b):016x}" == e["bundle_hash"]
+    prompts = meta["rows"]
+    ids = np.concatenate([np.array([O.BOS] + [ord(c) for c in p], np.int32) for p in prompts])
+    offs = np.concatenate([[0], np.cumsum([len(p) + 1 for p in prompts])]).astype(np.int64)
+    return b, prompts, ids, offs, e[str(budget)]
+
+
+@pytest.mark.parametrize("name", ["tiny_stops", "toy_stops"])
+@pytest.mark.parametrize("var", ["eos", "pad", "bos", "mix"])
+@pytest.mark.parametrize("budget", [1, 3, 8])
+def test_oracle_stop_paths_vs_golden(name, var, budget):
+    """EOS / PAD / BOS emission (runtime.cpp:286-298) on bundles whose tied-head rows for those ids
+    are scaled up: the restatement's rendered outputs, per-row madds (= each row's number of
+    advances, runtime.cpp:327-345) and the call total equal the reference's (golden fixtures)."""
+    b, prompts, ids, offs, want = stop_case(name, var, budget)
+    om = O.OracleModel(b)
+    oi, ol, madds = om.decode_ids(ids, offs, budget, threads=8)
+    assert [O.render(oi[i], ol[i]) for i in range(len(prompts))] == want["outputs"]
+    assert madds == want["madds"]
+    if name == "tiny_stops":
+        for i in range(len(prompts)):
+            _, _, m1 = om.decode_ids(ids[offs[i]:offs[i + 1]], np.array([0, offs[i + 1] - offs[i]]), budget)
+            assert m1 == want["row_madds"][i], i
+    # the fixture really exercises the path: some rows stop on EOS or emit PAD/BOS
+    if var in ("eos", "mix"):
+        assert any(ol[i] < budget and 0 < ol[i] for i in range(len(prompts))) or budget == 1
+        assert any(ol[i] == 0 for i in range(len(prompts)))  # EOS on the first prediction
+    if var in ("pad", "bos", "mix"):
+        assert any(np.isin(oi[i, :ol[i]], [O.PAD, O.BOS]).any() for i in range(len(prompts)))
