@@ -89,6 +89,9 @@ int iolm_cuda_bundle_hash(const iolm_cuda_ctx* ctx, uint64_t* out);
 int iolm_cuda_config(const iolm_cuda_ctx* ctx, iolm_cuda_model_config* out);
 /* Per-layer pruning info: active head count and FFN width of layer l (model.hpp:30-31). */
 int iolm_cuda_layer_shape(const iolm_cuda_ctx* ctx, int32_t layer, int32_t* heads, int32_t* ffn);
+/* ModelConfig::active_heads[layer] (model.hpp:29): the surviving heads' ORIGINAL indices, ascending.
+ * heads: capacity cap (>= n_heads always suffices); *n receives the count. */
+int iolm_cuda_layer_heads(const iolm_cuda_ctx* ctx, int32_t layer, int32_t* heads, int32_t cap, int32_t* n);
 
 /*
  * Replaces ModelRuntime::batch_decode(prompts, max_new_tokens, counter) (runtime.cpp:241-309).

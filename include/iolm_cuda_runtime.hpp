@@ -15,7 +15,9 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -95,23 +97,83 @@ inline void check(int st) {
   }
 }
 
+#ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
+using Config = iolm::ModelConfig;  // config() returns the reference's own type (runtime.hpp:41)
+using Logits = iolm::Matrix;       // forward() returns the reference's own type (runtime.hpp:48)
+#else
+// Mirror of iolm::ModelConfig (proj/include/iolm/model.hpp:20-41): same fields and accessors.
 struct Config {
-  int vocab_size, d_model, n_layers, n_heads, d_ff, max_seq_len, head_dim;
+  int vocab_size = 131, d_model = 0, n_layers = 0, n_heads = 0, d_ff = 0, max_seq_len = 0;
+  std::vector<std::vector<int>> active_heads;  // per layer, original head indices, ascending
+  std::vector<int> active_ffn;                 // per layer
+  int head_dim() const { return d_model / n_heads; }
+  int layer_heads(int layer) const { return static_cast<int>(active_heads[layer].size()); }
+  int layer_ffn(int layer) const { return active_ffn[layer]; }
 };
+// Mirror of iolm::Matrix (proj/include/iolm/matrix.hpp:28-46): row-major f32 rows x cols.
+struct Logits {
+  int rows = 0;
+  int cols = 0;
+  std::vector<float> data;
+  Logits() = default;
+  Logits(int r, int c, std::vector<float> v) : rows(r), cols(c), data(std::move(v)) {}
+  float at(int r, int c) const { return data[static_cast<size_t>(r) * cols + c]; }
+  const float* row(int r) const { return data.data() + static_cast<size_t>(r) * cols; }
+};
+#endif
+
+// ModelConfig of a context through the C ABI (iolm_cuda_config / layer_shape / layer_heads).
+inline Config read_config(const iolm_cuda_ctx* ctx) {
+  iolm_cuda_model_config c{};
+  check(iolm_cuda_config(ctx, &c));
+  Config cfg;
+  cfg.vocab_size = c.vocab_size;
+  cfg.d_model = c.d_model;
+  cfg.n_layers = c.n_layers;
+  cfg.n_heads = c.n_heads;
+  cfg.d_ff = c.d_ff;
+  cfg.max_seq_len = c.max_seq_len;
+  cfg.active_heads.resize(c.n_layers);
+  cfg.active_ffn.resize(c.n_layers);
+  for (int l = 0; l < c.n_layers; ++l) {
+    int32_t heads = 0, ffn = 0, n = 0;
+    check(iolm_cuda_layer_shape(ctx, l, &heads, &ffn));
+    std::vector<int32_t> idx(static_cast<size_t>(c.n_heads));
+    check(iolm_cuda_layer_heads(ctx, l, idx.data(), c.n_heads, &n));
+    cfg.active_heads[l].assign(idx.begin(), idx.begin() + n);
+    cfg.active_ffn[l] = ffn;
+  }
+  return cfg;
+}
 
 class ModelRuntime {
  public:
   explicit ModelRuntime(std::span<const uint8_t> bundle_bytes, int device = 0, const iolm_cuda_opts* opts = nullptr) {
     check(iolm_cuda_create(bundle_bytes.data(), bundle_bytes.size(), device, opts, &ctx_));
-    iolm_cuda_model_config c{};
-    check(iolm_cuda_config(ctx_, &c));
-    cfg_ = {c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.d_ff, c.max_seq_len, c.head_dim};
+    try {
+      cfg_ = read_config(ctx_);
+    } catch (...) {
+      iolm_cuda_destroy(ctx_);
+      throw;
+    }
   }
 #ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
   // Drop-in for ModelRuntime(const ModelBundle&): the bundle is handed over in its canonical
   // serialized form (model.cpp:311-346), so bundle_hash() is the reference's exactly.
-  explicit ModelRuntime(const iolm::ModelBundle& bundle, int device = 0)
-      : ModelRuntime(std::span<const uint8_t>(iolm::serialize_bundle(bundle)), device) {}
+  explicit ModelRuntime(const iolm::ModelBundle& bundle, int device = 0, const iolm_cuda_opts* opts = nullptr)
+      : ModelRuntime(std::span<const uint8_t>(iolm::serialize_bundle(bundle)), device, opts) {}
+
+  // What the reference-side patch (oracle/reference_gpu.patch) calls from
+  // iolm::ModelRuntime's constructor: a B200 runtime for `bundle` when the environment names a device
+  // (IOLM_CUDA_DEVICE=<index>; IOLM_CUDA_ACT_QUANT=1 runs q8 / sparse24_q8 bundles as W8A8), else null
+  // and the reference keeps its CPU path.
+  static std::shared_ptr<const ModelRuntime> from_env(const iolm::ModelBundle& bundle) {
+    const char* dev = std::getenv("IOLM_CUDA_DEVICE");
+    if (!dev || !*dev) return nullptr;
+    iolm_cuda_opts o{};
+    if (const char* aq = std::getenv("IOLM_CUDA_ACT_QUANT")) o.act_quant = std::atoi(aq) > 0 ? 1 : 0;
+    return std::make_shared<const ModelRuntime>(bundle, std::atoi(dev), &o);
+  }
 #endif
   ModelRuntime(const ModelRuntime&) = delete;
   ModelRuntime& operator=(const ModelRuntime&) = delete;
@@ -135,70 +197,72 @@ class ModelRuntime {
     return h;
   }
 
-  // Logits for every position, row-major [ids.size() x 131].
-  std::vector<float> forward(std::span<const int> ids, std::span<const uint8_t> mask, FlopCounter& counter) const {
-    if (ids.empty()) throw ContractViolation("forward: empty sequence");
-    if (!mask.empty() && mask.size() != ids.size()) throw ContractViolation("forward: mask length mismatch");
-    std::vector<int32_t> v(ids.begin(), ids.end());
-    std::vector<float> out(ids.size() * static_cast<size_t>(cfg_.vocab_size));
-    uint64_t madds = 0;
-    check(iolm_cuda_forward_logits(ctx_, v.data(), mask.empty() ? nullptr : mask.data(),
-                                   static_cast<int32_t>(v.size()), out.data(), &madds));
-    counter.add(madds);
-    return out;
-  }
-
+  // forward(ids, mask, counter, capture) (runtime.hpp:48-49): logits for every position, a
+  // [ids.size() x 131] matrix (iolm::Matrix with the reference types). Masked positions' rows are
+  // "not to be read" (runtime.hpp:44-47); they come back as zeros so the Matrix stays finite.
+  // With a CaptureSink, the inputs of every linear weight at the non-pad positions are recorded
+  // under the reference's capture-point names (capture_calibration, calib.cpp:44-51), captured on
+  // the GPU as bf16 and widened to f32.
 #ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
-  // forward(ids, mask, counter, CaptureSink*) (runtime.hpp:48-49): the calibration capture of
-  // capture_calibration (calib.cpp:44-51) - every linear weight's input rows for the non-pad
-  // positions, under the reference's capture-point names, captured on the GPU (bf16 -> f32).
-  std::vector<float> forward(std::span<const int> ids, std::span<const uint8_t> mask, FlopCounter& counter,
-                             iolm::CaptureSink* capture) const {
-    if (!capture) return forward(ids, mask, counter);
+  Logits forward(std::span<const int> ids, std::span<const uint8_t> mask, FlopCounter& counter,
+                 iolm::CaptureSink* capture = nullptr) const {
+#else
+  Logits forward(std::span<const int> ids, std::span<const uint8_t> mask, FlopCounter& counter) const {
+    void* capture = nullptr;
+#endif
     if (ids.empty()) throw ContractViolation("forward: empty sequence");
     if (!mask.empty() && mask.size() != ids.size()) throw ContractViolation("forward: mask length mismatch");
+    if (static_cast<int>(ids.size()) > cfg_.max_seq_len)
+      throw SequenceTooLong("forward: sequence length " + std::to_string(ids.size()) + " exceeds max_seq_len " +
+                            std::to_string(cfg_.max_seq_len));
     const int n = static_cast<int>(ids.size());
-    std::vector<int> kh(cfg_.n_layers), f(cfg_.n_layers);
-    size_t total = 0;
-    for (int l = 0; l < cfg_.n_layers; ++l) {
-      int32_t heads = 0, ffn = 0;
-      check(iolm_cuda_layer_shape(ctx_, l, &heads, &ffn));
-      kh[l] = heads * cfg_.head_dim;
-      f[l] = ffn;
-      total += static_cast<size_t>(n) * (2 * cfg_.d_model + kh[l] + f[l]);
-    }
     std::vector<int32_t> v(ids.begin(), ids.end());
     std::vector<float> out(static_cast<size_t>(n) * cfg_.vocab_size);
-    std::vector<uint16_t> cap(total);
     uint64_t madds = 0;
-    check(iolm_cuda_forward_capture(ctx_, v.data(), mask.empty() ? nullptr : mask.data(), n, out.data(), cap.data(),
-                                    &madds));
-    counter.add(madds);
-    size_t off = 0;
-    std::vector<float> row;
-    auto take = [&](const std::string& point, int cols) {
-      for (int t = 0; t < n; ++t) {
-        if (mask.empty() || mask[t]) {
-          row.resize(cols);
-          for (int c = 0; c < cols; ++c) {
-            const uint32_t bits = static_cast<uint32_t>(cap[off + static_cast<size_t>(t) * cols + c]) << 16;
-            std::memcpy(&row[c], &bits, 4);
-          }
-          capture->add_row(point, row);
-        }
+    const uint8_t* m = mask.empty() ? nullptr : mask.data();
+    if (!capture) {
+      check(iolm_cuda_forward_logits(ctx_, v.data(), m, n, out.data(), &madds));
+    } else {
+#ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
+      std::vector<int> kh(cfg_.n_layers), f(cfg_.n_layers);
+      size_t total = 0;
+      for (int l = 0; l < cfg_.n_layers; ++l) {
+        kh[l] = cfg_.layer_heads(l) * cfg_.head_dim();
+        f[l] = cfg_.layer_ffn(l);
+        total += static_cast<size_t>(n) * (2 * cfg_.d_model + kh[l] + f[l]);
       }
-      off += static_cast<size_t>(n) * cols;
-    };
-    for (int l = 0; l < cfg_.n_layers; ++l) {
-      const std::string p = "layers." + std::to_string(l) + ".";
-      take(p + "attn_in", cfg_.d_model);
-      take(p + "attn_out_in", kh[l]);
-      take(p + "ffn_in", cfg_.d_model);
-      take(p + "ffn_mid", f[l]);
-    }
-    return out;
-  }
+      std::vector<uint16_t> cap(total);
+      check(iolm_cuda_forward_capture(ctx_, v.data(), m, n, out.data(), cap.data(), &madds));
+      size_t off = 0;
+      std::vector<float> row;
+      auto take = [&](const std::string& point, int cols) {
+        for (int t = 0; t < n; ++t) {
+          if (mask.empty() || mask[t]) {
+            row.resize(cols);
+            for (int c = 0; c < cols; ++c) {
+              const uint32_t bits = static_cast<uint32_t>(cap[off + static_cast<size_t>(t) * cols + c]) << 16;
+              std::memcpy(&row[c], &bits, 4);
+            }
+            capture->add_row(point, row);
+          }
+        }
+        off += static_cast<size_t>(n) * cols;
+      };
+      for (int l = 0; l < cfg_.n_layers; ++l) {
+        const std::string p = "layers." + std::to_string(l) + ".";
+        take(p + "attn_in", cfg_.d_model);
+        take(p + "attn_out_in", kh[l]);
+        take(p + "ffn_in", cfg_.d_model);
+        take(p + "ffn_mid", f[l]);
+      }
 #endif
+    }
+    counter.add(madds);
+    if (m)
+      for (int t = 0; t < n; ++t)
+        if (!m[t]) std::fill_n(out.begin() + static_cast<size_t>(t) * cfg_.vocab_size, cfg_.vocab_size, 0.0f);
+    return Logits(n, cfg_.vocab_size, std::move(out));
+  }
 
   std::string greedy_decode(std::string_view prompt, int max_new_tokens, FlopCounter& counter) const {
     const std::string p(prompt);
@@ -246,11 +310,12 @@ class ModelRuntime {
 
  private:
   explicit ModelRuntime(iolm_cuda_ctx* ctx) : ctx_(ctx) {
-    iolm_cuda_model_config c{};
-    const int st = iolm_cuda_config(ctx_, &c);
-    if (st != IOLM_OK) iolm_cuda_destroy(ctx_);
-    check(st);
-    cfg_ = {c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.d_ff, c.max_seq_len, c.head_dim};
+    try {
+      cfg_ = read_config(ctx_);
+    } catch (...) {
+      iolm_cuda_destroy(ctx_);
+      throw;
+    }
   }
   iolm_cuda_ctx* ctx_ = nullptr;
   Config cfg_{};

@@ -33,7 +33,7 @@ def build(ref: bool = True) -> None:
     """Compile the C restatement and (when the reference sources exist) the reference library."""
     targets = ["oracle"]
     if ref and REFERENCE_SRC.exists():
-        targets += ["ref", "dropin", "resolver"]
+        targets += ["ref", "dropin", "resolver", "patched"]
     subprocess.run(["make", "-s", "-C", str(HERE), "-j8", *targets], check=True)
 
 

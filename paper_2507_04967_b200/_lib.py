@@ -72,6 +72,7 @@ SIGNATURES = {
     "iolm_cuda_bundle_hash": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "iolm_cuda_config": (C.c_int, [C.c_void_p, C.POINTER(ModelConfigC)]),
     "iolm_cuda_layer_shape": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "iolm_cuda_layer_heads": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     "iolm_cuda_decode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                    C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]),
     "iolm_cuda_decode_device_ids": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,

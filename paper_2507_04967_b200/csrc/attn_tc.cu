@@ -383,14 +383,9 @@ using namespace iolmk;
 template <int HD>
 static void launch_tc(const AttnParams& p, cudaStream_t st) {
   constexpr int smem = static_cast<int>(TcCfg<HD>::SMEM);
-  static bool cfg = false;
-  if (!cfg) {
-    CUDA_OK(cudaFuncSetAttribute(attn_prefill_tc_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CUDA_OK(cudaFuncSetAttribute(attn_prefill_tc_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cfg = true;
-  }
-  static int sms = 0;
-  if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  ensure_smem(attn_prefill_tc_kernel<HD, false>, smem);
+  ensure_smem(attn_prefill_tc_kernel<HD, true>, smem);
+  const int sms = device_sms();
   const int items = p.n_groups * p.heads;
   const int grid = std::min(items, sms * (HD == 64 ? 2 : 1));  // persistent: every CTA walks items
   if (p.key_mask) launch_k(attn_prefill_tc_kernel<HD, true>, grid, 192, smem, st, p);

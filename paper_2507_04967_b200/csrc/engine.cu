@@ -1019,6 +1019,10 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
   const Step& s = sb.step;
   const int T = s.T();
   const int R = static_cast<int>(s.head_rows.size());
+  // The previous step on these buffers may still be reading h_meta (its H2D copy is async): e.g. the
+  // shared-prefix step, whose buffers are reused by the decode loop's second step without a
+  // process(). A never-recorded or already-processed event returns at once.
+  CUDA_OK(cudaEventSynchronize(sb.done));
   uint8_t* h = sb.h_meta.p;
   uint8_t* d = sb.d_meta.p;
   size_t off = 0;
@@ -1550,6 +1554,19 @@ extern "C" int iolm_cuda_layer_shape(const iolm_cuda_ctx* ctx, int32_t layer, in
     if (layer < 0 || layer >= c.n_layers) throw iolmh::ContractViolation("layer index out of range");
     *heads = c.layer_heads(layer);
     *ffn = c.layer_ffn(layer);
+  });
+}
+
+extern "C" int iolm_cuda_layer_heads(const iolm_cuda_ctx* ctx, int32_t layer, int32_t* heads, int32_t cap,
+                                     int32_t* n) {
+  return guarded([&] {
+    if (!ctx || !n) throw iolmh::ContractViolation("null argument");
+    const auto& c = ctx->eng->config();
+    if (layer < 0 || layer >= c.n_layers) throw iolmh::ContractViolation("layer index out of range");
+    const auto& h = c.active_heads[layer];
+    *n = static_cast<int32_t>(h.size());
+    if (cap < *n || (*n > 0 && !heads)) throw iolmh::ContractViolation("layer_heads: buffer too small");
+    for (size_t i = 0; i < h.size(); ++i) heads[i] = h[i];
   });
 }
 

@@ -17,11 +17,7 @@ static void launch_one(const CUtensorMap& A, const CUtensorMap& B, int M, int N,
                        cudaStream_t st, int grid_cap) {
   using Cfg = GemmCfg<BN, CG, W4>;
   auto kern = gemm_tn_kernel<BN, EPI, CG, I8, W4>;
-  static bool configured = false;
-  if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM)));
-    configured = true;
-  }
+  ensure_smem(kern, Cfg::SMEM);
   const int tiles = ((M + Cfg::TILE_M - 1) / Cfg::TILE_M) * ((N + BN - 1) / BN);
   int groups = std::min(tiles, grid_cap / CG);
   if (groups <= 0) return;

@@ -1125,7 +1125,7 @@ __global__ void decode_quant_bf16_kernel(const uint8_t* __restrict__ p, int enc,
       const uint8_t byte = p[r * rb + c / 2];
       const int nib = (c & 1) ? (byte >> 4) : (byte & 0xF);
       v = static_cast<float>(nib - 8) * s;
-    } else if (enc == 3) {
+    } else if (enc == 3 && c < (cols & ~3)) {  // tail columns past the last whole group stay 0 (model.cpp:178-199)
       const size_t groups = cols / 4, irb = (groups + 1) / 2;
       const int8_t* codes = reinterpret_cast<const int8_t*>(p);
       const uint8_t* idx = p + static_cast<size_t>(rows) * groups * 2;
@@ -1167,7 +1167,7 @@ __global__ void decode_codes_kernel(const uint8_t* __restrict__ p, int enc, int 
     const int8_t* codes = reinterpret_cast<const int8_t*>(p);
     const uint8_t* idx = p + static_cast<size_t>(rows) * groups * 2;
     scale_off = static_cast<size_t>(rows) * groups * 2 + rows * irb;
-    if (c < cols) {
+    if (c < (cols & ~3)) {  // the tail past the last whole group stays 0, as in model.cpp:178-199
       const size_t gidx = c / 4;
       const uint8_t byte = idx[r * irb + gidx / 2];
       const int nib = (gidx & 1) ? (byte >> 4) : (byte & 0xF);
@@ -1236,8 +1236,7 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
                cudaStream_t st, int8_t* q8, float* qscale) {
   if (M <= 0) return;
   const int nv = (d / 4 + 31) / 32;
-  static int sms = 0;
-  if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int sms = device_sms();
   if (std::getenv("IOLM_LN_LEGACY") == nullptr && nv > 10 && nv <= 32 && d % 4 == 0) {
     const int grid_s = std::min<int>((M + 3) / 4, sms * 2);
     const int v2 = (d / 4 + 63) / 64;  // float4 per thread with two warps per row
@@ -1280,14 +1279,8 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
     const int grid_b = std::min<int>((M + 7) / 8, sms * per_sm);
 #define LNB(V)                                                                                          \
   do {                                                                                                  \
-    static bool cfg = false;                                                                            \
-    if (!cfg) {                                                                                         \
-      CUDA_OK(cudaFuncSetAttribute(ln_bulk_kernel<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                   200 * 1024));                                                        \
-      CUDA_OK(cudaFuncSetAttribute(ln_bulk_kernel<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                   200 * 1024));                                                        \
-      cfg = true;                                                                                       \
-    }                                                                                                   \
+    ensure_smem(ln_bulk_kernel<V, true>, 200 * 1024);                                                   \
+    ensure_smem(ln_bulk_kernel<V, false>, 200 * 1024);                                                  \
     if (q8) launch_k<false>(ln_bulk_kernel<V, true>, grid_b, 288, bsmem, st, x, M, d, g, b, h, ldh, q8, qscale);      \
     else launch_k<false>(ln_bulk_kernel<V, false>, grid_b, 288, bsmem, st, x, M, d, g, b, h, ldh, q8, qscale);        \
   } while (0)
@@ -1338,8 +1331,7 @@ void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_
   // read hits L2) at 8 CTAs per SM: these launches are bound by load latency, not bytes
   else if (ch <= 4) launch_k(quant_rows_kernel<4>, grid, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
   else if (cols > 3072 && cols <= 5120) {  // measured: two-warp rows win at 4096 (C4 FFN), lose at 2560
-    static int sms = 0;
-    if (!sms) CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int sms = device_sms();
     const int grid2 = std::min<int>((M + 3) / 4, sms * 2);
     if (cols <= 4096) launch_k<false>(quant_rows2_kernel<8>, grid2, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
     else launch_k<false>(quant_rows2_kernel<10>, grid2, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
@@ -1383,16 +1375,8 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
 #define ATT(HD)                                                                                     \
   do {                                                                                              \
     constexpr int smem = static_cast<int>(PfCfg<HD>::SMEM);                                         \
-    static bool cfg = false;                                                                        \
-    if (!cfg) {                                                                                     \
-      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD, false>,                                  \
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));             \
-      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD, true>,                                   \
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));             \
-      CUDA_OK(cudaFuncSetAttribute(attn_prefill_kernel<HD, false>,                                  \
-                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));           \
-      cfg = true;                                                                                   \
-    }                                                                                               \
+    ensure_smem(attn_prefill_kernel<HD, false>, smem, 100);                                         \
+    ensure_smem(attn_prefill_kernel<HD, true>, smem);                                               \
     if (prefill.n_groups > 0) {                                                                     \
       const dim3 grid(prefill.n_groups, prefill.heads);                                             \
       if (prefill.key_mask)                                                                         \
@@ -1405,14 +1389,7 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
       const int ngrp = (decode.heads + hg - 1) / hg;                                                \
       const int nst = decode_stages();                                                              \
       const size_t sm = DecCfg<HD>::smem(hg, nst);                                                  \
-      static size_t dcfg = 0;                                                                       \
-      if (sm > dcfg) {                                                                              \
-        CUDA_OK(cudaFuncSetAttribute(attn_decode_kernel<HD>,                                        \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm))); \
-        CUDA_OK(cudaFuncSetAttribute(attn_decode_kernel<HD>,                                        \
-                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));         \
-        dcfg = sm;                                                                                  \
-      }                                                                                             \
+      ensure_smem(attn_decode_kernel<HD>, sm, 100);                                                 \
       launch_k(attn_decode_kernel<HD>, decode.n_groups * ngrp, 32 * (hg + 1), sm, st, decode, hg, ngrp, nst); \
     }                                                                                               \
   } while (0)
@@ -1434,12 +1411,7 @@ void launch_head(const float* x, int d, const int* rows, int n_rows, const float
   if (V > 256) throw Unsupported("head: vocabulary larger than the CTA");
   if (d % 4 != 0) throw Unsupported("head: d_model must be a multiple of 4");
   const size_t smem = sizeof(float) * (HEAD_ROWS * (d + V) + 2 * 64 * V) + 16;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    CUDA_OK(cudaFuncSetAttribute(head_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    configured = smem;
-  }
+  if (smem > 48 * 1024) ensure_smem(head_argmax_kernel, smem);
   launch_k(head_argmax_kernel, blocks_for(n_rows, HEAD_ROWS), 256, smem, st, x, d, rows, n_rows, g, b, embed_t, V,
                                                                        row_slot, next_tok, last_tok, logits_out);
   CUDA_OK(cudaGetLastError());

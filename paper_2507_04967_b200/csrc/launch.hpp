@@ -56,6 +56,18 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 }
 #define CUDA_OK(x) ::iolmh::cuda_check((x), #x, __FILE__, __LINE__)
 
+// Raises `func`'s dynamic shared memory limit to >= `bytes` (and sets the carveout when
+// carveout >= 0) on the CURRENT device. Function attributes are per device, so the configured set
+// is keyed by (device, function) and guarded by a mutex: engines on several GPUs, or on several
+// host threads, configure each kernel once per device (errors.cu).
+void ensure_func_smem(const void* func, size_t bytes, int carveout = -1);
+// SM count of the current device (cached per device).
+int device_sms();
+template <typename... KArgs>
+inline void ensure_smem(void (*kern)(KArgs...), size_t bytes, int carveout = -1) {
+  ensure_func_smem(reinterpret_cast<const void*>(kern), bytes, carveout);
+}
+
 // Programmatic dependent launch (ptx.cuh pdl_sync): on unless IOLM_PDL=0 (A/B measurements).
 bool pdl_enabled();
 inline int pdl_attr(cudaLaunchAttribute* at) {

@@ -93,11 +93,7 @@ template <int EPI>
 static void launch_sp_one(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, int K, int katoms_pad,
                           const GemmEpi& ep, cudaStream_t st, int grid_cap) {
   auto kern = gemm_sp_kernel<EPI>;
-  static bool configured = false;
-  if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SpCfg::SMEM)));
-    configured = true;
-  }
+  ensure_smem(kern, SpCfg::SMEM);
   const int tiles = ((ep.N + SpCfg::TILE_M - 1) / SpCfg::TILE_M) * ((ep.M + SpCfg::BN - 1) / SpCfg::BN);
   const int groups = std::min(tiles, grid_cap / 2);
   if (groups <= 0) return;

@@ -58,7 +58,7 @@ int main() {
   for (size_t t = 0; t < ids.size(); ++t) {
     double num = 0, den = 0;
     for (int v = 0; v < 131; ++v) {
-      const double x = la.at(static_cast<int>(t), v), y = lb[t * 131 + v];
+      const double x = la.at(static_cast<int>(t), v), y = lb.at(static_cast<int>(t), v);
       num += (x - y) * (x - y);
       den += x * x;
     }
