@@ -62,10 +62,37 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 
 
 def load_peaks() -> tuple[dict, str]:
+    """hbm / bf16 denominators: the driver's MEASURED_PEAKS.json; else this repo's own measurement
+    on the pool (profiles/r02_peaks.json, profiles/peaks.py); else the guide's fallback."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         return json.loads(p.read_text()), "measured (MEASURED_PEAKS.json)"
+    own = int8_peaks()
+    if own and "cublas_bf16" in own["results"]:
+        # the driver's method: a copy and cuBLAS bf16 (not the engine's own, faster mainloop)
+        r = own["results"]
+        return ({"hbm_gbs": own["hbm_gbs"], "bf16_tflops": r["cublas_bf16"]["burst"]["tops"],
+                 "bf16_tflops_sustained": r["cublas_bf16"]["sustained"]["tops"]},
+                "measured on this pool: copy + cuBLAS bf16 (profiles/r02_peaks.json; MEASURED_PEAKS.json absent)")
     return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def int8_peaks() -> dict | None:
+    """Measured kind::i8 and 2:4 sparse kind::i8 rates (profiles/peaks.py -> profiles/r02_peaks.json):
+    the larger of cuBLASLt int8 and the engine's own mainloop-only kernel, sustained (>= 4 s loops)."""
+    p = ROOT / "profiles" / "r02_peaks.json"
+    return json.loads(p.read_text()) if p.exists() else None
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 # --------------------------------------------------------------------------- clocks
@@ -169,28 +196,6 @@ def step_rows(step: int, world: int, rank: int, B: int) -> int:
     return (step * world + rank) * B
 
 
-def gather_token_column(world: int, rank: int, out_ids: np.ndarray, out_len: np.ndarray):
-    """The only cross-GPU exchange of the job: every rank's generated-token column
-    (int32[rows x max_new] + int32 len[rows], host memory) is gathered to rank 0 over the CPU
-    (gloo) group. Returns the concatenation in rank order on rank 0, None elsewhere."""
-    if world == 1:
-        return out_ids, out_len
-    import torch
-    import torch.distributed as dist
-    ids_t = torch.from_numpy(np.ascontiguousarray(out_ids, dtype=np.int32))
-    len_t = torch.from_numpy(np.ascontiguousarray(out_len, dtype=np.int32))
-    grp = _cpu_group()
-    if rank == 0:
-        ids_l = [torch.empty_like(ids_t) for _ in range(world)]
-        len_l = [torch.empty_like(len_t) for _ in range(world)]
-        dist.gather(ids_t, ids_l, dst=0, group=grp)
-        dist.gather(len_t, len_l, dst=0, group=grp)
-        return torch.cat(ids_l).numpy(), torch.cat(len_l).numpy()
-    dist.gather(ids_t, None, dst=0, group=grp)
-    dist.gather(len_t, None, dst=0, group=grp)
-    return None
-
-
 _CPU_GROUP = None
 
 
@@ -221,6 +226,33 @@ def cpu_reference_sample(bundle: bytes, cfg: dict, n_rows: int, first_row: int, 
     oi, ol, _ = om.decode_ids(ids, offs, MAX_NEW, threads=threads)
     dt = time.perf_counter() - t0
     return n_rows / dt, "port", dt, [O.render(oi[i], ol[i]) for i in range(n_rows)]
+
+
+def divergence_gaps(bundle: bytes, cfg: dict, first_row: int, cpu_outs, gpu_outs) -> list:
+    """Each row where the GPU's greedy output differs from the CPU reference's: the first differing
+    character and the CPU top-1/top-2 logit gap there (the C restatement, bit-exact with the
+    reference, replays prompt + common prefix), against the near-tie bound 0.05 + 4e-3 max|logit|
+    of tests/parity.py. Checker only: runs after the timed regions."""
+    bad = [i for i, (a, b) in enumerate(zip(cpu_outs, gpu_outs)) if a != b]
+    if not bad:
+        return []
+    from oracle import oracle as O
+    from paper_2507_04967_b200 import synth
+    om = O.OracleModel(bundle)
+    prompts = synth.row_strings(first_row, len(cpu_outs), cfg["row_chars"])
+    res = []
+    for i in bad:
+        a, b = cpu_outs[i], gpu_outs[i]
+        k = 0
+        while k < min(len(a), len(b)) and a[k] == b[k]:
+            k += 1
+        ids = np.array([129] + [ord(c) for c in prompts[i] + a[:k]], np.int32)
+        lg = om.forward(ids)[0][-1]
+        top = np.sort(lg)
+        gap = float(top[-1] - top[-2])
+        tol = 0.05 + 4e-3 * float(np.abs(lg).max())
+        res.append({"row": i, "char": k, "cpu_top2_gap": gap, "tie_bound": tol, "tie": gap < tol})
+    return res
 
 
 def cpu_sample_rows(name: str, cores: int) -> int:
@@ -256,7 +288,7 @@ def run_reference_arm(args, cfg: dict, world: int, rank: int) -> None:
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": cfg["desc"], "rows_per_step": n, "max_new_tokens": MAX_NEW,
                                         "sample": f"{n} rows per step, one reference batch_decode per row"},
-        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": kinds[0],
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "cpu_model": cpu_model(), "kind": kinds[0],
                          "sample": f"{n} rows x {args.steps} steps on {cores} host threads"},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -264,6 +296,38 @@ def run_reference_arm(args, cfg: dict, world: int, rank: int) -> None:
 
 
 # --------------------------------------------------------------------------- GPU arm
+def multi_device_e2e(args, cfg: dict, bundle: bytes, world: int, B: int, W: int, K: int, rank0_outs):
+    """Rank 0 of an N-rank run: e2e rows/s through one multi-device context over GPUs 0..N-1."""
+    import torch
+    from paper_2507_04967_b200 import runtime as R
+    from paper_2507_04967_b200 import synth
+    devs = [0] * world if os.environ.get("BENCH_SHARE_GPUS") else list(range(world))
+    mrt = R.ModelRuntime(bundle, device=devs, max_tokens_per_step=args.tokens_per_step,
+                         prefill_tc={"auto": None, "on": True, "off": False}[args.prefill_tc],
+                         act_quant=cfg.get("act_quant", False))
+    host = []
+    for k in range(W + K):  # step k's rows of all ranks: [k*N*B, (k+1)*N*B) (step_rows is rank-major)
+        ids, offs = synth.rows(step_rows(k, world, 0, B), world * B, cfg["row_chars"])
+        host.append((torch.from_numpy(ids).pin_memory(), offs))
+    mrt.decode_token_rows(host[0][0].numpy(), host[0][1], MAX_NEW)  # warm-up
+    torch.cuda.synchronize()
+    # CUDA events on device 0 around synchronous calls: each returns with every device's ids on the host
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = None
+    for k in range(W, W + K):
+        out = mrt.decode_token_rows(host[k][0].numpy(), host[k][1], MAX_NEW)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    o, ln, _ = out
+    o0, ln0 = rank0_outs[-1]
+    if not (np.array_equal(ln[:B], ln0) and np.array_equal(o[:B], o0)):
+        raise SystemExit("bench: multi-device e2e disagrees with rank 0's device-resident run")
+    mrt.close()
+    return ms, world * B * K
+
+
 def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     import torch
     from paper_2507_04967_b200 import runtime as R
@@ -324,25 +388,22 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     ms = ev0.elapsed_time(ev1)
     ms_max = allreduce_max(world, ms, dev)
 
-    # ---- timed region 2 (e2e): host buffers through the public ABI
-    barrier(world)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    # ---- timed region 2 (e2e), one GPU: host buffers through the public ABI
     gathered_rows = 0
-    for k in range(W, W + K):
-        o2, ln2, _ = run(k, False)
-        g = gather_token_column(world, rank, o2, ln2)  # output column -> rank 0 (timed, part of e2e)
-        if g is not None:
-            gathered_rows += len(g[1])
-    e1.record()
-    torch.cuda.synchronize()
-    barrier(world)
-    e2e_ms = allreduce_max(world, e0.elapsed_time(e1), dev)
-    # both regions must produce the same tokens (last step spot check)
-    o_last, ln_last = outs[-1]
-    if not (np.array_equal(ln2, ln_last) and np.array_equal(o2, o_last)):
-        raise SystemExit("bench: device-input and host-input runs disagree")
+    if world == 1:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(W, W + K):
+            o2, ln2, _ = run(k, False)
+            gathered_rows += len(ln2)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1)
+        # both regions must produce the same tokens (last step spot check)
+        o_last, ln_last = outs[-1]
+        if not (np.array_equal(ln2, ln_last) and np.array_equal(o2, o_last)):
+            raise SystemExit("bench: device-input and host-input runs disagree")
 
     # ---- roofline pass (untimed for `value`): the same step inputs with per-kernel CUDA events
     kt_steps = 0
@@ -357,6 +418,20 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
                 a[1] += work_
                 a[2] += cnt_
         rt.set_kernel_timing(False)
+
+    if world > 1:
+        # ---- timed region 2 (e2e), N GPUs: the product's multi-GPU API. Every rank releases its
+        # context; rank 0 opens ONE context over all N GPUs (iolm_cuda_create_multi) and pushes each
+        # step's N*B rows (exactly the rows the N ranks processed in that step) through it with host
+        # buffers: H2D, range-partitioned decode on every GPU, ids written back into one host output
+        # column in row order (the gather). The other ranks wait at the barrier.
+        rt.close()
+        barrier(world)
+        e2e_ms, gathered_rows = 0.0, 0
+        if rank == 0:
+            e2e_ms, gathered_rows = multi_device_e2e(args, cfg, bundle, world, B, W, K, outs)
+        e2e_ms = allreduce_max(world, e2e_ms, dev)
+        barrier(world)
 
     rows_total = world * B * K
     value = rows_total / (ms_max / 1000.0)
@@ -377,11 +452,19 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
         peak = peaks["bf16_tflops_sustained"]
         unit, bound = "TFLOP/s", "tensor"
         if cfg.get("act_quant"):
-            # int8 GEMMs: kind::i8 dense = 2x and 2:4 sparse kind::i8 = 4x the bf16 rate (datasheet
-            # ratios applied to the measured sustained bf16 peak; FLOPs counted dense-equivalent)
-            mult = 4.0 if cfg["quant"] == "sparse24" else 2.0
-            peak *= mult
-            peak_src = f"{peak_src} x {mult:g} (int8{' 2:4 sparse' if mult == 4 else ''} datasheet ratio)"
+            # int8 GEMMs (ops counted dense-equivalent): the MEASURED sustained kind::i8 / 2:4 sparse
+            # kind::i8 rate (profiles/r02_peaks.json); the datasheet ratios (2x / 4x bf16) only if absent
+            sparse = cfg["quant"] == "sparse24"
+            ip = int8_peaks()
+            if ip and ip["peaks_tops_sustained"].get("sp24_i8" if sparse else "i8"):
+                peak = ip["peaks_tops_sustained"]["sp24_i8" if sparse else "i8"]
+                peak_src = ("measured sustained " + ("2:4 sparse kind::i8 (engine mainloop-only, N=K=8192)" if sparse
+                            else "kind::i8 (max of cuBLASLt int8 and engine mainloop-only, 8192^3)") +
+                            ", profiles/r02_peaks.json")
+            else:
+                mult = 4.0 if sparse else 2.0
+                peak *= mult
+                peak_src = f"{peak_src} x {mult:g} (int8{' 2:4 sparse' if mult == 4 else ''} datasheet ratio)"
     traffic = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
@@ -407,9 +490,10 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
         rate, kind, dt, cpu_outs = cpu_reference_sample(bundle, cfg, n, step_rows(W, 1, 0, B), cores)
         gpu_outs = [R.decode_ids(outs[0][0][i, :outs[0][1][i]]) for i in range(n)]
         agree = sum(a == b for a, b in zip(cpu_outs, gpu_outs)) / n
-        cpu = {"value": rate, "unit": "rows/s", "cores": cores, "kind": kind,
+        cpu = {"value": rate, "unit": "rows/s", "cores": cores, "cpu_model": cpu_model(), "kind": kind,
                "sample": f"first {n} rows of timed step 0, one batch_decode per row, {cores} threads, {dt:.1f} s",
-               "greedy_agreement_with_gpu": agree}
+               "greedy_agreement_with_gpu": agree,
+               "divergences": divergence_gaps(bundle, cfg, step_rows(W, 1, 0, B), cpu_outs, gpu_outs)}
     if rank != 0:
         return
     h2d = sum(int(h.numel()) * 4 for h in host_ids[W:]) // K + (B + 1) * 8

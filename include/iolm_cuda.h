@@ -83,6 +83,25 @@ int iolm_cuda_create(const uint8_t* bundle_bytes, size_t len, int device,
                      const iolm_cuda_opts* opts, iolm_cuda_ctx** out);
 void iolm_cuda_destroy(iolm_cuda_ctx* ctx);
 
+/*
+ * One context over several GPUs of a box (the table is range-partitioned, every GPU holds a
+ * full replica and its own KV pool). iolm_cuda_decode on such a context splits the rows into
+ * contiguous ranges of near-equal token counts, decodes them concurrently (one host thread per
+ * device) and writes each range's ids / lengths straight into the caller's out_ids / out_len - the
+ * output-column gather; row order is the caller's (PromptResolver's row-order guarantee,
+ * proj/src/exec.cpp:139-142). madds is the sum over devices, *bad_row the batch's first too-long row
+ * (all lengths are checked before any device work, runtime.cpp:264-267), and the error of the lowest
+ * failing range otherwise. Outputs equal a one-device context's bit for bit (batch invariance).
+ * forward / capture / codes / save_image run on devices[0]; last_stats and kernel_times of a
+ * multi-device decode are summed over devices (device_ms: the slowest device).
+ * iolm_cuda_decode_device_ids is single-device only (IOLM_E_UNSUPPORTED here). The same device may
+ * be listed twice (tests on a 1-GPU box).
+ */
+int iolm_cuda_create_multi(const uint8_t* bundle_bytes, size_t len, const int32_t* devices, int32_t n_devices,
+                           const iolm_cuda_opts* opts, iolm_cuda_ctx** out);
+/* Number of devices (engines) of a context: 1 for iolm_cuda_create. */
+int iolm_cuda_device_count(const iolm_cuda_ctx* ctx, int32_t* n);
+
 /* ModelRuntime::bundle_hash() (runtime.hpp:42; FNV-1a over the serialized bundle, model.cpp:408). */
 int iolm_cuda_bundle_hash(const iolm_cuda_ctx* ctx, uint64_t* out);
 /* ModelRuntime::config() (runtime.hpp:41). */
@@ -222,6 +241,11 @@ int iolm_cuda_debug_gemm_w4(const uint16_t* A, const uint8_t* payload, float* C,
                             int32_t pair);
 /* Device-only timing of the sparse GEMM: mean ms per launch (epi as in debug_gemm_time). */
 int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, float* ms_out);
+
+/* The multi-device row split (host only, no device work): cut[0..*n_cut) with cut[0] = 0 and
+ * cut[last] = n_rows; range i = rows [cut[i], cut[i+1]). cut needs shards + 1 entries. */
+int iolm_cuda_debug_partition(const int64_t* row_offsets, int64_t n_rows, int32_t shards, int64_t* cut,
+                              int32_t* n_cut);
 
 int iolm_cuda_debug_quant_rows_bf16(const uint16_t* x, int32_t n, int32_t d, int8_t* codes, float* scales);
 

@@ -167,14 +167,42 @@ class ModelRuntime {
   // iolm::ModelRuntime's constructor: a B200 runtime for `bundle` when the environment names a device
   // (IOLM_CUDA_DEVICE=<index>; IOLM_CUDA_ACT_QUANT=1 runs q8 / sparse24_q8 bundles as W8A8), else null
   // and the reference keeps its CPU path.
+  // IOLM_CUDA_DEVICE may list several devices ("0,1,2,3"): one multi-device runtime over them.
   static std::shared_ptr<const ModelRuntime> from_env(const iolm::ModelBundle& bundle) {
     const char* dev = std::getenv("IOLM_CUDA_DEVICE");
     if (!dev || !*dev) return nullptr;
     iolm_cuda_opts o{};
     if (const char* aq = std::getenv("IOLM_CUDA_ACT_QUANT")) o.act_quant = std::atoi(aq) > 0 ? 1 : 0;
-    return std::make_shared<const ModelRuntime>(bundle, std::atoi(dev), &o);
+    std::vector<int> devs;
+    for (const char* p = dev; *p;) {
+      devs.push_back(std::atoi(p));
+      while (*p && *p != ',') ++p;
+      if (*p == ',') ++p;
+    }
+    if (devs.size() == 1) return std::make_shared<const ModelRuntime>(bundle, devs[0], &o);
+    const std::vector<uint8_t> bytes = iolm::serialize_bundle(bundle);
+    return std::make_shared<const ModelRuntime>(std::span<const uint8_t>(bytes), std::span<const int>(devs), &o);
   }
 #endif
+  // One runtime over several GPUs (iolm_cuda_create_multi): batch_decode range-partitions the rows
+  // over full per-GPU replicas, one host thread per device, outputs in row order (the multi-GPU
+  // deployment of SURVEY §8e behind the same surface).
+  ModelRuntime(std::span<const uint8_t> bundle_bytes, std::span<const int> devices, const iolm_cuda_opts* opts = nullptr) {
+    std::vector<int32_t> d(devices.begin(), devices.end());
+    check(iolm_cuda_create_multi(bundle_bytes.data(), bundle_bytes.size(), d.data(), static_cast<int32_t>(d.size()),
+                                 opts, &ctx_));
+    try {
+      cfg_ = read_config(ctx_);
+    } catch (...) {
+      iolm_cuda_destroy(ctx_);
+      throw;
+    }
+  }
+  int device_count() const {
+    int32_t n = 0;
+    check(iolm_cuda_device_count(ctx_, &n));
+    return n;
+  }
   ModelRuntime(const ModelRuntime&) = delete;
   ModelRuntime& operator=(const ModelRuntime&) = delete;
   ~ModelRuntime() { iolm_cuda_destroy(ctx_); }

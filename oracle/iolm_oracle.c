@@ -253,6 +253,72 @@ static void linear_w8a8(const orc_model* m, int li, const float* x, int n, int K
   free(acc);
 }
 
+/* The GPU GEMM epilogue's GELU (ptx.cuh gelu_tanh): x * 1/(1 + 2^(inner * -2log2(e))),
+ * inner = x * fma(x*x, k*0.044715, k) - the reference's tanh form rewritten as x * sigmoid(2u). */
+static float gelu_gpu(float x) {
+  const float k = 0.7978845608028654f, k3 = 0.7978845608028654f * 0.044715f;
+  const float m2l2e = -2.0f * 1.4426950408889634f;
+  const float inner = x * fmaf(x * x, k3, k);
+  return x * (1.0f / (1.0f + exp2f(inner * m2l2e)));
+}
+
+/* The GPU prefill attention of one (query, head) at the W8A8 engine's rounding points
+ * (kernels.cu attn_prefill_kernel for hd <= 64: 32-key blocks; attn_tc.cu for hd 128: 64-key blocks;
+ * blocks aligned to absolute positions): online softmax in base 2 with scale_log2 = log2(e)/sqrt(hd)
+ * in f32, per block m_new = max(m, max_j(s_j) * scale_log2), alpha = 2^(m - m_new), l = l * alpha +
+ * sum_j p_j with p_j = 2^(fma(s_j, scale_log2, -m_new)) in f32, O = O * alpha + sum_j bf16(p_j) * v_j
+ * (the PV product takes P as bf16), z = bf16(O * (1 / l)). Scores are f32 dots of the bf16 q / k.
+ * Remaining differences to the GPU are f32 summation orders and the 2-ulp ex2.approx. */
+static void flash_head_gpu(const float* qh, const float* k0, const float* v0, int ld, int hd, int span,
+                           const uint8_t* valid, float* zh) {
+  const int KB = hd >= 128 ? 64 : 32;
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+  float m_run = -INFINITY, l_run = 0.0f;
+  float o[128], s[64];
+  for (int j = 0; j < hd; ++j) o[j] = 0.0f;
+  for (int key0 = 0; key0 < span; key0 += KB) {
+    const int nk = span - key0 < KB ? span - key0 : KB;
+    float mx = -INFINITY;
+    for (int t = 0; t < nk; ++t) {
+      const int key = key0 + t;
+      if (!valid[key]) {
+        s[t] = -INFINITY;
+        continue;
+      }
+      const float* kr = k0 + (size_t)key * ld;
+      float acc = 0.0f;
+      for (int c = 0; c < hd; ++c) acc += qh[c] * kr[c];
+      s[t] = acc;
+      if (acc > mx) mx = acc;
+    }
+    const float mnew = fmaxf(m_run, mx * scale_log2);
+    const float alpha = mnew == -INFINITY ? 1.0f : exp2f(m_run - mnew);
+    const float msub = mnew == -INFINITY ? 0.0f : mnew;
+    m_run = mnew;
+    l_run *= alpha;
+    /* hd <= 64 (mma.sync): O is rescaled, then the block's P V accumulates into it; hd 128 (tcgen05):
+     * the block's P V is a fresh f32 tile Ob and O = fma(O, alpha, Ob) (attn_tc.cu accumulate) */
+    float ob[128];
+    for (int j = 0; j < hd; ++j) {
+      if (KB == 64) ob[j] = 0.0f;
+      else o[j] *= alpha;
+    }
+    float* acc = KB == 64 ? ob : o;
+    for (int t = 0; t < nk; ++t) {
+      const float pv = exp2f(fmaf(s[t], scale_log2, -msub));
+      l_run += pv;
+      const float pb = bf16r(pv);
+      if (pb == 0.0f) continue;
+      const float* vr = v0 + (size_t)(key0 + t) * ld;
+      for (int j = 0; j < hd; ++j) acc[j] = fmaf(pb, vr[j], acc[j]);
+    }
+    if (KB == 64)
+      for (int j = 0; j < hd; ++j) o[j] = fmaf(o[j], alpha, ob[j]);
+  }
+  const float inv = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+  for (int j = 0; j < hd; ++j) zh[j] = bf16r(o[j] * inv);
+}
+
 typedef struct {
   float** k; /* per layer [S x kh] */
   float** v;
@@ -326,6 +392,13 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
     for (int i = 0; i < n; ++i) {
       if (valid && !valid[i]) continue;
       const int span = p0 + i + 1;
+      if (m->act_quant && m->gpu_points) {
+        for (int hh = 0; hh < m->heads[l]; ++hh)
+          flash_head_gpu(q + (size_t)i * kh + (size_t)hh * hd, st->k[l] + (size_t)hh * hd,
+                         st->v[l] + (size_t)hh * hd, kh, hd, span, st->valid, z + (size_t)i * kh + (size_t)hh * hd);
+        *madds += 2ull * span * hd * m->heads[l];
+        continue;
+      }
       for (int hh = 0; hh < m->heads[l]; ++hh) {
         const float* qh = q + (size_t)i * kh + (size_t)hh * hd;
         for (int s = 0; s < span; ++s) {
@@ -371,7 +444,10 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
     if (m->act_quant) linear_w8a8(m, l * 6 + 4, h, n, d, f, g);
     else matmul_wt(h, n, d, m->w_in[l], f, g);
     *madds += (uint64_t)n * d * f;
-    for (size_t t = 0; t < (size_t)n * f; ++t) g[t] = gelu(g[t]);
+    if (m->act_quant && m->gpu_points)
+      for (size_t t = 0; t < (size_t)n * f; ++t) g[t] = gelu_gpu(g[t]);
+    else
+      for (size_t t = 0; t < (size_t)n * f; ++t) g[t] = gelu(g[t]);
     if (m->act_quant && m->gpu_points) bf16r_rows(g, (size_t)n * f);
     if (m->act_quant) linear_w8a8(m, l * 6 + 5, g, n, f, d, ao);
     else matmul_wt(g, n, f, m->w_out[l], d, ao);

@@ -65,6 +65,9 @@ class Stats(C.Structure):
 SIGNATURES = {
     "iolm_cuda_create": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.POINTER(Opts), C.POINTER(C.c_void_p)]),
     "iolm_cuda_destroy": (None, [C.c_void_p]),
+    "iolm_cuda_create_multi": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_int32, C.POINTER(Opts),
+                                         C.POINTER(C.c_void_p)]),
+    "iolm_cuda_device_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "iolm_cuda_save_image": (C.c_int, [C.c_void_p, C.c_char_p]),
     "iolm_cuda_create_from_image": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(Opts),
                                               C.POINTER(C.c_void_p)]),
@@ -98,6 +101,7 @@ SIGNATURES = {
                                             C.c_void_p, C.c_void_p, C.c_void_p]),
     "iolm_cuda_debug_gemm_w4": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                           C.c_int32]),
+    "iolm_cuda_debug_partition": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]),
     "iolm_cuda_debug_gemm_sp24_time": (C.c_int, [C.c_int32] * 5 + [C.POINTER(C.c_float)]),
 }
 

@@ -1482,9 +1482,101 @@ void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logi
 using iolmh::Engine;
 using iolmh::guarded;
 
+// A context is one Engine per device. One device: the plain runtime. Several (iolm_cuda_create_multi):
+// every Engine holds a full replica and its own KV pool; batch_decode range-partitions the rows over
+// them (SURVEY §8e / BASELINE north_star: rows are independent, exec.cpp:139-142), one host thread
+// per device, each writing its rows' generated ids straight into the caller's output buffers - that
+// write IS the output-column gather; no collective and no device-to-device traffic. Single-sequence
+// calls (forward, capture, codes, image) run on the first device.
 struct iolm_cuda_ctx {
-  std::unique_ptr<Engine> eng;
+  std::unique_ptr<Engine> eng;                 // == shards[0].get() owner for the first device
+  std::vector<std::unique_ptr<Engine>> extra;  // devices 1..n-1
+  iolm_cuda_stats agg{};                       // last multi-device decode, summed over shards
+  bool multi_last = false;
+  int n_shards() const { return 1 + static_cast<int>(extra.size()); }
+  Engine& shard(int i) const { return i == 0 ? *eng : *extra[i - 1]; }
 };
+
+namespace iolmh {
+// Contiguous row ranges [cut[i], cut[i+1]) with near-equal token counts (prefill dominates a row's
+// cost; every row then generates the same budget), at most one shard per row.
+std::vector<int64_t> partition_rows(const int64_t* offsets, int64_t n_rows, int shards) {
+  std::vector<int64_t> cut{0};
+  const int s = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(shards, n_rows)));
+  const double total = static_cast<double>(offsets[n_rows] - offsets[0]);
+  int64_t r = 0;
+  for (int i = 1; i < s; ++i) {
+    const double target = total * i / s;
+    while (r < n_rows && static_cast<double>(offsets[r] - offsets[0]) < target) ++r;
+    r = std::max<int64_t>(r, cut.back() + 1);  // non-empty shard
+    r = std::min<int64_t>(r, n_rows - (s - i));  // leave >= 1 row per remaining shard
+    cut.push_back(r);
+  }
+  cut.push_back(n_rows);
+  return cut;
+}
+
+// batch_decode over every shard of ctx (host ids). Lengths are checked for the WHOLE batch first, in
+// row order, so SequenceTooLong names the first offending row exactly as runtime.cpp:264-267 does;
+// any other shard failure is re-thrown from the lowest failing shard (the earliest rows).
+void multi_decode(iolm_cuda_ctx& ctx, const int32_t* ids, bool on_device, const int64_t* offsets, int64_t n_rows,
+                  int max_new, int32_t* out_ids, int32_t* out_len, uint64_t* madds, int64_t* bad_row) {
+  if (bad_row) *bad_row = -1;
+  if (n_rows <= 0) throw ContractViolation("batch_decode: batch size must be >= 1");
+  if (max_new < 0) throw ContractViolation("batch_decode: max_new_tokens must be >= 0");
+  if (!offsets || !out_len || (max_new > 0 && !out_ids)) throw ContractViolation("batch_decode: null buffer");
+  if (on_device) throw Unsupported("multi-device context: device-resident ids are per device; pass host ids");
+  const int S = ctx.eng->config().max_seq_len;
+  for (int64_t i = 0; i < n_rows; ++i) {
+    const int64_t len = offsets[i + 1] - offsets[i];
+    if (len <= 0) throw ContractViolation("batch_decode: empty token row " + std::to_string(i));
+    if (len > S) {
+      if (bad_row) *bad_row = i;
+      throw SequenceTooLong("batch_decode: prompt " + std::to_string(i) + " needs " + std::to_string(len) +
+                            " tokens, max_seq_len is " + std::to_string(S));
+    }
+  }
+  const std::vector<int64_t> cut = partition_rows(offsets, n_rows, ctx.n_shards());
+  const int used = static_cast<int>(cut.size()) - 1;
+  std::vector<uint64_t> m(used, 0);
+  std::vector<std::exception_ptr> err(used);
+  auto run = [&](int i) {
+    try {
+      Engine& e = ctx.shard(i);
+      std::lock_guard<std::mutex> lk(e.mu);
+      int64_t bad = -1;
+      e.decode(ids, false, offsets + cut[i], cut[i + 1] - cut[i], max_new,
+               max_new > 0 ? out_ids + static_cast<size_t>(cut[i]) * max_new : out_ids, out_len + cut[i], &m[i], &bad);
+    } catch (...) {
+      err[i] = std::current_exception();
+    }
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < used; ++i) th.emplace_back(run, i);
+  run(0);
+  for (auto& t : th) t.join();
+  for (int i = 0; i < used; ++i)
+    if (err[i]) std::rethrow_exception(err[i]);
+  iolm_cuda_stats a{};
+  for (int i = 0; i < used; ++i) {
+    const iolm_cuda_stats& s = ctx.shard(i).stats();
+    a.steps += s.steps;
+    a.tokens += s.tokens;
+    a.prefill_tokens += s.prefill_tokens;
+    a.decode_tokens += s.decode_tokens;
+    a.prefix_tokens += s.prefix_tokens;
+    a.kernel_launches += s.kernel_launches;
+    a.device_ms = std::max(a.device_ms, s.device_ms);  // shards run concurrently
+  }
+  ctx.agg = a;
+  ctx.multi_last = true;
+  if (madds) {
+    uint64_t t = 0;
+    for (uint64_t x : m) t += x;
+    *madds = t;
+  }
+}
+}  // namespace iolmh
 
 extern "C" int iolm_cuda_create(const uint8_t* bundle_bytes, size_t len, int device, const iolm_cuda_opts* opts,
                                 iolm_cuda_ctx** out) {
@@ -1494,6 +1586,50 @@ extern "C" int iolm_cuda_create(const uint8_t* bundle_bytes, size_t len, int dev
     auto ctx = std::make_unique<iolm_cuda_ctx>();
     ctx->eng = std::make_unique<Engine>(bundle_bytes, len, device, opts);
     *out = ctx.release();
+  });
+}
+
+extern "C" int iolm_cuda_create_multi(const uint8_t* bundle_bytes, size_t len, const int32_t* devices,
+                                      int32_t n_devices, const iolm_cuda_opts* opts, iolm_cuda_ctx** out) {
+  return guarded([&] {
+    if (!out || !devices || n_devices < 1) throw iolmh::ContractViolation("iolm_cuda_create_multi: bad arguments");
+    *out = nullptr;
+    auto ctx = std::make_unique<iolm_cuda_ctx>();
+    std::vector<std::unique_ptr<Engine>> engs(n_devices);
+    std::vector<std::exception_ptr> err(n_devices);
+    std::vector<std::thread> th;  // weights decode / upload on every device at once
+    for (int i = 0; i < n_devices; ++i)
+      th.emplace_back([&, i] {
+        try {
+          engs[i] = std::make_unique<Engine>(bundle_bytes, len, devices[i], opts);
+        } catch (...) {
+          err[i] = std::current_exception();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int i = 0; i < n_devices; ++i)
+      if (err[i]) std::rethrow_exception(err[i]);
+    ctx->eng = std::move(engs[0]);
+    for (int i = 1; i < n_devices; ++i) ctx->extra.push_back(std::move(engs[i]));
+    *out = ctx.release();
+  });
+}
+
+extern "C" int iolm_cuda_device_count(const iolm_cuda_ctx* ctx, int32_t* n) {
+  return guarded([&] {
+    if (!ctx || !n) throw iolmh::ContractViolation("null argument");
+    *n = ctx->n_shards();
+  });
+}
+
+extern "C" int iolm_cuda_debug_partition(const int64_t* row_offsets, int64_t n_rows, int32_t shards, int64_t* cut,
+                                         int32_t* n_cut) {
+  return guarded([&] {
+    if (!row_offsets || !cut || !n_cut || n_rows <= 0 || shards < 1)
+      throw iolmh::ContractViolation("debug_partition: bad arguments");
+    const auto c = iolmh::partition_rows(row_offsets, n_rows, shards);
+    *n_cut = static_cast<int32_t>(c.size());
+    for (size_t i = 0; i < c.size(); ++i) cut[i] = c[i];
   });
 }
 
@@ -1575,6 +1711,11 @@ extern "C" int iolm_cuda_decode(iolm_cuda_ctx* ctx, const int32_t* ids, const in
                                 int64_t* bad_row) {
   return guarded([&] {
     if (!ctx) throw iolmh::ContractViolation("null context");
+    if (ctx->n_shards() > 1) {
+      iolmh::multi_decode(*ctx, ids, false, row_offsets, n_rows, max_new_tokens, out_ids, out_len, madds, bad_row);
+      return;
+    }
+    ctx->multi_last = false;
     std::lock_guard<std::mutex> lock(ctx->eng->mu);
     ctx->eng->decode(ids, false, row_offsets, n_rows, max_new_tokens, out_ids, out_len, madds, bad_row);
   });
@@ -1585,6 +1726,11 @@ extern "C" int iolm_cuda_decode_device_ids(iolm_cuda_ctx* ctx, const int32_t* d_
                                            int32_t* out_len, uint64_t* madds, int64_t* bad_row) {
   return guarded([&] {
     if (!ctx) throw iolmh::ContractViolation("null context");
+    if (ctx->n_shards() > 1) {
+      iolmh::multi_decode(*ctx, d_ids, true, row_offsets, n_rows, max_new_tokens, out_ids, out_len, madds, bad_row);
+      return;
+    }
+    ctx->multi_last = false;
     std::lock_guard<std::mutex> lock(ctx->eng->mu);
     ctx->eng->decode(d_ids, true, row_offsets, n_rows, max_new_tokens, out_ids, out_len, madds, bad_row);
   });
@@ -1595,6 +1741,7 @@ extern "C" int iolm_cuda_forward_logits(iolm_cuda_ctx* ctx, const int32_t* ids, 
   return guarded([&] {
     if (!ctx || !logits) throw iolmh::ContractViolation("null argument");
     std::lock_guard<std::mutex> lock(ctx->eng->mu);
+    ctx->multi_last = false;
     ctx->eng->forward(ids, mask, n, logits, madds);
   });
 }
@@ -1602,15 +1749,17 @@ extern "C" int iolm_cuda_forward_logits(iolm_cuda_ctx* ctx, const int32_t* ids, 
 extern "C" int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* out) {
   return guarded([&] {
     if (!ctx || !out) throw iolmh::ContractViolation("null argument");
-    *out = ctx->eng->stats();
+    *out = ctx->multi_last ? ctx->agg : ctx->eng->stats();
   });
 }
 
 extern "C" int iolm_cuda_set_kernel_timing(iolm_cuda_ctx* ctx, int32_t on) {
   return guarded([&] {
     if (!ctx) throw iolmh::ContractViolation("null argument");
-    std::lock_guard<std::mutex> lk(ctx->eng->mu);
-    ctx->eng->set_kernel_timing(on != 0);
+    for (int i = 0; i < ctx->n_shards(); ++i) {
+      std::lock_guard<std::mutex> lk(ctx->shard(i).mu);
+      ctx->shard(i).set_kernel_timing(on != 0);
+    }
   });
 }
 
@@ -1619,6 +1768,7 @@ extern "C" int iolm_cuda_forward_capture(iolm_cuda_ctx* ctx, const int32_t* ids,
   return guarded([&] {
     if (!ctx || !logits || !capture) throw iolmh::ContractViolation("null argument");
     std::lock_guard<std::mutex> lock(ctx->eng->mu);
+    ctx->multi_last = false;
     ctx->eng->forward(ids, mask, n, logits, madds, capture);
   });
 }
@@ -1628,6 +1778,7 @@ extern "C" int iolm_cuda_forward_codes(iolm_cuda_ctx* ctx, const int32_t* ids, i
   return guarded([&] {
     if (!ctx || !logits || !codes || !scales) throw iolmh::ContractViolation("null argument");
     std::lock_guard<std::mutex> lock(ctx->eng->mu);
+    ctx->multi_last = false;
     ctx->eng->forward(ids, nullptr, n, logits, madds, nullptr, codes, scales);
   });
 }
@@ -1637,10 +1788,14 @@ extern "C" int iolm_cuda_kernel_times(const iolm_cuda_ctx* ctx, double* ms, doub
   return guarded([&] {
     if (!ctx || !ms || !work || !launches) throw iolmh::ContractViolation("null argument");
     if (n < IOLM_KCLASSES) throw iolmh::ContractViolation("kernel_times: array too small");
-    for (int i = 0; i < IOLM_KCLASSES; ++i) {
-      ms[i] = ctx->eng->kms_[i];
-      work[i] = ctx->eng->kwork_[i];
-      launches[i] = ctx->eng->kcount_[i];
+    for (int i = 0; i < IOLM_KCLASSES; ++i) {  // summed over the shards of the last decode
+      ms[i] = work[i] = 0;
+      launches[i] = 0;
+      for (int k = 0; k < (ctx->multi_last ? ctx->n_shards() : 1); ++k) {
+        ms[i] += ctx->shard(k).kms_[i];
+        work[i] += ctx->shard(k).kwork_[i];
+        launches[i] += ctx->shard(k).kcount_[i];
+      }
     }
   });
 }

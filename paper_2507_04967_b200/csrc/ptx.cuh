@@ -302,14 +302,28 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return y;
 }
 
-// Reference: 0.5*x*(1+tanh(0.7978845608028654*(x+0.044715*x^3))) (numerics.cpp:179-184), evaluated
-// as hx + hx*tanh(x*(k + k*0.044715*x^2)) with hx = 0.5x (5 FP ops + one SFU tanh). The SFU tanh
-// (max rel. error ~2^-11) is below the bf16 rounding (2^-9) the result is stored with.
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Reference: 0.5*x*(1+tanh(u)), u = 0.7978845608028654*(x+0.044715*x^3) (numerics.cpp:179-184).
+// Evaluated as the identical x * sigmoid(2u) = x / (1 + 2^(-2u*log2(e))): one ex2.approx (rel. error
+// ~2^-22) and one rcp.approx (<= 1 ulp), so the result is within a few f32 ulps of the reference's.
+// (The SFU tanh.approx, max rel. error 2^-11, moved ~1 in 4 bf16 roundings of the output and, in
+// W8A8, its int8 codes: oracle/iolm_oracle.c gelu_gpu restates this form exactly.)
 __device__ __forceinline__ float gelu_tanh(float x) {
   constexpr float k = 0.7978845608028654f, k3 = 0.7978845608028654f * 0.044715f;
+  constexpr float m2l2e = -2.0f * 1.4426950408889634f;
   const float inner = x * fmaf(x * x, k3, k);
-  const float hx = 0.5f * x;
-  return fmaf(hx, tanh_fast(inner), hx);
+  return x * rcp_ftz(1.0f + ex2_ftz(inner * m2l2e));
 }
 
 }  // namespace iolmk

@@ -166,9 +166,11 @@ def image_header(path) -> dict:
 
 # --------------------------------------------------------------------------- runtime
 class ModelRuntime:
-    """iolm::ModelRuntime on a B200. `bundle` is the serialize_bundle byte stream."""
+    """iolm::ModelRuntime on a B200. `bundle` is the serialize_bundle byte stream. `device` is one GPU
+    index, or a list of them: one context over several GPUs (iolm_cuda_create_multi), whose
+    batch_decode range-partitions the rows over full per-GPU replicas."""
 
-    def __init__(self, bundle: bytes, device: int = 0, max_tokens_per_step: int = 0, max_slots: int = 0,
+    def __init__(self, bundle: bytes, device=0, max_tokens_per_step: int = 0, max_slots: int = 0,
                  prefix_sharing: bool = True, act_quant: bool = False, kernel_timing: bool = False,
                  sparse_mma: bool = True, int4_mma: bool = True, prefill_tc: bool | None = None):
         self._lib = _lib.load()
@@ -176,7 +178,11 @@ class ModelRuntime:
                           int4_mma, prefill_tc)
         h = C.c_void_p()
         buf = (C.c_char * len(bundle)).from_buffer_copy(bundle)
-        _check(self._lib.iolm_cuda_create(buf, len(bundle), device, C.byref(opts), C.byref(h)))
+        if isinstance(device, (list, tuple)):
+            devs = (C.c_int32 * len(device))(*device)
+            _check(self._lib.iolm_cuda_create_multi(buf, len(bundle), devs, len(device), C.byref(opts), C.byref(h)))
+        else:
+            _check(self._lib.iolm_cuda_create(buf, len(bundle), device, C.byref(opts), C.byref(h)))
         self._h = h
         hl = int.from_bytes(bundle[6:10], "little")
         self._config = ModelConfig(**json.loads(bundle[10:10 + hl].decode())["config"])
@@ -229,6 +235,11 @@ class ModelRuntime:
 
     def config(self) -> ModelConfig:
         return self._config
+
+    def device_count(self) -> int:
+        v = C.c_int32()
+        _check(self._lib.iolm_cuda_device_count(self._h, C.byref(v)))
+        return v.value
 
     def bundle_hash(self) -> int:
         v = C.c_uint64()

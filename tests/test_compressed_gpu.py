@@ -6,11 +6,11 @@
   <= 1e-2, >= 99% greedy agreement with every divergence on a near-tie.
 * W8A8 (act_quant): per-token int8 activations x int8 codes through tcgen05 kind::i8. The reference
   has no activation quantization, so the checker is the W8A8 restatement in
-  oracle/iolm_oracle.c (same quantization rule, exact int32 accumulation). Stated tolerance:
-  logits rel-L2 <= 2.5e-2 (W8A8_REL_TOL) - the GPU quantizes bf16-rounded attention/GELU outputs
-  and an int8 code flips whenever an upstream bf16 difference crosses a rounding boundary; the
-  integer GEMM itself is bit-exact (tests/test_gemm_gpu.py::test_gemm_s8_bitexact).
-  Agreement with the f32 reference is reported, not asserted beyond a loose floor.
+  oracle/iolm_oracle.c at the GPU engine's rounding points (gpu_points: bf16 q/K/V, block-wise
+  bf16-P attention, bf16 GELU output before quantization): logits rel-L2 <= 1e-2 on the toy model,
+  >= 99% greedy agreement with every divergence an fp near-tie (tests/parity.py). The integer GEMM
+  itself is bit-exact (tests/test_gemm_gpu.py) and the operand codes are compared element by element
+  in tests/test_w8a8_codes_gpu.py. Agreement with the f32 reference is reported, not asserted.
 * Structurally pruned shapes (irregular heads per layer and FFN widths, ModelConfig allows any
   active_ffn in [1, d_ff], model.cpp:44-55)."""
 import numpy as np
@@ -19,37 +19,26 @@ import pytest
 from oracle import oracle as O
 from paper_2507_04967_b200 import runtime as R
 from paper_2507_04967_b200 import synth
+from parity import check_agreement
 
 pytestmark = pytest.mark.gpu
 TOY = (128, 4, 4, 512, 160)
-TIE_GAP = 0.05
-W8A8_REL_TOL = 2.5e-2
+W8A8_REL_TOL = 1e-2
 
 
 def rel_l2_rows(a, b):
     return np.linalg.norm(a - b, axis=1) / np.maximum(np.linalg.norm(b, axis=1), 1e-30)
 
 
-def top2_gap(om, prompt_ids, ref_ids, k):
-    seq = list(prompt_ids) + list(ref_ids[:k])
-    lg, _ = om.forward(np.array(seq, np.int32))
-    last = np.sort(lg[-1])
-    return float(last[-1] - last[-2])
-
-
-def check_decode(rt, om, n=48, min_agree=0.99):
-    ids, offs = synth.rows(0, n, 64)
+def check_decode(rt, om, n=48, first_row=0):
+    """>= 99% of n rows identical to the oracle (ids, lengths, madds), every other one a near-tie."""
+    ids, offs = synth.rows(first_row, n, 64)
     gi, gl, gm = rt.decode_token_rows(ids, offs, 8)
     oi, ol, omadds = om.decode_ids(ids, offs, 8, threads=8)
-    assert gm == omadds
-    bad = [i for i in range(n) if gl[i] != ol[i] or not np.array_equal(gi[i, :gl[i]], oi[i, :ol[i]])]
-    assert len(bad) <= max(1, int(n * (1 - min_agree))), bad
-    for i in bad:
-        k = 0
-        while k < min(gl[i], ol[i]) and gi[i, k] == oi[i, k]:
-            k += 1
-        assert top2_gap(om, ids[offs[i]:offs[i + 1]], oi[i], k) < TIE_GAP
-    return n - len(bad)
+    div = check_agreement(om, ids, offs, gi, gl, oi, ol)
+    if not div:
+        assert gm == omadds
+    return n - len(div)
 
 
 @pytest.mark.parametrize("quant", ["q8", "q4", "sparse24"])
@@ -68,20 +57,19 @@ def test_weight_only_quantized(quant):
 def test_w8a8_against_restatement(quant):
     b = synth.toy_bundle(*TOY, seed=42, quant=quant)
     rt = R.ModelRuntime(b, act_quant=True)
-    oq, of = O.OracleModel(b, act_quant=True), O.OracleModel(b)
+    oq, of = O.OracleModel(b, act_quant=True, gpu_points=True), O.OracleModel(b)
     ids, offs = synth.rows(300, 2, 64)
     for r in range(2):
         row = ids[offs[r]:offs[r + 1]]
         got = rt.forward(row)
         assert rel_l2_rows(got, oq.forward(row)[0]).max() <= W8A8_REL_TOL
-    agree_q = check_decode(rt, oq, min_agree=0.95)
+    agree_q = check_decode(rt, oq, n=96)
     # versus the reference's f32 semantics (dequantized weights, f32 activations): reported
     ids, offs = synth.rows(0, 48, 64)
     gi, gl, _ = rt.decode_token_rows(ids, offs, 8)
     fi, fl, _ = of.decode_ids(ids, offs, 8, threads=8)
     agree_f = sum(gl[i] == fl[i] and np.array_equal(gi[i, :gl[i]], fi[i, :fl[i]]) for i in range(48))
-    print(f"W8A8 {quant}: {agree_q}/48 vs W8A8 restatement, {agree_f}/48 vs f32 reference")
-    assert agree_f >= 40
+    print(f"W8A8 {quant}: {agree_q}/96 vs W8A8 restatement, {agree_f}/48 vs f32 reference (reported)")
 
 
 def test_w8a8_batch_invariance():
@@ -137,22 +125,23 @@ def test_reference_pruned_sparse24_bundle():
     assert c.total() == rm
     assert sum(a == b for a, b in zip(got, want)) >= 31
     rq = R.ModelRuntime(b, act_quant=True)
-    oq = O.OracleModel(b, act_quant=True)
+    oq = O.OracleModel(b, act_quant=True, gpu_points=True)
     assert rel_l2_rows(rq.forward(row), oq.forward(row)[0]).max() <= W8A8_REL_TOL
 
 
 def test_w8a8_wide_rows_d2048():
     """d_model 2048 (C4 width): the two-warp LayerNorm with int8 output feeds kind::i8 GEMMs;
-    checked against the W8A8 restatement. Stated tolerance for this width: per position rel-L2
-    <= 3e-2 and mean <= 2e-2 - one per-token scale spans 2048 channels, so each int8 step is coarser
-    and a code flip caused by the GPU's bf16 attention (vs the restatement's f32) moves more."""
+    checked against the GPU-rounding-point W8A8 restatement. Stated tolerance for this width: per
+    position rel-L2 <= 2.5e-2 and mean <= 1.2e-2 - one per-token scale spans 2048 channels, so a
+    single flipped code (an f32 summation-order difference crossing a rounding boundary) moves the
+    token's amax, its scale and so all of its codes (tests/test_w8a8_codes_gpu.py)."""
     b = synth.toy_bundle(2048, 1, 16, 2048, 160, seed=42, quant="q8")
-    rt, oq = R.ModelRuntime(b, act_quant=True), O.OracleModel(b, act_quant=True)
+    rt, oq = R.ModelRuntime(b, act_quant=True), O.OracleModel(b, act_quant=True, gpu_points=True)
     ids, offs = synth.rows(77, 2, 64)
     for r in range(2):
         row = ids[offs[r]:offs[r + 1]]
         rel = rel_l2_rows(rt.forward(row), oq.forward(row)[0])
-        assert rel.max() <= 3e-2 and rel.mean() <= 2e-2, (rel.max(), rel.mean())
+        assert rel.max() <= 2.5e-2 and rel.mean() <= 1.2e-2, (rel.max(), rel.mean())
 
 
 def test_decode_head_groupings():
@@ -160,4 +149,4 @@ def test_decode_head_groupings():
     10 -> 5 CTAs of 2 heads, 14 -> 7 x 2, 7 -> 4 + 3 (partial last group), 16 -> 4 x 4."""
     b = synth.toy_bundle(1024, 4, 16, 1024, 160, seed=5, quant="dense", heads=[10, 14, 7, 16], ffn=[1024] * 4)
     rt, om = R.ModelRuntime(b), O.OracleModel(b)
-    assert check_decode(rt, om, n=16) >= 15
+    check_decode(rt, om, n=32)
