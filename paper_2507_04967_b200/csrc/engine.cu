@@ -406,6 +406,7 @@ class Engine {
   void upload_weights(const BundleView& b);
   void alloc_runtime();
   void set_prefix_pages(int prefix_pages);
+  void setup_l2_persistence();
   void add_prefill(Step& s, int slot, int64_t src_base, int p_begin, int p_end, bool want_head,
                    int64_t owner) const;
   void launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d_key_mask, float* d_logits);
@@ -758,6 +759,35 @@ void Engine::upload_weights(const BundleView& b) {
   CUDA_OK(cudaStreamSynchronize(stream_));
 }
 
+// L2 residency of the fp32 residual stream x (T x d): every layer reads it in two LayerNorms and
+// read-modify-writes it in two residual GEMM epilogues, so keeping it in the 126 MB L2 turns those
+// passes from HBM- into L2-bandwidth work. An access-policy window on the engine stream marks x's
+// lines persisting (hitRatio = the persisting set-aside / window when x does not fit).
+// IOLM_L2_PERSIST=<MB of set-aside> (0: off) - A/B switch, see DESIGN.md.
+void Engine::setup_l2_persistence() {
+  const char* e = std::getenv("IOLM_L2_PERSIST");
+  if (!e) return;
+  const double mb = std::atof(e);
+  if (mb <= 0) return;
+  int maxp = 0, maxw = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device_));
+  CUDA_OK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device_));
+  const size_t xb = static_cast<size_t>(T_max_) * d_ * sizeof(float);
+  const size_t win = std::min<size_t>(xb, static_cast<size_t>(maxw));
+  const size_t persist = std::min<size_t>(static_cast<size_t>(mb * 1048576.0), static_cast<size_t>(maxp));
+  CUDA_OK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = x_.p;
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(persist) / win));
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  CUDA_OK(cudaStreamSetAttribute(stream_, cudaStreamAttributeAccessPolicyWindow, &v));
+  if (std::getenv("IOLM_L2_VERBOSE"))
+    std::fprintf(stderr, "L2 persist: max set-aside %d B, max window %d B, x %zu B, window %zu, set-aside %zu, hit %.3f\n",
+                 maxp, maxw, xb, win, persist, v.accessPolicyWindow.hitRatio);
+}
+
 // Decodes the tensors of one GEMM (stacked along N, e.g. wq|wk|wv) into the chosen weight form.
 void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<std::string>& names, int K,
                                int ld) {
@@ -846,6 +876,7 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
 void Engine::alloc_runtime() {
   const size_t T = T_max_;
   x_.alloc(T * d_);
+  setup_l2_persistence();
   h_.alloc(T * d_);
   q_.alloc(T * kh_max_);
   z_.alloc(T * kh_max_);

@@ -218,7 +218,7 @@ __device__ __forceinline__ int swz(int r, int g) { return r * 32 + ((g ^ (r & 7)
 template <int EPI>
 __device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* tile, int m_base, int n0, float (&v)[32],
                                                    int lane, const QkvRow* rows = nullptr,
-                                                   const CUtensorMap* tmC = nullptr) {
+                                                   const CUtensorMap* tmC = nullptr, uint32_t* seq = nullptr) {
   const int rr = lane >> 3, gg = lane & 7;  // coalesced phase: row rr + 4i, column group gg
   if constexpr (EPI == EPI_GELU_BF16) {
 #pragma unroll
@@ -226,8 +226,15 @@ __device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* til
   }
   if constexpr (EPI == EPI_RESID_F32 || EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
     if (ep.tma_out) {
-      // the tile may still be the source of this warp's previous bulk store
-      if (lane == 0) bulk_wait_read0();
+      if constexpr (EPI != EPI_RESID_F32) {
+        // bf16 boxes are 2 KB: the warp's 4 KB tile holds two, used alternately, so writing this
+        // chunk only waits for the store issued two chunks ago (not the previous one) to be read
+        tile += ((*seq)++ & 1u) * 512;
+        if (lane == 0) bulk_wait_read1();
+      } else {
+        // the tile may still be the source of this warp's previous bulk store
+        if (lane == 0) bulk_wait_read0();
+      }
       __syncwarp();
       if constexpr (EPI == EPI_RESID_F32) {
         // fp32 32 x 32 box in the SWIZZLE_128B layout (16-byte chunk g of row r at g ^ (r & 7)):
@@ -530,6 +537,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
     float* s_tile = reinterpret_cast<float*>(s_warp);                 // 32 x 32 fp32 (4 KB)
     QkvRow* s_rows = reinterpret_cast<QkvRow*>(s_warp + 4096);        // the warp's 32 row destinations
     const bool has_ws = ep.w_scale != nullptr;
+    uint32_t store_seq = 0;  // bulk stores issued by this warp (staging half selection)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = group; tile < num_tiles; tile += n_groups) {
@@ -595,7 +603,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rc[j]);
             }
-            warp_tile_epilogue<EPI>(ep, s_tile, m_base, n0, v, lane, s_rows, &tmC);
+            warp_tile_epilogue<EPI>(ep, s_tile, m_base, n0, v, lane, s_rows, &tmC, &store_seq);
             continue;
           }
         }
