@@ -189,6 +189,16 @@ int iolm_cuda_create_from_image(const char* path, uint64_t expected_hash, int de
                                 const iolm_cuda_opts* opts, iolm_cuda_ctx** out);
 int iolm_cuda_image_info(const char* path, uint64_t* bundle_hash, iolm_cuda_model_config* cfg);
 
+/*
+ * Calibration Gram matrix (the GPTQ / compensated-2:4 Hessian): h[cols x cols] =
+ * scale * X^T X in f64 for X = x[rows x cols] f32 row-major (host buffers; device work on `device`).
+ * Replaces fastmath::gram_accumulate under build_hessian (proj/src/calib.cpp:64-74,
+ * proj/src/fastmath.cpp:79-100): every element is the same sequential f64 sum over samples in the
+ * same order of exact f32 x f32 products, so h is BIT-IDENTICAL to the reference's. The shim's
+ * iolm::cuda::build_hessian adds the damping exactly as the reference does.
+ */
+int iolm_cuda_gram(int device, const float* x, int64_t rows, int32_t cols, double scale, double* h);
+
 /* Counters of the last decode/forward call on this context. */
 int iolm_cuda_last_stats(const iolm_cuda_ctx* ctx, iolm_cuda_stats* out);
 

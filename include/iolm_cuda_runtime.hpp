@@ -349,4 +349,26 @@ class ModelRuntime {
   Config cfg_{};
 };
 
+#ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
+// build_hessian (proj/src/calib.cpp:64-74) with the Gram matrix on the GPU (iolm_cuda_gram): H =
+// 2 X^T X + lambda I, lambda = lambda_rel * mean(diag(2 X^T X)) - bit-identical to the reference's.
+inline iolm::MatrixD build_hessian(const iolm::Matrix& x, double lambda_rel, int device = 0) {
+  if (x.rows < 1) throw iolm::EmptyCalibration("build_hessian: no calibration samples");
+  iolm::MatrixD h(x.cols, x.cols);
+  check(iolm_cuda_gram(device, x.data.data(), x.rows, x.cols, 2.0, h.data.data()));
+  double diag_mean = 0.0;
+  for (int i = 0; i < h.rows; ++i) diag_mean += h.at(i, i);
+  diag_mean /= h.rows;
+  const double lambda = lambda_rel * diag_mean;
+  for (int i = 0; i < h.rows; ++i) h.at(i, i) += lambda;
+  return h;
+}
+
+// The device the reference-side patch uses for calibration work: the first of IOLM_CUDA_DEVICE, or -1.
+inline int env_device() {
+  const char* dev = std::getenv("IOLM_CUDA_DEVICE");
+  return dev && *dev ? std::atoi(dev) : -1;
+}
+#endif
+
 }  // namespace iolm::cuda

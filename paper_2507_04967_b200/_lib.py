@@ -87,6 +87,7 @@ SIGNATURES = {
                                             C.POINTER(C.c_uint64)]),
     "iolm_cuda_forward_codes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.POINTER(C.c_uint64)]),
+    "iolm_cuda_gram": (C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_void_p]),
     "iolm_cuda_last_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
     "iolm_cuda_last_error": (C.c_char_p, []),
     "iolm_cuda_set_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),

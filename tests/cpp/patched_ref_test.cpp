@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <set>
 #include <string>
 #include <vector>
@@ -289,6 +290,38 @@ int main() {
     }
     std::printf("capture_calibration: %zu points, worst rel-L2 %.3e\n", a.inputs.size(), worst);
     EXPECT(worst <= 1e-2, "capture rel-L2 <= 1e-2");
+  }
+
+  // build_hessian (calib.cpp:64-74) with IOLM_CUDA_DEVICE set: the Gram matrix runs on the GPU and
+  // must be BIT-identical; so GPTQ (quant.cpp:51) through apply_recipe yields the identical bundle
+  {
+    std::vector<std::string> cal(prompts.begin(), prompts.begin() + 32);
+    iolm::Rng r1(5);
+    const iolm::CalibrationSet calib = iolm::capture_calibration(cpu, cal, 32, r1);
+    size_t checked = 0, identical = 0;
+    for (const auto& [point, m] : calib.inputs) {
+      unsetenv("IOLM_CUDA_DEVICE");
+      const iolm::MatrixD hc = iolm::build_hessian(m, 0.01);
+      setenv("IOLM_CUDA_DEVICE", "0", 1);
+      const iolm::MatrixD hg = iolm::build_hessian(m, 0.01);
+      unsetenv("IOLM_CUDA_DEVICE");
+      ++checked;
+      identical += hc.rows == hg.rows && hc.cols == hg.cols &&
+                   std::memcmp(hc.data.data(), hg.data.data(), hc.data.size() * sizeof(double)) == 0;
+    }
+    std::printf("build_hessian on the GPU: %zu/%zu capture points bit-identical (%d x %d samples x features at attn_in)\n",
+                identical, checked, calib.inputs.begin()->second.rows, calib.inputs.begin()->second.cols);
+    EXPECT(checked > 0 && identical == checked, "build_hessian bit-identical");
+    iolm::CompressionRecipe gptq;
+    gptq.quantize = iolm::CompressionRecipe::QuantizeStep{8, iolm::CompressionRecipe::QuantizeStep::Method::gptq};
+    unsetenv("IOLM_CUDA_DEVICE");
+    const auto bc = iolm::apply_recipe(bundle, gptq, calib);
+    setenv("IOLM_CUDA_DEVICE", "0", 1);
+    const auto bg = iolm::apply_recipe(bundle, gptq, calib);
+    unsetenv("IOLM_CUDA_DEVICE");
+    std::printf("apply_recipe(gptq 8-bit) with the GPU Hessian: bundle hash %s\n",
+                bc.hash() == bg.hash() ? "identical" : "DIFFERENT");
+    EXPECT(bc.hash() == bg.hash(), "GPTQ bundle identical with the GPU Hessian");
   }
 
   // validate(candidate, baseline): an 8-bit RTN candidate against the baseline, both on the GPU

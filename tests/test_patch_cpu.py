@@ -26,7 +26,7 @@ def test_patch_applies_to_reference():
 def test_patch_touches_only_the_runtime_seam():
     text = (ROOT / "oracle" / "reference_gpu.patch").read_text()
     files = sorted(l.split()[1] for l in text.splitlines() if l.startswith("+++ "))
-    assert files == ["b/include/iolm/runtime.hpp", "b/src/CMakeLists.txt", "b/src/runtime.cpp"]
+    assert files == ["b/include/iolm/runtime.hpp", "b/src/CMakeLists.txt", "b/src/calib.cpp", "b/src/runtime.cpp"]
 
 
 @pytest.mark.skipif(not (ROOT / "oracle" / "_ref" / "patched" / "libiolm_ref_gpu.so").exists(),
