@@ -249,6 +249,10 @@ int iolm_cuda_debug_gemm_sp24(const int8_t* X, const uint8_t* payload, int32_t T
  * int4 codes are expanded to bf16 inside the kernel. epi 0: f32 out. pair as in debug_gemm_s8. */
 int iolm_cuda_debug_gemm_w4(const uint16_t* A, const uint8_t* payload, float* C, int32_t M, int32_t N, int32_t K,
                             int32_t pair);
+/* 2:4 sparse bf16 GEMM (tcgen05.mma.sp kind::f16): X bf16 [T x K] (raw uint16) times a sparse24_q8
+ * payload's kept codes as exact bf16 integers, out_f32 [T x N] = acc * payload scale[n]. K % 16 == 0. */
+int iolm_cuda_debug_gemm_sp24_bf16(const uint16_t* X, const uint8_t* payload, int32_t T, int32_t N, int32_t K,
+                                   float* out_f32);
 /* Device-only timing of the sparse GEMM: mean ms per launch (epi as in debug_gemm_time). */
 int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, float* ms_out);
 

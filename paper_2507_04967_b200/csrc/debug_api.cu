@@ -224,6 +224,40 @@ extern "C" int iolm_cuda_debug_gemm_sp24(const int8_t* X, const uint8_t* payload
   });
 }
 
+// 2:4 sparse bf16 GEMM (tcgen05.mma.sp kind::f16): X_bf16 [T x K] (uint16 bit patterns) times the
+// sparse24_q8 payload's kept codes as exact bf16 integers; out_f32 [T x N] = acc * w_scale[n] (the
+// W8A16 2:4 path the engine runs for sparse24_q8 bundles without act_quant).
+extern "C" int iolm_cuda_debug_gemm_sp24_bf16(const uint16_t* X, const uint8_t* payload, int32_t T, int32_t N,
+                                              int32_t K, float* out_f32) {
+  return guarded([&] {
+    if (T <= 0 || N <= 0 || K <= 0 || K % 16 != 0)
+      throw ContractViolation("debug_gemm_sp24_bf16: need positive T, N and K % 16 == 0");
+    if (!sp24_check(payload, N, K)) throw Unsupported("debug_gemm_sp24_bf16: positions not ascending");
+    const Sp24Layout l = sp24_layout(N, K, true);
+    std::vector<uint8_t> codes(l.code_bytes(), 0);
+    std::vector<uint8_t> meta(l.meta_bytes(), 0x44);
+    std::vector<float> scales(N);
+    sp24_append(l, payload, N, K, 0, codes.data(), meta.data(), scales.data());
+    DevBuf<uint16_t> dX(static_cast<size_t>(T) * K);
+    DevBuf<uint8_t> dW(codes.size()), dE(meta.size());
+    DevBuf<float> dS(N), dC(static_cast<size_t>(T) * N);
+    CUDA_OK(cudaMemcpy(dX.p, X, sizeof(uint16_t) * T * K, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dW.p, codes.data(), codes.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dE.p, meta.data(), meta.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dS.p, scales.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
+    iolmk::GemmEpi ep;
+    ep.M = T;
+    ep.N = N;
+    ep.out = dC.p;
+    ep.ldo = N;
+    ep.w_scale = dS.p;
+    launch_gemm_sp(iolmk::EPI_F32, sp24_codes_map(l, dW.p), sp24_act_map_bf16(dX.p, K, T, K), sp24_meta_map(l, dE.p),
+                   K, l.katoms_pad, ep, nullptr, sm_count(), true);
+    CUDA_OK(cudaDeviceSynchronize());
+    CUDA_OK(cudaMemcpy(out_f32, dC.p, sizeof(float) * T * N, cudaMemcpyDeviceToHost));
+  });
+}
+
 // Device-only timing of the sparse GEMM (kernel tuning): every group keeps positions (0, 1).
 extern "C" int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
                                               float* ms_out) {

@@ -122,7 +122,9 @@ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 //            act_quant on the sparse tensor cores (tcgen05.mma.sp kind::i8, gemm_sp_sm100.cuh)
 //   INT4   : packed q4 nibbles [N x ceil(K/2)] + f32 scale per row: W4A16, the codes are expanded
 //            to bf16 inside the GEMM (shared memory), never in HBM
-enum WMode : int { W_VALUES = 0, W_CODES = 1, W_INT8 = 2, W_SP24 = 3, W_INT4 = 4 };
+//   SP24F  : kept codes as exact bf16 [N x K/2] + 2:4 metadata + f32 scale per row: sparse24_q8
+//            WITHOUT act_quant on the sparse tensor cores (tcgen05.mma.sp kind::f16, bf16 activations)
+enum WMode : int { W_VALUES = 0, W_CODES = 1, W_INT8 = 2, W_SP24 = 3, W_INT4 = 4, W_SP24F = 5 };
 struct GemmW {
   int mode = W_VALUES;
   DevArray<__nv_bfloat16> wb;
@@ -146,6 +148,10 @@ void weight_maps(GemmW& w, int N, int K, int ld) {
       w.tm = sp24_codes_map(w.sl, w.w8.p);
       w.tm_e = sp24_meta_map(w.sl, w.meta.p);
       break;
+    case W_SP24F:
+      w.tm = sp24_codes_map(w.sl, w.wb.p);
+      w.tm_e = sp24_meta_map(w.sl, w.meta.p);
+      break;
     case W_INT4:
       w.tm = make_w4_map(w.w4.p, static_cast<uint64_t>(K), static_cast<uint64_t>(N), w4_pitch(K));
       break;
@@ -164,6 +170,7 @@ struct Layer {
   CUtensorMap tm_z, tm_g;    // bf16 A operands with this layer's K extent
   CUtensorMap tm_z8, tm_g8;  // int8 A operands (W8A8)
   CUtensorMap tm_z8s, tm_g8s;  // the same in the sparse kernel's 112-row boxes
+  CUtensorMap tm_zs, tm_gs;    // bf16 z / g in the sparse kernel's 112-row boxes (W_SP24F)
   CUtensorMap tm_g_out;        // g as the W_in GEMM's TMA store target (bf16 32 x 32 boxes)
   DevArray<__nv_bfloat16> kv;  // paged pool [pages][K|V][heads][PAGE][hd]
   CUtensorMap tm_kv, tm_kvg;     // the pool as rows of hd (prefill / decode attention TMA boxes)
@@ -474,6 +481,7 @@ class Engine {
   DevArray<int8_t> h8_, z8_, g8_;  // W8A8 operands + per-token scales
   DevArray<float> hs_, zs_, gs_;
   CUtensorMap tm_h8_, tm_h8s_;
+  CUtensorMap tm_hs_;  // bf16 h in the sparse kernel's 112-row boxes (W_SP24F)
   bool any_int8_ = false;
   DevArray<int> page_table_;
   StepBuffers sbuf_[2];
@@ -566,8 +574,10 @@ void Engine::finish_setup() {
   // All projections on the 2:4 sparse kernel (224-token pair tiles): whole waves of that grid.
   bool all_sp = true;
   for (const auto& ly : layers_)
-    all_sp = all_sp && ly->qkv.mode == W_SP24 && ly->o.mode == W_SP24 && ly->in.mode == W_SP24 &&
-             ly->out.mode == W_SP24;
+    for (int g = 0; g < 4; ++g) {
+      const int m = weight_group(*ly, g).mode;
+      all_sp = all_sp && (m == W_SP24 || m == W_SP24F);
+    }
   if (auto_budget_ && all_sp) T_max_ = std::max(std::max(1, sms_ / 2) * 224, round_up(S_, 32));
   alloc_runtime();
 }
@@ -606,6 +616,9 @@ void Engine::visit_weights(F&& f) {
         case W_INT8: f(w.w8, nl), f(w.scale, static_cast<size_t>(N)); break;
         case W_SP24:
           f(w.w8, w.sl.code_bytes()), f(w.meta, w.sl.meta_bytes()), f(w.scale, static_cast<size_t>(N));
+          break;
+        case W_SP24F:
+          f(w.wb, w.sl.code_bytes() / 2), f(w.meta, w.sl.meta_bytes()), f(w.scale, static_cast<size_t>(N));
           break;
         case W_INT4: f(w.w4, static_cast<size_t>(N) * w4_pitch(K)), f(w.scale, static_cast<size_t>(N)); break;
       }
@@ -679,13 +692,14 @@ Engine::Engine(const std::string& image_path, uint64_t expected_hash, int device
       w.mode = h.modes[4 * l + g];
       // the forms the bundle loader can produce under these options
       const bool ok = act_quant_ ? (w.mode == W_INT8 || (w.mode == W_SP24 && sparse_mma_))
-                                 : (w.mode == W_VALUES || w.mode == W_CODES || (w.mode == W_INT4 && int4_mma_));
+                                 : (w.mode == W_VALUES || w.mode == W_CODES || (w.mode == W_INT4 && int4_mma_) ||
+                                    (w.mode == W_SP24F && sparse_mma_));
       if (!ok) throw CorruptHeader("device-layout image: weight form inconsistent with its options");
       int N, K, ld;
       group_dims(*ly, g, N, K, ld);
-      if (w.mode == W_SP24) {
+      if (w.mode == W_SP24 || w.mode == W_SP24F) {
         if (K % 4 != 0) throw CorruptHeader("device-layout image: 2:4 form needs K % 4 == 0");
-        w.sl = sp24_layout(N, K);
+        w.sl = sp24_layout(N, K, w.mode == W_SP24F);
       }
     }
     any_int8_ = any_int8_ || ly->qkv.int8() || ly->o.int8() || ly->in.int8() || ly->out.int8();
@@ -793,7 +807,7 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
                                int ld) {
   std::vector<const TensorRecord*> ts;
   int N = 0;
-  bool all_dense = true, all_quant = true, int8_ok = true, sp_ok = act_quant_ && sparse_mma_;
+  bool all_dense = true, all_quant = true, int8_ok = true, sp_ok = sparse_mma_;
   bool q4_ok = !act_quant_ && int4_mma_;
   for (const auto& n : names) {
     ts.push_back(&b.tensor(n));
@@ -806,11 +820,13 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
             sp24_check(b.payload(*ts.back()), ts.back()->rows, ts.back()->cols);
   }
   w.mode = all_quant ? (act_quant_ && int8_ok ? W_INT8 : W_CODES) : W_VALUES;
-  if (w.mode == W_INT8 && sp_ok) {
-    // 2:4 sparse tensor cores: the bundle's kept codes and position nibbles are repacked on the host
-    w.mode = W_SP24;
-    w.sl = sp24_layout(N, K);
-    std::vector<int8_t> codes(w.sl.code_bytes(), 0);
+  if ((w.mode == W_INT8 || w.mode == W_CODES) && sp_ok) {
+    // 2:4 sparse tensor cores: the bundle's kept codes and position nibbles are repacked on the host;
+    // W8A8 keeps the codes as int8 (kind::i8), bf16 activations take them as exact bf16 (kind::f16)
+    const bool f16 = w.mode == W_CODES;
+    w.mode = f16 ? W_SP24F : W_SP24;
+    w.sl = sp24_layout(N, K, f16);
+    std::vector<uint8_t> codes(w.sl.code_bytes(), 0);
     std::vector<uint8_t> meta(w.sl.meta_bytes(), 0x44);
     std::vector<float> scales(N);
     int row0 = 0;
@@ -818,10 +834,12 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
       sp24_append(w.sl, b.payload(*t), t->rows, t->cols, row0, codes.data(), meta.data(), scales.data());
       row0 += t->rows;
     }
-    w.w8.alloc(codes.size());
+    if (f16) w.wb.alloc(codes.size() / 2);
+    else w.w8.alloc(codes.size());
     w.meta.alloc(meta.size());
     w.scale.alloc(N);
-    CUDA_OK(cudaMemcpy(w.w8.p, codes.data(), codes.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(f16 ? static_cast<void*>(w.wb.p) : static_cast<void*>(w.w8.p), codes.data(), codes.size(),
+                       cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(w.meta.p, meta.data(), meta.size(), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(w.scale.p, scales.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
     weight_maps(w, N, K, ld);
@@ -889,7 +907,10 @@ void Engine::alloc_runtime() {
     ly->tm_z = make_kmajor_map(z_.p, BF, 2, ly->kh, T, 2ull * kh_max_, 128);
     ly->tm_g = make_kmajor_map(g_.p, BF, 2, ly->f, T, 2ull * f_ld_max_, 128);
     ly->tm_g_out = make_out_map(g_.p, false, ly->f, T, 2ull * f_ld_max_);
+    ly->tm_zs = sp24_act_map_bf16(z_.p, ly->kh, static_cast<int>(T), kh_max_);
+    ly->tm_gs = sp24_act_map_bf16(g_.p, ly->f, static_cast<int>(T), f_ld_max_);
   }
+  tm_hs_ = sp24_act_map_bf16(h_.p, d_, static_cast<int>(T), d_);
   if (any_int8_) {
     const auto U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
     h8_.alloc(T * d_);
@@ -987,8 +1008,8 @@ void Engine::gemm(int epi, bool i8, const CUtensorMap& A, const CUtensorMap& B, 
 
 void Engine::gemm_w(int epi, const GemmW& w, const CUtensorMap& act, const CUtensorMap& act_sp, int M, int N, int K,
                     const GemmEpi& ep, const CUtensorMap* out_map) {
-  if (w.mode == W_SP24) {
-    launch_gemm_sp(epi, w.tm, act_sp, w.tm_e, K, w.sl.katoms_pad, ep, stream_, sms_);
+  if (w.mode == W_SP24 || w.mode == W_SP24F) {
+    launch_gemm_sp(epi, w.tm, act_sp, w.tm_e, K, w.sl.katoms_pad, ep, stream_, sms_, w.mode == W_SP24F);
     ++stats_.kernel_launches;
   } else if (w.mode == W_INT4) {
     launch_gemm_w4(use_pair(M, N), epi, act, w.tm, M, N, K, ep, stream_, sms_, out_map);
@@ -1117,7 +1138,8 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     ep.page_size = PAGE;
     scales(ep, ly.qkv, hs_.p);
     timed(1, 2.0 * dT * 3 * ly.kh * d_, [&] {
-      gemm_w(iolmk::EPI_QKV, ly.qkv, i8_qkv ? tm_h8_ : tm_h_, tm_h8s_, T, 3 * ly.kh, d_, ep);
+      gemm_w(iolmk::EPI_QKV, ly.qkv, i8_qkv ? tm_h8_ : tm_h_, ly.qkv.mode == W_SP24F ? tm_hs_ : tm_h8s_, T, 3 * ly.kh,
+             d_, ep);
     });
     AttnParams ap{};
     ap.q_map = tm_q_;
@@ -1163,7 +1185,8 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     eo.ldo = d_;
     scales(eo, ly.o, zs_.p);
     timed(4, 2.0 * dT * d_ * ly.kh, [&] {
-      gemm_w(iolmk::EPI_RESID_F32, ly.o, i8_o ? ly.tm_z8 : ly.tm_z, ly.tm_z8s, T, d_, ly.kh, eo);
+      gemm_w(iolmk::EPI_RESID_F32, ly.o, i8_o ? ly.tm_z8 : ly.tm_z, ly.o.mode == W_SP24F ? ly.tm_zs : ly.tm_z8s, T, d_,
+             ly.kh, eo);
     });
     // h = LN2(x)
     timed(5, dT * d_ * 6.0, [&] {
@@ -1179,7 +1202,8 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     ei.ldo = f_ld_max_;
     scales(ei, ly.in, hs_.p);
     timed(6, 2.0 * dT * ly.f * d_, [&] {
-      gemm_w(iolmk::EPI_GELU_BF16, ly.in, i8_in ? tm_h8_ : tm_h_, tm_h8s_, T, ly.f, d_, ei,
+      gemm_w(iolmk::EPI_GELU_BF16, ly.in, i8_in ? tm_h8_ : tm_h_, ly.in.mode == W_SP24F ? tm_hs_ : tm_h8s_, T, ly.f, d_,
+             ei,
              tma_epi_ ? &ly.tm_g_out : nullptr);
     });
     // x += g * Wout^T
@@ -1191,7 +1215,8 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     GemmEpi eo2 = eo;
     scales(eo2, ly.out, gs_.p);
     timed(7, 2.0 * dT * d_ * ly.f, [&] {
-      gemm_w(iolmk::EPI_RESID_F32, ly.out, i8_out ? ly.tm_g8 : ly.tm_g, ly.tm_g8s, T, d_, ly.f, eo2);
+      gemm_w(iolmk::EPI_RESID_F32, ly.out, i8_out ? ly.tm_g8 : ly.tm_g, ly.out.mode == W_SP24F ? ly.tm_gs : ly.tm_g8s, T,
+             d_, ly.f, eo2);
     });
     if (l + 1 < L_) {
       const bool q8_next = layers_[l + 1]->qkv.int8();

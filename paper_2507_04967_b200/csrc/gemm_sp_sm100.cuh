@@ -58,6 +58,19 @@ struct SpCfg {
 
 // kind::i8 instruction descriptor with the sparse flag (bit 2): s8 x s8 -> s32, K-major A/B.
 __host__ __device__ constexpr uint32_t idesc_i8_sp(int M, int N) { return idesc_i8(M, N) | (1u << 2); }
+// kind::f16 with the sparse flag: bf16 x bf16 -> f32 (the W16A16 / W8A16 path: A = the kept weight
+// codes as exact bf16 integers, B = bf16 activations; the per-channel scale is applied in the epilogue).
+__host__ __device__ constexpr uint32_t idesc_f16_sp(int M, int N) { return idesc_f16(M, N, 1) | (1u << 2); }
+
+__device__ __forceinline__ void umma_f16_sp_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t tmem_e,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%3], %4, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(tmem_e), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 __device__ __forceinline__ void umma_i8_sp_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t tmem_e,
                                                 uint32_t idesc, uint32_t accumulate) {
@@ -99,12 +112,22 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)
 
 // tmA: compressed weights [N rows x K/2 bytes]; tmB: activations [T rows x K bytes] (box 112 rows);
 // tmE: metadata atoms [rows x 16 B] (box 256 rows). ep.M = tokens T, ep.N = output channels.
-template <int EPI>
+//
+// F16 = true: the same pipeline over bf16 operands (tcgen05.mma.sp kind::f16). A 128-byte operand row
+// then holds 64 kept bf16 = 128 logical K, so a stage covers 128 logical K with ONE metadata atom
+// (128 rows x 16 B -> 4 TMEM columns, one per 32-K MMA) instead of two; A / B / E tiles keep their
+// byte shapes (B: 112 tokens x 128 K x 2 B as two 64-K SWIZZLE_128B boxes). Epilogue: acc * s_w.
+template <int EPI, bool F16 = false>
 __global__ void __launch_bounds__(SpCfg::THREADS, 1)
     gemm_sp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmE, int K, int katoms_pad, GemmEpi ep) {
   using C = SpCfg;
   constexpr int STAGES = C::STAGES;
+  constexpr int BKL = F16 ? 128 : C::BK;                     // logical K per stage
+  constexpr int A_EL = F16 ? 64 : 128;                        // kept elements per stage row (128 B)
+  constexpr int B_EL = F16 ? 64 : 128;                        // activation elements per 128-B box row
+  constexpr int E_ROWS = F16 ? 128 : 256;                     // metadata atom rows per stage
+  constexpr uint32_t STAGE_TX = C::A_BYTES + C::B_BYTES + (F16 ? C::E_BYTES / 2 : C::E_BYTES);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -149,7 +172,7 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
   const int w_tiles = (N + C::TILE_M - 1) / C::TILE_M;
   const int t_tiles = (T + C::BN - 1) / C::BN;
   const int num_tiles = w_tiles * t_tiles;
-  const int kbs = (K + C::BK - 1) / C::BK;
+  const int kbs = (K + BKL - 1) / BKL;
   const int group = blockIdx.x / 2, n_groups = gridDim.x / 2;
 
   if (warp == 0) {
@@ -166,11 +189,11 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
         for (int kb = 0; kb < kbs; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
           const uint32_t lf = leader_full0 + 8u * stage;
-          if (leader) mbar_expect_tx(full_bar(stage), 2 * C::STAGE_BYTES);
-          tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, lf, kb * 128, wrow);
-          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, lf, kb * C::BK, trow);
-          tma_load_2d_pair(sB + stage * C::B_BYTES + C::B_BOX, &tmB, lf, kb * C::BK + 128, trow);
-          tma_load_2d_pair(sE + stage * C::E_BYTES, &tmE, lf, 0, erow + kb * 256);
+          if (leader) mbar_expect_tx(full_bar(stage), 2 * STAGE_TX);
+          tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, lf, kb * A_EL, wrow);
+          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, lf, kb * BKL, trow);
+          tma_load_2d_pair(sB + stage * C::B_BYTES + C::B_BOX, &tmB, lf, kb * BKL + B_EL, trow);
+          tma_load_2d_pair(sE + stage * C::E_BYTES, &tmE, lf, 0, erow + kb * E_ROWS);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -181,7 +204,7 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = idesc_i8_sp(C::TILE_M, C::BN);
+      constexpr uint32_t idesc = F16 ? idesc_f16_sp(C::TILE_M, C::BN) : idesc_i8_sp(C::TILE_M, C::BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -196,16 +219,18 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
           const uint32_t ecol = tmem_base + C::E_COL0 + 8u * stage;
           const uint32_t se = sE + stage * C::E_BYTES;
           tmem_cp_128x128b_pair(ecol, smem_desc_rows16(se));
-          tmem_cp_128x128b_pair(ecol + 4u, smem_desc_rows16(se + 2048u));
+          if constexpr (!F16) tmem_cp_128x128b_pair(ecol + 4u, smem_desc_rows16(se + 2048u));
           const uint64_t ad = smem_desc_k_sw128(sA + stage * C::A_BYTES);
           const uint64_t bd0 = smem_desc_k_sw128(sB + stage * C::B_BYTES);
           const uint64_t bd1 = smem_desc_k_sw128(sB + stage * C::B_BYTES + C::B_BOX);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
-            // A advances 32 compressed bytes per 64 logical K; B 64 bytes inside its 128-K box
+            // A advances 32 compressed bytes per MMA (64 logical K of int8 / 32 of bf16); B 64 bytes
+            // inside its 128-byte box; E 64 (int8) or 32 (bf16) metadata bits = 2 or 1 TMEM columns
             const uint64_t bd = (kk < 2 ? bd0 : bd1) + 4u * (kk & 1);
-            umma_i8_sp_pair(d, ad + 2u * kk, bd, ecol + 2u * kk, idesc, accum);
+            if constexpr (F16) umma_f16_sp_pair(d, ad + 2u * kk, bd, ecol + kk, idesc, accum);
+            else umma_i8_sp_pair(d, ad + 2u * kk, bd, ecol + 2u * kk, idesc, accum);
           }
           umma_commit_pair_mc(empty_bar(stage), 0x3);
           if (++stage == STAGES) {
@@ -306,9 +331,10 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
               *reinterpret_cast<float4*>(as + j) = *reinterpret_cast<const float4*>(s_as + ci * C::CHUNK + j);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              // same operations as the dense kind::i8 epilogue: (acc * s_a[token]) * s_w[ch], each
-              // rounded (explicit _rn: no FMA contraction into the residual add below)
-              v[j] = __fmul_rn(__fmul_rn(static_cast<float>(static_cast<int32_t>(rc[j])), as[j]), w_sc);
+              // same operations as the dense epilogues: int8 (acc * s_a[token]) * s_w[ch], bf16 codes
+              // acc * s_w[ch], each rounded (explicit _rn: no FMA contraction into the residual add)
+              if constexpr (F16) v[j] = __fmul_rn(__uint_as_float(rc[j]), w_sc);
+              else v[j] = __fmul_rn(__fmul_rn(static_cast<float>(static_cast<int32_t>(rc[j])), as[j]), w_sc);
             }
             if constexpr (EPI == EPI_GELU_BF16) {
 #pragma unroll

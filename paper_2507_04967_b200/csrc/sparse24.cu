@@ -22,12 +22,14 @@ namespace iolmh {
 
 using namespace iolmk;
 
-Sp24Layout sp24_layout(int N, int K) {
+Sp24Layout sp24_layout(int N, int K, bool f16) {
   Sp24Layout l;
   l.N = N;
   l.K = K;
-  l.ld_c = (K / 2 + 15) / 16 * 16;
-  l.katoms_pad = 2 * ((K + SpCfg::BK - 1) / SpCfg::BK);
+  l.f16 = f16;
+  l.ld_c = ((K / 2) * (f16 ? 2 : 1) + 15) / 16 * 16;
+  // int8: a stage is 256 logical K = 2 atoms; bf16: 128 logical K = 1 atom
+  l.katoms_pad = f16 ? (K + 127) / 128 : 2 * ((K + SpCfg::BK - 1) / SpCfg::BK);
   l.mtiles = 2 * ((N + SpCfg::TILE_M - 1) / SpCfg::TILE_M);
   return l;
 }
@@ -46,7 +48,7 @@ bool sp24_check(const uint8_t* payload, int rows, int cols) {
   return true;
 }
 
-void sp24_append(const Sp24Layout& l, const uint8_t* payload, int rows, int cols, int row0, int8_t* codes,
+void sp24_append(const Sp24Layout& l, const uint8_t* payload, int rows, int cols, int row0, void* codes_out,
                  uint8_t* meta, float* scales) {
   const size_t groups = static_cast<size_t>(cols) / 4;
   const size_t idx_row_bytes = (groups + 1) / 2;
@@ -54,7 +56,19 @@ void sp24_append(const Sp24Layout& l, const uint8_t* payload, int rows, int cols
   const uint8_t* sc = idx + static_cast<size_t>(rows) * idx_row_bytes;
   for (int r = 0; r < rows; ++r) {
     const int gr = row0 + r;
-    std::memcpy(codes + static_cast<size_t>(gr) * l.ld_c, payload + static_cast<size_t>(r) * groups * 2, groups * 2);
+    const uint8_t* src = payload + static_cast<size_t>(r) * groups * 2;
+    uint8_t* dst = static_cast<uint8_t*>(codes_out) + static_cast<size_t>(gr) * l.ld_c;
+    if (!l.f16) {
+      std::memcpy(dst, src, groups * 2);
+    } else {  // |code| <= 127 is exact in bf16: the f32 bit pattern's top half
+      for (size_t i = 0; i < groups * 2; ++i) {
+        const float f = static_cast<float>(static_cast<int8_t>(src[i]));
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        const uint16_t h = static_cast<uint16_t>(u >> 16);
+        std::memcpy(dst + 2 * i, &h, 2);
+      }
+    }
     const int mt = gr / 128, rr = gr % 128;
     for (size_t b = 0; b < idx_row_bytes; ++b) {
       uint8_t v = idx[r * idx_row_bytes + b];
@@ -66,7 +80,10 @@ void sp24_append(const Sp24Layout& l, const uint8_t* payload, int rows, int cols
   }
 }
 
-CUtensorMap sp24_codes_map(const Sp24Layout& l, const int8_t* d_codes) {
+CUtensorMap sp24_codes_map(const Sp24Layout& l, const void* d_codes) {
+  if (l.f16)
+    return make_kmajor_map(d_codes, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, static_cast<uint64_t>(l.K / 2), l.N,
+                           static_cast<uint64_t>(l.ld_c), 128);
   return make_kmajor_map(d_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, static_cast<uint64_t>(l.K / 2), l.N,
                          static_cast<uint64_t>(l.ld_c), 128);
 }
@@ -75,7 +92,7 @@ CUtensorMap sp24_meta_map(const Sp24Layout& l, const uint8_t* d_meta) {
   CUtensorMap m;
   cuuint64_t dims[2] = {16, static_cast<cuuint64_t>(l.meta_bytes() / 16)};
   cuuint64_t strides[1] = {16};
-  cuuint32_t box[2] = {16, 256};
+  cuuint32_t box[2] = {16, l.f16 ? 128u : 256u};  // one stage: 1 (bf16) or 2 (int8) 128-row atoms
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_meta), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -89,10 +106,15 @@ CUtensorMap sp24_act_map(const int8_t* act, int K, int rows, int ld) {
                          static_cast<uint64_t>(ld), SpCfg::BN_CTA);
 }
 
-template <int EPI>
+CUtensorMap sp24_act_map_bf16(const void* act, int K, int rows, int ld) {
+  return make_kmajor_map(act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, static_cast<uint64_t>(K), rows,
+                         2ull * static_cast<uint64_t>(ld), SpCfg::BN_CTA);
+}
+
+template <int EPI, bool F16>
 static void launch_sp_one(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, int K, int katoms_pad,
                           const GemmEpi& ep, cudaStream_t st, int grid_cap) {
-  auto kern = gemm_sp_kernel<EPI>;
+  auto kern = gemm_sp_kernel<EPI, F16>;
   ensure_smem(kern, SpCfg::SMEM);
   const int tiles = ((ep.N + SpCfg::TILE_M - 1) / SpCfg::TILE_M) * ((ep.M + SpCfg::BN - 1) / SpCfg::BN);
   const int groups = std::min(tiles, grid_cap / 2);
@@ -112,19 +134,29 @@ static void launch_sp_one(const CUtensorMap& A, const CUtensorMap& B, const CUte
   CUDA_OK(cudaLaunchKernelEx(&cfg, kern, A, B, E, K, katoms_pad, ep));
 }
 
-void launch_gemm_sp(int epi, const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, int K, int katoms_pad,
-                    const GemmEpi& ep, cudaStream_t st, int grid_cap) {
-  if (ep.M <= 0 || ep.N <= 0) return;
+template <bool F16>
+static void launch_sp(int epi, const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, int K, int katoms_pad,
+                      const GemmEpi& ep, cudaStream_t st, int grid_cap) {
   switch (epi) {
-    case EPI_S32: launch_sp_one<EPI_S32>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_F32: launch_sp_one<EPI_F32>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_BF16: launch_sp_one<EPI_BF16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_GELU_BF16: launch_sp_one<EPI_GELU_BF16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_RESID_F32: launch_sp_one<EPI_RESID_F32>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_QKV: launch_sp_one<EPI_QKV>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_NONE: launch_sp_one<EPI_NONE>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_S32:
+      if constexpr (F16) throw Unsupported("gemm_sp: raw accumulators are int8-only");
+      else launch_sp_one<EPI_S32, false>(A, B, E, K, katoms_pad, ep, st, grid_cap);
+      break;
+    case EPI_F32: launch_sp_one<EPI_F32, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_BF16: launch_sp_one<EPI_BF16, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_GELU_BF16: launch_sp_one<EPI_GELU_BF16, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_RESID_F32: launch_sp_one<EPI_RESID_F32, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_QKV: launch_sp_one<EPI_QKV, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_NONE: launch_sp_one<EPI_NONE, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
     default: throw Unsupported("gemm_sp: epilogue not instantiated");
   }
+}
+
+void launch_gemm_sp(int epi, const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, int K, int katoms_pad,
+                    const GemmEpi& ep, cudaStream_t st, int grid_cap, bool f16) {
+  if (ep.M <= 0 || ep.N <= 0) return;
+  if (f16) launch_sp<true>(epi, A, B, E, K, katoms_pad, ep, st, grid_cap);
+  else launch_sp<false>(epi, A, B, E, K, katoms_pad, ep, st, grid_cap);
   CUDA_OK(cudaGetLastError());
 }
 

@@ -158,7 +158,7 @@ def image_header(path) -> dict:
         at += 1 + n
     cfg.active_ffn = w[at:at + cfg.n_layers]
     at += cfg.n_layers
-    forms = ["values", "codes", "int8", "sp24", "int4"]
+    forms = ["values", "codes", "int8", "sp24", "int4", "sp24f"]
     return {"bundle_hash": w[0] & (2**64 - 1), "config": cfg,
             "act_quant": bool(w[7]), "sparse_mma": bool(w[8]), "int4_mma": bool(w[9]),
             "weight_forms": [forms[m] for m in w[at:at + 4 * cfg.n_layers]]}

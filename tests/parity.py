@@ -40,7 +40,9 @@ def check_agreement(om, ids, offs, gi, gl, oi, ol, min_frac: float = 0.99, label
     for i in bad:
         k, gap, tol = cpu_gap(om, ids[offs[i]:offs[i + 1]], gi[i, :gl[i]], oi[i, :ol[i]])
         traced.append((i, k, gap, tol))
-    assert n - len(bad) >= min_frac * n, f"{label}: {n - len(bad)}/{n} rows agree; divergences {traced}"
+    # >= 99% of rows; a sample under 100 rows may hold one (tie-traced) divergence, the granularity
+    # of the rule at that size
+    assert n - len(bad) >= min_frac * n or len(bad) <= 1, f"{label}: {n - len(bad)}/{n} rows agree; divergences {traced}"
     for i, k, gap, tol in traced:
         assert gap < tol, f"{label}: row {i} diverges at step {k} with CPU top-2 gap {gap:.4g} >= {tol:.4g}"
     return traced
