@@ -48,6 +48,10 @@ CONFIGS = {
                heads=[10] * 24, ffn=[2560] * 24,
                desc="C3: C1 model pruned 50% (10 of 20 heads, FFN 2560) + 2:4 magnitude + q8 (sparse24_q8), "
                     "W8A8, 32+64, 8 new"),
+    "c3-bf16": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="sparse24",
+                    heads=[10] * 24, ffn=[2560] * 24,
+                    desc="C3 model (pruned 50% + 2:4 + q8 codes, sparse24_q8) with bf16 activations - the drop-in "
+                         "default without act_quant: 2:4 sparse tensor cores kind::f16, 32+64, 8 new"),
     "c3b": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="sparse24", act_quant=True,
                 heads=[7 + l % 6 for l in range(24)], ffn=[2500 + 12 * l for l in range(24)],
                 desc="C3b: C1 model with irregular per-layer pruning (7-12 of 20 heads, FFN 2500 + 12 l) + 2:4 + q8 "
@@ -342,7 +346,7 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
                               ffn=cfg.get("ffn"))
     rt = R.ModelRuntime(bundle, device=local, kernel_timing=True, max_tokens_per_step=args.tokens_per_step,
                         prefill_tc={"auto": None, "on": True, "off": False}[args.prefill_tc],
-                        act_quant=cfg.get("act_quant", False))
+                        act_quant=cfg.get("act_quant", False), sparse_mma=args.sparse_mma == "on")
     # this rank's rows for every warmup + timed step, host (pinned) and device copies
     host_ids, dev_ids, offsets = [], [], []
     for k in range(W + K):
@@ -451,6 +455,11 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
         achieved = work / (kms / 1000.0) / 1e12
         peak = peaks["bf16_tflops_sustained"]
         unit, bound = "TFLOP/s", "tensor"
+        if cfg["quant"] == "sparse24" and not cfg.get("act_quant"):
+            ip = int8_peaks()
+            if ip and ip["peaks_tops_sustained"].get("sp24_bf16"):
+                peak = ip["peaks_tops_sustained"]["sp24_bf16"]
+                peak_src = "measured sustained 2:4 sparse kind::f16 (engine mainloop-only), profiles/r02_peaks.json"
         if cfg.get("act_quant"):
             # int8 GEMMs (ops counted dense-equivalent): the MEASURED sustained kind::i8 / 2:4 sparse
             # kind::i8 rate (profiles/r02_peaks.json); the datasheet ratios (2x / 4x bf16) only if absent
@@ -539,6 +548,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prefill-tc", choices=["auto", "on", "off"], default="auto",
                     help="prefill attention kernel: tcgen05 (on), mma.sync (off), engine default (auto)")
+    ap.add_argument("--sparse-mma", choices=["on", "off"], default="on",
+                    help="2:4 bundles: sparse tensor cores (on) or weights expanded to dense codes (off), A/B")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="no per-kernel CUDA events (A/B check of their overhead; no roofline)")
     args = ap.parse_args()

@@ -255,6 +255,8 @@ int iolm_cuda_debug_gemm_sp24_bf16(const uint16_t* X, const uint8_t* payload, in
                                    float* out_f32);
 /* Device-only timing of the sparse GEMM: mean ms per launch (epi as in debug_gemm_time). */
 int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, float* ms_out);
+/* The same for the bf16 (kind::f16) sparse kernel. */
+int iolm_cuda_debug_gemm_sp24_bf16_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, float* ms_out);
 
 /* The multi-device row split (host only, no device work): cut[0..*n_cut) with cut[0] = 0 and
  * cut[last] = n_rows; range i = rows [cut[i], cut[i+1]). cut needs shards + 1 entries. */

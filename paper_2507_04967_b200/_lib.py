@@ -106,6 +106,7 @@ SIGNATURES = {
     "iolm_cuda_debug_gemm_sp24_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                                  C.c_void_p]),
     "iolm_cuda_debug_gemm_sp24_time": (C.c_int, [C.c_int32] * 5 + [C.POINTER(C.c_float)]),
+    "iolm_cuda_debug_gemm_sp24_bf16_time": (C.c_int, [C.c_int32] * 5 + [C.POINTER(C.c_float)]),
 }
 
 _LIB = None

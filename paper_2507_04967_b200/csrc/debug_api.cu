@@ -238,6 +238,7 @@ extern "C" int iolm_cuda_debug_gemm_sp24_bf16(const uint16_t* X, const uint8_t* 
     std::vector<uint8_t> meta(l.meta_bytes(), 0x44);
     std::vector<float> scales(N);
     sp24_append(l, payload, N, K, 0, codes.data(), meta.data(), scales.data());
+    sp24_finalize(l, meta.data());
     DevBuf<uint16_t> dX(static_cast<size_t>(T) * K);
     DevBuf<uint8_t> dW(codes.size()), dE(meta.size());
     DevBuf<float> dS(N), dC(static_cast<size_t>(T) * N);
@@ -259,42 +260,51 @@ extern "C" int iolm_cuda_debug_gemm_sp24_bf16(const uint16_t* X, const uint8_t* 
 }
 
 // Device-only timing of the sparse GEMM (kernel tuning): every group keeps positions (0, 1).
+static void sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, bool f16, float* ms_out) {
+  if (T <= 0 || N <= 0 || K <= 0 || K % 16 != 0 || iters <= 0) throw ContractViolation("debug_gemm_sp24_time");
+  const Sp24Layout l = sp24_layout(N, K, f16);
+  const size_t xb = static_cast<size_t>(T) * K * (f16 ? 2 : 1);
+  DevBuf<uint8_t> dX(xb), dW(l.code_bytes());
+  DevBuf<uint8_t> dE(l.meta_bytes());
+  DevBuf<float> dS(N), dA(T), dC(static_cast<size_t>(T) * N);
+  CUDA_OK(cudaMemset(dX.p, 0x11, xb));
+  CUDA_OK(cudaMemset(dW.p, 0x13, l.code_bytes()));
+  CUDA_OK(cudaMemset(dE.p, 0x44, l.meta_bytes()));
+  CUDA_OK(cudaMemset(dS.p, 0, sizeof(float) * N));
+  CUDA_OK(cudaMemset(dA.p, 0, sizeof(float) * T));
+  CUDA_OK(cudaMemset(dC.p, 0, sizeof(float) * T * N));
+  iolmk::GemmEpi ep;
+  ep.M = T;
+  ep.N = N;
+  ep.out = dC.p;
+  ep.ldo = N;
+  ep.a_scale = f16 ? nullptr : dA.p;
+  ep.w_scale = dS.p;
+  const CUtensorMap ta = sp24_codes_map(l, dW.p), te = sp24_meta_map(l, dE.p);
+  const CUtensorMap tb = f16 ? sp24_act_map_bf16(dX.p, K, T, K) : sp24_act_map(reinterpret_cast<int8_t*>(dX.p), K, T, K);
+  cudaEvent_t e0, e1;
+  CUDA_OK(cudaEventCreate(&e0));
+  CUDA_OK(cudaEventCreate(&e1));
+  launch_gemm_sp(epi, ta, tb, te, K, l.katoms_pad, ep, nullptr, sm_count(), f16);
+  CUDA_OK(cudaEventRecord(e0));
+  for (int i = 0; i < iters; ++i) launch_gemm_sp(epi, ta, tb, te, K, l.katoms_pad, ep, nullptr, sm_count(), f16);
+  CUDA_OK(cudaEventRecord(e1));
+  CUDA_OK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+  *ms_out = ms / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
 extern "C" int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
                                               float* ms_out) {
-  return guarded([&] {
-    if (T <= 0 || N <= 0 || K <= 0 || K % 16 != 0 || iters <= 0) throw ContractViolation("debug_gemm_sp24_time");
-    const Sp24Layout l = sp24_layout(N, K);
-    DevBuf<int8_t> dX(static_cast<size_t>(T) * K), dW(l.code_bytes());
-    DevBuf<uint8_t> dE(l.meta_bytes());
-    DevBuf<float> dS(N), dA(T), dC(static_cast<size_t>(T) * N);
-    CUDA_OK(cudaMemset(dX.p, 0x11, static_cast<size_t>(T) * K));
-    CUDA_OK(cudaMemset(dW.p, 0x13, l.code_bytes()));
-    CUDA_OK(cudaMemset(dE.p, 0x44, l.meta_bytes()));
-    CUDA_OK(cudaMemset(dS.p, 0, sizeof(float) * N));
-    CUDA_OK(cudaMemset(dA.p, 0, sizeof(float) * T));
-    CUDA_OK(cudaMemset(dC.p, 0, sizeof(float) * T * N));
-    iolmk::GemmEpi ep;
-    ep.M = T;
-    ep.N = N;
-    ep.out = dC.p;
-    ep.ldo = N;
-    ep.a_scale = dA.p;
-    ep.w_scale = dS.p;
-    const CUtensorMap ta = sp24_codes_map(l, dW.p), tb = sp24_act_map(dX.p, K, T, K), te = sp24_meta_map(l, dE.p);
-    cudaEvent_t e0, e1;
-    CUDA_OK(cudaEventCreate(&e0));
-    CUDA_OK(cudaEventCreate(&e1));
-    launch_gemm_sp(epi, ta, tb, te, K, l.katoms_pad, ep, nullptr, sm_count());
-    CUDA_OK(cudaEventRecord(e0));
-    for (int i = 0; i < iters; ++i) launch_gemm_sp(epi, ta, tb, te, K, l.katoms_pad, ep, nullptr, sm_count());
-    CUDA_OK(cudaEventRecord(e1));
-    CUDA_OK(cudaEventSynchronize(e1));
-    float ms = 0;
-    CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
-    *ms_out = ms / iters;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-  });
+  return guarded([&] { sp24_time(T, N, K, epi, iters, false, ms_out); });
+}
+
+extern "C" int iolm_cuda_debug_gemm_sp24_bf16_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
+                                                   float* ms_out) {
+  return guarded([&] { sp24_time(T, N, K, epi, iters, true, ms_out); });
 }
 
 extern "C" int iolm_cuda_debug_gemm_w4(const uint16_t* A, const uint8_t* payload, float* C, int32_t M, int32_t N,

@@ -834,6 +834,7 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
       sp24_append(w.sl, b.payload(*t), t->rows, t->cols, row0, codes.data(), meta.data(), scales.data());
       row0 += t->rows;
     }
+    sp24_finalize(w.sl, meta.data());
     if (f16) w.wb.alloc(codes.size() / 2);
     else w.w8.alloc(codes.size());
     w.meta.alloc(meta.size());

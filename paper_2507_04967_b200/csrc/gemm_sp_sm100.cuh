@@ -229,7 +229,9 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
             // A advances 32 compressed bytes per MMA (64 logical K of int8 / 32 of bf16); B 64 bytes
             // inside its 128-byte box; E 64 (int8) or 32 (bf16) metadata bits = 2 or 1 TMEM columns
             const uint64_t bd = (kk < 2 ? bd0 : bd1) + 4u * (kk & 1);
-            if constexpr (F16) umma_f16_sp_pair(d, ad + 2u * kk, bd, ecol + kk, idesc, accum);
+            // kind::f16: the metadata address must be 2-column aligned; an odd column is selected
+            // with the instruction descriptor's sparse id2 field (bits [0, 2))
+            if constexpr (F16) umma_f16_sp_pair(d, ad + 2u * kk, bd, (ecol + kk) & ~1u, idesc | ((ecol + kk) & 1u), accum);
             else umma_i8_sp_pair(d, ad + 2u * kk, bd, ecol + 2u * kk, idesc, accum);
           }
           umma_commit_pair_mc(empty_bar(stage), 0x3);

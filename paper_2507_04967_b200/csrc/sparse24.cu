@@ -80,6 +80,30 @@ void sp24_append(const Sp24Layout& l, const uint8_t* payload, int rows, int cols
   }
 }
 
+// kind::f16 reads one 32-bit metadata word per lane per MMA (32 logical K = 8 groups) with the halves
+// of rows r and r + 8 (r % 16 < 8) interleaved: lane r holds [row r groups 0-3 | row r+8 groups 0-3]
+// and lane r + 8 holds [row r groups 4-7 | row r+8 groups 4-7] (measured with profiles/sp16_probe.py:
+// identity activations expose the positions the tensor core applied). kind::i8 takes each row's own
+// 64 bits per MMA unchanged.
+void sp24_finalize(const Sp24Layout& l, uint8_t* meta) {
+  if (!l.f16) return;
+  const size_t atoms = static_cast<size_t>(l.mtiles) * l.katoms_pad;
+  for (size_t a = 0; a < atoms; ++a)
+    for (int blk = 0; blk < 128; blk += 16)
+      for (int i = 0; i < 8; ++i) {
+        uint8_t* ra = meta + (a * 128 + blk + i) * 16;
+        uint8_t* rb = ra + 8 * 16;
+        for (int w = 0; w < 4; ++w) {
+          uint32_t A, B;
+          std::memcpy(&A, ra + 4 * w, 4);
+          std::memcpy(&B, rb + 4 * w, 4);
+          const uint32_t na = (A & 0xFFFFu) | (B << 16), nb = (A >> 16) | (B & 0xFFFF0000u);
+          std::memcpy(ra + 4 * w, &na, 4);
+          std::memcpy(rb + 4 * w, &nb, 4);
+        }
+      }
+}
+
 CUtensorMap sp24_codes_map(const Sp24Layout& l, const void* d_codes) {
   if (l.f16)
     return make_kmajor_map(d_codes, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, static_cast<uint64_t>(l.K / 2), l.N,

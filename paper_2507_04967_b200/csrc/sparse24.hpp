@@ -28,6 +28,8 @@ bool sp24_check(const uint8_t* payload, int rows, int cols);
 // codes: int8 [N x ld_c], or for l.f16 the same codes as exact bf16 integers (uint16 bit patterns).
 void sp24_append(const Sp24Layout& l, const uint8_t* payload, int rows, int cols, int row0, void* codes,
                  uint8_t* meta, float* scales);
+// After every tensor of a group is appended: the kind::f16 metadata layout (a no-op for int8).
+void sp24_finalize(const Sp24Layout& l, uint8_t* meta);
 CUtensorMap sp24_codes_map(const Sp24Layout& l, const void* d_codes);
 CUtensorMap sp24_meta_map(const Sp24Layout& l, const uint8_t* d_meta);
 // int8 activation operand [rows x K] (row pitch ld bytes) in the sparse kernel's 112-row boxes.

@@ -66,6 +66,8 @@ def engine_timed(kind: str, T: int, N: int, K: int, seconds: float) -> dict:
         ms = C.c_float()
         if kind == "sp24_i8":
             st = lib.iolm_cuda_debug_gemm_sp24_time(T, N, K, 6, iters, C.byref(ms))
+        elif kind == "sp24_bf16":
+            st = lib.iolm_cuda_debug_gemm_sp24_bf16_time(T, N, K, 6, iters, C.byref(ms))
         else:
             st = lib.iolm_cuda_debug_gemm_time(T, N, K, 6, 1, 1 if kind == "i8" else 0, iters, C.byref(ms))
         if st:
@@ -99,7 +101,7 @@ def main():
     del a, b, ai, bi
     torch.cuda.empty_cache()
     T, N, K = 16384, 8192, 8192
-    for kind in ("bf16", "i8", "sp24_i8"):
+    for kind in ("bf16", "i8", "sp24_i8", "sp24_bf16"):
         res[f"engine_mainloop_{kind}"] = {m: engine_timed(kind, T, N, K, s) for m, s in (("burst", 0.2), ("sustained", 4.0))}
         res[f"engine_mainloop_{kind}"]["shape"] = [T, N, K]
     src = torch.empty(1 << 30, device="cuda", dtype=torch.float32)
@@ -118,12 +120,13 @@ def main():
         "bf16": best(["cublas_bf16", "engine_mainloop_bf16"]),
         "i8": best(["cublaslt_i8", "engine_mainloop_i8"]),
         "sp24_i8": best(["engine_mainloop_sp24_i8"]),
+        "sp24_bf16": best(["engine_mainloop_sp24_bf16"]),
     }
     out["hbm_gbs"] = res["hbm_copy"]["gbs"]
     out["peaks_tops_burst"] = {
         k: max(res[x]["burst"]["tops"] for x in xs if "burst" in res.get(x, {}))
         for k, xs in (("bf16", ["cublas_bf16", "engine_mainloop_bf16"]), ("i8", ["cublaslt_i8", "engine_mainloop_i8"]),
-                      ("sp24_i8", ["engine_mainloop_sp24_i8"]))}
+                      ("sp24_i8", ["engine_mainloop_sp24_i8"]), ("sp24_bf16", ["engine_mainloop_sp24_bf16"]))}
     text = json.dumps(out, indent=1)
     print(text)
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
