@@ -49,9 +49,11 @@ typedef struct iolm_cuda_opts {
   int32_t page_size;           /* KV page size in tokens (default 16) */
   int32_t act_quant;           /* 1: W8A8 int8 activations for q8 / sparse24 weights (default 0) */
   int32_t prefix_sharing;      /* -1: off; 0/1: share the common prompt prefix KV (default on) */
-  int32_t use_cuda_graph;      /* reserved */
+  int32_t use_cuda_graph;      /* reserved, ignored: steps are enqueued asynchronously (programmatic dependent
+                                  launch between kernels), so the host runs ahead of the device */
   int32_t kernel_timing;       /* 1: time every kernel class with CUDA events (iolm_cuda_kernel_times) */
-  int32_t sparse_mma;          /* -1: expand sparse24_q8 to dense int8; 0/1: 2:4 sparse tensor cores (W8A8) */
+  int32_t sparse_mma;          /* -1: expand sparse24_q8 to dense codes; 0/1: 2:4 sparse tensor cores (kind::i8 with
+                                  act_quant, kind::f16 over bf16 activations without) */
   int32_t int4_mma;            /* -1: expand q4 codes to bf16 in HBM; 0/1: int4 in HBM, expanded in smem (W4A16) */
   int32_t prefill_tc;          /* prefill attention: -1 mma.sync; 0 default (tcgen05 for hd 128); 1 tcgen05 for hd 64 too */
   int32_t reserved[6];

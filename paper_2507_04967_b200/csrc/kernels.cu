@@ -160,12 +160,28 @@ __global__ void __launch_bounds__(256, MAXV <= 10 ? 4 : 2) ln_kernel(const float
 // Streaming LayerNorm: persistent warps walk rows gw, gw + nw, ... and load row i+1 into registers
 // before normalising row i, so every warp always has a row's loads in flight (the one-row-per-warp
 // kernel above idles its memory traffic during each row's reductions). Same arithmetic.
+// gb_smem: the gain / bias rows are first copied to shared memory (every row re-reads them: 2 x d
+// floats per row from L1 otherwise), dynamic smem = 2 d floats.
+__device__ __forceinline__ void ln_stage_gb(const float*& g, const float*& b, int d, int gb_smem) {
+  if (!gb_smem) return;
+  extern __shared__ __align__(16) float ln_gb[];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    ln_gb[i] = g[i];
+    ln_gb[d + i] = b[i];
+  }
+  __syncthreads();
+  g = ln_gb;
+  b = ln_gb + d;
+}
+
 template <int MAXV, bool Q8>
 __global__ void __launch_bounds__(256, 2) ln_stream_kernel(const float* __restrict__ x, int M, int d,
-                                                           const float* __restrict__ g, const float* __restrict__ b,
+                                                           const float* g, const float* b,
                                                            __nv_bfloat16* __restrict__ h, int ldh,
-                                                           int8_t* __restrict__ q8, float* __restrict__ qscale) {
+                                                           int8_t* __restrict__ q8, float* __restrict__ qscale,
+                                                           int gb_smem) {
   pdl_sync();
+  ln_stage_gb(g, b, d, gb_smem);
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * 8;
   int row = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -189,10 +205,12 @@ __global__ void __launch_bounds__(256, 2) ln_stream_kernel(const float* __restri
 // named barrier per pair (ids 1-4); the arithmetic per element is the one-warp kernel's.
 template <int MAXV, bool Q8>
 __global__ void __launch_bounds__(256, 2) ln_stream2_kernel(const float* __restrict__ x, int M, int d,
-                                                            const float* __restrict__ g, const float* __restrict__ b,
+                                                            const float* g, const float* b,
                                                             __nv_bfloat16* __restrict__ h, int ldh,
-                                                            int8_t* __restrict__ q8, float* __restrict__ qscale) {
+                                                            int8_t* __restrict__ q8, float* __restrict__ qscale,
+                                                            int gb_smem) {
   pdl_sync();
+  ln_stage_gb(g, b, d, gb_smem);
   __shared__ float red[4][2][3][2];  // [pair][row parity][reduction][half]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, half = warp & 1, t = half * 32 + lane;
@@ -1237,15 +1255,21 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
   if (M <= 0) return;
   const int nv = (d / 4 + 31) / 32;
   const int sms = device_sms();
+  // gain / bias staged in shared memory (IOLM_LN_GB_SMEM=0: read through L1 every row, A/B switch)
+  static const int gbf = [] {
+    const char* e = std::getenv("IOLM_LN_GB_SMEM");
+    return e == nullptr || std::string(e) != "0" ? 1 : 0;
+  }();
+  const size_t gbs = gbf ? 2ull * d * sizeof(float) : 0;
   if (std::getenv("IOLM_LN_LEGACY") == nullptr && nv > 10 && nv <= 32 && d % 4 == 0) {
     const int grid_s = std::min<int>((M + 3) / 4, sms * 2);
     const int v2 = (d / 4 + 63) / 64;  // float4 per thread with two warps per row
     if (v2 <= 8) {
-      if (q8) launch_k<false>(ln_stream2_kernel<8, true>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);
-      else launch_k<false>(ln_stream2_kernel<8, false>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);
+      if (q8) launch_k<false>(ln_stream2_kernel<8, true>, grid_s, 256, gbs, st, x, M, d, g, b, h, ldh, q8, qscale, gbf);
+      else launch_k<false>(ln_stream2_kernel<8, false>, grid_s, 256, gbs, st, x, M, d, g, b, h, ldh, q8, qscale, gbf);
     } else {
-      if (q8) launch_k<false>(ln_stream2_kernel<16, true>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);
-      else launch_k<false>(ln_stream2_kernel<16, false>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);
+      if (q8) launch_k<false>(ln_stream2_kernel<16, true>, grid_s, 256, gbs, st, x, M, d, g, b, h, ldh, q8, qscale, gbf);
+      else launch_k<false>(ln_stream2_kernel<16, false>, grid_s, 256, gbs, st, x, M, d, g, b, h, ldh, q8, qscale, gbf);
     }
     CUDA_OK(cudaGetLastError());
     return;
@@ -1254,8 +1278,8 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
     const int grid_s = std::min<int>((M + 7) / 8, sms * 2);
 #define LNS(V)                                                                                             \
   do {                                                                                                     \
-    if (q8) launch_k<false>(ln_stream_kernel<V, true>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);            \
-    else launch_k<false>(ln_stream_kernel<V, false>, grid_s, 256, 0, st, x, M, d, g, b, h, ldh, q8, qscale);              \
+    if (q8) launch_k<false>(ln_stream_kernel<V, true>, grid_s, 256, gbs, st, x, M, d, g, b, h, ldh, q8, qscale, gbf);     \
+    else launch_k<false>(ln_stream_kernel<V, false>, grid_s, 256, gbs, st, x, M, d, g, b, h, ldh, q8, qscale, gbf);       \
   } while (0)
     switch (nv) {
       case 1: LNS(1); break;
