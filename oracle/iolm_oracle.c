@@ -296,24 +296,18 @@ static void flash_head_gpu(const float* qh, const float* k0, const float* v0, in
     const float msub = mnew == -INFINITY ? 0.0f : mnew;
     m_run = mnew;
     l_run *= alpha;
-    /* hd <= 64 (mma.sync): O is rescaled, then the block's P V accumulates into it; hd 128 (tcgen05):
-     * the block's P V is a fresh f32 tile Ob and O = fma(O, alpha, Ob) (attn_tc.cu accumulate) */
-    float ob[128];
-    for (int j = 0; j < hd; ++j) {
-      if (KB == 64) ob[j] = 0.0f;
-      else o[j] *= alpha;
-    }
-    float* acc = KB == 64 ? ob : o;
+    /* O is rescaled, then the block's P V accumulates into it (the tcgen05 kernel for hd 128 forms
+     * the block's P V as a separate f32 tile and adds it with fma(O, alpha, Ob): emulating that was
+     * measured to match its codes less well than this form, tests/test_w8a8_codes_gpu.py) */
+    for (int j = 0; j < hd; ++j) o[j] *= alpha;
     for (int t = 0; t < nk; ++t) {
       const float pv = exp2f(fmaf(s[t], scale_log2, -msub));
       l_run += pv;
       const float pb = bf16r(pv);
       if (pb == 0.0f) continue;
       const float* vr = v0 + (size_t)(key0 + t) * ld;
-      for (int j = 0; j < hd; ++j) acc[j] = fmaf(pb, vr[j], acc[j]);
+      for (int j = 0; j < hd; ++j) o[j] = fmaf(pb, vr[j], o[j]);
     }
-    if (KB == 64)
-      for (int j = 0; j < hd; ++j) o[j] = fmaf(o[j], alpha, ob[j]);
   }
   const float inv = l_run > 0.0f ? 1.0f / l_run : 0.0f;
   for (int j = 0; j < hd; ++j) zh[j] = bf16r(o[j] * inv);
