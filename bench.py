@@ -37,20 +37,20 @@ CONFIGS = {
     "c0": dict(dims=(128, 4, 4, 512, 160), row_chars=64, quant="dense",
                desc="C0: toy decoder (128,4,4,512,160) dense, 32-token prefix + 64-token row, 8 new tokens"),
     "c1": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="dense",
-               desc="C1: 0.5B-class decoder (1280,24,20,5120,128) bf16 dense, 32-token prefix + 64-token row, "
+               desc="C1: 0.5B-class decoder (1280,24,20,5120,128) fp16 dense, 32-token prefix + 64-token row, "
                     "8 new tokens"),
     "c2-w8a8": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="q8", act_quant=True,
                     desc="C2: C1 model, q8_perchannel RTN weights + per-token int8 activations (W8A8, "
                          "tcgen05 kind::i8), 32+64 tokens, 8 new tokens"),
     "c2-w4a16": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="q4",
-                     desc="C2: C1 model, q4_perchannel RTN weights, bf16 activations (W4A16), 32+64, 8 new"),
+                     desc="C2: C1 model, q4_perchannel RTN weights, fp16 activations (W4A16), 32+64, 8 new"),
     "c3": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="sparse24", act_quant=True,
                heads=[10] * 24, ffn=[2560] * 24,
                desc="C3: C1 model pruned 50% (10 of 20 heads, FFN 2560) + 2:4 magnitude + q8 (sparse24_q8), "
                     "W8A8, 32+64, 8 new"),
-    "c3-bf16": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="sparse24",
+    "c3-f16": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="sparse24",
                     heads=[10] * 24, ffn=[2560] * 24,
-                    desc="C3 model (pruned 50% + 2:4 + q8 codes, sparse24_q8) with bf16 activations - the drop-in "
+                    desc="C3 model (pruned 50% + 2:4 + q8 codes, sparse24_q8) with fp16 activations - the drop-in "
                          "default without act_quant: 2:4 sparse tensor cores kind::f16, 32+64, 8 new"),
     "c3b": dict(dims=(1280, 24, 20, 5120, 128), row_chars=64, quant="sparse24", act_quant=True,
                 heads=[7 + l % 6 for l in range(24)], ffn=[2500 + 12 * l for l in range(24)],
@@ -66,7 +66,7 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 
 
 def load_peaks() -> tuple[dict, str]:
-    """hbm / bf16 denominators: the driver's MEASURED_PEAKS.json; else this repo's own measurement
+    """hbm / 16-bit tensor denominators (fp16 and bf16 run at the same tcgen05 kind::f16 rate): the driver's MEASURED_PEAKS.json; else this repo's own measurement
     on the pool (profiles/r02_peaks.json, profiles/peaks.py); else the guide's fallback."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -510,7 +510,7 @@ def run_gpu_arm(args, cfg: dict, world: int, rank: int, local: int) -> None:
     line = {
         "metric": "rows/sec", "value": value, "unit": "rows/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "s8 x s8 -> s32 (W8A8)" if cfg.get("act_quant") else "bf16", "data": "synthetic (seeded rows, random-init weights: ToyModelParams::init seed 42)",
+        "dtype": "s8 x s8 -> s32 (W8A8)" if cfg.get("act_quant") else "f16", "data": "synthetic (seeded rows, random-init weights: ToyModelParams::init seed 42)",
         "config": {"workload": cfg["desc"], "rows_per_step_per_gpu": B, "max_new_tokens": MAX_NEW,
                    "tokens_per_engine_step": args.tokens_per_step or (
                        "SMs/2 x 224 (16576 on B200: whole waves of the 2:4 sparse kernel's 224-token tiles)"

@@ -53,9 +53,9 @@ typedef struct iolm_cuda_opts {
                                   launch between kernels), so the host runs ahead of the device */
   int32_t kernel_timing;       /* 1: time every kernel class with CUDA events (iolm_cuda_kernel_times) */
   int32_t sparse_mma;          /* -1: expand sparse24_q8 to dense codes; 0/1: 2:4 sparse tensor cores (kind::i8 with
-                                  act_quant, kind::f16 over bf16 activations without) */
-  int32_t int4_mma;            /* -1: expand q4 codes to bf16 in HBM; 0/1: int4 in HBM, expanded in smem (W4A16) */
-  int32_t prefill_tc;          /* prefill attention: -1 mma.sync; 0 default (tcgen05 for hd 128); 1 tcgen05 for hd 64 too */
+                                  act_quant, kind::f16 over fp16 activations without) */
+  int32_t int4_mma;            /* -1: expand q4 codes to fp16 in HBM; 0/1: int4 in HBM, expanded in smem (W4A16) */
+  int32_t prefill_tc;          /* prefill attention: -1 mma.sync; 0 default (tcgen05: 128-query tiles for hd 128, head-pair tiles for hd 64); 1 128-query tiles for hd 64 too */
   int32_t reserved[6];
 } iolm_cuda_opts;
 
@@ -146,7 +146,7 @@ int iolm_cuda_forward_logits(iolm_cuda_ctx* ctx, const int32_t* ids, const uint8
 /*
  * forward with calibration capture (ModelRuntime::forward(ids, mask, counter, CaptureSink*),
  * runtime.hpp:22-28 / :48-49, used by capture_calibration, proj/src/calib.cpp:20-62): logits as in
- * iolm_cuda_forward_logits, plus the inputs every linear weight saw, as bf16 bit patterns, for ALL n
+ * iolm_cuda_forward_logits, plus the inputs every linear weight saw, as fp16 bit patterns, for ALL n
  * positions (the caller drops masked rows, as the reference records non-pad positions only).
  * Layout, layer by layer: [attn_in n x d][attn_out_in n x kh_l][ffn_in n x d][ffn_mid n x f_l]
  * (capture points "layers.<l>.attn_in" = LN1 output, "attn_out_in" = attention output, "ffn_in" =
@@ -172,7 +172,7 @@ int iolm_cuda_forward_codes(iolm_cuda_ctx* ctx, const int32_t* ids, int32_t n, f
  * whole serialized bundle, decode every tensor (ModelRegistry::lookup, proj/src/optimize.cpp:
  * 139-151; deserialize_bundle / ModelBundle::hash, proj/src/model.cpp:348-411; ModelRuntime ctor,
  * proj/src/runtime.cpp:60-89). An image holds the weights exactly as this engine keeps them in HBM
- * (bf16 / int8 / 2:4-compressed codes + pre-tiled metadata / packed int4, per-row scales), the model
+ * (fp16 / int8 / 2:4-compressed codes + pre-tiled metadata / packed int4, per-row scales), the model
  * config and the bundle hash, so loading is a streamed file read + H2D copy: no hashing, no decode,
  * no host repack, and half the bytes of the f32 bundle for dense models.
  *
@@ -221,10 +221,10 @@ const char* iolm_cuda_last_error(void);
 
 /* ---- kernel-level entry points used by the parity tests (device work, host buffers) ---- */
 
-/* C[M x N] = A[M x K] * W[N x K]^T with bf16 operands (raw uint16 bit patterns), f32 result,
+/* C[M x N] = A[M x K] * W[N x K]^T with fp16 operands (raw uint16 bit patterns), f32 result,
  * through the production tcgen05 GEMM. epi: 0 f32 store, 2 GELU (result returned as f32 after a
- * bf16 round trip). bn: 256 = 2-SM 256x256 tiles (CTA pairs), 128 = single-CTA 128x128 tiles. */
-int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, float* C, int32_t M, int32_t N,
+ * fp16 round trip). bn: 256 = 2-SM 256x256 tiles (CTA pairs), 128 = single-CTA 128x128 tiles. */
+int iolm_cuda_debug_gemm_f16(const uint16_t* A, const uint16_t* W, float* C, int32_t M, int32_t N,
                               int32_t K, int32_t bn, int32_t epi);
 
 /* W8A8 integer GEMM: C_i32[M x N] = A_s8[M x K] * W_s8[N x K]^T through tcgen05 kind::i8.
@@ -233,12 +233,12 @@ int iolm_cuda_debug_gemm_s8(const int8_t* A, const int8_t* W, int32_t* C, int32_
                             int32_t K, int32_t pair);
 
 /* Device-only GEMM timing (kernel tuning): mean ms per launch of `iters` launches on synthetic
- * operands. epi: 0 f32, 1 bf16, 2 gelu, 3 residual-add, 5 s32 (i8 only), 6 none (mainloop only).
- * i8: 0 bf16 x bf16, 1 s8 x s8 (W8A8), 2 bf16 x int4 (W4A16, K % 32 == 0). */
+ * operands. epi: 0 f32, 1 fp16, 2 gelu, 3 residual-add, 5 s32 (i8 only), 6 none (mainloop only).
+ * i8: 0 fp16 x fp16, 1 s8 x s8 (W8A8), 2 fp16 x int4 (W4A16, K % 32 == 0). */
 int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_t epi, int32_t pair, int32_t i8,
                               int32_t iters, float* ms_out);
 
-/* Per-token int8 activation quantization (the W8A8 rule) of bf16 rows [n x d] on the
+/* Per-token int8 activation quantization (the W8A8 rule) of fp16 rows [n x d] on the
  * device: codes [n x d] and one f32 scale per row. */
 /* 2:4 sparse W8A8 GEMM on the sparse tensor cores (tcgen05.mma.sp kind::i8): X_s8 [T x K] times a
  * sparse24_q8 tensor payload W [N x K] exactly as stored in a bundle (proj/src/model.cpp:255-290).
@@ -246,26 +246,26 @@ int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_t epi, int3
  * -> out_f32 (w_scale = the payload's per-row scales). K % 16 == 0. */
 int iolm_cuda_debug_gemm_sp24(const int8_t* X, const uint8_t* payload, int32_t T, int32_t N, int32_t K,
                               int32_t epi, const float* a_scale, int32_t* out_s32, float* out_f32);
-/* W4A16 GEMM: C[M x N] = A_bf16[M x K] * (codes(W) * scale)^T with W a q4_perchannel tensor payload
+/* W4A16 GEMM: C[M x N] = A_f16[M x K] * (codes(W) * scale)^T with W a q4_perchannel tensor payload
  * exactly as stored in a bundle (nibble rows + per-row f32 scales, proj/src/model.cpp:164-176); the
- * int4 codes are expanded to bf16 inside the kernel. epi 0: f32 out. pair as in debug_gemm_s8. */
+ * int4 codes are expanded to fp16 inside the kernel. epi 0: f32 out. pair as in debug_gemm_s8. */
 int iolm_cuda_debug_gemm_w4(const uint16_t* A, const uint8_t* payload, float* C, int32_t M, int32_t N, int32_t K,
                             int32_t pair);
-/* 2:4 sparse bf16 GEMM (tcgen05.mma.sp kind::f16): X bf16 [T x K] (raw uint16) times a sparse24_q8
- * payload's kept codes as exact bf16 integers, out_f32 [T x N] = acc * payload scale[n]. K % 16 == 0. */
-int iolm_cuda_debug_gemm_sp24_bf16(const uint16_t* X, const uint8_t* payload, int32_t T, int32_t N, int32_t K,
+/* 2:4 sparse fp16 GEMM (tcgen05.mma.sp kind::f16): X fp16 [T x K] (raw uint16) times a sparse24_q8
+ * payload's kept codes as exact fp16 integers, out_f32 [T x N] = acc * payload scale[n]. K % 16 == 0. */
+int iolm_cuda_debug_gemm_sp24_f16(const uint16_t* X, const uint8_t* payload, int32_t T, int32_t N, int32_t K,
                                    float* out_f32);
 /* Device-only timing of the sparse GEMM: mean ms per launch (epi as in debug_gemm_time). */
 int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, float* ms_out);
-/* The same for the bf16 (kind::f16) sparse kernel. */
-int iolm_cuda_debug_gemm_sp24_bf16_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, float* ms_out);
+/* The same for the fp16 (kind::f16) sparse kernel. */
+int iolm_cuda_debug_gemm_sp24_f16_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters, float* ms_out);
 
 /* The multi-device row split (host only, no device work): cut[0..*n_cut) with cut[0] = 0 and
  * cut[last] = n_rows; range i = rows [cut[i], cut[i+1]). cut needs shards + 1 entries. */
 int iolm_cuda_debug_partition(const int64_t* row_offsets, int64_t n_rows, int32_t shards, int64_t* cut,
                               int32_t* n_cut);
 
-int iolm_cuda_debug_quant_rows_bf16(const uint16_t* x, int32_t n, int32_t d, int8_t* codes, float* scales);
+int iolm_cuda_debug_quant_rows_f16(const uint16_t* x, int32_t n, int32_t d, int8_t* codes, float* scales);
 
 #ifdef __cplusplus
 }

@@ -146,6 +146,23 @@ inline Config read_config(const iolm_cuda_ctx* ctx) {
   return cfg;
 }
 
+// IEEE binary16 bit pattern -> f32 (exact; the engine's captured activations are fp16).
+inline float f16_to_f32(uint16_t h) {
+  const uint32_t sign = static_cast<uint32_t>(h & 0x8000u) << 16;
+  uint32_t e = (h >> 10) & 0x1Fu, m = h & 0x3FFu, bits;
+  if (e == 0x1F) bits = sign | 0x7F800000u | (m << 13);  // inf / nan
+  else if (e != 0) bits = sign | ((e + 112u) << 23) | (m << 13);
+  else if (m == 0) bits = sign;
+  else {  // subnormal: renormalise
+    e = 113;
+    while (!(m & 0x400u)) { m <<= 1; --e; }
+    bits = sign | (e << 23) | ((m & 0x3FFu) << 13);
+  }
+  float f;
+  std::memcpy(&f, &bits, 4);
+  return f;
+}
+
 class ModelRuntime {
  public:
   explicit ModelRuntime(std::span<const uint8_t> bundle_bytes, int device = 0, const iolm_cuda_opts* opts = nullptr) {
@@ -230,7 +247,7 @@ class ModelRuntime {
   // "not to be read" (runtime.hpp:44-47); they come back as zeros so the Matrix stays finite.
   // With a CaptureSink, the inputs of every linear weight at the non-pad positions are recorded
   // under the reference's capture-point names (capture_calibration, calib.cpp:44-51), captured on
-  // the GPU as bf16 and widened to f32.
+  // the GPU as fp16 and widened to f32.
 #ifdef IOLM_CUDA_WITH_REFERENCE_TYPES
   Logits forward(std::span<const int> ids, std::span<const uint8_t> mask, FlopCounter& counter,
                  iolm::CaptureSink* capture = nullptr) const {
@@ -267,10 +284,7 @@ class ModelRuntime {
         for (int t = 0; t < n; ++t) {
           if (mask.empty() || mask[t]) {
             row.resize(cols);
-            for (int c = 0; c < cols; ++c) {
-              const uint32_t bits = static_cast<uint32_t>(cap[off + static_cast<size_t>(t) * cols + c]) << 16;
-              std::memcpy(&row[c], &bits, 4);
-            }
+            for (int c = 0; c < cols; ++c) row[c] = f16_to_f32(cap[off + static_cast<size_t>(t) * cols + c]);
             capture->add_row(point, row);
           }
         }

@@ -197,22 +197,36 @@ typedef struct {
   const int8_t* const* wcodes_t;
   const float* const* wscale;
   /* act_quant only: 1 = the GPU W8A8 engine's rounding points - q/k/v leave the QKV GEMM epilogue
-   * as bf16 (KV pages, q operand), the attention output z and the GELU output g are bf16 before
-   * they are quantized (engine.cu launch_step; kernels.cu quant_rows_kernel). bf16 = RNE of f32. */
+   * as fp16 (KV pages, q operand), the attention output z and the GELU output g are fp16 before
+   * they are quantized (engine.cu launch_step; kernels.cu quant_rows_kernel). fp16 = RNE of f32. */
   int gpu_points;
 } orc_model;
 
-/* f32 -> bf16 -> f32, round to nearest even (cvt.rn.bf16.f32 / __float2bfloat16_rn). */
-static float bf16r(float x) {
+/* f32 -> IEEE binary16 -> f32, round to nearest even (cvt.rn.f16.f32 / __float2half_rn): the GPU
+ * engine's 16-bit storage type (paper_2507_04967_b200/csrc/dtype.hpp). Subnormal halves keep the
+ * 2^-24 quantum; magnitudes >= 65520 become inf. */
+static float h16r(float x) {
   uint32_t u;
   memcpy(&u, &x, 4);
-  if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
-  u &= 0xffff0000u;
-  memcpy(&x, &u, 4);
+  const uint32_t sign = u & 0x80000000u, a = u & 0x7fffffffu;
+  if (a >= 0x7f800000u) return x; /* inf / nan */
+  float ax;
+  memcpy(&ax, &a, 4);
+  uint32_t r;
+  if (ax >= 65520.0f) {
+    r = 0x7f800000u;
+  } else if (ax < 6.103515625e-05f) { /* subnormal half: multiples of 2^-24 */
+    const float q = rintf(ax * 16777216.0f) * 5.9604644775390625e-08f;
+    memcpy(&r, &q, 4);
+  } else { /* 10 mantissa bits: round away the low 13 */
+    r = (a + 0xfffu + ((a >> 13) & 1u)) & ~0x1fffu;
+  }
+  r |= sign;
+  memcpy(&x, &r, 4);
   return x;
 }
-static void bf16r_rows(float* p, size_t n) {
-  for (size_t i = 0; i < n; ++i) p[i] = bf16r(p[i]);
+static void h16r_rows(float* p, size_t n) {
+  for (size_t i = 0; i < n; ++i) p[i] = h16r(p[i]);
 }
 
 /* Capture of the int8 GEMM operands of one W8A8 forward (orc_forward_codes): per layer the codes of
@@ -263,15 +277,19 @@ static float gelu_gpu(float x) {
 }
 
 /* The GPU prefill attention of one (query, head) at the W8A8 engine's rounding points
- * (kernels.cu attn_prefill_kernel for hd <= 64: 32-key blocks; attn_tc.cu for hd 128: 64-key blocks;
+ * (kernels.cu attn_prefill_kernel for hd <= 32: 32-key blocks, exact running max; attn_tc.cu
+ * attn_prefill_hp_kernel for hd 64: 32-key blocks, reference max moved only by a jump of more than
+ * HP_RESCALE = 8; attn_tc.cu attn_prefill_tc_kernel for hd 128: 64-key blocks, exact running max;
  * blocks aligned to absolute positions): online softmax in base 2 with scale_log2 = log2(e)/sqrt(hd)
- * in f32, per block m_new = max(m, max_j(s_j) * scale_log2), alpha = 2^(m - m_new), l = l * alpha +
- * sum_j p_j with p_j = 2^(fma(s_j, scale_log2, -m_new)) in f32, O = O * alpha + sum_j bf16(p_j) * v_j
- * (the PV product takes P as bf16), z = bf16(O * (1 / l)). Scores are f32 dots of the bf16 q / k.
+ * in f32, per block ms = max_j(s_j) * scale_log2, m_new = max(m, ms) (hd 64: m_new = ms only when
+ * m = -inf or ms > m + 8, else m), alpha = 2^(m - m_new), l = l * alpha + sum_j p_j with
+ * p_j = 2^(fma(s_j, scale_log2, -m_new)) in f32, O = O * alpha + sum_j fp16(p_j) * v_j (the PV product
+ * takes P as fp16), z = fp16(O * (1 / l)). Scores are f32 dots of the fp16 q / k.
  * Remaining differences to the GPU are f32 summation orders and the 2-ulp ex2.approx. */
 static void flash_head_gpu(const float* qh, const float* k0, const float* v0, int ld, int hd, int span,
                            const uint8_t* valid, float* zh) {
   const int KB = hd >= 128 ? 64 : 32;
+  const int stale = hd == 64; /* attn_prefill_hp_kernel's reference-max rule */
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   float m_run = -INFINITY, l_run = 0.0f;
   float o[128], s[64];
@@ -291,8 +309,10 @@ static void flash_head_gpu(const float* qh, const float* k0, const float* v0, in
       s[t] = acc;
       if (acc > mx) mx = acc;
     }
-    const float mnew = fmaxf(m_run, mx * scale_log2);
-    const float alpha = mnew == -INFINITY ? 1.0f : exp2f(m_run - mnew);
+    const float ms = mx * scale_log2;
+    float mnew = fmaxf(m_run, ms);
+    if (stale) mnew = (m_run == -INFINITY || ms > m_run + 8.0f) ? ms : m_run;
+    const float alpha = (mnew == -INFINITY || m_run == -INFINITY) ? 1.0f : exp2f(m_run - mnew);
     const float msub = mnew == -INFINITY ? 0.0f : mnew;
     m_run = mnew;
     l_run *= alpha;
@@ -303,14 +323,14 @@ static void flash_head_gpu(const float* qh, const float* k0, const float* v0, in
     for (int t = 0; t < nk; ++t) {
       const float pv = exp2f(fmaf(s[t], scale_log2, -msub));
       l_run += pv;
-      const float pb = bf16r(pv);
+      const float pb = h16r(pv);
       if (pb == 0.0f) continue;
       const float* vr = v0 + (size_t)(key0 + t) * ld;
       for (int j = 0; j < hd; ++j) o[j] = fmaf(pb, vr[j], o[j]);
     }
   }
   const float inv = l_run > 0.0f ? 1.0f / l_run : 0.0f;
-  for (int j = 0; j < hd; ++j) zh[j] = bf16r(o[j] * inv);
+  for (int j = 0; j < hd; ++j) zh[j] = h16r(o[j] * inv);
 }
 
 typedef struct {
@@ -374,9 +394,9 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
       matmul_wt(h, n, d, m->wv[l], kh, vn);
     }
     if (m->act_quant && m->gpu_points) {
-      bf16r_rows(q, (size_t)n * kh);
-      bf16r_rows(kn, (size_t)n * kh);
-      bf16r_rows(vn, (size_t)n * kh);
+      h16r_rows(q, (size_t)n * kh);
+      h16r_rows(kn, (size_t)n * kh);
+      h16r_rows(vn, (size_t)n * kh);
     }
     *madds += 3ull * n * d * kh;
     for (int i = 0; i < n; ++i) {
@@ -429,7 +449,7 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
         *madds += (uint64_t)span * hd;
       }
     }
-    if (m->act_quant && m->gpu_points) bf16r_rows(z, (size_t)n * kh);
+    if (m->act_quant && m->gpu_points) h16r_rows(z, (size_t)n * kh);
     if (m->act_quant) linear_w8a8(m, l * 6 + 3, z, n, kh, d, ao);
     else matmul_wt(z, n, kh, m->wo[l], d, ao);
     *madds += (uint64_t)n * kh * d;
@@ -442,7 +462,7 @@ static void advance(const orc_model* m, orc_state* st, const int* toks, const ui
       for (size_t t = 0; t < (size_t)n * f; ++t) g[t] = gelu_gpu(g[t]);
     else
       for (size_t t = 0; t < (size_t)n * f; ++t) g[t] = gelu(g[t]);
-    if (m->act_quant && m->gpu_points) bf16r_rows(g, (size_t)n * f);
+    if (m->act_quant && m->gpu_points) h16r_rows(g, (size_t)n * f);
     if (m->act_quant) linear_w8a8(m, l * 6 + 5, g, n, f, d, ao);
     else matmul_wt(g, n, f, m->w_out[l], d, ao);
     *madds += (uint64_t)n * f * d;

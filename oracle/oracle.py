@@ -146,7 +146,7 @@ class OracleModel:
     def __init__(self, bundle: bytes | dict, act_quant: bool = False, gpu_points: bool = False):
         """act_quant: the W8A8 restatement (per-token int8 activations, int8 weight codes, exact
         int32 accumulation) - requires q8 / sparse24_q8 encodings for every linear weight.
-        gpu_points (W8A8 only): round q/k/v, the attention output and the GELU output to bf16 where
+        gpu_points (W8A8 only): round q/k/v, the attention output and the GELU output to fp16 where
         the GPU engine stores them, before they are quantized (W8A8 semantics)."""
         b = parse_bundle(bundle, with_codes=act_quant) if isinstance(bundle, (bytes, bytearray)) else bundle
         cfg, T = b["config"], b["tensors"]

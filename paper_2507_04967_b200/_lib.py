@@ -92,10 +92,10 @@ SIGNATURES = {
     "iolm_cuda_last_error": (C.c_char_p, []),
     "iolm_cuda_set_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
     "iolm_cuda_kernel_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
-    "iolm_cuda_debug_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+    "iolm_cuda_debug_gemm_f16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                             C.c_int32, C.c_int32, C.c_int32]),
     "iolm_cuda_debug_gemm_time": (C.c_int, [C.c_int32] * 7 + [C.POINTER(C.c_float)]),
-    "iolm_cuda_debug_quant_rows_bf16": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "iolm_cuda_debug_quant_rows_f16": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "iolm_cuda_debug_gemm_s8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                           C.c_int32, C.c_int32]),
     "iolm_cuda_debug_gemm_sp24": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
@@ -103,10 +103,10 @@ SIGNATURES = {
     "iolm_cuda_debug_gemm_w4": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                           C.c_int32]),
     "iolm_cuda_debug_partition": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]),
-    "iolm_cuda_debug_gemm_sp24_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+    "iolm_cuda_debug_gemm_sp24_f16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                                  C.c_void_p]),
     "iolm_cuda_debug_gemm_sp24_time": (C.c_int, [C.c_int32] * 5 + [C.POINTER(C.c_float)]),
-    "iolm_cuda_debug_gemm_sp24_bf16_time": (C.c_int, [C.c_int32] * 5 + [C.POINTER(C.c_float)]),
+    "iolm_cuda_debug_gemm_sp24_f16_time": (C.c_int, [C.c_int32] * 5 + [C.POINTER(C.c_float)]),
 }
 
 _LIB = None

@@ -10,7 +10,7 @@
 #include "tma_host.hpp"
 
 namespace iolmh {
-void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_t* dst, int ldd, float* scale,
+void launch_quant_rows(const h16* src, int lds, int M, int cols, int8_t* dst, int ldd, float* scale,
                        cudaStream_t st);
 }
 
@@ -36,7 +36,7 @@ int sm_count() {
 
 }  // namespace
 
-extern "C" int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, float* C,
+extern "C" int iolm_cuda_debug_gemm_f16(const uint16_t* A, const uint16_t* W, float* C,
                                          int32_t M, int32_t N, int32_t K, int32_t bn,
                                          int32_t epi) {
   static const bool use_tma_epi =
@@ -46,19 +46,19 @@ extern "C" int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, f
       throw ContractViolation("debug_gemm: need positive M,N and K % 8 == 0");
     DevBuf<uint16_t> dA(static_cast<size_t>(M) * K), dW(static_cast<size_t>(N) * K);
     DevBuf<float> dC(static_cast<size_t>(M) * N);
-    DevBuf<__nv_bfloat16> dG(static_cast<size_t>(M) * N);
+    DevBuf<h16> dG(static_cast<size_t>(M) * N);
     CUDA_OK(cudaMemcpy(dA.p, A, sizeof(uint16_t) * M * K, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(dW.p, W, sizeof(uint16_t) * N * K, cudaMemcpyHostToDevice));
-    CUtensorMap ta = make_kmajor_map(dA.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, M, 2ull * K, 128);
-    CUtensorMap tb = make_kmajor_map(dW.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, N, 2ull * K, 128);
+    CUtensorMap ta = make_kmajor_map(dA.p, H16_TMA, 2, K, M, 2ull * K, 128);
+    CUtensorMap tb = make_kmajor_map(dW.p, H16_TMA, 2, K, N, 2ull * K, 128);
     iolmk::GemmEpi ep;
     ep.M = M;
     ep.N = N;
     if (epi == iolmk::EPI_F32) {
       ep.out = dC.p;
       ep.ldo = N;
-    } else if (epi == iolmk::EPI_GELU_BF16 || epi == iolmk::EPI_BF16) {
-      if (N % 8 != 0) throw ContractViolation("debug_gemm: bf16 epilogue needs N % 8 == 0");
+    } else if (epi == iolmk::EPI_GELU_H16 || epi == iolmk::EPI_H16) {
+      if (N % 8 != 0) throw ContractViolation("debug_gemm: fp16 epilogue needs N % 8 == 0");
       ep.out = dG.p;
       ep.ldo = N;
     } else if (epi == iolmk::EPI_RESID_F32) {
@@ -71,16 +71,16 @@ extern "C" int iolm_cuda_debug_gemm_bf16(const uint16_t* A, const uint16_t* W, f
     // the TMA store / reduce-add epilogue, as the engine runs it (N multiple of 8 keeps rows 16-B aligned)
     CUtensorMap tc;
     const CUtensorMap* out_map = nullptr;
-    if (use_tma_epi && N % 8 == 0 && (epi == iolmk::EPI_RESID_F32 || epi == iolmk::EPI_GELU_BF16 || epi == iolmk::EPI_BF16)) {
+    if (use_tma_epi && N % 8 == 0 && (epi == iolmk::EPI_RESID_F32 || epi == iolmk::EPI_GELU_H16 || epi == iolmk::EPI_H16)) {
       tc = epi == iolmk::EPI_RESID_F32 ? make_out_map(dC.p, true, N, M, 4ull * N) : make_out_map(dG.p, false, N, M, 2ull * N);
       out_map = &tc;
     }
     launch_gemm(bn == 256, false, epi, ta, tb, M, N, K, ep, nullptr, sm_count(), out_map);
     CUDA_OK(cudaDeviceSynchronize());
-    if (epi == iolmk::EPI_GELU_BF16 || epi == iolmk::EPI_BF16) {
-      std::vector<__nv_bfloat16> h(static_cast<size_t>(M) * N);
+    if (epi == iolmk::EPI_GELU_H16 || epi == iolmk::EPI_H16) {
+      std::vector<h16> h(static_cast<size_t>(M) * N);
       CUDA_OK(cudaMemcpy(h.data(), dG.p, h.size() * 2, cudaMemcpyDeviceToHost));
-      for (size_t i = 0; i < h.size(); ++i) C[i] = __bfloat162float(h[i]);
+      for (size_t i = 0; i < h.size(); ++i) C[i] = __half2float(h[i]);
     } else {
       CUDA_OK(cudaMemcpy(C, dC.p, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
     }
@@ -109,7 +109,7 @@ extern "C" int iolm_cuda_debug_gemm_s8(const int8_t* A, const int8_t* W, int32_t
   });
 }
 
-extern "C" int iolm_cuda_debug_quant_rows_bf16(const uint16_t* x, int32_t n, int32_t d, int8_t* codes,
+extern "C" int iolm_cuda_debug_quant_rows_f16(const uint16_t* x, int32_t n, int32_t d, int8_t* codes,
                                                float* scales) {
   return guarded([&] {
     if (n <= 0 || d <= 0 || d % 8 != 0) throw ContractViolation("debug_quant_rows: need d % 8 == 0");
@@ -117,7 +117,7 @@ extern "C" int iolm_cuda_debug_quant_rows_bf16(const uint16_t* x, int32_t n, int
     DevBuf<int8_t> dc(static_cast<size_t>(n) * d);
     DevBuf<float> ds(n);
     CUDA_OK(cudaMemcpy(dx.p, x, sizeof(uint16_t) * n * d, cudaMemcpyHostToDevice));
-    launch_quant_rows(reinterpret_cast<const __nv_bfloat16*>(dx.p), d, n, d, dc.p, d, ds.p, nullptr);
+    launch_quant_rows(reinterpret_cast<const h16*>(dx.p), d, n, d, dc.p, d, ds.p, nullptr);
     CUDA_OK(cudaDeviceSynchronize());
     CUDA_OK(cudaMemcpy(codes, dc.p, static_cast<size_t>(n) * d, cudaMemcpyDeviceToHost));
     CUDA_OK(cudaMemcpy(scales, ds.p, sizeof(float) * n, cudaMemcpyDeviceToHost));
@@ -125,7 +125,7 @@ extern "C" int iolm_cuda_debug_quant_rows_bf16(const uint16_t* x, int32_t n, int
 }
 
 // Device-only GEMM timing for kernel tuning: random operands, `iters` back-to-back launches timed
-// with CUDA events; returns the mean ms per launch. epi: 0 f32, 1 bf16, 2 gelu, 3 resid, 5 s32.
+// with CUDA events; returns the mean ms per launch. epi: 0 f32, 1 fp16, 2 gelu, 3 resid, 5 s32.
 extern "C" int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_t epi, int32_t pair, int32_t i8,
                                          int32_t iters, float* ms_out) {
   return guarded([&] {
@@ -139,9 +139,9 @@ extern "C" int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_
     CUDA_OK(cudaMemset(dC.p, 0, sizeof(float) * M * N));
     CUDA_OK(cudaMemset(ws.p, 0, sizeof(float) * N));
     CUDA_OK(cudaMemset(as.p, 0, sizeof(float) * M));
-    const auto dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    const bool w4 = i8 == 2;  // W4A16: bf16 activations, packed int4 weights (K/2 bytes per row)
-    const auto dt_a = w4 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : dt;
+    const auto dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : H16_TMA;
+    const bool w4 = i8 == 2;  // W4A16: fp16 activations, packed int4 weights (K/2 bytes per row)
+    const auto dt_a = w4 ? H16_TMA : dt;
     const size_t eb_a = w4 ? 2 : eb;
     if (w4) i8 = 0;
     CUtensorMap ta = make_kmajor_map(dA.p, dt_a, static_cast<int>(eb_a), K, M, eb_a * K, 128);
@@ -161,7 +161,7 @@ extern "C" int iolm_cuda_debug_gemm_time(int32_t M, int32_t N, int32_t K, int32_
         std::getenv("IOLM_GEMM_TMA_EPI") == nullptr || std::string(std::getenv("IOLM_GEMM_TMA_EPI")) != "0";
     CUtensorMap tc;
     const CUtensorMap* out_map = nullptr;
-    if (use_tma_epi && N % 8 == 0 && (epi == iolmk::EPI_RESID_F32 || epi == iolmk::EPI_GELU_BF16 || epi == iolmk::EPI_BF16)) {
+    if (use_tma_epi && N % 8 == 0 && (epi == iolmk::EPI_RESID_F32 || epi == iolmk::EPI_GELU_H16 || epi == iolmk::EPI_H16)) {
       tc = make_out_map(dC.p, epi == iolmk::EPI_RESID_F32, N, M, (epi == iolmk::EPI_RESID_F32 ? 4ull : 2ull) * N);
       out_map = &tc;
     }
@@ -224,15 +224,15 @@ extern "C" int iolm_cuda_debug_gemm_sp24(const int8_t* X, const uint8_t* payload
   });
 }
 
-// 2:4 sparse bf16 GEMM (tcgen05.mma.sp kind::f16): X_bf16 [T x K] (uint16 bit patterns) times the
-// sparse24_q8 payload's kept codes as exact bf16 integers; out_f32 [T x N] = acc * w_scale[n] (the
+// 2:4 sparse fp16 GEMM (tcgen05.mma.sp kind::f16): X_h16 [T x K] (uint16 bit patterns) times the
+// sparse24_q8 payload's kept codes as exact fp16 integers; out_f32 [T x N] = acc * w_scale[n] (the
 // W8A16 2:4 path the engine runs for sparse24_q8 bundles without act_quant).
-extern "C" int iolm_cuda_debug_gemm_sp24_bf16(const uint16_t* X, const uint8_t* payload, int32_t T, int32_t N,
+extern "C" int iolm_cuda_debug_gemm_sp24_f16(const uint16_t* X, const uint8_t* payload, int32_t T, int32_t N,
                                               int32_t K, float* out_f32) {
   return guarded([&] {
     if (T <= 0 || N <= 0 || K <= 0 || K % 16 != 0)
-      throw ContractViolation("debug_gemm_sp24_bf16: need positive T, N and K % 16 == 0");
-    if (!sp24_check(payload, N, K)) throw Unsupported("debug_gemm_sp24_bf16: positions not ascending");
+      throw ContractViolation("debug_gemm_sp24_h16: need positive T, N and K % 16 == 0");
+    if (!sp24_check(payload, N, K)) throw Unsupported("debug_gemm_sp24_h16: positions not ascending");
     const Sp24Layout l = sp24_layout(N, K, true);
     std::vector<uint8_t> codes(l.code_bytes(), 0);
     std::vector<uint8_t> meta(l.meta_bytes(), 0x44);
@@ -252,7 +252,7 @@ extern "C" int iolm_cuda_debug_gemm_sp24_bf16(const uint16_t* X, const uint8_t* 
     ep.out = dC.p;
     ep.ldo = N;
     ep.w_scale = dS.p;
-    launch_gemm_sp(iolmk::EPI_F32, sp24_codes_map(l, dW.p), sp24_act_map_bf16(dX.p, K, T, K), sp24_meta_map(l, dE.p),
+    launch_gemm_sp(iolmk::EPI_F32, sp24_codes_map(l, dW.p), sp24_act_map_h16(dX.p, K, T, K), sp24_meta_map(l, dE.p),
                    K, l.katoms_pad, ep, nullptr, sm_count(), true);
     CUDA_OK(cudaDeviceSynchronize());
     CUDA_OK(cudaMemcpy(out_f32, dC.p, sizeof(float) * T * N, cudaMemcpyDeviceToHost));
@@ -281,7 +281,7 @@ static void sp24_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iter
   ep.a_scale = f16 ? nullptr : dA.p;
   ep.w_scale = dS.p;
   const CUtensorMap ta = sp24_codes_map(l, dW.p), te = sp24_meta_map(l, dE.p);
-  const CUtensorMap tb = f16 ? sp24_act_map_bf16(dX.p, K, T, K) : sp24_act_map(reinterpret_cast<int8_t*>(dX.p), K, T, K);
+  const CUtensorMap tb = f16 ? sp24_act_map_h16(dX.p, K, T, K) : sp24_act_map(reinterpret_cast<int8_t*>(dX.p), K, T, K);
   cudaEvent_t e0, e1;
   CUDA_OK(cudaEventCreate(&e0));
   CUDA_OK(cudaEventCreate(&e1));
@@ -302,7 +302,7 @@ extern "C" int iolm_cuda_debug_gemm_sp24_time(int32_t T, int32_t N, int32_t K, i
   return guarded([&] { sp24_time(T, N, K, epi, iters, false, ms_out); });
 }
 
-extern "C" int iolm_cuda_debug_gemm_sp24_bf16_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
+extern "C" int iolm_cuda_debug_gemm_sp24_f16_time(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
                                                    float* ms_out) {
   return guarded([&] { sp24_time(T, N, K, epi, iters, true, ms_out); });
 }
@@ -318,7 +318,7 @@ extern "C" int iolm_cuda_debug_gemm_w4(const uint16_t* A, const uint8_t* payload
     CUDA_OK(cudaMemcpy(dA.p, A, sizeof(uint16_t) * M * K, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy2D(dW.p, ld4, payload, rb, rb, N, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(dS.p, payload + rb * N, sizeof(float) * N, cudaMemcpyHostToDevice));
-    CUtensorMap ta = make_kmajor_map(dA.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, M, 2ull * K, 128);
+    CUtensorMap ta = make_kmajor_map(dA.p, H16_TMA, 2, K, M, 2ull * K, 128);
     CUtensorMap tb = make_w4_map(dW.p, K, N, ld4);
     iolmk::GemmEpi ep;
     ep.M = M;

@@ -2,13 +2,13 @@
 //
 // Replaces iolm::ModelRuntime (proj/src/runtime.cpp:60-345):
 //   * construction: the bundle is parsed/validated like the reference (bundle.cu), every linear
-//     weight is decoded ONCE on the device into the GEMM operand layout (bf16, K-major = the
+//     weight is decoded ONCE on the device into the GEMM operand layout (fp16, K-major = the
 //     bundle's own [out x in] layout, so no transpose), norms/embeddings stay fp32;
 //   * batch_decode: a continuous-batching scheduler. Each engine step is ONE batched forward over
 //     a token list mixing (a) one generated token for every live sequence and (b) the prompt tokens
 //     of newly admitted rows, so every GEMM runs at M = thousands of rows. The common prompt prefix
 //     of the call is prefilled once into shared KV pages that every row's page table references.
-//   * K/V live in a paged bf16 pool (16-token pages); attention reads through per-slot page tables.
+//   * K/V live in a paged fp16 pool (16-token pages); attention reads through per-slot page tables.
 //   * steps are pipelined: whether a row keeps decoding is decided by its emitted count and its
 //     length alone, except for EOS, so step k+1 is planned and launched before step k's tokens are
 //     read back. A row that hits EOS gets one speculative token in the next step; it is discarded.
@@ -41,25 +41,26 @@ using iolmk::AttnGroup;
 using iolmk::AttnParams;
 using iolmk::GemmEpi;
 
-void launch_ln(const float* x, int M, int d, const float* g, const float* b, __nv_bfloat16* h, int ldh,
+void launch_ln(const float* x, int M, int d, const float* g, const float* b, h16* h, int ldh,
                cudaStream_t st, int8_t* q8, float* qscale);
 void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_slot, const int* tok_pos,
                      const int32_t* last_tok, int M, int d, const float* tok_embed, const float* pos_embed, float* x,
-                     const float* g, const float* b, __nv_bfloat16* h, int ldh, cudaStream_t st, int8_t* q8,
+                     const float* g, const float* b, h16* h, int ldh, cudaStream_t st, int8_t* q8,
                      float* qscale);
-void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_t* dst, int ldd, float* scale,
+void launch_quant_rows(const h16* src, int lds, int M, int cols, int8_t* dst, int ldd, float* scale,
                        cudaStream_t st);
 void launch_decode_codes(const void* payload, int enc, int rows, int cols, void* dst, bool int8, int ld,
                          float* scales, cudaStream_t st);
 void launch_attention(const AttnParams& prefill, const AttnParams& decode, int hd, cudaStream_t st);
 bool launch_prefill_tc(const AttnParams& prefill, int hd, cudaStream_t st);
+void launch_prefill_hp(const AttnParams& prefill, cudaStream_t st);
 int decode_heads_per_cta(int heads, int hd);
 void launch_head(const float* x, int d, const int* rows, int n_rows, const float* g, const float* b,
                  const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
                  float* logits_out, cudaStream_t st);
 void launch_lcp(const int32_t* ids, const int64_t* offsets, int64_t n_rows, int limit, int* out, cudaStream_t st);
 void launch_check_ids(const int32_t* ids, int64_t n, int V, int* bad, cudaStream_t st);
-void launch_decode_weight(const void* payload, int enc, int rows, int cols, __nv_bfloat16* dst, int ld,
+void launch_decode_weight(const void* payload, int enc, int rows, int cols, h16* dst, int ld,
                           cudaStream_t st);
 void launch_transpose(const float* src, int rows, int cols, float* dst, cudaStream_t st);
 
@@ -114,20 +115,20 @@ int round_up(int x, int m) { return (x + m - 1) / m * m; }
 size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
 // Weights of one GEMM ([N x K], K-major as stored in the bundle) in one of three forms:
-//   VALUES : bf16(value)                       dense_f32 tensors (or mixed-encoding groups)
-//   CODES  : bf16(code) + f32 scale per row    q8 / q4 / sparse24 without activation quant (W8A16,
-//            W4A16): integer codes are exact in bf16, the scale is applied in the GEMM epilogue
+//   VALUES : fp16(value)                       dense_f32 tensors (or mixed-encoding groups)
+//   CODES  : fp16(code) + f32 scale per row    q8 / q4 / sparse24 without activation quant (W8A16,
+//            W4A16): integer codes are exact in fp16, the scale is applied in the GEMM epilogue
 //   INT8   : int8 code + f32 scale per row     q8 / sparse24 with act_quant (W8A8, kind::i8)
 //   SP24   : kept int8 codes [N x K/2] + 2:4 metadata + f32 scale per row: sparse24_q8 with
 //            act_quant on the sparse tensor cores (tcgen05.mma.sp kind::i8, gemm_sp_sm100.cuh)
 //   INT4   : packed q4 nibbles [N x ceil(K/2)] + f32 scale per row: W4A16, the codes are expanded
-//            to bf16 inside the GEMM (shared memory), never in HBM
-//   SP24F  : kept codes as exact bf16 [N x K/2] + 2:4 metadata + f32 scale per row: sparse24_q8
-//            WITHOUT act_quant on the sparse tensor cores (tcgen05.mma.sp kind::f16, bf16 activations)
+//            to fp16 inside the GEMM (shared memory), never in HBM
+//   SP24F  : kept codes as exact fp16 [N x K/2] + 2:4 metadata + f32 scale per row: sparse24_q8
+//            WITHOUT act_quant on the sparse tensor cores (tcgen05.mma.sp kind::f16, fp16 activations)
 enum WMode : int { W_VALUES = 0, W_CODES = 1, W_INT8 = 2, W_SP24 = 3, W_INT4 = 4, W_SP24F = 5 };
 struct GemmW {
   int mode = W_VALUES;
-  DevArray<__nv_bfloat16> wb;
+  DevArray<h16> wb;
   DevArray<int8_t> w8;
   DevArray<float> scale;
   CUtensorMap tm;
@@ -159,7 +160,7 @@ void weight_maps(GemmW& w, int N, int K, int ld) {
       w.tm = make_kmajor_map(w.w8.p, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, N, static_cast<uint64_t>(ld), 128);
       break;
     default:
-      w.tm = make_kmajor_map(w.wb.p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, N, 2ull * ld, 128);
+      w.tm = make_kmajor_map(w.wb.p, H16_TMA, 2, K, N, 2ull * ld, 128);
   }
 }
 
@@ -167,12 +168,12 @@ struct Layer {
   int heads = 0, kh = 0, f = 0;
   DevArray<float> ln1_g, ln1_b, ln2_g, ln2_b;
   GemmW qkv, o, in, out;
-  CUtensorMap tm_z, tm_g;    // bf16 A operands with this layer's K extent
+  CUtensorMap tm_z, tm_g;    // fp16 A operands with this layer's K extent
   CUtensorMap tm_z8, tm_g8;  // int8 A operands (W8A8)
   CUtensorMap tm_z8s, tm_g8s;  // the same in the sparse kernel's 112-row boxes
-  CUtensorMap tm_zs, tm_gs;    // bf16 z / g in the sparse kernel's 112-row boxes (W_SP24F)
-  CUtensorMap tm_g_out;        // g as the W_in GEMM's TMA store target (bf16 32 x 32 boxes)
-  DevArray<__nv_bfloat16> kv;  // paged pool [pages][K|V][heads][PAGE][hd]
+  CUtensorMap tm_zs, tm_gs;    // fp16 z / g in the sparse kernel's 112-row boxes (W_SP24F)
+  CUtensorMap tm_g_out;        // g as the W_in GEMM's TMA store target (fp16 32 x 32 boxes)
+  DevArray<h16> kv;  // paged pool [pages][K|V][heads][PAGE][hd]
   CUtensorMap tm_kv, tm_kvg;     // the pool as rows of hd (prefill / decode attention TMA boxes)
 };
 
@@ -229,9 +230,10 @@ struct StepBuffers {
 };
 
 // ------------------------------------------------ device-layout image I/O (iolm_cuda_save_image)
-// File: "IOLMDL01" | u64 header words | int64 header words | per weight array: u64 bytes + bytes |
-// u64 checksum. The checksum combines one ImageSum per section (header, each array).
-constexpr char kImageMagic[8] = {'I', 'O', 'L', 'M', 'D', 'L', '0', '1'};
+// File: "IOLMDL02" | u64 header words | int64 header words | per weight array: u64 bytes + bytes |
+// u64 checksum. The checksum combines one ImageSum per section (header, each array). Version 02:
+// 16-bit arrays hold fp16 (version 01 held bf16 and is rejected as a bad magic).
+constexpr char kImageMagic[8] = {'I', 'O', 'L', 'M', 'D', 'L', '0', '2'};
 constexpr size_t kImageChunk = 32ull << 20;  // pinned staging chunk (2 in flight)
 constexpr uint64_t kSumPrime = 0x100000001B3ull;
 
@@ -440,6 +442,7 @@ class Engine {
   bool int4_mma_ = true;
   bool prefill_tc_ = true;  // tcgen05 prefill attention (hd 128 by default, hd 64 on request)
   bool prefill_tc_force_ = false;
+  bool prefill_hp_ = true;  // hd 64: tcgen05 head-pair tiles (attn_tc.cu attn_prefill_hp_kernel)
   // TMA-store epilogue of the W_in GEMM (IOLM_GEMM_TMA_EPI=0 disables, for A/B measurements):
   // measured 3% faster than the warp's coalesced stores at the C1 shape
   bool tma_epi_ = std::getenv("IOLM_GEMM_TMA_EPI") == nullptr || std::string(std::getenv("IOLM_GEMM_TMA_EPI")) != "0";
@@ -474,14 +477,14 @@ class Engine {
   std::vector<std::unique_ptr<Layer>> layers_;
   DevArray<float> tok_embed_, tok_embed_t_, pos_embed_, lnf_g_, lnf_b_;
   DevArray<float> x_;
-  DevArray<__nv_bfloat16> h_, q_, z_, g_;
+  DevArray<h16> h_, q_, z_, g_;
   CUtensorMap tm_h_, tm_q_;
   // (the TMA reduce-add epilogue for the residual GEMMs exists - GemmEpi::tma_out with an fp32 map -
   // but measured 2% slower than the coalesced read-modify-write at the C1 shapes, so it is unused)
   DevArray<int8_t> h8_, z8_, g8_;  // W8A8 operands + per-token scales
   DevArray<float> hs_, zs_, gs_;
   CUtensorMap tm_h8_, tm_h8s_;
-  CUtensorMap tm_hs_;  // bf16 h in the sparse kernel's 112-row boxes (W_SP24F)
+  CUtensorMap tm_hs_;  // fp16 h in the sparse kernel's 112-row boxes (W_SP24F)
   bool any_int8_ = false;
   DevArray<int> page_table_;
   StepBuffers sbuf_[2];
@@ -491,9 +494,9 @@ class Engine {
   DevArray<float> d_logits_;
   DevArray<uint8_t> d_mask_;
   // calibration capture (forward with a CaptureSink, runtime.hpp:22-28): per layer the four linear
-  // inputs [attn_in n x d][attn_out_in n x kh][ffn_in n x d][ffn_mid n x f] as bf16, back to back
-  DevArray<__nv_bfloat16> d_cap_;
-  __nv_bfloat16* cap_ = nullptr;  // non-null while a capturing forward is being launched
+  // inputs [attn_in n x d][attn_out_in n x kh][ffn_in n x d][ffn_mid n x f] as fp16, back to back
+  DevArray<h16> d_cap_;
+  h16* cap_ = nullptr;  // non-null while a capturing forward is being launched
   size_t cap_off_ = 0;
   // W8A8 capture (iolm_cuda_forward_codes): the int8 operand codes of the same four points and their
   // per-token scales [4 x n] per layer
@@ -552,9 +555,11 @@ void Engine::setup(int device, const iolm_cuda_opts* opts) {
     ktime_ = opts->kernel_timing != 0;
     if (opts->sparse_mma < 0) sparse_mma_ = false;
     if (opts->int4_mma < 0) int4_mma_ = false;
-    if (opts->prefill_tc < 0) prefill_tc_ = false;
+    if (opts->prefill_tc < 0) prefill_tc_ = prefill_hp_ = false;
     prefill_tc_force_ = opts->prefill_tc > 0;
   }
+  // hd 64: 64-query chunks run as head-pair tcgen05 tiles unless the 128-query kernel is forced
+  prefill_hp_ = prefill_hp_ && hd_ == 64 && !prefill_tc_force_;
   // measured (bench C1 / C4): for hd 64 rows of 64 + 32 tokens the mma.sync kernel is faster (the
   // 128-query tcgen05 tile is half empty); hd 128 / 544-token rows gain 40% (C4 prefill 158 -> 225 TFLOP/s)
   if (hd_ != 128 && !(hd_ == 64 && prefill_tc_force_)) prefill_tc_ = false;
@@ -822,7 +827,7 @@ void Engine::load_gemm_weights(const BundleView& b, GemmW& w, const std::vector<
   w.mode = all_quant ? (act_quant_ && int8_ok ? W_INT8 : W_CODES) : W_VALUES;
   if ((w.mode == W_INT8 || w.mode == W_CODES) && sp_ok) {
     // 2:4 sparse tensor cores: the bundle's kept codes and position nibbles are repacked on the host;
-    // W8A8 keeps the codes as int8 (kind::i8), bf16 activations take them as exact bf16 (kind::f16)
+    // W8A8 keeps the codes as int8 (kind::i8), fp16 activations take them as exact fp16 (kind::f16)
     const bool f16 = w.mode == W_CODES;
     w.mode = f16 ? W_SP24F : W_SP24;
     w.sl = sp24_layout(N, K, f16);
@@ -900,18 +905,18 @@ void Engine::alloc_runtime() {
   q_.alloc(T * kh_max_);
   z_.alloc(T * kh_max_);
   g_.alloc(T * f_ld_max_);
-  CUDA_OK(cudaMemset(z_.p, 0, T * kh_max_ * sizeof(__nv_bfloat16)));
-  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUDA_OK(cudaMemset(z_.p, 0, T * kh_max_ * sizeof(h16)));
+  const auto BF = H16_TMA;
   tm_h_ = make_kmajor_map(h_.p, BF, 2, d_, T, 2ull * d_, 128);
-  tm_q_ = make_rows_map_bf16(q_.p, kh_max_, T, 2ull * kh_max_, std::min(hd_, 64), 64);
+  tm_q_ = make_rows_map_h16(q_.p, kh_max_, T, 2ull * kh_max_, std::min(hd_, 64), 64);
   for (auto& ly : layers_) {
     ly->tm_z = make_kmajor_map(z_.p, BF, 2, ly->kh, T, 2ull * kh_max_, 128);
     ly->tm_g = make_kmajor_map(g_.p, BF, 2, ly->f, T, 2ull * f_ld_max_, 128);
     ly->tm_g_out = make_out_map(g_.p, false, ly->f, T, 2ull * f_ld_max_);
-    ly->tm_zs = sp24_act_map_bf16(z_.p, ly->kh, static_cast<int>(T), kh_max_);
-    ly->tm_gs = sp24_act_map_bf16(g_.p, ly->f, static_cast<int>(T), f_ld_max_);
+    ly->tm_zs = sp24_act_map_h16(z_.p, ly->kh, static_cast<int>(T), kh_max_);
+    ly->tm_gs = sp24_act_map_h16(g_.p, ly->f, static_cast<int>(T), f_ld_max_);
   }
-  tm_hs_ = sp24_act_map_bf16(h_.p, d_, static_cast<int>(T), d_);
+  tm_hs_ = sp24_act_map_h16(h_.p, d_, static_cast<int>(T), d_);
   if (any_int8_) {
     const auto U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
     h8_.alloc(T * d_);
@@ -958,10 +963,10 @@ void Engine::alloc_runtime() {
   for (auto& ly : layers_) {
     const size_t elems = pages * 2 * ly->heads * PAGE * hd_;
     ly->kv.alloc(elems);
-    CUDA_OK(cudaMemset(ly->kv.p, 0, elems * sizeof(__nv_bfloat16)));
-    ly->tm_kv = make_rows_map_bf16(ly->kv.p, hd_, pages * 2 * ly->heads * PAGE, 2ull * hd_,
+    CUDA_OK(cudaMemset(ly->kv.p, 0, elems * sizeof(h16)));
+    ly->tm_kv = make_rows_map_h16(ly->kv.p, hd_, pages * 2 * ly->heads * PAGE, 2ull * hd_,
                                    std::min(hd_, 64), PAGE);
-    ly->tm_kvg = make_rows_map_bf16(ly->kv.p, hd_, pages * 2 * ly->heads * PAGE, 2ull * hd_, std::min(hd_, 64),
+    ly->tm_kvg = make_rows_map_h16(ly->kv.p, hd_, pages * 2 * ly->heads * PAGE, 2ull * hd_, std::min(hd_, 64),
                                     decode_heads_per_cta(ly->heads, hd_) * PAGE);
   }
   page_table_.alloc(static_cast<size_t>(max_slots_ + 1) * pps_);
@@ -1165,6 +1170,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     if (pre.n_groups) {
       timed(2, 4.0 * hd_ * ly.heads * pre_keys, [&] {
         if (prefill_tc_) launch_prefill_tc(pre, hd_, stream_);
+        else if (prefill_hp_ && d_key_mask == nullptr) launch_prefill_hp(pre, stream_);
         else launch_attention(pre, none, hd_, stream_);
       });
       ++stats_.kernel_launches;
@@ -1203,7 +1209,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     ei.ldo = f_ld_max_;
     scales(ei, ly.in, hs_.p);
     timed(6, 2.0 * dT * ly.f * d_, [&] {
-      gemm_w(iolmk::EPI_GELU_BF16, ly.in, i8_in ? tm_h8_ : tm_h_, ly.in.mode == W_SP24F ? tm_hs_ : tm_h8s_, T, ly.f, d_,
+      gemm_w(iolmk::EPI_GELU_H16, ly.in, i8_in ? tm_h8_ : tm_h_, ly.in.mode == W_SP24F ? tm_hs_ : tm_h8s_, T, ly.f, d_,
              ei,
              tma_epi_ ? &ly.tm_g_out : nullptr);
     });
@@ -1430,7 +1436,7 @@ void Engine::decode(const int32_t* ids, bool ids_on_device, const int64_t* offse
 
 void Engine::capture_point(int point, int T, int cols) {
   if (cap_) {
-    const __nv_bfloat16* src = point == 1 ? z_.p : point == 3 ? g_.p : h_.p;
+    const h16* src = point == 1 ? z_.p : point == 3 ? g_.p : h_.p;
     const int ld = point == 1 ? kh_max_ : point == 3 ? f_ld_max_ : d_;
     CUDA_OK(cudaMemcpy2DAsync(cap_ + cap_off_, static_cast<size_t>(cols) * 2, src, static_cast<size_t>(ld) * 2,
                               static_cast<size_t>(cols) * 2, T, cudaMemcpyDeviceToDevice, stream_));
@@ -1508,7 +1514,7 @@ void Engine::forward(const int32_t* ids, const uint8_t* mask, int n, float* logi
   cap8_ = nullptr;
   capsc_ = nullptr;
   if (capture)
-    CUDA_OK(cudaMemcpyAsync(capture, d_cap_.p, cap_elems * sizeof(__nv_bfloat16), cudaMemcpyDeviceToHost, stream_));
+    CUDA_OK(cudaMemcpyAsync(capture, d_cap_.p, cap_elems * sizeof(h16), cudaMemcpyDeviceToHost, stream_));
   if (codes) {
     CUDA_OK(cudaMemcpyAsync(codes, d_cap8_.p, cap_elems, cudaMemcpyDeviceToHost, stream_));
     CUDA_OK(cudaMemcpyAsync(code_scales, d_capsc_.p, sizeof(float) * 4 * n * L_, cudaMemcpyDeviceToHost, stream_));

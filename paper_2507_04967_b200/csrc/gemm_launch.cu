@@ -1,5 +1,5 @@
 // Host launchers for the tcgen05 GEMM instantiations.
-//   bf16 x bf16 -> fp32 (kind::f16) and s8 x s8 -> s32 (kind::i8, W8A8), each as
+//   fp16 x fp16 -> fp32 (kind::f16) and s8 x s8 -> s32 (kind::i8, W8A8), each as
 //   2-SM pairs (CG = 2, 256 x 256 tiles, clusters of 2) or single-CTA (CG = 1, 128 x 128 tiles).
 // Every TMA box is 128 rows x 128 bytes, so one tensor map per operand serves both shapes.
 #include "gemm_sm100.cuh"
@@ -46,8 +46,8 @@ static void dispatch_epi(int epi, const CUtensorMap& A, const CUtensorMap& B, in
     case EPI_S32:
       if constexpr (I8) return launch_one<BN, EPI_S32, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
       break;
-    case EPI_BF16: return launch_one<BN, EPI_BF16, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
-    case EPI_GELU_BF16: return launch_one<BN, EPI_GELU_BF16, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_H16: return launch_one<BN, EPI_H16, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_GELU_H16: return launch_one<BN, EPI_GELU_H16, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
     case EPI_RESID_F32: return launch_one<BN, EPI_RESID_F32, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
     case EPI_QKV: return launch_one<BN, EPI_QKV, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
     case EPI_NONE: return launch_one<BN, EPI_NONE, CG, I8>(A, B, M, N, K, ep, st, grid_cap);
@@ -56,14 +56,14 @@ static void dispatch_epi(int epi, const CUtensorMap& A, const CUtensorMap& B, in
   throw Unsupported("gemm: epilogue not instantiated for this operand type");
 }
 
-// W4A16: B is the packed int4 weight map (make_w4_map), expanded to bf16 in shared memory.
+// W4A16: B is the packed int4 weight map (make_w4_map), expanded to fp16 in shared memory.
 template <int BN, int CG>
 static void dispatch_w4(int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, const GemmEpi& ep,
                         cudaStream_t st, int grid_cap) {
   switch (epi) {
     case EPI_F32: return launch_one<BN, EPI_F32, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
-    case EPI_BF16: return launch_one<BN, EPI_BF16, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
-    case EPI_GELU_BF16: return launch_one<BN, EPI_GELU_BF16, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_H16: return launch_one<BN, EPI_H16, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
+    case EPI_GELU_H16: return launch_one<BN, EPI_GELU_H16, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
     case EPI_RESID_F32: return launch_one<BN, EPI_RESID_F32, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
     case EPI_QKV: return launch_one<BN, EPI_QKV, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
     case EPI_NONE: return launch_one<BN, EPI_NONE, CG, false, true>(A, B, M, N, K, ep, st, grid_cap);
@@ -76,7 +76,7 @@ void launch_gemm_w4(bool pair, int epi, const CUtensorMap& A, const CUtensorMap&
                     const GemmEpi& ep_in, cudaStream_t st, int grid_cap, const CUtensorMap* out_map) {
   if (M <= 0 || N <= 0) return;
   GemmEpi ep = ep_in;
-  ep.tma_out = out_map != nullptr && (epi == EPI_RESID_F32 || epi == EPI_BF16 || epi == EPI_GELU_BF16);
+  ep.tma_out = out_map != nullptr && (epi == EPI_RESID_F32 || epi == EPI_H16 || epi == EPI_GELU_H16);
   g_out_map = out_map;
   if (pair) dispatch_w4<256, 2>(epi, A, B, M, N, K, ep, st, grid_cap);
   else dispatch_w4<128, 1>(epi, A, B, M, N, K, ep, st, grid_cap);
@@ -88,7 +88,7 @@ void launch_gemm(bool pair, bool i8, int epi, const CUtensorMap& A, const CUtens
                  const GemmEpi& ep_in, cudaStream_t st, int grid_cap, const CUtensorMap* out_map) {
   if (M <= 0 || N <= 0) return;
   GemmEpi ep = ep_in;
-  ep.tma_out = out_map != nullptr && (epi == EPI_RESID_F32 || epi == EPI_BF16 || epi == EPI_GELU_BF16);
+  ep.tma_out = out_map != nullptr && (epi == EPI_RESID_F32 || epi == EPI_H16 || epi == EPI_GELU_H16);
   g_out_map = out_map;
   if (pair) {
     if (i8) dispatch_epi<256, 2, true>(epi, A, B, M, N, K, ep, st, grid_cap);

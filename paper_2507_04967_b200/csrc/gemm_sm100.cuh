@@ -1,6 +1,6 @@
 // Persistent, warp-specialised tcgen05 GEMM for sm_100a:  C[M x N] = A[M x K] * W[N x K]^T
 //
-//   A  : activations, K-major (row-major [M x K]), bf16 (or int8 for the W8A8 variant)
+//   A  : activations, K-major (row-major [M x K]), fp16 (or int8 for the W8A8 variant)
 //   W  : weights as stored in the bundle, [out x in] = [N x K] row-major, i.e. also K-major
 //        (the reference applies x * W^T via transposed copies, runtime.cpp:80-85; on the GPU the
 //        bundle layout is already the K-major B operand, so no transpose is materialised)
@@ -22,10 +22,10 @@ namespace iolmk {
 
 enum EpiMode : int {
   EPI_F32 = 0,        // out f32 [M x ldo]
-  EPI_BF16 = 1,       // out bf16 [M x ldo]
-  EPI_GELU_BF16 = 2,  // out bf16 gelu(acc)
+  EPI_H16 = 1,       // out fp16 [M x ldo]
+  EPI_GELU_H16 = 2,  // out fp16 gelu(acc)
   EPI_RESID_F32 = 3,  // resid f32 [M x ldo] += acc   (x += z*Wo^T, x += g*Wout^T)
-  EPI_QKV = 4,        // cols [0,kh) -> q bf16; [kh,2kh) -> K pages; [2kh,3kh) -> V pages
+  EPI_QKV = 4,        // cols [0,kh) -> q fp16; [kh,2kh) -> K pages; [2kh,3kh) -> V pages
   EPI_S32 = 5,        // raw int32 accumulators [M x ldo] (integer GEMM parity tests)
   EPI_NONE = 6,       // kernel tuning only: accumulators are drained but not read (mainloop rate)
 };
@@ -35,7 +35,7 @@ struct GemmEpi {
   void* out = nullptr;
   int ldo = 0;
   // QKV scatter into the paged KV pool of one layer. Page layout: [page][K|V][head][PAGE][hd].
-  __nv_bfloat16* kv_layer = nullptr;
+  h16* kv_layer = nullptr;
   const int* tok_slot = nullptr;
   const int* tok_pos = nullptr;
   const int* page_table = nullptr;
@@ -45,7 +45,7 @@ struct GemmEpi {
   // W8A8 dequant epilogue: acc_i32 * a_scale[row] * w_scale[col]
   const float* a_scale = nullptr;
   const float* w_scale = nullptr;
-  // RESID / BF16 / GELU: write full 32 x 32 chunks with TMA (store, or reduce-add into x) from the
+  // RESID / H16 / GELU: write full 32 x 32 chunks with TMA (store, or reduce-add into x) from the
   // warp's staging tile instead of per-thread global stores (the kernel's tmC describes `out`)
   int tma_out = 0;
 };
@@ -55,7 +55,7 @@ struct GemmEpi {
 // tcgen05.mma.cta_group::2, and each CTA drains its 128 accumulator lanes from its own TMEM.
 // W4 = true: W4A16. The weights stay int4 (the bundle's q4 nibbles, re-pitched) in HBM; TMA
 // stages the packed tile (BN_CTA rows x 32 B per 64 K) and CONV_WARPS converter warps expand it
-// in shared memory into the bf16 SWIZZLE_128B operand tile the MMA reads (code - 8, exact in bf16;
+// in shared memory into the fp16 SWIZZLE_128B operand tile the MMA reads (code - 8, exact in fp16;
 // the per-channel scale is applied in the epilogue as for the other code forms).
 template <int BN, int CG, bool W4 = false>
 struct GemmCfg {
@@ -79,24 +79,24 @@ struct GemmCfg {
   static_assert(!W4 || BN_CTA == 128, "W4 converter maps one thread per staged weight row");
 };
 
-// Expands 4 packed bytes (8 int4 codes, low nibble first) into 4 bf16x2 words of (nibble - 8):
-// bf16(128 + n) has bit pattern 0x4300 | n, and 128 + n - 136 is exact in bf16. Byte permutes build
-// the 0x43nn halves (12 instructions per 8 codes).
+// Expands 4 packed bytes (8 int4 codes, low nibble first) into 4 f16x2 words of (nibble - 8):
+// fp16(1024 + n) has bit pattern 0x6400 | n, and 1024 + n - 1032 is exact in fp16. Byte permutes build
+// the 0x64nn halves (12 instructions per 8 codes).
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
   return r;
 }
-__device__ __forceinline__ void int4x8_to_bf16(uint32_t x, uint32_t (&w)[4]) {
+__device__ __forceinline__ void int4x8_to_h16(uint32_t x, uint32_t (&w)[4]) {
   const uint32_t lo = x & 0x0F0F0F0Fu, hi = (x >> 4) & 0x0F0F0F0Fu;  // codes 0,2,4,6 / 1,3,5,7
   const uint32_t u = prmt(lo, hi, 0x5140u), v = prmt(lo, hi, 0x7362u);  // codes 0..3 / 4..7 in order
-  const uint32_t c43 = 0x43434343u;
-  const uint32_t t[4] = {prmt(u, c43, 0x4140u), prmt(u, c43, 0x4342u), prmt(v, c43, 0x4140u),
-                         prmt(v, c43, 0x4342u)};
-  const __nv_bfloat162 off = __floats2bfloat162_rn(136.f, 136.f);
+  const uint32_t c64 = 0x64646464u;
+  const uint32_t t[4] = {prmt(u, c64, 0x4140u), prmt(u, c64, 0x4342u), prmt(v, c64, 0x4140u),
+                         prmt(v, c64, 0x4342u)};
+  const h16x2 off = __floats2half2_rn(1032.f, 1032.f);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    __nv_bfloat162 h = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&t[i]), off);
+    h16x2 h = __hsub2(*reinterpret_cast<const h16x2*>(&t[i]), off);
     w[i] = *reinterpret_cast<uint32_t*>(&h);
   }
 }
@@ -107,26 +107,26 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 template <int EPI>
 __device__ __forceinline__ void epi_apply(const GemmEpi& ep, int m, int n0, float (&v)[32]) {
   const int N = ep.N;
-  if constexpr (EPI == EPI_GELU_BF16) {
+  if constexpr (EPI == EPI_GELU_H16) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
   }
-  if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
-    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n0;
+  if constexpr (EPI == EPI_H16 || EPI == EPI_GELU_H16) {
+    h16* o = static_cast<h16*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n0;
     if (n0 + 32 <= N && (ep.ldo & 7) == 0) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint4 w;
-        w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
-        w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
-        w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
-        w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+        w.x = pack_h16x2(v[8 * j + 0], v[8 * j + 1]);
+        w.y = pack_h16x2(v[8 * j + 2], v[8 * j + 3]);
+        w.z = pack_h16x2(v[8 * j + 4], v[8 * j + 5]);
+        w.w = pack_h16x2(v[8 * j + 6], v[8 * j + 7]);
         reinterpret_cast<uint4*>(o)[j] = w;
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) o[j] = __float2bfloat16_rn(v[j]);
+        if (n0 + j < N) o[j] = __float2half_rn(v[j]);
     }
   } else if constexpr (EPI == EPI_F32) {
     float* o = static_cast<float*>(ep.out) + static_cast<size_t>(m) * ep.ldo + n0;
@@ -165,9 +165,9 @@ __device__ __forceinline__ void epi_apply(const GemmEpi& ep, int m, int n0, floa
 // Per-row destinations of the QKV epilogue, resolved once per tile: the q row and the K/V rows of
 // this token's page slot (page layout [page][K|V][head][PAGE][hd]).
 struct QkvRow {
-  __nv_bfloat16* q;
-  __nv_bfloat16* k;  // head 0 of this token's K row
-  __nv_bfloat16* v;
+  h16* q;
+  h16* k;  // head 0 of this token's K row
+  h16* v;
 };
 __device__ __forceinline__ QkvRow qkv_row(const GemmEpi& ep, int m) {
   QkvRow r;
@@ -175,9 +175,9 @@ __device__ __forceinline__ QkvRow qkv_row(const GemmEpi& ep, int m) {
   const int pos = ep.tok_pos[m];
   const int page = ep.page_table[static_cast<size_t>(slot) * ep.max_pages + (pos >> 4)];
   const size_t head_stride = static_cast<size_t>(ep.page_size) << ep.hd_shift;
-  __nv_bfloat16* kp = ep.kv_layer + static_cast<size_t>(page) * 2 * ep.heads * head_stride +
+  h16* kp = ep.kv_layer + static_cast<size_t>(page) * 2 * ep.heads * head_stride +
                       (static_cast<size_t>(pos & 15) << ep.hd_shift);
-  r.q = static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(m) * ep.ldo;
+  r.q = static_cast<h16*>(ep.out) + static_cast<size_t>(m) * ep.ldo;
   r.k = kp;
   r.v = kp + ep.heads * head_stride;
   return r;
@@ -190,11 +190,11 @@ __device__ __forceinline__ void qkv_store(const GemmEpi& ep, const QkvRow& row, 
     const int n = n0 + 8 * j;
     if (n >= ep.N) break;
     uint4 w;
-    w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
-    w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
-    w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
-    w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
-    __nv_bfloat16* dst;
+    w.x = pack_h16x2(v[8 * j + 0], v[8 * j + 1]);
+    w.y = pack_h16x2(v[8 * j + 2], v[8 * j + 3]);
+    w.z = pack_h16x2(v[8 * j + 4], v[8 * j + 5]);
+    w.w = pack_h16x2(v[8 * j + 6], v[8 * j + 7]);
+    h16* dst;
     if (n < kh) {
       dst = row.q + n;
     } else {
@@ -220,14 +220,14 @@ __device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* til
                                                    int lane, const QkvRow* rows = nullptr,
                                                    const CUtensorMap* tmC = nullptr, uint32_t* seq = nullptr) {
   const int rr = lane >> 3, gg = lane & 7;  // coalesced phase: row rr + 4i, column group gg
-  if constexpr (EPI == EPI_GELU_BF16) {
+  if constexpr (EPI == EPI_GELU_H16) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
   }
-  if constexpr (EPI == EPI_RESID_F32 || EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
+  if constexpr (EPI == EPI_RESID_F32 || EPI == EPI_H16 || EPI == EPI_GELU_H16) {
     if (ep.tma_out) {
       if constexpr (EPI != EPI_RESID_F32) {
-        // bf16 boxes are 2 KB: the warp's 4 KB tile holds two, used alternately, so writing this
+        // fp16 boxes are 2 KB: the warp's 4 KB tile holds two, used alternately, so writing this
         // chunk only waits for the store issued two chunks ago (not the previous one) to be read
         tile += ((*seq)++ & 1u) * 512;
         if (lane == 0) bulk_wait_read1();
@@ -243,15 +243,15 @@ __device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* til
         for (int g = 0; g < 8; ++g)
           *reinterpret_cast<float4*>(tile + swz(lane, g)) = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
       } else {
-        // bf16 32 x 32 box, SWIZZLE_64B: 16-byte chunk k of 64-byte row r at k ^ ((r >> 1) & 3)
+        // fp16 32 x 32 box, SWIZZLE_64B: 16-byte chunk k of 64-byte row r at k ^ ((r >> 1) & 3)
         uint8_t* trow = reinterpret_cast<uint8_t*>(tile) + lane * 64;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           uint4 w;
-          w.x = pack_bf16x2(v[8 * k + 0], v[8 * k + 1]);
-          w.y = pack_bf16x2(v[8 * k + 2], v[8 * k + 3]);
-          w.z = pack_bf16x2(v[8 * k + 4], v[8 * k + 5]);
-          w.w = pack_bf16x2(v[8 * k + 6], v[8 * k + 7]);
+          w.x = pack_h16x2(v[8 * k + 0], v[8 * k + 1]);
+          w.y = pack_h16x2(v[8 * k + 2], v[8 * k + 3]);
+          w.z = pack_h16x2(v[8 * k + 4], v[8 * k + 5]);
+          w.w = pack_h16x2(v[8 * k + 6], v[8 * k + 7]);
           *reinterpret_cast<uint4*>(trow + ((k ^ ((lane >> 1) & 3)) << 4)) = w;
         }
       }
@@ -306,18 +306,18 @@ __device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* til
       const float4 b = *reinterpret_cast<const float4*>(tile + swz(lr, 2 * q4 + 1));
       if (m_base + lr < ep.M) {
         uint4 w;
-        w.x = pack_bf16x2(a.x, a.y);
-        w.y = pack_bf16x2(a.z, a.w);
-        w.z = pack_bf16x2(b.x, b.y);
-        w.w = pack_bf16x2(b.z, b.w);
+        w.x = pack_h16x2(a.x, a.y);
+        w.y = pack_h16x2(a.z, a.w);
+        w.z = pack_h16x2(b.x, b.y);
+        w.w = pack_h16x2(b.z, b.w);
         const QkvRow& rw = rows[lr];
-        __nv_bfloat16* dst = (region == 0 ? rw.q : region == 1 ? rw.k : rw.v) + off;
+        h16* dst = (region == 0 ? rw.q : region == 1 ? rw.k : rw.v) + off;
         *reinterpret_cast<uint4*>(dst) = w;
       }
     }
-  } else {  // bf16 output: 4 lanes x 16 B = one 64-byte row segment, 8 rows per instruction
+  } else {  // fp16 output: 4 lanes x 16 B = one 64-byte row segment, 8 rows per instruction
     const int r8 = lane >> 2, q4 = lane & 3;
-    __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(ep.out) + n0 + q4 * 8;
+    h16* ob = static_cast<h16*>(ep.out) + n0 + q4 * 8;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int lr = r8 + 8 * i;
@@ -326,10 +326,10 @@ __device__ __forceinline__ void warp_tile_epilogue(const GemmEpi& ep, float* til
       const int row = m_base + lr;
       if (row < ep.M) {
         uint4 w;
-        w.x = pack_bf16x2(a.x, a.y);
-        w.y = pack_bf16x2(a.z, a.w);
-        w.z = pack_bf16x2(b.x, b.y);
-        w.w = pack_bf16x2(b.z, b.w);
+        w.x = pack_h16x2(a.x, a.y);
+        w.y = pack_h16x2(a.z, a.w);
+        w.z = pack_h16x2(b.x, b.y);
+        w.w = pack_h16x2(b.z, b.w);
         *reinterpret_cast<uint4*>(ob + static_cast<size_t>(row) * ep.ldo) = w;
       }
     }
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = I8 ? idesc_i8(128 * CG, BN) : idesc_f16(128 * CG, BN, 1);
+      constexpr uint32_t idesc = I8 ? idesc_i8(128 * CG, BN) : idesc_f16(128 * CG, BN, H16_FMT);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               uint32_t w[4];
-              int4x8_to_bf16(words[c], w);
+              int4x8_to_h16(words[c], w);
               *reinterpret_cast<uint4*>(dst_row + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
             }
           }
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
         if (ci + 1 < NCH) tmem_ld_32x32b_x32(tbase + c + 32, r[(ci + 1) & 1]);
         const uint32_t(&rc)[32] = r[ci & 1];
         const int m_base = mt * C::TILE_M + static_cast<int>(rank) * C::BM + q * 32;  // warp's first row
-        if constexpr (EPI == EPI_RESID_F32 || EPI == EPI_BF16 || EPI == EPI_GELU_BF16 || EPI == EPI_QKV) {
+        if constexpr (EPI == EPI_RESID_F32 || EPI == EPI_H16 || EPI == EPI_GELU_H16 || EPI == EPI_QKV) {
           // full 32-column chunk with aligned rows: coalesced path through the warp's smem tile
           // (QKV: a chunk never straddles q/K/V or a head when hd >= 32)
           const bool full = n0 + 32 <= N && (ep.ldo & 7) == 0 && (EPI != EPI_QKV || ep.hd_shift >= 5);
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG, W4>::THREADS, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = static_cast<float>(static_cast<int32_t>(rc[j])) * a_sc * s_scale[c + j];
             } else {
-              if (has_ws) {  // W8A16 / W4A16: codes as exact bf16 integers, scale here
+              if (has_ws) {  // W8A16 / W4A16: codes as exact fp16 integers, scale here
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rc[j]) * s_scale[c + j];
               } else {

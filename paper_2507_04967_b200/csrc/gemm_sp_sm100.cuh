@@ -58,9 +58,9 @@ struct SpCfg {
 
 // kind::i8 instruction descriptor with the sparse flag (bit 2): s8 x s8 -> s32, K-major A/B.
 __host__ __device__ constexpr uint32_t idesc_i8_sp(int M, int N) { return idesc_i8(M, N) | (1u << 2); }
-// kind::f16 with the sparse flag: bf16 x bf16 -> f32 (the W16A16 / W8A16 path: A = the kept weight
-// codes as exact bf16 integers, B = bf16 activations; the per-channel scale is applied in the epilogue).
-__host__ __device__ constexpr uint32_t idesc_f16_sp(int M, int N) { return idesc_f16(M, N, 1) | (1u << 2); }
+// kind::f16 with the sparse flag: fp16 x fp16 -> f32 (the W16A16 / W8A16 path: A = the kept weight
+// codes as exact fp16 integers, B = fp16 activations; the per-channel scale is applied in the epilogue).
+__host__ __device__ constexpr uint32_t idesc_f16_sp(int M, int N) { return idesc_f16(M, N, H16_FMT) | (1u << 2); }
 
 __device__ __forceinline__ void umma_f16_sp_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t tmem_e,
                                                  uint32_t idesc, uint32_t accumulate) {
@@ -113,8 +113,8 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)
 // tmA: compressed weights [N rows x K/2 bytes]; tmB: activations [T rows x K bytes] (box 112 rows);
 // tmE: metadata atoms [rows x 16 B] (box 256 rows). ep.M = tokens T, ep.N = output channels.
 //
-// F16 = true: the same pipeline over bf16 operands (tcgen05.mma.sp kind::f16). A 128-byte operand row
-// then holds 64 kept bf16 = 128 logical K, so a stage covers 128 logical K with ONE metadata atom
+// F16 = true: the same pipeline over fp16 operands (tcgen05.mma.sp kind::f16). A 128-byte operand row
+// then holds 64 kept fp16 = 128 logical K, so a stage covers 128 logical K with ONE metadata atom
 // (128 rows x 16 B -> 4 TMEM columns, one per 32-K MMA) instead of two; A / B / E tiles keep their
 // byte shapes (B: 112 tokens x 128 K x 2 B as two 64-K SWIZZLE_128B boxes). Epilogue: acc * s_w.
 template <int EPI, bool F16 = false>
@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
-            // A advances 32 compressed bytes per MMA (64 logical K of int8 / 32 of bf16); B 64 bytes
-            // inside its 128-byte box; E 64 (int8) or 32 (bf16) metadata bits = 2 or 1 TMEM columns
+            // A advances 32 compressed bytes per MMA (64 logical K of int8 / 32 of fp16); B 64 bytes
+            // inside its 128-byte box; E 64 (int8) or 32 (fp16) metadata bits = 2 or 1 TMEM columns
             const uint64_t bd = (kk < 2 ? bd0 : bd1) + 4u * (kk & 1);
             // kind::f16: the metadata address must be 2-column aligned; an odd column is selected
             // with the instruction descriptor's sparse id2 field (bits [0, 2))
@@ -333,12 +333,12 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
               *reinterpret_cast<float4*>(as + j) = *reinterpret_cast<const float4*>(s_as + ci * C::CHUNK + j);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              // same operations as the dense epilogues: int8 (acc * s_a[token]) * s_w[ch], bf16 codes
+              // same operations as the dense epilogues: int8 (acc * s_a[token]) * s_w[ch], fp16 codes
               // acc * s_w[ch], each rounded (explicit _rn: no FMA contraction into the residual add)
               if constexpr (F16) v[j] = __fmul_rn(__uint_as_float(rc[j]), w_sc);
               else v[j] = __fmul_rn(__fmul_rn(static_cast<float>(static_cast<int32_t>(rc[j])), as[j]), w_sc);
             }
-            if constexpr (EPI == EPI_GELU_BF16) {
+            if constexpr (EPI == EPI_GELU_H16) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) v[j] = gelu_tanh(v[j]);
             }
@@ -352,21 +352,21 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
               for (int j = 0; j < 16; ++j)
                 if (j < jn && ch_ok && t0 + j < T) xcol[static_cast<size_t>(t0 + j) * ep.ldo] = __fadd_rn(xo[j], v[j]);
             } else {
-              // bf16 outputs: lane pairs exchange one value so that every store is a 4-byte
+              // fp16 outputs: lane pairs exchange one value so that every store is a 4-byte
               // channel pair; even lanes write token j, odd lanes token j + 1
               const bool odd = lane & 1;
               const int c0 = ch & ~1;
               if constexpr (EPI != EPI_QKV) {
                 if (jn == C::CHUNK && t0 + C::CHUNK <= T && c0 + 1 < N) {
                   // whole chunk in range: one 4-byte store per token pair, pointer stepped by 2 rows
-                  uint32_t* dst = reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(ep.out) +
+                  uint32_t* dst = reinterpret_cast<uint32_t*>(static_cast<h16*>(ep.out) +
                                                               static_cast<size_t>(t0 + (odd ? 1 : 0)) * ep.ldo + c0);
-                  const size_t step = static_cast<size_t>(ep.ldo);  // 2 rows of bf16 = ldo uint32
+                  const size_t step = static_cast<size_t>(ep.ldo);  // 2 rows of fp16 = ldo uint32
 #pragma unroll
                   for (int j = 0; j < 16; j += 2) {
                     const float send = odd ? v[j] : v[j + 1];
                     const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-                    *dst = odd ? pack_bf16x2(recv, v[j + 1]) : pack_bf16x2(v[j], recv);
+                    *dst = odd ? pack_h16x2(recv, v[j + 1]) : pack_h16x2(v[j], recv);
                     dst += step;
                   }
                   continue;
@@ -378,19 +378,19 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
                 const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
                 const int jj = j + (odd ? 1 : 0);
                 const int tok = t0 + jj;
-                const uint32_t packed = odd ? pack_bf16x2(recv, v[j + 1]) : pack_bf16x2(v[j], recv);
+                const uint32_t packed = odd ? pack_h16x2(recv, v[j + 1]) : pack_h16x2(v[j], recv);
                 if (jj < jn && tok < T && c0 < N) {
-                  __nv_bfloat16* dst;
+                  h16* dst;
                   if constexpr (EPI == EPI_QKV) {
                     const QkvRow& rw = s_rows[ci * C::CHUNK + jj];
                     dst = (region == 0 ? rw.q : region == 1 ? rw.k : rw.v) + (off & ~1);
                   } else {
-                    dst = static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(tok) * ep.ldo + c0;
+                    dst = static_cast<h16*>(ep.out) + static_cast<size_t>(tok) * ep.ldo + c0;
                   }
                   if (c0 + 1 < N) {
                     *reinterpret_cast<uint32_t*>(dst) = packed;
                   } else {
-                    *dst = __ushort_as_bfloat16(static_cast<unsigned short>(packed & 0xffffu));
+                    *dst = __ushort_as_half(static_cast<unsigned short>(packed & 0xffffu));
                   }
                 }
               }

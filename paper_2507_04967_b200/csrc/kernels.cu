@@ -1,6 +1,6 @@
 // Non-GEMM kernels of the prompt() hot path on sm_100a:
 //   embed_ln_kernel   x = tok_embed[id] + pos_embed[pos]; h = LN1(x)       (runtime.cpp:122-141)
-//   ln_kernel         h = LN(x) -> bf16 GEMM operand                        (numerics.cpp:158-177)
+//   ln_kernel         h = LN(x) -> fp16 GEMM operand                        (numerics.cpp:158-177)
 //   attn_prefill      causal flash attention over paged KV, mma.sync tiles  (runtime.cpp:152-174)
 //   attn_decode       one query per sequence, split by absolute 32-key chunks
 //   head_argmax       final LN + tied head (fp32) + greedy argmax           (runtime.cpp:202-215,
@@ -38,7 +38,7 @@ __device__ __forceinline__ float warp_max(float v) {
 
 // ------------------------------------------------------------------ LayerNorm
 // One warp per row. Two-pass mean / variance in fp32 over the row held in registers. Writes the
-// bf16 GEMM operand, or (Q8) per-token int8 codes + the row scale for the W8A8 GEMMs.
+// fp16 GEMM operand, or (Q8) per-token int8 codes + the row scale for the W8A8 GEMMs.
 template <int MAXV>
 __device__ __forceinline__ void ln_load_row(const float* __restrict__ xr, int d, int lane, float4 (&v)[MAXV]) {
   const int nv = d >> 2;
@@ -51,13 +51,13 @@ __device__ __forceinline__ void ln_load_row(const float* __restrict__ xr, int d,
 
 template <int MAXV, bool Q8 = false>
 __device__ __forceinline__ void ln_finish_row(float4 (&v)[MAXV], int d, const float* __restrict__ g,
-                                              const float* __restrict__ b, __nv_bfloat16* __restrict__ hr,
+                                              const float* __restrict__ b, h16* __restrict__ hr,
                                               int lane, int8_t* __restrict__ q8 = nullptr,
                                               float* __restrict__ qscale = nullptr);
 
 template <int MAXV, bool Q8 = false>
 __device__ __forceinline__ void ln_row_warp(const float* __restrict__ xr, int d, const float* __restrict__ g,
-                                            const float* __restrict__ b, __nv_bfloat16* __restrict__ hr,
+                                            const float* __restrict__ b, h16* __restrict__ hr,
                                             int lane, int8_t* __restrict__ q8 = nullptr,
                                             float* __restrict__ qscale = nullptr) {
   float4 v[MAXV];
@@ -67,7 +67,7 @@ __device__ __forceinline__ void ln_row_warp(const float* __restrict__ xr, int d,
 
 template <int MAXV, bool Q8>
 __device__ __forceinline__ void ln_finish_row(float4 (&v)[MAXV], int d, const float* __restrict__ g,
-                                              const float* __restrict__ b, __nv_bfloat16* __restrict__ hr,
+                                              const float* __restrict__ b, h16* __restrict__ hr,
                                               int lane, int8_t* __restrict__ q8, float* __restrict__ qscale) {
   const int nv = d >> 2;
   float s = 0.f;
@@ -131,8 +131,8 @@ __device__ __forceinline__ void ln_finish_row(float4 (&v)[MAXV], int d, const fl
         const float4 gg = reinterpret_cast<const float4*>(g)[idx];
         const float4 bb = reinterpret_cast<const float4*>(b)[idx];
         uint2 w;
-        w.x = pack_bf16x2((v[i].x - mean) * inv * gg.x + bb.x, (v[i].y - mean) * inv * gg.y + bb.y);
-        w.y = pack_bf16x2((v[i].z - mean) * inv * gg.z + bb.z, (v[i].w - mean) * inv * gg.w + bb.w);
+        w.x = pack_h16x2((v[i].x - mean) * inv * gg.x + bb.x, (v[i].y - mean) * inv * gg.y + bb.y);
+        w.y = pack_h16x2((v[i].z - mean) * inv * gg.z + bb.z, (v[i].w - mean) * inv * gg.w + bb.w);
         reinterpret_cast<uint2*>(hr)[idx] = w;
       }
     }
@@ -144,7 +144,7 @@ __device__ __forceinline__ void ln_finish_row(float4 (&v)[MAXV], int d, const fl
 template <int MAXV, bool Q8>
 __global__ void __launch_bounds__(256, MAXV <= 10 ? 4 : 2) ln_kernel(const float* __restrict__ x, int M, int d,
                                                  const float* __restrict__ g, const float* __restrict__ b,
-                                                 __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
+                                                 h16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
                                                  float* __restrict__ qscale) {
   pdl_sync();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -177,7 +177,7 @@ __device__ __forceinline__ void ln_stage_gb(const float*& g, const float*& b, in
 template <int MAXV, bool Q8>
 __global__ void __launch_bounds__(256, 2) ln_stream_kernel(const float* __restrict__ x, int M, int d,
                                                            const float* g, const float* b,
-                                                           __nv_bfloat16* __restrict__ h, int ldh,
+                                                           h16* __restrict__ h, int ldh,
                                                            int8_t* __restrict__ q8, float* __restrict__ qscale,
                                                            int gb_smem) {
   pdl_sync();
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256, 2) ln_stream_kernel(const float* __restri
 template <int MAXV, bool Q8>
 __global__ void __launch_bounds__(256, 2) ln_stream2_kernel(const float* __restrict__ x, int M, int d,
                                                             const float* g, const float* b,
-                                                            __nv_bfloat16* __restrict__ h, int ldh,
+                                                            h16* __restrict__ h, int ldh,
                                                             int8_t* __restrict__ q8, float* __restrict__ qscale,
                                                             int gb_smem) {
   pdl_sync();
@@ -294,8 +294,8 @@ __global__ void __launch_bounds__(256, 2) ln_stream2_kernel(const float* __restr
           const float4 gg = reinterpret_cast<const float4*>(g)[idx];
           const float4 bb = reinterpret_cast<const float4*>(b)[idx];
           uint2 w;
-          w.x = pack_bf16x2((cur[i].x - mean) * inv * gg.x + bb.x, (cur[i].y - mean) * inv * gg.y + bb.y);
-          w.y = pack_bf16x2((cur[i].z - mean) * inv * gg.z + bb.z, (cur[i].w - mean) * inv * gg.w + bb.w);
+          w.x = pack_h16x2((cur[i].x - mean) * inv * gg.x + bb.x, (cur[i].y - mean) * inv * gg.y + bb.y);
+          w.y = pack_h16x2((cur[i].z - mean) * inv * gg.z + bb.z, (cur[i].w - mean) * inv * gg.w + bb.w);
           hr[idx] = w;
         }
       }
@@ -312,7 +312,7 @@ constexpr int LN_STAGES = 2;
 template <int MAXV, bool Q8>
 __global__ void __launch_bounds__(288) ln_bulk_kernel(const float* __restrict__ x, int M, int d,
                                                       const float* __restrict__ g, const float* __restrict__ b,
-                                                      __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
+                                                      h16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
                                                       float* __restrict__ qscale) {
   pdl_sync();
   extern __shared__ __align__(128) uint8_t lsm[];
@@ -362,18 +362,18 @@ __global__ void __launch_bounds__(288) ln_bulk_kernel(const float* __restrict__ 
   }
 }
 
-// Per-token int8 quantization of a bf16 activation matrix (attention output z, GELU output g).
+// Per-token int8 quantization of a fp16 activation matrix (attention output z, GELU output g).
 // One warp per row. CH > 0: the row (cols = 256*CH, multiple of 8) stays in registers between the
 // amax and the code pass; CH == 0: generic two-pass version (any width).
 template <int CH>
-__global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const __nv_bfloat16* __restrict__ src, int lds, int M,
+__global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const h16* __restrict__ src, int lds, int M,
                                                          int cols, int8_t* __restrict__ dst, int ldd,
                                                          float* __restrict__ scale) {
   pdl_sync();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= M) return;
   const int lane = threadIdx.x & 31;
-  const __nv_bfloat16* r = src + static_cast<size_t>(row) * lds;
+  const h16* r = src + static_cast<size_t>(row) * lds;
   int8_t* o = dst + static_cast<size_t>(row) * ldd;
   if constexpr (CH > 0) {
     uint4 u[CH];
@@ -382,10 +382,10 @@ __global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const 
     for (int i = 0; i < CH; ++i) {
       const int c = (lane + 32 * i) * 8;
       u[i] = c < cols ? *reinterpret_cast<const uint4*>(r + c) : make_uint4(0, 0, 0, 0);
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+      const h16x2* h2 = reinterpret_cast<const h16x2*>(&u[i]);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h2[j]);
+        const float2 f = __half22float2(h2[j]);
         amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
       }
     }
@@ -397,12 +397,12 @@ __global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const 
     for (int i = 0; i < CH; ++i) {
       const int c = (lane + 32 * i) * 8;
       if (c >= cols) break;
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+      const h16x2* h2 = reinterpret_cast<const h16x2*>(&u[i]);
       uint2 w;
       int8_t* wb = reinterpret_cast<int8_t*>(&w);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h2[j]);
+        const float2 f = __half22float2(h2[j]);
         wb[2 * j] = quant_one(f.x, sd, inv_sd);
         wb[2 * j + 1] = quant_one(f.y, sd, inv_sd);
       }
@@ -411,13 +411,13 @@ __global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const 
   } else {
     const int cols8 = cols & ~7;
     float amax = 0.f;
-    for (int c = cols8 + lane; c < cols; c += 32) amax = fmaxf(amax, fabsf(__bfloat162float(r[c])));
+    for (int c = cols8 + lane; c < cols; c += 32) amax = fmaxf(amax, fabsf(__half2float(r[c])));
     for (int c = lane * 8; c < cols8; c += 256) {
       const uint4 u = *reinterpret_cast<const uint4*>(r + c);
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const h16x2* h2 = reinterpret_cast<const h16x2*>(&u);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h2[j]);
+        const float2 f = __half22float2(h2[j]);
         amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
       }
     }
@@ -425,15 +425,15 @@ __global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const 
     const float sd = amax == 0.f ? 1.f : amax / 127.0f;
     const float inv_sd = 1.0f / sd;
     if (lane == 0) scale[row] = sd;
-    for (int c = cols8 + lane; c < cols; c += 32) o[c] = quant_one(__bfloat162float(r[c]), sd, inv_sd);
+    for (int c = cols8 + lane; c < cols; c += 32) o[c] = quant_one(__half2float(r[c]), sd, inv_sd);
     for (int c = lane * 8; c < cols8; c += 256) {
       const uint4 u = *reinterpret_cast<const uint4*>(r + c);
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const h16x2* h2 = reinterpret_cast<const h16x2*>(&u);
       uint2 w;
       int8_t* wb = reinterpret_cast<int8_t*>(&w);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h2[j]);
+        const float2 f = __half22float2(h2[j]);
         wb[2 * j] = quant_one(f.x, sd, inv_sd);
         wb[2 * j + 1] = quant_one(f.y, sd, inv_sd);
       }
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(256, CH == 0 ? 8 : 4) quant_rows_kernel(const 
 // next row's slice in registers (16-B chunks t + 64 i), amax combined under a 64-thread named barrier.
 // Same per-element rule as quant_rows_kernel.
 template <int CH>
-__global__ void __launch_bounds__(256, 2) quant_rows2_kernel(const __nv_bfloat16* __restrict__ src, int lds, int M,
+__global__ void __launch_bounds__(256, 2) quant_rows2_kernel(const h16* __restrict__ src, int lds, int M,
                                                              int cols, int8_t* __restrict__ dst, int ldd,
                                                              float* __restrict__ scale) {
   pdl_sync();
@@ -471,10 +471,10 @@ __global__ void __launch_bounds__(256, 2) quant_rows2_kernel(const __nv_bfloat16
     float amax = 0.f;
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&cur[i]);
+      const h16x2* h2 = reinterpret_cast<const h16x2*>(&cur[i]);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h2[j]);
+        const float2 f = __half22float2(h2[j]);
         amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
       }
     }
@@ -490,12 +490,12 @@ __global__ void __launch_bounds__(256, 2) quant_rows2_kernel(const __nv_bfloat16
     for (int i = 0; i < CH; ++i) {
       const int c = t + 64 * i;
       if (c < nch) {
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&cur[i]);
+        const h16x2* h2 = reinterpret_cast<const h16x2*>(&cur[i]);
         uint2 w;
         int8_t* wb = reinterpret_cast<int8_t*>(&w);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float2 f = __bfloat1622float2(h2[j]);
+          const float2 f = __half22float2(h2[j]);
           wb[2 * j] = quant_one(f.x, sd, inv_sd);
           wb[2 * j + 1] = quant_one(f.y, sd, inv_sd);
         }
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(256)
                     const int* __restrict__ tok_slot, const int* __restrict__ tok_pos,
                     const int32_t* __restrict__ last_tok, int M, int d, const float* __restrict__ tok_embed,
                     const float* __restrict__ pos_embed, float* __restrict__ x, const float* __restrict__ g,
-                    const float* __restrict__ b, __nv_bfloat16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
+                    const float* __restrict__ b, h16* __restrict__ h, int ldh, int8_t* __restrict__ q8,
                     float* __restrict__ qscale) {
   pdl_sync();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -554,9 +554,9 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32(p)));
 }
-__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void mma_h16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
@@ -595,7 +595,7 @@ struct PfCfg {
   static constexpr size_t SMEM = 1024 + Q_BYTES + ST * STAGE_BYTES + 64;
 };
 
-// Byte offset of element (r, c) in a [R x HD] bf16 tile stored as NCB swizzled [R x CB] boxes.
+// Byte offset of element (r, c) in a [R x HD] fp16 tile stored as NCB swizzled [R x CB] boxes.
 template <int HD>
 __device__ __forceinline__ uint32_t pf_off(int R, int r, int c) {
   using C = PfCfg<HD>;
@@ -709,8 +709,8 @@ __global__ void __launch_bounds__(128, PfCfg<HD>::MINB) attn_prefill_kernel(cons
           if (np == 1 && !need1) break;
           uint32_t b[4];
           ldsm_x4(b, sK + pf_off<HD>(PF_KB, np * 16 + (lane & 7) + (lane >> 4) * 8, kc * 16 + ((lane >> 3) & 1) * 8));
-          mma_bf16(s[2 * np], qf[kc], b[0], b[1]);
-          mma_bf16(s[2 * np + 1], qf[kc], b[2], b[3]);
+          mma_h16(s[2 * np], qf[kc], b[0], b[1]);
+          mma_h16(s[2 * np + 1], qf[kc], b[2], b[3]);
         }
       }
       // chunks entirely at or below the warp's first query need no causal mask (warp-uniform)
@@ -771,16 +771,16 @@ __global__ void __launch_bounds__(128, PfCfg<HD>::MINB) attn_prefill_kernel(cons
       for (int kc = 0; kc < 2; ++kc) {
         if (kc == 1 && !need1) break;
         uint32_t a[4];
-        a[0] = pack_bf16x2(s[2 * kc][0], s[2 * kc][1]);
-        a[1] = pack_bf16x2(s[2 * kc][2], s[2 * kc][3]);
-        a[2] = pack_bf16x2(s[2 * kc + 1][0], s[2 * kc + 1][1]);
-        a[3] = pack_bf16x2(s[2 * kc + 1][2], s[2 * kc + 1][3]);
+        a[0] = pack_h16x2(s[2 * kc][0], s[2 * kc][1]);
+        a[1] = pack_h16x2(s[2 * kc][2], s[2 * kc][3]);
+        a[2] = pack_h16x2(s[2 * kc + 1][0], s[2 * kc + 1][1]);
+        a[3] = pack_h16x2(s[2 * kc + 1][2], s[2 * kc + 1][3]);
 #pragma unroll
         for (int dn = 0; dn < HD / 16; ++dn) {
           uint32_t b[4];
           ldsm_x4_t(b, sV + pf_off<HD>(PF_KB, kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, dn * 16 + (lane >> 4) * 8));
-          mma_bf16(o[2 * dn], a, b[0], b[1]);
-          mma_bf16(o[2 * dn + 1], a, b[2], b[3]);
+          mma_h16(o[2 * dn], a, b[0], b[1]);
+          mma_h16(o[2 * dn + 1], a, b[2], b[3]);
         }
       }
     }
@@ -800,8 +800,8 @@ __global__ void __launch_bounds__(128, PfCfg<HD>::MINB) attn_prefill_kernel(cons
 #pragma unroll
   for (int i = 0; i < HD / 8; ++i) {
     const int col = i * 8 + 2 * tq;
-    *reinterpret_cast<uint32_t*>(gQ + pf_off<HD>(64, qrow0, col)) = pack_bf16x2(o[i][0] * inv[0], o[i][1] * inv[0]);
-    *reinterpret_cast<uint32_t*>(gQ + pf_off<HD>(64, qrow0 + 8, col)) = pack_bf16x2(o[i][2] * inv[1], o[i][3] * inv[1]);
+    *reinterpret_cast<uint32_t*>(gQ + pf_off<HD>(64, qrow0, col)) = pack_h16x2(o[i][0] * inv[0], o[i][1] * inv[0]);
+    *reinterpret_cast<uint32_t*>(gQ + pf_off<HD>(64, qrow0 + 8, col)) = pack_h16x2(o[i][2] * inv[1], o[i][3] * inv[1]);
   }
   __syncwarp();
   constexpr int CPR = HD / 8;  // 16-B chunks per row
@@ -848,7 +848,7 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
   const uint32_t HALF = static_cast<uint32_t>(R) * HD * 2;
   const uint32_t STAGE = 2 * HALF;
   const uint32_t full0 = sbase + nst * STAGE, empty0 = full0 + 8 * DSTAGES_MAX;
-  __nv_bfloat16* sOut = reinterpret_cast<__nv_bfloat16*>(gbase + nst * STAGE + 16 * DSTAGES_MAX);
+  h16* sOut = reinterpret_cast<h16*>(gbase + nst * STAGE + 16 * DSTAGES_MAX);
 
   const int gi = blockIdx.x / n_hgroups;
   const int hgi = blockIdx.x - gi * n_hgroups;
@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
 #pragma unroll
   for (int ks = 0; ks < HD / 16; ++ks) qb[ks][0] = qb[ks][1] = 0u;
   if (active && gq == 0) {
-    const __nv_bfloat16* qr = p.q + static_cast<size_t>(grp.m0) * p.ldq + (h0 + h) * HD;
+    const h16* qr = p.q + static_cast<size_t>(grp.m0) * p.ldq + (h0 + h) * HD;
 #pragma unroll
     for (int ks = 0; ks < HD / 16; ++ks) {
       qb[ks][0] = *reinterpret_cast<const uint32_t*>(qr + ks * 16 + 2 * tq);
@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
       for (int ks = 0; ks < HD / 16; ++ks) {
         uint32_t a[4];
         ldsm_x4(a, sK + pf_off<HD>(R, h * PAGE + (lane & 15), ks * 16 + (lane >> 4) * 8));
-        mma_bf16(sc, a, qb[ks][0], qb[ks][1]);
+        mma_h16(sc, a, qb[ks][0], qb[ks][1]);
       }
       // lanes tq == 0: sc[0] = score of key gq, sc[2] = score of key gq + 8 (of this page)
       const int key0 = pg * PAGE + gq, key1 = key0 + 8;
@@ -945,7 +945,7 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
       l = l * alpha + psum;
       m = mnew;
       // p^T as column 0 of the B operand: lane t < 4 needs keys 2t, 2t+1 (b0) and 8+2t, 9+2t (b1)
-      const uint32_t pk = pack_bf16x2(p0, p1);
+      const uint32_t pk = pack_h16x2(p0, p1);
       const uint32_t u = __shfl_sync(0xffffffffu, pk, (lane & 3) * 8);
       const uint32_t w = __shfl_sync(0xffffffffu, pk, (lane & 3) * 8 + 4);
       const uint32_t b0 = lane < 4 ? __byte_perm(u, w, 0x5410) : 0u;
@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
         o[mt][2] *= alpha;
         uint32_t a[4];
         ldsm_x4_t(a, sV + pf_off<HD>(R, h * PAGE + (lane & 7) + (lane >> 4) * 8, mt * 16 + ((lane >> 3) & 1) * 8));
-        mma_bf16(o[mt], a, b0, b1);
+        mma_h16(o[mt], a, b0, b1);
       }
     }
     __syncwarp();
@@ -966,12 +966,12 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
   if (!active) return;
   // lanes tq == 0 hold O[16mt + gq] (o[mt][0]) and O[16mt + gq + 8] (o[mt][2])
   const float inv = l > 0.f ? 1.f / l : 0.f;
-  __nv_bfloat16* so = sOut + h * HD;
+  h16* so = sOut + h * HD;
   if (tq == 0) {
 #pragma unroll
     for (int mt = 0; mt < HD / 16; ++mt) {
-      so[mt * 16 + gq] = __float2bfloat16_rn(o[mt][0] * inv);
-      so[mt * 16 + gq + 8] = __float2bfloat16_rn(o[mt][2] * inv);
+      so[mt * 16 + gq] = __float2half_rn(o[mt][0] * inv);
+      so[mt * 16 + gq + 8] = __float2half_rn(o[mt][2] * inv);
     }
   }
   __syncwarp();
@@ -1117,17 +1117,17 @@ __global__ void check_ids_kernel(const int32_t* __restrict__ ids, int64_t n, int
 }
 
 // Weight decode: bundle payload -> device GEMM operand (row-major [rows x ld], zero padded).
-__global__ void decode_dense_bf16_kernel(const float* __restrict__ src, int rows, int cols, __nv_bfloat16* dst,
+__global__ void decode_dense_h16_kernel(const float* __restrict__ src, int rows, int cols, h16* dst,
                                          int ld) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(rows) * ld) return;
   const int r = static_cast<int>(i / ld), c = static_cast<int>(i % ld);
-  dst[i] = c < cols ? __float2bfloat16_rn(src[static_cast<size_t>(r) * cols + c]) : __float2bfloat16_rn(0.f);
+  dst[i] = c < cols ? __float2half_rn(src[static_cast<size_t>(r) * cols + c]) : __float2half_rn(0.f);
 }
 
-// q8 / q4 / sparse24 payload -> dequantized bf16 value code*scale (model.cpp:153-199).
-__global__ void decode_quant_bf16_kernel(const uint8_t* __restrict__ p, int enc, int rows, int cols,
-                                         __nv_bfloat16* dst, int ld) {
+// q8 / q4 / sparse24 payload -> dequantized fp16 value code*scale (model.cpp:153-199).
+__global__ void decode_quant_h16_kernel(const uint8_t* __restrict__ p, int enc, int rows, int cols,
+                                         h16* dst, int ld) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(rows) * ld) return;
   const int r = static_cast<int>(i / ld), c = static_cast<int>(i % ld);
@@ -1157,10 +1157,10 @@ __global__ void decode_quant_bf16_kernel(const uint8_t* __restrict__ p, int enc,
       if (j == p1) v = static_cast<float>(codes[(r * groups + gidx) * 2 + 1]) * s;
     }
   }
-  dst[i] = __float2bfloat16_rn(v);
+  dst[i] = __float2half_rn(v);
 }
 
-// Quantized payload -> the integer codes only (exact as bf16 for |code| <= 127), zero padded;
+// Quantized payload -> the integer codes only (exact as fp16 for |code| <= 127), zero padded;
 // scales[r] receives the per-row f32 scale. The scale is applied in the GEMM epilogue.
 template <typename T>
 __global__ void decode_codes_kernel(const uint8_t* __restrict__ p, int enc, int rows, int cols, T* dst, int ld,
@@ -1195,7 +1195,7 @@ __global__ void decode_codes_kernel(const uint8_t* __restrict__ p, int enc, int 
     }
   }
   if constexpr (sizeof(T) == 1) dst[i] = static_cast<int8_t>(code);
-  else dst[i] = __int2bfloat16_rn(code);
+  else dst[i] = __int2half_rn(code);
   if (c == 0) {
     float s;
     memcpy(&s, p + scale_off + 4ull * r, 4);
@@ -1250,12 +1250,12 @@ int decode_heads_per_cta(int heads, int hd) {
 
 static inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
-void launch_ln(const float* x, int M, int d, const float* g, const float* b, __nv_bfloat16* h, int ldh,
+void launch_ln(const float* x, int M, int d, const float* g, const float* b, h16* h, int ldh,
                cudaStream_t st, int8_t* q8, float* qscale) {
   if (M <= 0) return;
   const int nv = (d / 4 + 31) / 32;
   const int sms = device_sms();
-  // gain / bias staged in shared memory for the bf16 output (measured: C1 LN 237 -> 224 ms; the int8
+  // gain / bias staged in shared memory for the fp16 output (measured: C1 LN 237 -> 224 ms; the int8
   // output variant is 3-6% slower with it, C3 / C4). IOLM_LN_GB_SMEM=0 / 1 forces it off / on (A/B).
   static const int gb_env = [] {
     const char* e = std::getenv("IOLM_LN_GB_SMEM");
@@ -1298,7 +1298,7 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
     return;
   }
   const size_t bsmem = 256 + static_cast<size_t>(LN_STAGES) * 8 * d * 4;
-  // the bulk-streamed variant pays off for the int8 (W8A8) output; the bf16 output keeps the
+  // the bulk-streamed variant pays off for the int8 (W8A8) output; the fp16 output keeps the
   // register-resident one-warp-per-row kernel (measured faster at d = 1280)
   if (q8 && d % 128 == 0 && (nv == 10 || nv == 16 || nv == 8 || nv == 4) && bsmem <= 200 * 1024) {
     const int per_sm = bsmem <= 100 * 1024 ? 2 : 1;
@@ -1346,7 +1346,7 @@ void launch_ln(const float* x, int M, int d, const float* g, const float* b, __n
   CUDA_OK(cudaGetLastError());
 }
 
-void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_t* dst, int ldd, float* scale,
+void launch_quant_rows(const h16* src, int lds, int M, int cols, int8_t* dst, int ldd, float* scale,
                        cudaStream_t st) {
   if (M <= 0) return;
   if (lds % 8 != 0 || ldd % 8 != 0) throw Unsupported("quant_rows: leading dimensions must be multiples of 8");
@@ -1367,7 +1367,7 @@ void launch_quant_rows(const __nv_bfloat16* src, int lds, int M, int cols, int8_
 
 void launch_embed_ln(const int32_t* ids, const int64_t* tok_src, const int* tok_slot, const int* tok_pos,
                      const int32_t* last_tok, int M, int d, const float* tok_embed, const float* pos_embed, float* x,
-                     const float* g, const float* b, __nv_bfloat16* h, int ldh, cudaStream_t st, int8_t* q8,
+                     const float* g, const float* b, h16* h, int ldh, cudaStream_t st, int8_t* q8,
                      float* qscale) {
   if (M <= 0) return;
   const unsigned grid = blocks_for(M, 8);
@@ -1453,14 +1453,14 @@ void launch_check_ids(const int32_t* ids, int64_t n, int V, int* bad, cudaStream
   CUDA_OK(cudaGetLastError());
 }
 
-void launch_decode_weight(const void* payload, int enc, int rows, int cols, __nv_bfloat16* dst, int ld,
+void launch_decode_weight(const void* payload, int enc, int rows, int cols, h16* dst, int ld,
                           cudaStream_t st) {
   const int64_t n = static_cast<int64_t>(rows) * ld;
   if (enc == 0)
-    decode_dense_bf16_kernel<<<blocks_for(n, 256), 256, 0, st>>>(static_cast<const float*>(payload), rows, cols,
+    decode_dense_h16_kernel<<<blocks_for(n, 256), 256, 0, st>>>(static_cast<const float*>(payload), rows, cols,
                                                                  dst, ld);
   else
-    decode_quant_bf16_kernel<<<blocks_for(n, 256), 256, 0, st>>>(static_cast<const uint8_t*>(payload), enc, rows,
+    decode_quant_h16_kernel<<<blocks_for(n, 256), 256, 0, st>>>(static_cast<const uint8_t*>(payload), enc, rows,
                                                                  cols, dst, ld);
   CUDA_OK(cudaGetLastError());
 }
@@ -1473,8 +1473,8 @@ void launch_decode_codes(const void* payload, int enc, int rows, int cols, void*
     decode_codes_kernel<int8_t><<<blocks_for(n, 256), 256, 0, st>>>(static_cast<const uint8_t*>(payload), enc, rows,
                                                                     cols, static_cast<int8_t*>(dst), ld, scales);
   else
-    decode_codes_kernel<__nv_bfloat16><<<blocks_for(n, 256), 256, 0, st>>>(
-        static_cast<const uint8_t*>(payload), enc, rows, cols, static_cast<__nv_bfloat16*>(dst), ld, scales);
+    decode_codes_kernel<h16><<<blocks_for(n, 256), 256, 0, st>>>(
+        static_cast<const uint8_t*>(payload), enc, rows, cols, static_cast<h16*>(dst), ld, scales);
   CUDA_OK(cudaGetLastError());
 }
 

@@ -2,7 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
-#include <cuda_bf16.h>
+#include "dtype.hpp"
 
 namespace iolmk {
 
@@ -20,11 +20,11 @@ struct AttnParams {
   CUtensorMap q_map;   // prefill: q buffer [T x ldq] as [CB-wide swizzled boxes x 64 rows]
   CUtensorMap kv_map;  // prefill: layer pool as rows of hd ([page][K|V][heads][PAGE] rows), 16-row boxes
   CUtensorMap kvg_map; // decode: the same rows in boxes of decode_heads_per_cta(heads, hd) * PAGE rows
-  const __nv_bfloat16* q;  // [T x ldq] (head h at columns h*hd ..)
+  const h16* q;  // [T x ldq] (head h at columns h*hd ..)
   int ldq;
-  __nv_bfloat16* z;  // [T x ldz] output
+  h16* z;  // [T x ldz] output
   int ldz;
-  const __nv_bfloat16* kv;  // layer pool: [page][K|V][heads][PAGE][hd]
+  const h16* kv;  // layer pool: [page][K|V][heads][PAGE][hd]
   const int* page_table;    // [slots x max_pages]
   int max_pages;
   int heads;

@@ -3,7 +3,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
-#include <cuda_bf16.h>
+#include "dtype.hpp"
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -97,10 +97,10 @@ void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaSt
 // ---- launchers (gemm_launch.cu, kernels.cu)
 // pair: 2-SM 256x256 tiles (clusters of 2) vs single-CTA 128x128 tiles; i8: W8A8 kind::i8.
 // out_map (optional): TMA map of ep.out for the RESID (reduce-add) / BF16 / GELU epilogues - fp32
-// [M x ldo] boxes 32 x 32 SWIZZLE_128B, or bf16 boxes 32 x 32 SWIZZLE_64B (make_out_map_*).
+// [M x ldo] boxes 32 x 32 SWIZZLE_128B, or fp16 boxes 32 x 32 SWIZZLE_64B (make_out_map_*).
 void launch_gemm(bool pair, bool i8, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
                  const iolmk::GemmEpi& ep, cudaStream_t st, int grid_cap, const CUtensorMap* out_map = nullptr);
-// W4A16: B = packed int4 weights [N x ceil(K/2) bytes] (make_w4_map), expanded to bf16 in smem.
+// W4A16: B = packed int4 weights [N x ceil(K/2) bytes] (make_w4_map), expanded to fp16 in smem.
 void launch_gemm_w4(bool pair, int epi, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
                     const iolmk::GemmEpi& ep, cudaStream_t st, int grid_cap, const CUtensorMap* out_map = nullptr);
 

@@ -3,7 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
-#include <cuda_bf16.h>
+#include "dtype.hpp"
 
 namespace iolmk {
 
@@ -225,7 +225,7 @@ __device__ __forceinline__ void umma_commit_pair_mc(uint32_t bar, uint16_t mask)
       : "memory");
 }
 
-// D[tmem] (+)= A[smem desc] * B[smem desc]^T, kind::f16 (bf16/fp16 in, fp32 accumulate).
+// D[tmem] (+)= A[smem desc] * B[smem desc]^T, kind::f16 (fp16/fp16 in, fp32 accumulate).
 __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -282,7 +282,7 @@ __device__ __forceinline__ uint64_t smem_desc_k_sw128(uint32_t saddr) {
 }
 
 // Instruction descriptor, kind::f16 with fp32 accumulate, both operands K-major.
-// ab_fmt: 0 = f16, 1 = bf16.
+// ab_fmt: 0 = f16, 1 = fp16.
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, uint32_t ab_fmt) {
   return (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
          (static_cast<uint32_t>(M >> 4) << 24);
@@ -293,8 +293,8 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+__device__ __forceinline__ uint32_t pack_h16x2(float lo, float hi) {
+  h16x2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
@@ -319,7 +319,7 @@ __device__ __forceinline__ float rcp_ftz(float x) {
 // Reference: 0.5*x*(1+tanh(u)), u = 0.7978845608028654*(x+0.044715*x^3) (numerics.cpp:179-184).
 // Evaluated as the identical x * sigmoid(2u) = x / (1 + 2^(-2u*log2(e))): one ex2.approx (rel. error
 // ~2^-22) and one rcp.approx (<= 1 ulp), so the result is within a few f32 ulps of the reference's.
-// (The SFU tanh.approx, max rel. error 2^-11, moved ~1 in 4 bf16 roundings of the output and, in
+// (The SFU tanh.approx, max rel. error 2^-11, moved ~1 in 4 fp16 roundings of the output and, in
 // W8A8, its int8 codes: oracle/iolm_oracle.c gelu_gpu restates this form exactly.)
 __device__ __forceinline__ float gelu_tanh(float x) {
   constexpr float k = 0.7978845608028654f, k3 = 0.7978845608028654f * 0.044715f;

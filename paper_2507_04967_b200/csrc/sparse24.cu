@@ -28,7 +28,7 @@ Sp24Layout sp24_layout(int N, int K, bool f16) {
   l.K = K;
   l.f16 = f16;
   l.ld_c = ((K / 2) * (f16 ? 2 : 1) + 15) / 16 * 16;
-  // int8: a stage is 256 logical K = 2 atoms; bf16: 128 logical K = 1 atom
+  // int8: a stage is 256 logical K = 2 atoms; fp16: 128 logical K = 1 atom
   l.katoms_pad = f16 ? (K + 127) / 128 : 2 * ((K + SpCfg::BK - 1) / SpCfg::BK);
   l.mtiles = 2 * ((N + SpCfg::TILE_M - 1) / SpCfg::TILE_M);
   return l;
@@ -60,12 +60,9 @@ void sp24_append(const Sp24Layout& l, const uint8_t* payload, int rows, int cols
     uint8_t* dst = static_cast<uint8_t*>(codes_out) + static_cast<size_t>(gr) * l.ld_c;
     if (!l.f16) {
       std::memcpy(dst, src, groups * 2);
-    } else {  // |code| <= 127 is exact in bf16: the f32 bit pattern's top half
+    } else {  // |code| <= 127 is exact in fp16
       for (size_t i = 0; i < groups * 2; ++i) {
-        const float f = static_cast<float>(static_cast<int8_t>(src[i]));
-        uint32_t u;
-        std::memcpy(&u, &f, 4);
-        const uint16_t h = static_cast<uint16_t>(u >> 16);
+        const uint16_t h = f16_bits_of_int(static_cast<int8_t>(src[i]));
         std::memcpy(dst + 2 * i, &h, 2);
       }
     }
@@ -106,7 +103,7 @@ void sp24_finalize(const Sp24Layout& l, uint8_t* meta) {
 
 CUtensorMap sp24_codes_map(const Sp24Layout& l, const void* d_codes) {
   if (l.f16)
-    return make_kmajor_map(d_codes, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, static_cast<uint64_t>(l.K / 2), l.N,
+    return make_kmajor_map(d_codes, H16_TMA, 2, static_cast<uint64_t>(l.K / 2), l.N,
                            static_cast<uint64_t>(l.ld_c), 128);
   return make_kmajor_map(d_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, static_cast<uint64_t>(l.K / 2), l.N,
                          static_cast<uint64_t>(l.ld_c), 128);
@@ -116,7 +113,7 @@ CUtensorMap sp24_meta_map(const Sp24Layout& l, const uint8_t* d_meta) {
   CUtensorMap m;
   cuuint64_t dims[2] = {16, static_cast<cuuint64_t>(l.meta_bytes() / 16)};
   cuuint64_t strides[1] = {16};
-  cuuint32_t box[2] = {16, l.f16 ? 128u : 256u};  // one stage: 1 (bf16) or 2 (int8) 128-row atoms
+  cuuint32_t box[2] = {16, l.f16 ? 128u : 256u};  // one stage: 1 (fp16) or 2 (int8) 128-row atoms
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_meta), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -130,8 +127,8 @@ CUtensorMap sp24_act_map(const int8_t* act, int K, int rows, int ld) {
                          static_cast<uint64_t>(ld), SpCfg::BN_CTA);
 }
 
-CUtensorMap sp24_act_map_bf16(const void* act, int K, int rows, int ld) {
-  return make_kmajor_map(act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, static_cast<uint64_t>(K), rows,
+CUtensorMap sp24_act_map_h16(const void* act, int K, int rows, int ld) {
+  return make_kmajor_map(act, H16_TMA, 2, static_cast<uint64_t>(K), rows,
                          2ull * static_cast<uint64_t>(ld), SpCfg::BN_CTA);
 }
 
@@ -167,8 +164,8 @@ static void launch_sp(int epi, const CUtensorMap& A, const CUtensorMap& B, const
       else launch_sp_one<EPI_S32, false>(A, B, E, K, katoms_pad, ep, st, grid_cap);
       break;
     case EPI_F32: launch_sp_one<EPI_F32, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_BF16: launch_sp_one<EPI_BF16, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_GELU_BF16: launch_sp_one<EPI_GELU_BF16, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_H16: launch_sp_one<EPI_H16, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_GELU_H16: launch_sp_one<EPI_GELU_H16, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
     case EPI_RESID_F32: launch_sp_one<EPI_RESID_F32, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
     case EPI_QKV: launch_sp_one<EPI_QKV, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
     case EPI_NONE: launch_sp_one<EPI_NONE, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;

@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include "dtype.hpp"
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -48,10 +50,10 @@ inline CUtensorMap make_kmajor_map(const void* ptr, CUtensorMapDataType dt, int 
   return m;
 }
 
-// bf16 row tensor [rows x inner] read in boxes of box_inner elements x box_rows, swizzled over the
+// fp16 row tensor [rows x inner] read in boxes of box_inner elements x box_rows, swizzled over the
 // box's row span (128/64/32 B -> SWIZZLE_128B/64B/32B). Used by the prefill attention for the q
 // buffer and the paged KV pool.
-inline CUtensorMap make_rows_map_bf16(const void* ptr, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
+inline CUtensorMap make_rows_map_h16(const void* ptr, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
                                       uint32_t box_inner, uint32_t box_rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, rows};
@@ -65,7 +67,7 @@ inline CUtensorMap make_rows_map_bf16(const void* ptr, uint64_t inner, uint64_t 
                                              : CU_TENSOR_MAP_SWIZZLE_NONE;
   if (sw == CU_TENSOR_MAP_SWIZZLE_NONE || (row_stride_bytes % 16) != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
     throw std::runtime_error("row TMA map: unsupported box width or misaligned tensor");
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+  CUresult r = encode_fn()(&m, H16_TMA, 2, const_cast<void*>(ptr), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -94,7 +96,7 @@ inline CUtensorMap make_w4_map(const void* ptr, uint64_t K, uint64_t rows, uint6
 }
 
 // GEMM output boxes of 32 x 32 for the TMA epilogue: fp32 [rows x cols] with SWIZZLE_128B (the
-// epilogue's swz() staging layout), bf16 [rows x cols] with SWIZZLE_64B.
+// epilogue's swz() staging layout), fp16 [rows x cols] with SWIZZLE_64B.
 inline CUtensorMap make_out_map(const void* ptr, bool f32, uint64_t cols, uint64_t rows, uint64_t row_stride_bytes) {
   CUtensorMap m;
   cuuint64_t dims[2] = {cols, rows};
@@ -103,7 +105,7 @@ inline CUtensorMap make_out_map(const void* ptr, bool f32, uint64_t cols, uint64
   cuuint32_t es[2] = {1, 1};
   if ((row_stride_bytes % 16) != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
     throw std::runtime_error("output map must be 16-byte aligned with a 16-byte row stride");
-  CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : H16_TMA, 2,
                            const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

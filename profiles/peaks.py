@@ -67,7 +67,7 @@ def engine_timed(kind: str, T: int, N: int, K: int, seconds: float) -> dict:
         if kind == "sp24_i8":
             st = lib.iolm_cuda_debug_gemm_sp24_time(T, N, K, 6, iters, C.byref(ms))
         elif kind == "sp24_bf16":
-            st = lib.iolm_cuda_debug_gemm_sp24_bf16_time(T, N, K, 6, iters, C.byref(ms))
+            st = lib.iolm_cuda_debug_gemm_sp24_f16_time(T, N, K, 6, iters, C.byref(ms))
         else:
             st = lib.iolm_cuda_debug_gemm_time(T, N, K, 6, 1, 1 if kind == "i8" else 0, iters, C.byref(ms))
         if st:

@@ -83,7 +83,7 @@ int main() {
   }
   EXPECT(threw, "ContractViolation");
   // calibration capture (capture_calibration, calib.cpp:20-62) on the GPU: same capture points,
-  // shapes, and rows (bf16 capture of the f32 activations: rel-L2 per point <= 1e-2)
+  // shapes, and rows (fp16 capture of the f32 activations: rel-L2 per point <= 1e-2)
   {
     std::vector<std::string> cal(prompts.begin(), prompts.begin() + 4);
     cal[1].resize(20);

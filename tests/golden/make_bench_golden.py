@@ -31,7 +31,7 @@ from oracle import oracle as O  # noqa: E402
 from paper_2507_04967_b200 import synth  # noqa: E402
 
 HERE = Path(__file__).resolve().parent
-ROWS = {"c1": 100, "c2-w8a8": 100, "c2-w4a16": 100, "c3": 100, "c3b": 100, "c4": 16, "c3-bf16": 100}
+ROWS = {"c1": 100, "c2-w8a8": 100, "c2-w4a16": 100, "c3": 100, "c3b": 100, "c4": 16, "c3-f16": 100}
 FIRST_ROW = 0
 MAX_NEW = 8
 

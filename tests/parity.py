@@ -4,7 +4,7 @@ and every divergence must be traced to an fp tie").
 
 A divergence at step k is a tie when the CPU top-1 / top-2 logit gap at that step is below
     TIE_ABS + TIE_REL * max|logit|
-i.e. within the stated logits tolerance (rel <= 1e-2) of the bf16/fp32 GPU arithmetic: a gap that
+i.e. within the stated logits tolerance (rel <= 1e-2) of the fp16/fp32 GPU arithmetic: a gap that
 small can flip under a relative logit perturbation of a few 1e-3.
 """
 from __future__ import annotations

@@ -131,7 +131,7 @@ def test_cpp_shim_compiles(with_ref, tmp_path):
 
 def _image_bytes(words, arrays=b""):
     w = np.asarray(words, dtype="<i8")
-    return b"IOLMDL01" + len(w).to_bytes(8, "little") + w.tobytes() + arrays
+    return b"IOLMDL02" + len(w).to_bytes(8, "little") + w.tobytes() + arrays
 
 
 def _image_info(path):
@@ -160,7 +160,7 @@ def test_device_image_header_validation(tmp_path):
         q.write_bytes(data)
         return _image_info(q)[0]
 
-    assert status(b"IOLMDL02" + _image_bytes(words)[8:]) == _lib.IOLM_E_CORRUPT_HEADER      # magic
+    assert status(b"IOLMDL01" + _image_bytes(words)[8:]) == _lib.IOLM_E_CORRUPT_HEADER      # magic (v01: bf16 arrays)
     assert status(_image_bytes(words)[:40]) == _lib.IOLM_E_TRUNCATED_BLOB                   # short
     assert status(_image_bytes(words[:-1])) == _lib.IOLM_E_CORRUPT_HEADER                   # words
     assert status(_image_bytes(words + [0])) == _lib.IOLM_E_CORRUPT_HEADER                  # trailing

@@ -22,7 +22,7 @@ from parity import TIE_ABS, TIE_REL
 
 pytestmark = pytest.mark.gpu
 GOLD = Path(__file__).resolve().parent / "golden"
-CONFIGS = ["c1", "c2-w8a8", "c2-w4a16", "c3", "c3b", "c4", "c3-bf16"]
+CONFIGS = ["c1", "c2-w8a8", "c2-w4a16", "c3", "c3b", "c4", "c3-f16"]
 
 
 @pytest.mark.parametrize("name", CONFIGS)

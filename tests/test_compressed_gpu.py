@@ -1,13 +1,13 @@
 """Compressed and pruned bundles on the GPU (BASELINE configs C2/C3 at toy scale).
 
 * q8 / q4 / sparse24_q8 weights WITHOUT activation quantization (W8A16 / W4A16): the integer codes
-  run as exact bf16 integers with the per-channel scale applied in the GEMM epilogue. Checked against
+  run as exact fp16 integers with the per-channel scale applied in the GEMM epilogue. Checked against
   the reference semantics (weights dequantized to f32 at load, runtime.cpp:66-85): logits rel-L2
   <= 1e-2, >= 99% greedy agreement with every divergence on a near-tie.
 * W8A8 (act_quant): per-token int8 activations x int8 codes through tcgen05 kind::i8. The reference
   has no activation quantization, so the checker is the W8A8 restatement in
-  oracle/iolm_oracle.c at the GPU engine's rounding points (gpu_points: bf16 q/K/V, block-wise
-  bf16-P attention, bf16 GELU output before quantization): logits rel-L2 <= 1e-2 on the toy model,
+  oracle/iolm_oracle.c at the GPU engine's rounding points (gpu_points: fp16 q/K/V, block-wise
+  fp16-P attention, fp16 GELU output before quantization): logits rel-L2 <= 1e-2 on the toy model,
   >= 99% greedy agreement with every divergence an fp near-tie (tests/parity.py). The integer GEMM
   itself is bit-exact (tests/test_gemm_gpu.py) and the operand codes are compared element by element
   in tests/test_w8a8_codes_gpu.py. Agreement with the f32 reference is reported, not asserted.

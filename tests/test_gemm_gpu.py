@@ -1,5 +1,5 @@
-"""Parity of the production tcgen05 GEMM (bf16 operands, fp32 accumulate) against an fp32
-reference of the same op on the same bf16-rounded inputs (the reference's `matmul`,
+"""Parity of the production tcgen05 GEMM (fp16 operands, fp32 accumulate) against an fp32
+reference of the same op on the same fp16-rounded inputs (the reference's `matmul`,
 proj/src/numerics.cpp:56-76, is the f32 sum of the same products)."""
 import ctypes as C
 
@@ -9,23 +9,22 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def bf16_bits(x: np.ndarray) -> np.ndarray:
-    u = x.astype(np.float32).view(np.uint32).astype(np.uint64)
-    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
-    return r
+def h16_bits(x: np.ndarray) -> np.ndarray:
+    """IEEE fp16 bit patterns of x (round to nearest even), the engine's 16-bit operand type."""
+    return np.ascontiguousarray(x, np.float32).astype(np.float16).view(np.uint16)
 
 
 def bits_to_f32(b: np.ndarray) -> np.ndarray:
-    return (b.astype(np.uint32) << 16).view(np.float32)
+    return b.view(np.float16).astype(np.float32)
 
 
 def run_gemm(lib, A, W, bn=256, epi=0, C0=None):
     M, K = A.shape
     N = W.shape[0]
-    a = np.ascontiguousarray(bf16_bits(A))
-    w = np.ascontiguousarray(bf16_bits(W))
+    a = np.ascontiguousarray(h16_bits(A))
+    w = np.ascontiguousarray(h16_bits(W))
     out = np.zeros((M, N), np.float32) if C0 is None else C0.copy()
-    st = lib.iolm_cuda_debug_gemm_bf16(a.ctypes.data, w.ctypes.data, out.ctypes.data, M, N, K, bn, epi)
+    st = lib.iolm_cuda_debug_gemm_f16(a.ctypes.data, w.ctypes.data, out.ctypes.data, M, N, K, bn, epi)
     assert st == 0, lib.iolm_cuda_last_error()
     return out, bits_to_f32(a).reshape(M, K), bits_to_f32(w).reshape(N, K)
 
@@ -84,11 +83,11 @@ def test_activation_quantizer_bitexact(engine_lib):
     x = (rng.standard_normal((257, 1280)) * rng.uniform(0.01, 30, size=(257, 1))).astype(np.float32)
     x[3] = 0.0
     x[7, :5] = [2.5, -3.5, 127.0, -0.5, 1.5]  # exact half-integers once scaled
-    bits = bf16_bits(x)
+    bits = h16_bits(x)
     xf = bits_to_f32(bits).reshape(x.shape)
     codes = np.zeros(x.shape, np.int8)
     scales = np.zeros(x.shape[0], np.float32)
-    st = engine_lib.iolm_cuda_debug_quant_rows_bf16(np.ascontiguousarray(bits).ctypes.data, x.shape[0], x.shape[1],
+    st = engine_lib.iolm_cuda_debug_quant_rows_f16(np.ascontiguousarray(bits).ctypes.data, x.shape[0], x.shape[1],
                                                     codes.ctypes.data, scales.ctypes.data)
     assert st == 0, engine_lib.iolm_cuda_last_error()
     rc, rs = O.quant_rows_s8(xf)
@@ -103,13 +102,13 @@ def test_activation_quantizer_widths_and_near_ties(engine_lib, d):
     from oracle import oracle as O
     rng = np.random.default_rng(d)
     x = rng.standard_normal((33, d)).astype(np.float32)
-    x[:, 0] = 127.0  # amax 127 -> scale 1.0: integers and exact halves stay exact in bf16
+    x[:, 0] = 127.0  # amax 127 -> scale 1.0: integers and exact halves stay exact in fp16
     x[:, 1:9] = [0.5, 1.5, -2.5, 3.5, 126.5, -0.5, 2.5000002, 1.4999999]
-    bits = bf16_bits(x)
+    bits = h16_bits(x)
     xf = bits_to_f32(bits).reshape(x.shape)
     codes = np.zeros(x.shape, np.int8)
     scales = np.zeros(x.shape[0], np.float32)
-    st = engine_lib.iolm_cuda_debug_quant_rows_bf16(np.ascontiguousarray(bits).ctypes.data, x.shape[0], d,
+    st = engine_lib.iolm_cuda_debug_quant_rows_f16(np.ascontiguousarray(bits).ctypes.data, x.shape[0], d,
                                                     codes.ctypes.data, scales.ctypes.data)
     if d % 8:
         assert st != 0  # the debug entry requires d % 8 == 0; the engine path handles any width

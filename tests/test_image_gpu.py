@@ -4,7 +4,7 @@ An image is the pre-tiled cache a registry keeps next to a bundle (ModelRegistry
 proj/src/optimize.cpp:139-160): the weights in this engine's HBM layout, the config and the bundle
 hash. The bar is bit-identity: a runtime loaded from an image must produce exactly the ids, lengths,
 FlopCounter totals and logits of the runtime built from the bundle, in every weight form the engine
-has (bf16 values, W8A16 codes, W8A8 int8, 2:4 sparse int8, packed int4), on pruned shapes. The
+has (fp16 values, W8A16 codes, W8A8 int8, 2:4 sparse int8, packed int4), on pruned shapes. The
 failure modes map to the reference's: bad magic / checksum -> CorruptHeader, short file ->
 TruncatedBlob; another bundle or other weight options -> StaleImage (rebuild from the bundle)."""
 import numpy as np

@@ -1,7 +1,7 @@
 """GPU parity of the sm_100a runtime against the CPU reference (oracle/_ref, the reference compiled
 unmodified) and the C restatement, on the same seeded bundles and synthetic rows.
 
-Tolerances (BASELINE.json north_star): logits rel-L2 <= 1e-2 per row (bf16 GEMM operands, fp32
+Tolerances (BASELINE.json north_star): logits rel-L2 <= 1e-2 per row (fp16 GEMM operands, fp32
 accumulate / residual / LN / softmax); greedy ids identical on >= 99% of rows, and every divergent
 row must sit on an fp near-tie of the CPU logits at the step where it diverges."""
 import numpy as np
@@ -184,7 +184,7 @@ def test_parity_production_head_dims(cfg, row_chars, n_rows):
                          ids=["hd64", "hd128-long"])
 def test_prefill_tc_matches_mma_sync(cfg, row_chars):
     """tcgen05 prefill attention (128-query tiles, TMEM S / O, 64-key blocks) against the mma.sync
-    kernel on the same engine: logits agree to bf16 rounding (<= 5e-3 rel-L2) and both keep the
+    kernel on the same engine: logits agree to fp16 rounding (<= 5e-3 rel-L2) and both keep the
     oracle tolerance; greedy ids agree; batch invariance holds with the tcgen05 kernel."""
     b = synth.toy_bundle(*cfg, seed=42)
     tc, mm = R.ModelRuntime(b, prefill_tc=True), R.ModelRuntime(b, prefill_tc=False)

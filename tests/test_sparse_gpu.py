@@ -135,23 +135,22 @@ def test_engine_sparse_long_rows_hd128():
     assert np.array_equal(gl, dl) and np.array_equal(gi, di)
 
 
-# ---------------------------------------------------------------- bf16 activations (kind::f16 .sp)
+# ---------------------------------------------------------------- fp16 activations (kind::f16 .sp)
 
-def bf16_bits(x):
-    u = np.ascontiguousarray(x, np.float32).view(np.uint32)
-    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
-    return r, (r.astype(np.uint32) << 16).view(np.float32)
+def h16_bits(x):
+    h = np.ascontiguousarray(x, np.float32).astype(np.float16)
+    return h.view(np.uint16), h.astype(np.float32)
 
 
 @pytest.mark.parametrize("T,N,K", [(224, 256, 256), (300, 1920, 1280), (77, 1280, 2560), (513, 130, 2512), (5, 16, 16)])
-def test_sp24_bf16_gemm(engine_lib, T, N, K):
-    """tcgen05.mma.sp kind::f16 over the payload's kept codes as exact bf16 and bf16 activations,
-    epilogue acc * s_w: against an f64 product of the same bf16 values (fp32 accumulation bound)."""
+def test_sp24_f16_gemm(engine_lib, T, N, K):
+    """tcgen05.mma.sp kind::f16 over the payload's kept codes as exact fp16 and fp16 activations,
+    epilogue acc * s_w: against an f64 product of the same fp16 values (fp32 accumulation bound)."""
     rng = np.random.default_rng(T + 5 * N + 11 * K)
     payload, Wd, scales = make_sparse24(rng, N, K)
-    xb, xf = bf16_bits(rng.standard_normal((T, K)).astype(np.float32))
+    xb, xf = h16_bits(rng.standard_normal((T, K)).astype(np.float32))
     out = np.zeros((T, N), np.float32)
-    st = engine_lib.iolm_cuda_debug_gemm_sp24_bf16(xb.ctypes.data, payload.ctypes.data, T, N, K, out.ctypes.data)
+    st = engine_lib.iolm_cuda_debug_gemm_sp24_f16(xb.ctypes.data, payload.ctypes.data, T, N, K, out.ctypes.data)
     assert st == 0, engine_lib.iolm_cuda_last_error()
     want = (xf.astype(np.float64) @ Wd.astype(np.float64).T) * scales[None, :].astype(np.float64)
     bound = (np.abs(xf).astype(np.float64) @ np.abs(Wd).astype(np.float64).T) * scales[None, :] * 4e-6 + 1e-30
@@ -160,11 +159,11 @@ def test_sp24_bf16_gemm(engine_lib, T, N, K):
 
 @pytest.mark.parametrize("heads,ffn", [(None, None), ([2, 2, 2, 2], [256, 256, 256, 256]),
                                        ([1, 3, 2, 4], [124, 500, 260, 388])])
-def test_engine_sparse_bf16_matches_dense_codes(heads, ffn):
-    """sparse24_q8 WITHOUT act_quant (the drop-in default): the 2:4 sparse tensor cores on bf16
-    activations (W_SP24F) against the same engine with the codes expanded to dense bf16 (sparse_mma
+def test_engine_sparse_f16_matches_dense_codes(heads, ffn):
+    """sparse24_q8 WITHOUT act_quant (the drop-in default): the 2:4 sparse tensor cores on fp16
+    activations (W_SP24F) against the same engine with the codes expanded to dense fp16 (sparse_mma
     off): logits to fp32-accumulation-order rounding, greedy ids identical but for near-ties, and the
-    reference semantics (f32 oracle) within the bf16 tolerance."""
+    reference semantics (f32 oracle) within the fp16 tolerance."""
     from oracle import oracle as O
     from parity import check_agreement
     b = synth.toy_bundle(*TOY, seed=42, quant="sparse24", heads=heads, ffn=ffn)
@@ -181,6 +180,6 @@ def test_engine_sparse_bf16_matches_dense_codes(heads, ffn):
     ids, offs = synth.rows(0, 64, 64)
     gi, gl, gm = sp.decode_token_rows(ids, offs, 8)
     oi, ol, om_m = om.decode_ids(ids, offs, 8, threads=8)
-    check_agreement(om, ids, offs, gi, gl, oi, ol, label="sp24 bf16")
+    check_agreement(om, ids, offs, gi, gl, oi, ol, label="sp24 fp16")
     one, l1, _ = sp.decode_token_rows(ids[offs[5]:offs[6]], np.array([0, offs[6] - offs[5]]), 8)
     assert l1[0] == gl[5] and np.array_equal(one[0, :l1[0]], gi[5, :gl[5]])  # batch invariance
