@@ -19,6 +19,7 @@
 // Keys are processed in blocks aligned to absolute positions, so a query's arithmetic never depends
 // on which other queries share its tile (batch invariance, test_model.cpp:240-267).
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "launch.hpp"
@@ -293,6 +294,11 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
         for (int c = 0; c < KB; c += 32)
           tmem_ld_32x32b_x32(lane_base + C::S_COL + b * KB + c, *reinterpret_cast<uint32_t(*)[32]>(sr + c));
         tmem_ld_wait();
+        // S(g) is in registers: release its TMEM buffer now, so S(g + 2) overlaps this softmax (P(g)
+        // is still protected: it is read by PV(g), which accumulate(g) waits for before P(g + 2))
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty(b));
         float mx = -INFINITY;
 #pragma unroll
         for (int i = 0; i < KB; ++i) {
@@ -335,10 +341,7 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (generic writes) -> tensor core
         __syncwarp();
-        if (lane == 0) {  // p_full before s_empty: S(g + 2) completing implies every P(g) arrival
-          mbar_arrive(p_full(b));
-          mbar_arrive(s_empty(b));
-        }
+        if (lane == 0) mbar_arrive(p_full(b));
         if (kb > 0) accumulate(g - 1, alpha_prev);
         alpha_prev = alpha;
       }
@@ -391,16 +394,19 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
 // TMEM 256 columns (S double-buffered 2 x 64, O 128), ~97 KB smem: two CTAs per SM, each a
 // producer warp, an MMA warp and one softmax warpgroup.
 constexpr float HP_RESCALE = 8.0f;
+template <int QB, int NST_>
 struct HpCfg {
   static constexpr int KB = 32;                         // keys per block (2 pages)
-  static constexpr int NST = 3;                         // K/V ring depth
+  static constexpr int NST = NST_;                      // K/V ring depth
+  static constexpr int QBUF = QB;                       // Q tiles (next item's Q prefetched when 2)
   static constexpr uint32_t Q_BYTES = 128 * 128;        // 2 heads x 64 rows x 128 B
   static constexpr uint32_t KT_BYTES = 2 * KB * 128;    // K of both heads (also V)
   static constexpr uint32_t STAGE_BYTES = 2 * KT_BYTES; // K then V
   static constexpr uint32_t P_BYTES = 128 * KB * 2;     // 128 rows x 64 B, SWIZZLE_64B K-major
   static constexpr uint32_t TMEM_COLS = 256;
   static constexpr uint32_t S_COL = 0, O_COL = 128;
-  static constexpr size_t SMEM = 1024 + 2 * Q_BYTES + NST * STAGE_BYTES + 2 * P_BYTES + 256;
+  static constexpr size_t SMEM = 1024 + QB * Q_BYTES + NST * STAGE_BYTES + 2 * P_BYTES + 256;
+  static_assert(SMEM <= 115712, "two CTAs per SM");
 };
 
 // K-major SWIZZLE_64B operand (the P tile: 64-byte rows, 8-row atoms of 512 B, SBO = 512).
@@ -427,15 +433,15 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-template <int HD>
+template <int HD, int QB, int NSTG>
 __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_constant__ AttnParams p) {
   static_assert(HD == 64, "head-pair tiles are laid out for hd 64");
-  using C = HpCfg;
+  using C = HpCfg<QB, NSTG>;
   constexpr int KB = C::KB, NST = C::NST;
   extern __shared__ __align__(1024) uint8_t tsm[];
   const uint32_t raw = smem_u32(tsm);
   const uint32_t sQ = (raw + 1023u) & ~1023u;  // two Q buffers
-  const uint32_t sKV = sQ + 2 * C::Q_BYTES;
+  const uint32_t sKV = sQ + QB * C::Q_BYTES;
   const uint32_t sP = sKV + NST * C::STAGE_BYTES;
   const uint32_t bars = sP + 2 * C::P_BYTES;
   auto kv_full = [&](int s) { return bars + 8u * s; };
@@ -476,7 +482,7 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   // finite Q / K / V everywhere: columns of the other head (or of a missing odd head) are multiplied
   // but never read, and must not carry NaN bit patterns into rows that are read
-  for (uint32_t i = threadIdx.x; i < (2 * C::Q_BYTES + NST * C::STAGE_BYTES) / 16; i += blockDim.x)
+  for (uint32_t i = threadIdx.x; i < (QB * C::Q_BYTES + NST * C::STAGE_BYTES) / 16; i += blockDim.x)
     *reinterpret_cast<uint4*>(tsm + (sQ - raw) + 16 * i) = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
@@ -511,9 +517,9 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
       const int last_key = grp.pos0 + grp.nq - 1;
       const int nkb = last_key / KB + 1;
       const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
-      const int qb = qi & 1;
+      const int qb = qi % QB;
       if (lane == 0) {
-        mbar_wait(q_empty(qb), ((qi >> 1) & 1) ^ 1u);
+        mbar_wait(q_empty(qb), ((qi / QB) & 1) ^ 1u);
         mbar_expect_tx(q_full(qb), has1 ? C::Q_BYTES : C::Q_BYTES / 2);
         tma_load_2d(sQ + qb * C::Q_BYTES, &p.q_map, q_full(qb), h0 * HD, grp.m0);
         if (has1) tma_load_2d(sQ + qb * C::Q_BYTES + C::Q_BYTES / 2, &p.q_map, q_full(qb), (h0 + 1) * HD, grp.m0);
@@ -582,8 +588,8 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
       };
       while (pc.item < n_items) {
         if (sc.item < n_items) {
-          const int s = sc.g % NST, b = sc.g & 1, qb = sc.qi & 1;
-          if ((sc.kb != 0 || mbar_try_wait(q_full(qb), (sc.qi >> 1) & 1)) &&
+          const int s = sc.g % NST, b = sc.g & 1, qb = sc.qi % QB;
+          if ((sc.kb != 0 || mbar_try_wait(q_full(qb), (sc.qi / QB) & 1)) &&
               mbar_try_wait(kv_full(s), (sc.g / NST) & 1) && mbar_try_wait(s_empty(b), ((sc.g >> 1) & 1) ^ 1u)) {
             tc_fence_after();
             const uint32_t d = tmem + C::S_COL + b * 2 * KB;
@@ -689,6 +695,10 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
           uint32_t sr[KB];
           tmem_ld_32x32b_x32(lane_base + C::S_COL + b * 2 * KB + hs * KB, sr);
           tmem_ld_wait();
+          // S(g) is in registers: release its TMEM buffer now, so S(g + 2) overlaps this softmax
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_empty(b));
           if (key0 + KB - 1 > warp_min_pos) {  // the block straddles the warp's diagonal
             const int lim = qpos - key0;       // keys key0 + i with i <= lim are visible
 #pragma unroll
@@ -748,13 +758,17 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
           for (int c4 = 0; c4 < KB / 8; ++c4)
             *reinterpret_cast<uint4*>(prow0 + b * C::P_BYTES + ((c4 ^ pswz) << 4)) = make_uint4(0, 0, 0, 0);
         }
+        if (!live) {
+          // a warp that skipped this block releases S here; it too waits for PV(g - 2) before its
+          // p_full arrival, so no warp's arrival for block g can land in block g - 2's phase
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_empty(b));
+          if (!warp_live) mbar_wait(p_empty(b), ((g >> 1) & 1) ^ 1u);
+        }
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (generic writes) -> tensor core
         __syncwarp();
-        if (lane == 0) {  // p_full before s_empty: S(g + 2) completing implies every P(g) arrival
-          mbar_arrive(p_full(b));
-          mbar_arrive(s_empty(b));
-        }
+        if (lane == 0) mbar_arrive(p_full(b));
         if (kb == 0 && pend.g_last >= 0) finish(pend);  // the previous item's O (PV(g) waits for it)
       }
       pend.z = warp_live && qr < grp.nq ? p.z + static_cast<size_t>(grp.m0 + qr) * p.ldz + h * HD : nullptr;
@@ -802,14 +816,17 @@ bool launch_prefill_tc(const AttnParams& p, int hd, cudaStream_t st) {
   return true;
 }
 
-// hd 64 prompt chunks of <= 64 queries (the mma.sync kernel's groups), no key mask.
+// hd 64 prompt chunks of <= 64 queries (the mma.sync kernel's groups), no key mask. Two Q tiles and
+// three K/V stages (measured: one Q tile + four stages, and an L2 prefetch of the next item's pages,
+// were both slower, profiles/r02_experiments.md).
 void launch_prefill_hp(const AttnParams& p, cudaStream_t st) {
   if (p.n_groups <= 0) return;
-  constexpr int smem = static_cast<int>(HpCfg::SMEM);
-  ensure_smem(attn_prefill_hp_kernel<64>, smem);
+  constexpr int QB = 2, NSTG = 3;
+  constexpr int smem = static_cast<int>(HpCfg<QB, NSTG>::SMEM);
+  ensure_smem(attn_prefill_hp_kernel<64, QB, NSTG>, smem);
   const int items = p.n_groups * ((p.heads + 1) / 2);
   const int grid = std::min(items, 2 * device_sms());
-  launch_k(attn_prefill_hp_kernel<64>, grid, 192, smem, st, p);
+  launch_k(attn_prefill_hp_kernel<64, QB, NSTG>, grid, 192, smem, st, p);
   CUDA_OK(cudaGetLastError());
 }
 

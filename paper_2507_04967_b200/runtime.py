@@ -144,7 +144,7 @@ def image_header(path) -> dict:
     """Header of a device-layout image (format: iolm_cuda.h, iolm_cuda_save_image): bundle hash,
     model config (with the active head ids), the weight options and per-layer weight forms."""
     with open(path, "rb") as f:
-        if f.read(8) != b"IOLMDL01":
+        if f.read(8) != b"IOLMDL02":
             raise CorruptHeader("device-layout image: bad magic")
         nw = int.from_bytes(f.read(8), "little")
         w = np.frombuffer(f.read(8 * nw), dtype="<i8").tolist()
