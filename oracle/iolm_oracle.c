@@ -278,18 +278,17 @@ static float gelu_gpu(float x) {
 
 /* The GPU prefill attention of one (query, head) at the W8A8 engine's rounding points
  * (kernels.cu attn_prefill_kernel for hd <= 32: 32-key blocks, exact running max; attn_tc.cu
- * attn_prefill_hp_kernel for hd 64: 32-key blocks, reference max moved only by a jump of more than
- * HP_RESCALE = 8; attn_tc.cu attn_prefill_tc_kernel for hd 128: 64-key blocks, exact running max;
- * blocks aligned to absolute positions): online softmax in base 2 with scale_log2 = log2(e)/sqrt(hd)
- * in f32, per block ms = max_j(s_j) * scale_log2, m_new = max(m, ms) (hd 64: m_new = ms only when
+ * attn_prefill_hp_kernel for hd 64 and 128: 32-key blocks, reference max moved only by a jump of
+ * more than HP_RESCALE = 8; blocks aligned to absolute positions): online softmax in base 2 with scale_log2 = log2(e)/sqrt(hd)
+ * in f32, per block ms = max_j(s_j) * scale_log2, m_new = max(m, ms) (hd >= 64: m_new = ms only when
  * m = -inf or ms > m + 8, else m), alpha = 2^(m - m_new), l = l * alpha + sum_j p_j with
  * p_j = 2^(fma(s_j, scale_log2, -m_new)) in f32, O = O * alpha + sum_j fp16(p_j) * v_j (the PV product
  * takes P as fp16), z = fp16(O * (1 / l)). Scores are f32 dots of the fp16 q / k.
  * Remaining differences to the GPU are f32 summation orders and the 2-ulp ex2.approx. */
 static void flash_head_gpu(const float* qh, const float* k0, const float* v0, int ld, int hd, int span,
                            const uint8_t* valid, float* zh) {
-  const int KB = hd >= 128 ? 64 : 32;
-  const int stale = hd == 64; /* attn_prefill_hp_kernel's reference-max rule */
+  const int KB = 32;
+  const int stale = hd >= 64; /* attn_prefill_hp_kernel's reference-max rule */
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   float m_run = -INFINITY, l_run = 0.0f;
   float o[128], s[64];
@@ -316,9 +315,8 @@ static void flash_head_gpu(const float* qh, const float* k0, const float* v0, in
     const float msub = mnew == -INFINITY ? 0.0f : mnew;
     m_run = mnew;
     l_run *= alpha;
-    /* O is rescaled, then the block's P V accumulates into it (the tcgen05 kernel for hd 128 forms
-     * the block's P V as a separate f32 tile and adds it with fma(O, alpha, Ob): emulating that was
-     * measured to match its codes less well than this form, tests/test_w8a8_codes_gpu.py) */
+    /* O is rescaled (only on a reference-max move for hd >= 64), then the block's P V accumulates
+     * into it, as the tensor core accumulates into O in TMEM */
     for (int j = 0; j < hd; ++j) o[j] *= alpha;
     for (int t = 0; t < nk; ++t) {
       const float pv = exp2f(fmaf(s[t], scale_log2, -msub));

@@ -394,19 +394,23 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
 // TMEM 256 columns (S double-buffered 2 x 64, O 128), ~97 KB smem: two CTAs per SM, each a
 // producer warp, an MMA warp and one softmax warpgroup.
 constexpr float HP_RESCALE = 8.0f;
-template <int QB, int NST_>
+template <int HD, int QB, int NST_>
 struct HpCfg {
+  static constexpr int HPT = HD == 64 ? 2 : 1;          // heads per 128-lane tile
+  static constexpr int QPT = 128 / HPT;                 // queries per tile
+  static constexpr int NCH = HD / 64;                   // 64-column (128-byte) chunks per row
   static constexpr int KB = 32;                         // keys per block (2 pages)
   static constexpr int NST = NST_;                      // K/V ring depth
   static constexpr int QBUF = QB;                       // Q tiles (next item's Q prefetched when 2)
-  static constexpr uint32_t Q_BYTES = 128 * 128;        // 2 heads x 64 rows x 128 B
-  static constexpr uint32_t KT_BYTES = 2 * KB * 128;    // K of both heads (also V)
+  static constexpr uint32_t Q_BYTES = 128 * HD * 2;     // 128 rows x HD, NCH chunk regions of 16 KB
+  static constexpr uint32_t KCH_BYTES = HPT * KB * 128; // one 64-column chunk of the K block
+  static constexpr uint32_t KT_BYTES = NCH * KCH_BYTES; // K block (also V): HPT x KB keys x HD
   static constexpr uint32_t STAGE_BYTES = 2 * KT_BYTES; // K then V
   static constexpr uint32_t P_BYTES = 128 * KB * 2;     // 128 rows x 64 B, SWIZZLE_64B K-major
   static constexpr uint32_t TMEM_COLS = 256;
-  static constexpr uint32_t S_COL = 0, O_COL = 128;
+  static constexpr uint32_t S_COL = 0, O_COL = 128;     // S: 2 x HPT*KB columns; O: HPT*HD = 128
   static constexpr size_t SMEM = 1024 + QB * Q_BYTES + NST * STAGE_BYTES + 2 * P_BYTES + 256;
-  static_assert(SMEM <= 115712, "two CTAs per SM");
+  static_assert(HPT * HD == 128 && SMEM <= 115712, "128 O columns, two CTAs per SM");
 };
 
 // K-major SWIZZLE_64B operand (the P tile: 64-byte rows, 8-row atoms of 512 B, SBO = 512).
@@ -435,9 +439,8 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 
 template <int HD, int QB, int NSTG>
 __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_constant__ AttnParams p) {
-  static_assert(HD == 64, "head-pair tiles are laid out for hd 64");
-  using C = HpCfg<QB, NSTG>;
-  constexpr int KB = C::KB, NST = C::NST;
+  using C = HpCfg<HD, QB, NSTG>;
+  constexpr int KB = C::KB, NST = C::NST, HPT = C::HPT, QPT = C::QPT, NCH = C::NCH;
   extern __shared__ __align__(1024) uint8_t tsm[];
   const uint32_t raw = smem_u32(tsm);
   const uint32_t sQ = (raw + 1023u) & ~1023u;  // two Q buffers
@@ -456,12 +459,8 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
   const uint32_t tmem_slot = bars + 8u * (2 * NST + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int npairs = (p.heads + 1) >> 1;
+  const int npairs = (p.heads + HPT - 1) / HPT;  // head slots per group
   const int n_items = p.n_groups * npairs;
-  auto item_nkb = [&](int item) {
-    const AttnGroup& g = p.groups[item / npairs];
-    return (g.pos0 + g.nq - 1) / KB + 1;
-  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -512,17 +511,23 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++qi) {
       const AttnGroup ngrp = load_grp(item + gridDim.x);  // in flight during this item
       const int npid0 = load_pids(ngrp, item + gridDim.x);
-      const int h0 = 2 * (item % npairs);
-      const bool has1 = h0 + 1 < p.heads;
+      const int h0 = HPT * (item % npairs);
+      const int nh = min(HPT, p.heads - h0);  // live heads of the tile (1 for an odd last pair)
       const int last_key = grp.pos0 + grp.nq - 1;
       const int nkb = last_key / KB + 1;
       const int* pt = p.page_table + static_cast<size_t>(grp.slot) * p.max_pages;
       const int qb = qi % QB;
       if (lane == 0) {
         mbar_wait(q_empty(qb), ((qi / QB) & 1) ^ 1u);
-        mbar_expect_tx(q_full(qb), has1 ? C::Q_BYTES : C::Q_BYTES / 2);
-        tma_load_2d(sQ + qb * C::Q_BYTES, &p.q_map, q_full(qb), h0 * HD, grp.m0);
-        if (has1) tma_load_2d(sQ + qb * C::Q_BYTES + C::Q_BYTES / 2, &p.q_map, q_full(qb), (h0 + 1) * HD, grp.m0);
+        // 64 x 64 boxes: chunk c of head slot t, query rows r*64.. -> chunk region c, tile rows t*QPT + r*64
+        mbar_expect_tx(q_full(qb), nh * NCH * (QPT / 64) * 64 * 128);
+        for (int t = 0; t < nh; ++t)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int r = 0; r < QPT / 64; ++r)
+              tma_load_2d(sQ + qb * C::Q_BYTES + c * 128 * 128 + (t * QPT + r * 64) * 128, &p.q_map, q_full(qb),
+                          (h0 + t) * HD + c * 64, grp.m0 + r * 64);
       }
       int pid_base = 0, pid = pid0;  // page ids [0, 32) of the slot, prefetched
       for (int kb = 0; kb < nkb; ++kb, ++g) {
@@ -535,7 +540,7 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
         }
         if (lane == 0) {
           mbar_wait(kv_empty(s), ((g / NST) & 1) ^ 1u);
-          mbar_expect_tx(kv_full(s), npg * (has1 ? 4 : 2) * TC_PAGE * 128);
+          mbar_expect_tx(kv_full(s), npg * nh * NCH * 2 * TC_PAGE * 128);
         }
         const uint32_t dK = sKV + s * C::STAGE_BYTES, dV = dK + C::KT_BYTES;
         for (int j = 0; j < npg; ++j) {
@@ -543,14 +548,16 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
           if (lane == 0) {
             const int rk = ((page * 2 + 0) * p.heads + h0) * TC_PAGE;  // K rows of head h0
             const int rv = rk + p.heads * TC_PAGE;
-            // K: head h0 keys at rows 0-31, head h0+1 at rows 32-63 of the N = 64 B operand;
-            // V: one 32-key x 128-B MN-major chunk per head (LBO = KB * 128)
-            tma_load_2d(dK + j * TC_PAGE * 128, &p.kv_map, kv_full(s), 0, rk);
-            tma_load_2d(dV + j * TC_PAGE * 128, &p.kv_map, kv_full(s), 0, rv);
-            if (has1) {
-              tma_load_2d(dK + KB * 128 + j * TC_PAGE * 128, &p.kv_map, kv_full(s), 0, rk + TC_PAGE);
-              tma_load_2d(dV + KB * 128 + j * TC_PAGE * 128, &p.kv_map, kv_full(s), 0, rv + TC_PAGE);
-            }
+            // K: chunk c of head slot t at rows t*KB + j*16 of chunk region c (the N = HPT*KB B operand);
+            // V: MN-major, 64-wide N chunk (t*NCH + c) of KB keys (LBO = KB * 128)
+            for (int t = 0; t < nh; ++t)
+#pragma unroll
+              for (int c = 0; c < NCH; ++c) {
+                tma_load_2d(dK + c * C::KCH_BYTES + (t * KB + j * TC_PAGE) * 128, &p.kv_map, kv_full(s), c * 64,
+                            rk + t * TC_PAGE);
+                tma_load_2d(dV + (t * NCH + c) * KB * 128 + j * TC_PAGE * 128, &p.kv_map, kv_full(s), c * 64,
+                            rv + t * TC_PAGE);
+              }
           }
         }
       }
@@ -559,8 +566,8 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
     }
   } else if (warp == 1) {  // ---------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_f16(128, 2 * KB, H16_FMT);
-      constexpr uint32_t idesc_o = idesc_f16(128, 2 * HD, H16_FMT) | (1u << 16);  // B (V) MN-major
+      constexpr uint32_t idesc_s = idesc_f16(128, HPT * KB, H16_FMT);
+      constexpr uint32_t idesc_o = idesc_f16(128, HPT * HD, H16_FMT) | (1u << 16);  // B (V) MN-major
       // Two cursors: S runs ahead of PV (across items), and whichever MMA has its inputs ready is
       // issued first - a PV never waits behind the next block's K/V load, so ring stages are
       // released as early as possible. Each cursor holds the next item's block count, loaded when
@@ -592,11 +599,14 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
           if ((sc.kb != 0 || mbar_try_wait(q_full(qb), (sc.qi / QB) & 1)) &&
               mbar_try_wait(kv_full(s), (sc.g / NST) & 1) && mbar_try_wait(s_empty(b), ((sc.g >> 1) & 1) ^ 1u)) {
             tc_fence_after();
-            const uint32_t d = tmem + C::S_COL + b * 2 * KB;
+            const uint32_t d = tmem + C::S_COL + b * HPT * KB;
             const uint32_t sK = sKV + s * C::STAGE_BYTES, sq = sQ + qb * C::Q_BYTES;
 #pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk)
-              umma_f16(d, smem_desc_k_sw128(sq + kk * 32), smem_desc_k_sw128(sK + kk * 32), idesc_s, kk ? 1u : 0u);
+            for (int kk = 0; kk < HD / 16; ++kk) {
+              const uint32_t ch = kk / 4, ko = (kk % 4) * 32;
+              umma_f16(d, smem_desc_k_sw128(sq + ch * 128 * 128 + ko), smem_desc_k_sw128(sK + ch * C::KCH_BYTES + ko),
+                       idesc_s, kk ? 1u : 0u);
+            }
             umma_commit(s_full(b));
             if (sc.kb + 1 == sc.nkb) umma_commit(q_empty(qb));  // the item's last read of its Q tile
             advance(sc);
@@ -623,9 +633,9 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
   } else {  // ------------------------------------------------------------------ softmax warps
     const int q = warp & 3;          // TMEM lane quarter
     const int row = q * 32 + lane;   // tile row = TMEM lane
-    const int hs = row >> 6;         // 0: head h0, 1: head h0 + 1
-    const int qr = row & 63;         // query within the group
-    const int wq0 = (q & 1) * 32;    // the warp's first query within the group
+    const int hs = row / QPT;        // head slot of the row (hd 64: 0 = head h0, 1 = head h0 + 1)
+    const int qr = row % QPT;        // query within the group
+    const int wq0 = (q % (QPT / 32)) * 32;  // the warp's first query within the group
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t o_addr = lane_base + C::O_COL + hs * HD;
     uint8_t* const prow0 = tsm + (sP - raw) + row * 64;
@@ -676,7 +686,7 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
     AttnGroup grp = load_grp(blockIdx.x);
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const AttnGroup ngrp = load_grp(item + gridDim.x);  // in flight during this item
-      const int h = 2 * (item % npairs) + hs;
+      const int h = HPT * (item % npairs) + hs;
       const int last_key = grp.pos0 + grp.nq - 1;
       const int nkb = last_key / KB + 1;
       const int qpos = grp.pos0 + qr;
@@ -693,7 +703,7 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
         if (live) {
           tc_fence_after();
           uint32_t sr[KB];
-          tmem_ld_32x32b_x32(lane_base + C::S_COL + b * 2 * KB + hs * KB, sr);
+          tmem_ld_32x32b_x32(lane_base + C::S_COL + b * HPT * KB + hs * KB, sr);
           tmem_ld_wait();
           // S(g) is in registers: release its TMEM buffer now, so S(g + 2) overlaps this softmax
           tc_fence_before();
@@ -816,18 +826,22 @@ bool launch_prefill_tc(const AttnParams& p, int hd, cudaStream_t st) {
   return true;
 }
 
-// hd 64 prompt chunks of <= 64 queries (the mma.sync kernel's groups), no key mask. Two Q tiles and
-// three K/V stages (measured: one Q tile + four stages, and an L2 prefetch of the next item's pages,
-// were both slower, profiles/r02_experiments.md).
-void launch_prefill_hp(const AttnParams& p, cudaStream_t st) {
-  if (p.n_groups <= 0) return;
-  constexpr int QB = 2, NSTG = 3;
-  constexpr int smem = static_cast<int>(HpCfg<QB, NSTG>::SMEM);
-  ensure_smem(attn_prefill_hp_kernel<64, QB, NSTG>, smem);
-  const int items = p.n_groups * ((p.heads + 1) / 2);
-  const int grid = std::min(items, 2 * device_sms());
-  launch_k(attn_prefill_hp_kernel<64, QB, NSTG>, grid, 192, smem, st, p);
+// Prompt chunks without a key mask: hd 64 as head-pair tiles over 64-query chunks (two Q tiles, three
+// K/V stages: one Q tile + four stages, and an L2 prefetch of the next item's pages, were both slower,
+// profiles/r02_experiments.md); hd 128 as one head x 128-query chunks (one 32 KB Q tile, three stages:
+// two CTAs per SM). Returns false for other head sizes.
+bool launch_prefill_hp(const AttnParams& p, int hd, cudaStream_t st) {
+  if (p.n_groups <= 0) return true;
+  auto go = [&](auto kern, size_t smem, int hpt) {
+    ensure_smem(kern, smem);
+    const int items = p.n_groups * ((p.heads + hpt - 1) / hpt);
+    launch_k(kern, std::min(items, 2 * device_sms()), 192, smem, st, p);
+  };
+  if (hd == 64) go(attn_prefill_hp_kernel<64, 2, 3>, HpCfg<64, 2, 3>::SMEM, 2);
+  else if (hd == 128) go(attn_prefill_hp_kernel<128, 1, 3>, HpCfg<128, 1, 3>::SMEM, 1);
+  else return false;
   CUDA_OK(cudaGetLastError());
+  return true;
 }
 
 }  // namespace iolmh

@@ -53,7 +53,7 @@ void launch_decode_codes(const void* payload, int enc, int rows, int cols, void*
                          float* scales, cudaStream_t st);
 void launch_attention(const AttnParams& prefill, const AttnParams& decode, int hd, cudaStream_t st);
 bool launch_prefill_tc(const AttnParams& prefill, int hd, cudaStream_t st);
-void launch_prefill_hp(const AttnParams& prefill, cudaStream_t st);
+bool launch_prefill_hp(const AttnParams& prefill, int hd, cudaStream_t st);
 int decode_heads_per_cta(int heads, int hd);
 void launch_head(const float* x, int d, const int* rows, int n_rows, const float* g, const float* b,
                  const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
@@ -440,9 +440,9 @@ class Engine {
   bool act_quant_ = false;
   bool sparse_mma_ = true;
   bool int4_mma_ = true;
-  bool prefill_tc_ = true;  // tcgen05 prefill attention (hd 128 by default, hd 64 on request)
+  bool prefill_tc_ = true;  // 128-query tcgen05 prefill kernel (hd 128: masked forward; forced by prefill_tc = 1)
   bool prefill_tc_force_ = false;
-  bool prefill_hp_ = true;  // hd 64: tcgen05 head-pair tiles (attn_tc.cu attn_prefill_hp_kernel)
+  bool prefill_hp_ = true;  // hd 64 / 128: attn_tc.cu attn_prefill_hp_kernel (head-pair / one-head tiles)
   // TMA-store epilogue of the W_in GEMM (IOLM_GEMM_TMA_EPI=0 disables, for A/B measurements):
   // measured 3% faster than the warp's coalesced stores at the C1 shape
   bool tma_epi_ = std::getenv("IOLM_GEMM_TMA_EPI") == nullptr || std::string(std::getenv("IOLM_GEMM_TMA_EPI")) != "0";
@@ -558,11 +558,13 @@ void Engine::setup(int device, const iolm_cuda_opts* opts) {
     if (opts->prefill_tc < 0) prefill_tc_ = prefill_hp_ = false;
     prefill_tc_force_ = opts->prefill_tc > 0;
   }
-  // hd 64: 64-query chunks run as head-pair tcgen05 tiles unless the 128-query kernel is forced
-  prefill_hp_ = prefill_hp_ && hd_ == 64 && !prefill_tc_force_;
-  // measured (bench C1 / C4): for hd 64 rows of 64 + 32 tokens the mma.sync kernel is faster (the
-  // 128-query tcgen05 tile is half empty); hd 128 / 544-token rows gain 40% (C4 prefill 158 -> 225 TFLOP/s)
-  if (hd_ != 128 && !(hd_ == 64 && prefill_tc_force_)) prefill_tc_ = false;
+  // default: attn_prefill_hp_kernel (hd 64: 64-query chunks as head-pair tiles; hd 128: 128-query
+  // chunks); prefill_tc = 1 selects the round-1 128-query tcgen05 kernel, -1 the mma.sync kernel
+  prefill_hp_ = prefill_hp_ && (hd_ == 64 || hd_ == 128) && !prefill_tc_force_;
+  // the round-1 128-query kernel (attn_prefill_tc_kernel): when forced (hd 64 / 128), and for hd 128
+  // forward() calls with a key mask (the head-pair kernel has no masked variant; both use 128-query
+  // chunks at hd 128, so the chunking never depends on the mask)
+  prefill_tc_ = prefill_tc_ && (hd_ == 128 || (hd_ == 64 && prefill_tc_force_));
   // Default token budget: one 256-row GEMM M-tile per SM pair (74 x 256 = 18944 on a 148-SM B200),
   // so every projection's tile count is a whole number of waves of the persistent GEMM grid.
   auto_budget_ = T_max_ <= 0;
@@ -1169,8 +1171,8 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     none.n_groups = 0;
     if (pre.n_groups) {
       timed(2, 4.0 * hd_ * ly.heads * pre_keys, [&] {
-        if (prefill_tc_) launch_prefill_tc(pre, hd_, stream_);
-        else if (prefill_hp_ && d_key_mask == nullptr) launch_prefill_hp(pre, stream_);
+        if (prefill_hp_ && d_key_mask == nullptr) launch_prefill_hp(pre, hd_, stream_);
+        else if (prefill_tc_) launch_prefill_tc(pre, hd_, stream_);
         else launch_attention(pre, none, hd_, stream_);
       });
       ++stats_.kernel_launches;

@@ -1,11 +1,13 @@
-"""Head-pair tcgen05 prefill attention (attn_tc.cu attn_prefill_hp_kernel, the hd-64 default) against
-the mma.sync kernel (`prefill_tc=False`) and the CPU oracle.
+"""tcgen05 prefill attention with O in TMEM (attn_tc.cu attn_prefill_hp_kernel: head-pair tiles for
+hd 64, one head x 128 queries for hd 128 - the defaults) against the mma.sync kernel
+(`prefill_tc=False`) and the CPU oracle.
 
 Both kernels walk keys in 32-position blocks aligned to absolute positions, so they differ only in
 fp32 summation order inside a block: logits agree to fp16 rounding (<= 5e-3 rel-L2), both stay within
 the oracle tolerance (1e-2), and the head-pair kernel keeps batch invariance. Covers an even head
-count (C1 shape, 20 heads), an odd one (7 heads: the last pair has one live head), rows longer than
-one 64-query chunk, rows shorter than a page and rows whose last block is partial."""
+count (C1 shape, 20 heads), an odd one (7 heads: the last pair has one live head), hd 128 with rows up
+to 590 tokens (several 128-query chunks), rows longer than one chunk, rows shorter than a page and
+rows whose last block is partial."""
 import numpy as np
 import pytest
 
@@ -26,7 +28,8 @@ def _rows(lens, seed):
     return ids, offs
 
 
-@pytest.mark.parametrize("cfg", [(1280, 2, 20, 5120, 160), (448, 2, 7, 1024, 200)], ids=["h20", "h7"])
+@pytest.mark.parametrize("cfg", [(1280, 2, 20, 5120, 160), (448, 2, 7, 1024, 200), (512, 2, 4, 1024, 600)],
+                         ids=["h20", "h7", "hd128"])
 def test_prefill_hp_matches_mma_sync_and_oracle(cfg):
     b = synth.toy_bundle(*cfg, seed=42)
     hp, mm = R.ModelRuntime(b), R.ModelRuntime(b, prefill_tc=False)
