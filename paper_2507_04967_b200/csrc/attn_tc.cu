@@ -199,8 +199,8 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
       while (pc.item < n_items) {
         if (sc.item < n_items) {
           const int s = sc.g % NST, b = sc.g & 1, qb = sc.qi & 1;
-          if ((sc.kb != 0 || mbar_try_wait(q_full(qb), (sc.qi >> 1) & 1)) &&
-              mbar_try_wait(kv_full(s), (sc.g / NST) & 1) && mbar_try_wait(s_empty(b), ((sc.g >> 1) & 1) ^ 1u)) {
+          if ((sc.kb != 0 || mbar_test_wait(q_full(qb), (sc.qi >> 1) & 1)) &&
+              mbar_test_wait(kv_full(s), (sc.g / NST) & 1) && mbar_test_wait(s_empty(b), ((sc.g >> 1) & 1) ^ 1u)) {
             tc_fence_after();
             const uint32_t d = tmem + C::S_COL + b * KB;
             const uint32_t sK = sKV + s * C::STAGE_BYTES;
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
         }
         if (pc.g < sc.g) {  // S(pc) issued
           const int s = pc.g % NST, b = pc.g & 1;
-          if (mbar_try_wait(p_full(b), (pc.g >> 1) & 1) && mbar_try_wait(o_empty(b), ((pc.g >> 1) & 1) ^ 1u)) {
+          if (mbar_test_wait(p_full(b), (pc.g >> 1) & 1) && mbar_test_wait(o_empty(b), ((pc.g >> 1) & 1) ^ 1u)) {
             tc_fence_after();
             const uint32_t d = tmem + C::O_COL + b * HD;
             const uint32_t sV = sKV + s * C::STAGE_BYTES + C::KT_BYTES;
@@ -596,8 +596,8 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
       while (pc.item < n_items) {
         if (sc.item < n_items) {
           const int s = sc.g % NST, b = sc.g & 1, qb = sc.qi % QB;
-          if ((sc.kb != 0 || mbar_try_wait(q_full(qb), (sc.qi / QB) & 1)) &&
-              mbar_try_wait(kv_full(s), (sc.g / NST) & 1) && mbar_try_wait(s_empty(b), ((sc.g >> 1) & 1) ^ 1u)) {
+          if ((sc.kb != 0 || mbar_test_wait(q_full(qb), (sc.qi / QB) & 1)) &&
+              mbar_test_wait(kv_full(s), (sc.g / NST) & 1) && mbar_test_wait(s_empty(b), ((sc.g >> 1) & 1) ^ 1u)) {
             tc_fence_after();
             const uint32_t d = tmem + C::S_COL + b * HPT * KB;
             const uint32_t sK = sKV + s * C::STAGE_BYTES, sq = sQ + qb * C::Q_BYTES;
@@ -614,8 +614,8 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
         }
         if (pc.g < sc.g) {  // S(pc) issued
           const int s = pc.g % NST, b = pc.g & 1;
-          if (mbar_try_wait(p_full(b), (pc.g >> 1) & 1) &&
-              (pc.kb != 0 || mbar_try_wait(o_empty, (pc.qi & 1) ^ 1u))) {  // previous item's O read
+          if (mbar_test_wait(p_full(b), (pc.g >> 1) & 1) &&
+              (pc.kb != 0 || mbar_test_wait(o_empty, (pc.qi & 1) ^ 1u))) {  // previous item's O read
             tc_fence_after();
             const uint32_t sV = sKV + s * C::STAGE_BYTES + C::KT_BYTES;
             const uint32_t pb = sP + b * C::P_BYTES;
