@@ -569,64 +569,68 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
       constexpr uint32_t idesc_s = idesc_f16(128, HPT * KB, H16_FMT);
       constexpr uint32_t idesc_o = idesc_f16(128, HPT * HD, H16_FMT) | (1u << 16);  // B (V) MN-major
       // Two cursors: S runs ahead of PV (across items), and whichever MMA has its inputs ready is
-      // issued first - a PV never waits behind the next block's K/V load, so ring stages are
-      // released as early as possible. Each cursor holds the next item's block count, loaded when
-      // it entered the current item.
+      // issued first - a PV never waits behind the next block's K/V load. The MMAs are small
+      // (32-64 tensor cycles each), so this thread's own instruction count per block matters: ring
+      // slots and barrier parities advance incrementally (no div / mod), descriptors are bases plus
+      // 16-byte offsets (the start-address field is linear in the shared-memory address), and
+      // each cursor holds the next item's block count, loaded when it entered the current item.
       struct Cur {
-        int item, kb, nkb, nkb_next, g, qi;
+        int item, kb, nkb, nkb_next, qi;
+        int s, sph;  // K/V ring stage and its phase bit
+        int b, bph;  // S / P buffer and its phase bit
+        int qb, qph; // Q tile and its phase bit
+        int g;       // global block ordinal (S ahead of PV)
       };
       auto nkb_of = [&](int item) {
         const AttnGroup gr = load_grp(item);
         return (gr.pos0 + gr.nq - 1) / KB + 1;
       };
-      Cur sc{static_cast<int>(blockIdx.x), 0, 0, 0, 0, 0};
+      Cur sc{static_cast<int>(blockIdx.x), 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
       sc.nkb = nkb_of(sc.item);
       sc.nkb_next = nkb_of(sc.item + gridDim.x);
       Cur pc = sc;
       auto advance = [&](Cur& c) {
         ++c.g;
+        if (++c.s == NST) { c.s = 0; c.sph ^= 1; }
+        c.b ^= 1;
+        if (c.b == 0) c.bph ^= 1;
         if (++c.kb == c.nkb) {
           c.kb = 0;
           c.item += gridDim.x;
           ++c.qi;
+          if (++c.qb == QB) { c.qb = 0; c.qph ^= 1; }
           c.nkb = c.nkb_next;
           c.nkb_next = nkb_of(c.item + gridDim.x);
         }
       };
+      const uint64_t dq0 = smem_desc_k_sw128(sQ), dk0 = smem_desc_k_sw128(sKV);
+      const uint64_t dv0 = smem_desc_mn_sw128(sKV + C::KT_BYTES, KB * 128), dp0 = smem_desc_k_sw64(sP);
       while (pc.item < n_items) {
-        if (sc.item < n_items) {
-          const int s = sc.g % NST, b = sc.g & 1, qb = sc.qi % QB;
-          if ((sc.kb != 0 || mbar_test_wait(q_full(qb), (sc.qi / QB) & 1)) &&
-              mbar_test_wait(kv_full(s), (sc.g / NST) & 1) && mbar_test_wait(s_empty(b), ((sc.g >> 1) & 1) ^ 1u)) {
-            tc_fence_after();
-            const uint32_t d = tmem + C::S_COL + b * HPT * KB;
-            const uint32_t sK = sKV + s * C::STAGE_BYTES, sq = sQ + qb * C::Q_BYTES;
+        if (sc.item < n_items && (sc.kb != 0 || mbar_test_wait(q_full(sc.qb), sc.qph)) &&
+            mbar_test_wait(kv_full(sc.s), sc.sph) && mbar_test_wait(s_empty(sc.b), sc.bph ^ 1)) {
+          tc_fence_after();
+          const uint32_t d = tmem + C::S_COL + sc.b * HPT * KB;
+          const uint64_t aq = dq0 + (sc.qb * C::Q_BYTES >> 4), bk = dk0 + (sc.s * C::STAGE_BYTES >> 4);
 #pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk) {
-              const uint32_t ch = kk / 4, ko = (kk % 4) * 32;
-              umma_f16(d, smem_desc_k_sw128(sq + ch * 128 * 128 + ko), smem_desc_k_sw128(sK + ch * C::KCH_BYTES + ko),
-                       idesc_s, kk ? 1u : 0u);
-            }
-            umma_commit(s_full(b));
-            if (sc.kb + 1 == sc.nkb) umma_commit(q_empty(qb));  // the item's last read of its Q tile
-            advance(sc);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off_a = ((kk / 4) * 128 * 128 + (kk % 4) * 32) >> 4;
+            const uint32_t off_b = ((kk / 4) * C::KCH_BYTES + (kk % 4) * 32) >> 4;
+            umma_f16(d, aq + off_a, bk + off_b, idesc_s, kk ? 1u : 0u);
           }
+          umma_commit(s_full(sc.b));
+          if (sc.kb + 1 == sc.nkb) umma_commit(q_empty(sc.qb));  // the item's last read of its Q tile
+          advance(sc);
         }
-        if (pc.g < sc.g) {  // S(pc) issued
-          const int s = pc.g % NST, b = pc.g & 1;
-          if (mbar_test_wait(p_full(b), (pc.g >> 1) & 1) &&
-              (pc.kb != 0 || mbar_test_wait(o_empty, (pc.qi & 1) ^ 1u))) {  // previous item's O read
-            tc_fence_after();
-            const uint32_t sV = sKV + s * C::STAGE_BYTES + C::KT_BYTES;
-            const uint32_t pb = sP + b * C::P_BYTES;
+        if (pc.g < sc.g && mbar_test_wait(p_full(pc.b), pc.bph) &&
+            (pc.kb != 0 || mbar_test_wait(o_empty, (pc.qi & 1) ^ 1u))) {  // previous item's O read
+          tc_fence_after();
+          const uint64_t av = dv0 + (pc.s * C::STAGE_BYTES >> 4), ap = dp0 + (pc.b * C::P_BYTES >> 4);
 #pragma unroll
-            for (int kk = 0; kk < KB / 16; ++kk)
-              umma_f16(tmem + C::O_COL, smem_desc_k_sw64(pb + kk * 32), smem_desc_mn_sw128(sV + kk * 2048, KB * 128),
-                       idesc_o, (pc.kb > 0 || kk > 0) ? 1u : 0u);
-            umma_commit(p_empty(b));
-            umma_commit(kv_empty(s));
-            advance(pc);
-          }
+          for (int kk = 0; kk < KB / 16; ++kk)
+            umma_f16(tmem + C::O_COL, ap + (kk * 32 >> 4), av + (kk * 2048 >> 4), idesc_o, (pc.kb > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(p_empty(pc.b));
+          umma_commit(kv_empty(pc.s));
+          advance(pc);
         }
       }
     }
