@@ -485,6 +485,7 @@ class Engine {
   DevArray<float> hs_, zs_, gs_;
   CUtensorMap tm_h8_, tm_h8s_;
   CUtensorMap tm_hs_;  // fp16 h in the sparse kernel's 112-row boxes (W_SP24F)
+  CUtensorMap tm_x_resid_;  // x as the 2:4 GEMM's TMA reduce-add target (32 x 8 boxes)
   bool any_int8_ = false;
   DevArray<int> page_table_;
   StepBuffers sbuf_[2];
@@ -919,6 +920,7 @@ void Engine::alloc_runtime() {
     ly->tm_gs = sp24_act_map_h16(g_.p, ly->f, static_cast<int>(T), f_ld_max_);
   }
   tm_hs_ = sp24_act_map_h16(h_.p, d_, static_cast<int>(T), d_);
+  tm_x_resid_ = make_resid_map(x_.p, d_, T, 4ull * d_);
   if (any_int8_) {
     const auto U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
     h8_.alloc(T * d_);
@@ -1017,7 +1019,8 @@ void Engine::gemm(int epi, bool i8, const CUtensorMap& A, const CUtensorMap& B, 
 void Engine::gemm_w(int epi, const GemmW& w, const CUtensorMap& act, const CUtensorMap& act_sp, int M, int N, int K,
                     const GemmEpi& ep, const CUtensorMap* out_map) {
   if (w.mode == W_SP24 || w.mode == W_SP24F) {
-    launch_gemm_sp(epi, w.tm, act_sp, w.tm_e, K, w.sl.katoms_pad, ep, stream_, sms_, w.mode == W_SP24F);
+    launch_gemm_sp(epi, w.tm, act_sp, w.tm_e, K, w.sl.katoms_pad, ep, stream_, sms_, w.mode == W_SP24F,
+                   epi == iolmk::EPI_RESID_F32 && ep.out == x_.p ? &tm_x_resid_ : nullptr);
     ++stats_.kernel_launches;
   } else if (w.mode == W_INT4) {
     launch_gemm_w4(use_pair(M, N), epi, act, w.tm, M, N, K, ep, stream_, sms_, out_map);

@@ -54,6 +54,7 @@ struct SpCfg {
   static constexpr size_t SMEM =
       1024 + STAGES * STAGE_BYTES + 256 + EPI_WARPS * WTOK * sizeof(QkvRow) + EPI_WARPS * 64 * sizeof(float);
   static_assert(E_COL0 + 8 * STAGES <= TMEM_COLS, "TMEM budget");
+  static_assert(EPI_WARPS * 1024 <= EPI_WARPS * WTOK * 24, "RESID staging tiles fit in the QKV row area");
 };
 
 // kind::i8 instruction descriptor with the sparse flag (bit 2): s8 x s8 -> s32, K-major A/B.
@@ -120,7 +121,8 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)
 template <int EPI, bool F16 = false>
 __global__ void __launch_bounds__(SpCfg::THREADS, 1)
     gemm_sp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmE, int K, int katoms_pad, GemmEpi ep) {
+                   const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmX, int K,
+                   int katoms_pad, GemmEpi ep) {
   using C = SpCfg;
   constexpr int STAGES = C::STAGES;
   constexpr int BKL = F16 ? 128 : C::BK;                     // logical K per stage
@@ -288,7 +290,13 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
         for (int i = lane; i < C::WTOK; i += 32) s_rows[i] = tw0 + i < T ? qkv_row(ep, tw0 + i) : QkvRow{};
         __syncwarp();
       }
-      float* xcol = static_cast<float*>(ep.out) + ch;  // RESID: this channel's column of x
+      // RESID: this warp's 8-token x 32-channel staging tile (in the QKV destination area, unused
+      // by this epilogue): x += v leaves through TMA reduce-add boxes, so x is never loaded into
+      // registers and there is one shared store per element instead of a global load + store
+      // (1 KB per warp from the 256-aligned start of the area: TMA sources must be 128-byte aligned)
+      float* stage = reinterpret_cast<float*>(smem_raw + (bars + 256 - raw) + e * 1024);
+      const uint32_t stage_addr = smem_u32(stage);
+      const int ch0 = wt * C::TILE_M + static_cast<int>(rank) * C::BM + q * 32;  // the warp's first channel
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * C::BN);
@@ -307,12 +315,6 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
         const int t0 = tw0 + ci * C::CHUNK;  // first token of the chunk
         constexpr int JN_FULL = C::CHUNK;
         const int jn = (ci + 1) * C::CHUNK <= C::WTOK ? JN_FULL : C::WTOK - ci * C::CHUNK;  // tokens in chunk
-        float xo[C::CHUNK];
-        if constexpr (EPI == EPI_RESID_F32) {  // residual column loads in flight during the TMEM wait
-#pragma unroll
-          for (int j = 0; j < C::CHUNK; ++j)
-            xo[j] = (j < jn && ch_ok && t0 + j < T) ? xcol[static_cast<size_t>(t0 + j) * ep.ldo] : 0.f;
-        }
         tmem_ld_wait();
         if (ci + 1 < NCH) {
           if ((ci + 2) * C::CHUNK <= C::WTOK) tmem_ld_32x32b_x16(tbase + c_begin + (ci + 1) * C::CHUNK, r[(ci + 1) & 1]);
@@ -348,9 +350,24 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
               for (int j = 0; j < 16; ++j)
                 if (j < jn && ch_ok && t0 + j < T) o[static_cast<size_t>(t0 + j) * ep.ldo + ch] = v[j];
             } else if constexpr (EPI == EPI_RESID_F32) {
+              // two 8-token boxes per chunk; TMA clips tokens >= T and channels >= N. The tile is
+              // reused only once the previous box has been read out of shared memory.
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (j < jn && ch_ok && t0 + j < T) xcol[static_cast<size_t>(t0 + j) * ep.ldo] = __fadd_rn(xo[j], v[j]);
+              for (int h = 0; h < 2; ++h) {
+                if (h * 8 < jn && t0 + h * 8 < T) {
+                  if (lane == 0) bulk_wait_read0();
+                  __syncwarp();
+#pragma unroll
+                  for (int j = 0; j < 8; ++j)  // rows past T (inside the tensor map) add +0
+                    stage[j * 32 + lane] = t0 + h * 8 + j < T ? v[h * 8 + j] : 0.f;
+                  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                  __syncwarp();
+                  if (lane == 0) {
+                    tma_reduce_add_2d(&tmX, stage_addr, ch0, t0 + h * 8);
+                    bulk_commit();
+                  }
+                }
+              }
             } else {
               // fp16 outputs: lane pairs exchange one value so that every store is a 4-byte
               // channel pair; even lanes write token j, odd lanes token j + 1
@@ -404,6 +421,10 @@ __global__ void __launch_bounds__(SpCfg::THREADS, 1)
       if (lane == 0) mbar_arrive_remote(leader_tempty0 + 8u * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1u;
+    }
+    if constexpr (EPI == EPI_RESID_F32) {
+      if (lane == 0) bulk_wait0();  // every reduce-add into x complete before the grid ends
+      __syncwarp();
     }
   }
   tc_fence_before();

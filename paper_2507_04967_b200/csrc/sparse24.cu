@@ -133,8 +133,8 @@ CUtensorMap sp24_act_map_h16(const void* act, int K, int rows, int ld) {
 }
 
 template <int EPI, bool F16>
-static void launch_sp_one(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, int K, int katoms_pad,
-                          const GemmEpi& ep, cudaStream_t st, int grid_cap) {
+static void launch_sp_one(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, const CUtensorMap& X,
+                          int K, int katoms_pad, const GemmEpi& ep, cudaStream_t st, int grid_cap) {
   auto kern = gemm_sp_kernel<EPI, F16>;
   ensure_smem(kern, SpCfg::SMEM);
   const int tiles = ((ep.N + SpCfg::TILE_M - 1) / SpCfg::TILE_M) * ((ep.M + SpCfg::BN - 1) / SpCfg::BN);
@@ -152,32 +152,37 @@ static void launch_sp_one(const CUtensorMap& A, const CUtensorMap& B, const CUte
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1 + pdl_attr(&attr[1]);  // the kernel calls pdl_sync() after its prologue
-  CUDA_OK(cudaLaunchKernelEx(&cfg, kern, A, B, E, K, katoms_pad, ep));
+  CUDA_OK(cudaLaunchKernelEx(&cfg, kern, A, B, E, X, K, katoms_pad, ep));
 }
 
 template <bool F16>
-static void launch_sp(int epi, const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, int K, int katoms_pad,
-                      const GemmEpi& ep, cudaStream_t st, int grid_cap) {
+static void launch_sp(int epi, const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, const CUtensorMap& X,
+                      int K, int katoms_pad, const GemmEpi& ep, cudaStream_t st, int grid_cap) {
   switch (epi) {
     case EPI_S32:
       if constexpr (F16) throw Unsupported("gemm_sp: raw accumulators are int8-only");
-      else launch_sp_one<EPI_S32, false>(A, B, E, K, katoms_pad, ep, st, grid_cap);
+      else launch_sp_one<EPI_S32, false>(A, B, E, X, K, katoms_pad, ep, st, grid_cap);
       break;
-    case EPI_F32: launch_sp_one<EPI_F32, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_H16: launch_sp_one<EPI_H16, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_GELU_H16: launch_sp_one<EPI_GELU_H16, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_RESID_F32: launch_sp_one<EPI_RESID_F32, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_QKV: launch_sp_one<EPI_QKV, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
-    case EPI_NONE: launch_sp_one<EPI_NONE, F16>(A, B, E, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_F32: launch_sp_one<EPI_F32, F16>(A, B, E, X, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_H16: launch_sp_one<EPI_H16, F16>(A, B, E, X, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_GELU_H16: launch_sp_one<EPI_GELU_H16, F16>(A, B, E, X, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_RESID_F32: launch_sp_one<EPI_RESID_F32, F16>(A, B, E, X, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_QKV: launch_sp_one<EPI_QKV, F16>(A, B, E, X, K, katoms_pad, ep, st, grid_cap); break;
+    case EPI_NONE: launch_sp_one<EPI_NONE, F16>(A, B, E, X, K, katoms_pad, ep, st, grid_cap); break;
     default: throw Unsupported("gemm_sp: epilogue not instantiated");
   }
 }
 
 void launch_gemm_sp(int epi, const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, int K, int katoms_pad,
-                    const GemmEpi& ep, cudaStream_t st, int grid_cap, bool f16) {
+                    const GemmEpi& ep, cudaStream_t st, int grid_cap, bool f16, const CUtensorMap* resid_map) {
   if (ep.M <= 0 || ep.N <= 0) return;
-  if (f16) launch_sp<true>(epi, A, B, E, K, katoms_pad, ep, st, grid_cap);
-  else launch_sp<false>(epi, A, B, E, K, katoms_pad, ep, st, grid_cap);
+  CUtensorMap X = A;  // unused unless epi == EPI_RESID_F32
+  if (epi == EPI_RESID_F32) {
+    if (resid_map != nullptr) X = *resid_map;
+    else X = make_resid_map(static_cast<const float*>(ep.out), ep.N, ep.M, 4ull * ep.ldo);
+  }
+  if (f16) launch_sp<true>(epi, A, B, E, X, K, katoms_pad, ep, st, grid_cap);
+  else launch_sp<false>(epi, A, B, E, X, K, katoms_pad, ep, st, grid_cap);
   CUDA_OK(cudaGetLastError());
 }
 

@@ -38,6 +38,6 @@ CUtensorMap sp24_act_map(const int8_t* act, int K, int rows, int ld);
 CUtensorMap sp24_act_map_h16(const void* act, int K, int rows, int ld);
 // C = X * W^T with W the sparse operand: ep.M = tokens, ep.N = output channels.
 void launch_gemm_sp(int epi, const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& E, int K, int katoms_pad,
-                    const iolmk::GemmEpi& ep, cudaStream_t st, int grid_cap, bool f16 = false);
+                    const iolmk::GemmEpi& ep, cudaStream_t st, int grid_cap, bool f16 = false, const CUtensorMap* resid_map = nullptr);
 
 }  // namespace iolmh

@@ -113,4 +113,21 @@ inline CUtensorMap make_out_map(const void* ptr, bool f32, uint64_t cols, uint64
   return m;
 }
 
+// Residual stream x (fp32 [rows x cols]) as the target of the 2:4 GEMM's TMA reduce-add epilogue:
+// boxes of 32 channels x 8 tokens, no swizzle (the staging tile is plain row-major [8][32] floats).
+inline CUtensorMap make_resid_map(const float* ptr, uint64_t cols, uint64_t rows, uint64_t row_stride_bytes) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {32, 8};
+  cuuint32_t es[2] = {1, 1};
+  if ((row_stride_bytes % 16) != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
+    throw std::runtime_error("residual map must be 16-byte aligned with a 16-byte row stride");
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (residual) failed: " + std::to_string(r));
+  return m;
+}
+
 }  // namespace iolmh
