@@ -22,13 +22,16 @@ constexpr int PAGE = 16;
 // ------------------------------------------------------------------ per-token int8 (W8A8)
 // Activation quantization rule (the reference has none; modelled on its RTN weight
 // rule, quant.cpp:23-38, applied per token): s = amax/127 (amax == 0 -> 1), inv = 1/s (IEEE fp32),
-// q = clamp(rint(x * inv)) with the fp32 product rounded to nearest-even - one FMUL + one
-// cvt.rni.sat.s8.f32 per element. |x * inv| <= 127 * (1 + 2^-22), so the saturation never clips a
-// code. Restated bit-for-bit in oracle/iolm_oracle.c orc_quant_rows_s8.
+// q = clamp(rint(x * inv)) with the fp32 product rounded to nearest-even. |x * inv| <= 127 * (1 +
+// 2^-22), so the clamp never clips a code. Restated bit-for-bit in oracle/iolm_oracle.c
+// orc_quant_rows_s8. Evaluated on the FMA/ALU pipes instead of the XU
+// (cvt.rni.sat.s8.f32 is an XU conversion at a quarter of the FMA rate): after the clamp to
+// [-128, 127], adding 1.5 * 2^23 rounds to the nearest integer with ties to even (the sum's ulp is 1)
+// and leaves the two's-complement code in the low byte of the sum's bit pattern - the same result
+// as cvt.rni.sat.s8.f32 for every finite input.
 __device__ __forceinline__ int8_t quant_one(float x, float /*s*/, float inv_s) {
-  int r;
-  asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(r) : "f"(x * inv_s));
-  return static_cast<int8_t>(r);
+  const float y = fminf(fmaxf(x * inv_s, -128.f), 127.f);
+  return static_cast<int8_t>(__float_as_int(__fadd_rn(y, 12582912.f)) & 0xff);
 }
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -981,9 +984,12 @@ __global__ void __launch_bounds__(32 * 17) attn_decode_kernel(const __grid_const
 }
 
 // ------------------------------------------------------------------ head + argmax
-// 16 rows per CTA: final LN in fp32, logits = y * tok_embed^T with the fp32 embedding (transposed
-// copy, coalesced over the vocabulary), greedy argmax (strict >, ties to the lowest id).
-constexpr int HEAD_ROWS = 16;
+// 8 rows per CTA: final LN in fp32, logits = y * tok_embed^T with the fp32 embedding (transposed
+// copy, coalesced over the vocabulary), greedy argmax (strict >, ties to the lowest id). 8 rows and
+// 32-row E^T chunks keep two CTAs per SM (~2000 rows per step = 256 CTAs; 16 rows / 64-row chunks
+// left one under-filled CTA per SM). Every logit's k order is unchanged (ascending k).
+constexpr int HEAD_ROWS = 8;
+constexpr int HEAD_KC = 32;
 __global__ void __launch_bounds__(256)
     head_argmax_kernel(const float* __restrict__ x, int d, const int* __restrict__ rows, int n_rows,
                        const float* __restrict__ g, const float* __restrict__ b,
@@ -1019,9 +1025,9 @@ __global__ void __launch_bounds__(256)
   // logits = y * E^T: E^T streamed through a 2-stage cp.async ring of KC-row chunks (16-byte
   // copies, the next chunk in flight during the FMAs); each thread owns one vocabulary column and
   // accumulates all HEAD_ROWS rows in fp32, 4 k at a time.
-  constexpr int KC = 64;
+  constexpr int KC = HEAD_KC;
   float* set0 = slog + HEAD_ROWS * V;  // [2][KC][V]
-  const int chunk_floats = KC * V;     // multiple of 4 (KC = 64)
+  const int chunk_floats = KC * V;     // multiple of 4 (KC = 32)
   float acc[HEAD_ROWS];
 #pragma unroll
   for (int r = 0; r < HEAD_ROWS; ++r) acc[r] = 0.f;
@@ -1436,7 +1442,7 @@ void launch_head(const float* x, int d, const int* rows, int n_rows, const float
   if (n_rows <= 0) return;
   if (V > 256) throw Unsupported("head: vocabulary larger than the CTA");
   if (d % 4 != 0) throw Unsupported("head: d_model must be a multiple of 4");
-  const size_t smem = sizeof(float) * (HEAD_ROWS * (d + V) + 2 * 64 * V) + 16;
+  const size_t smem = sizeof(float) * (HEAD_ROWS * (d + V) + 2 * HEAD_KC * V) + 16;
   if (smem > 48 * 1024) ensure_smem(head_argmax_kernel, smem);
   launch_k(head_argmax_kernel, blocks_for(n_rows, HEAD_ROWS), 256, smem, st, x, d, rows, n_rows, g, b, embed_t, V,
                                                                        row_slot, next_tok, last_tok, logits_out);
