@@ -20,6 +20,7 @@
 // on which other queries share its tile (batch invariance, test_model.cpp:240-267).
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "kernels.cuh"
 #include "launch.hpp"
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(192, HD == 64 ? 2 : 1) attn_prefill_tc_kernel(
 // TMEM 256 columns (S double-buffered 2 x 64, O 128), ~97 KB smem: two CTAs per SM, each a
 // producer warp, an MMA warp and one softmax warpgroup.
 constexpr float HP_RESCALE = 8.0f;
-template <int HD, int QB, int NST_>
+template <int HD, int QB, int NST_, bool PT = false>
 struct HpCfg {
   static constexpr int HPT = HD == 64 ? 2 : 1;          // heads per 128-lane tile
   static constexpr int QPT = 128 / HPT;                 // queries per tile
@@ -406,7 +407,7 @@ struct HpCfg {
   static constexpr uint32_t KCH_BYTES = HPT * KB * 128; // one 64-column chunk of the K block
   static constexpr uint32_t KT_BYTES = NCH * KCH_BYTES; // K block (also V): HPT x KB keys x HD
   static constexpr uint32_t STAGE_BYTES = 2 * KT_BYTES; // K then V
-  static constexpr uint32_t P_BYTES = 128 * KB * 2;     // 128 rows x 64 B, SWIZZLE_64B K-major
+  static constexpr uint32_t P_BYTES = PT ? 0 : 128 * KB * 2;  // 128 rows x 64 B, SWIZZLE_64B K-major (PT: in TMEM)
   static constexpr uint32_t TMEM_COLS = 256;
   static constexpr uint32_t S_COL = 0, O_COL = 128;     // S: 2 x HPT*KB columns; O: HPT*HD = 128
   static constexpr size_t SMEM = 1024 + QB * Q_BYTES + NST * STAGE_BYTES + 2 * P_BYTES + 256;
@@ -435,11 +436,21 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-template <int HD, int QB, int NSTG>
+template <int HD, int QB, int NSTG, bool PT>
 __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_constant__ AttnParams p) {
-  using C = HpCfg<HD, QB, NSTG>;
+  // PT: P lives in TMEM over the consumed S columns of its block and PV takes A from TMEM
+  // (tcgen05.mma ... [a_tmem]): no shared-memory P tile, no generic -> async proxy fence
+  using C = HpCfg<HD, QB, NSTG, PT>;
   constexpr int KB = C::KB, NST = C::NST, HPT = C::HPT, QPT = C::QPT, NCH = C::NCH;
   extern __shared__ __align__(1024) uint8_t tsm[];
   const uint32_t raw = smem_u32(tsm);
@@ -607,7 +618,8 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
       const uint64_t dv0 = smem_desc_mn_sw128(sKV + C::KT_BYTES, KB * 128), dp0 = smem_desc_k_sw64(sP);
       while (pc.item < n_items) {
         if (sc.item < n_items && (sc.kb != 0 || mbar_test_wait(q_full(sc.qb), sc.qph)) &&
-            mbar_test_wait(kv_full(sc.s), sc.sph) && mbar_test_wait(s_empty(sc.b), sc.bph ^ 1)) {
+            mbar_test_wait(kv_full(sc.s), sc.sph) && mbar_test_wait(s_empty(sc.b), sc.bph ^ 1) &&
+            (!PT || mbar_test_wait(p_empty(sc.b), sc.bph ^ 1))) {  // PT: P(g - 2) read from buffer b
           tc_fence_after();
           const uint32_t d = tmem + C::S_COL + sc.b * HPT * KB;
           const uint64_t aq = dq0 + (sc.qb * C::Q_BYTES >> 4), bk = dk0 + (sc.s * C::STAGE_BYTES >> 4);
@@ -626,8 +638,14 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
           tc_fence_after();
           const uint64_t av = dv0 + (pc.s * C::STAGE_BYTES >> 4), ap = dp0 + (pc.b * C::P_BYTES >> 4);
 #pragma unroll
-          for (int kk = 0; kk < KB / 16; ++kk)
-            umma_f16(tmem + C::O_COL, ap + (kk * 32 >> 4), av + (kk * 2048 >> 4), idesc_o, (pc.kb > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < KB / 16; ++kk) {
+            const uint32_t accum = (pc.kb > 0 || kk > 0) ? 1u : 0u;
+            if constexpr (PT)
+              umma_f16_ts(tmem + C::O_COL, tmem + C::S_COL + pc.b * HPT * KB + kk * 8, av + (kk * 2048 >> 4), idesc_o,
+                          accum);
+            else
+              umma_f16(tmem + C::O_COL, ap + (kk * 32 >> 4), av + (kk * 2048 >> 4), idesc_o, accum);
+          }
           umma_commit(p_empty(pc.b));
           umma_commit(kv_empty(pc.s));
           advance(pc);
@@ -762,15 +780,28 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
           }
           l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
           mbar_wait(p_empty(b), ((g >> 1) & 1) ^ 1u);  // PV of block g - 2 has read this P buffer
+          if constexpr (PT) {
+            tmem_st_32x32b_x16(lane_base + C::S_COL + b * HPT * KB, pw);
+            tmem_st_wait();
+          } else {
 #pragma unroll
-          for (int c4 = 0; c4 < KB / 8; ++c4)
-            *reinterpret_cast<uint4*>(prow0 + b * C::P_BYTES + ((c4 ^ pswz) << 4)) =
-                make_uint4(pw[4 * c4], pw[4 * c4 + 1], pw[4 * c4 + 2], pw[4 * c4 + 3]);
+            for (int c4 = 0; c4 < KB / 8; ++c4)
+              *reinterpret_cast<uint4*>(prow0 + b * C::P_BYTES + ((c4 ^ pswz) << 4)) =
+                  make_uint4(pw[4 * c4], pw[4 * c4 + 1], pw[4 * c4 + 2], pw[4 * c4 + 3]);
+          }
         } else if (warp_live) {  // a block past the warp's last query: its P rows must add nothing
           mbar_wait(p_empty(b), ((g >> 1) & 1) ^ 1u);
+          if constexpr (PT) {
+            uint32_t z[16];
 #pragma unroll
-          for (int c4 = 0; c4 < KB / 8; ++c4)
-            *reinterpret_cast<uint4*>(prow0 + b * C::P_BYTES + ((c4 ^ pswz) << 4)) = make_uint4(0, 0, 0, 0);
+            for (int i = 0; i < 16; ++i) z[i] = 0u;
+            tmem_st_32x32b_x16(lane_base + C::S_COL + b * HPT * KB, z);
+            tmem_st_wait();
+          } else {
+#pragma unroll
+            for (int c4 = 0; c4 < KB / 8; ++c4)
+              *reinterpret_cast<uint4*>(prow0 + b * C::P_BYTES + ((c4 ^ pswz) << 4)) = make_uint4(0, 0, 0, 0);
+          }
         }
         if (!live) {
           // a warp that skipped this block releases S here; it too waits for PV(g - 2) before its
@@ -780,7 +811,7 @@ __global__ void __launch_bounds__(192, 2) attn_prefill_hp_kernel(const __grid_co
           if (!warp_live) mbar_wait(p_empty(b), ((g >> 1) & 1) ^ 1u);
         }
         tc_fence_before();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (generic writes) -> tensor core
+        if constexpr (!PT) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (generic) -> tensor core
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full(b));
         if (kb == 0 && pend.g_last >= 0) finish(pend);  // the previous item's O (PV(g) waits for it)
@@ -841,9 +872,21 @@ bool launch_prefill_hp(const AttnParams& p, int hd, cudaStream_t st) {
     const int items = p.n_groups * ((p.heads + hpt - 1) / hpt);
     launch_k(kern, std::min(items, 2 * device_sms()), 192, smem, st, p);
   };
-  if (hd == 64) go(attn_prefill_hp_kernel<64, 2, 3>, HpCfg<64, 2, 3>::SMEM, 2);
-  else if (hd == 128) go(attn_prefill_hp_kernel<128, 1, 3>, HpCfg<128, 1, 3>::SMEM, 1);
-  else return false;
+  // default: P in TMEM, PV with A from TMEM, one more K/V stage in the freed smem (C4 prefill -3%,
+  // C1 neutral); IOLM_HP_PT=0 selects the shared-memory P tile (A/B measurements)
+  static const bool pt = [] {
+    const char* e = std::getenv("IOLM_HP_PT");
+    return e == nullptr || std::string(e) != "0";
+  }();
+  if (hd == 64) {
+    if (pt) go(attn_prefill_hp_kernel<64, 2, 4, true>, HpCfg<64, 2, 4, true>::SMEM, 2);
+    else go(attn_prefill_hp_kernel<64, 2, 3, false>, HpCfg<64, 2, 3>::SMEM, 2);
+  } else if (hd == 128) {
+    if (pt) go(attn_prefill_hp_kernel<128, 1, 4, true>, HpCfg<128, 1, 4, true>::SMEM, 1);
+    else go(attn_prefill_hp_kernel<128, 1, 3, false>, HpCfg<128, 1, 3>::SMEM, 1);
+  } else {
+    return false;
+  }
   CUDA_OK(cudaGetLastError());
   return true;
 }
