@@ -1359,9 +1359,12 @@ void launch_quant_rows(const h16* src, int lds, int M, int cols, int8_t* dst, in
   const unsigned grid = blocks_for(M, 8);
   const int ch = (cols + 255) / 256;
   if (cols % 8 != 0) launch_k(quant_rows_kernel<0>, grid, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
-  // register-resident rows up to 1024 columns; wider rows take the two-pass kernel (its second
-  // read hits L2) at 8 CTAs per SM: these launches are bound by load latency, not bytes
+  // register-resident rows up to 1280 columns (measured, profiles/r02_experiments.md: C2-W8A8's 1280-wide
+  // attention output 223.6 -> 217.4 ms with the row in registers, while 2560 columns - C3's GELU output
+  // - lose 9% against the two-pass kernel); wider rows take the two-pass kernel (its second read hits
+  // L2) at 8 CTAs per SM: these launches are bound by load latency, not bytes
   else if (ch <= 4) launch_k(quant_rows_kernel<4>, grid, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
+  else if (ch <= 5) launch_k(quant_rows_kernel<5>, grid, 256, 0, st, src, lds, M, cols, dst, ldd, scale);
   else if (cols > 3072 && cols <= 5120) {  // measured: two-warp rows win at 4096 (C4 FFN), lose at 2560
     const int sms = device_sms();
     const int grid2 = std::min<int>((M + 3) / 4, sms * 2);
