@@ -547,7 +547,7 @@ def main() -> None:
     ap.add_argument("--tokens-per-step", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prefill-tc", choices=["auto", "on", "off"], default="auto",
-                    help="prefill attention kernel: tcgen05 (on), mma.sync (off), engine default (auto)")
+                    help="prefill attention kernel: engine default = O-in-TMEM tcgen05 kernel (auto), round-1 128-query tcgen05 kernel (on), mma.sync (off)")
     ap.add_argument("--sparse-mma", choices=["on", "off"], default="on",
                     help="2:4 bundles: sparse tensor cores (on) or weights expanded to dense codes (off), A/B")
     ap.add_argument("--no-kernel-timing", action="store_true",
