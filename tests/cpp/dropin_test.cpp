@@ -44,7 +44,40 @@ int main() {
   const auto b = gpu.batch_decode(prompts, 8, c2);
   int same = 0;
   for (size_t i = 0; i < a.size(); ++i) same += a[i] == b[i];
+  // >= 99% of rows (25 rows: at most one), and every differing row must sit on an fp near-tie of the
+  // reference's logits where it diverges: at the first differing character k, the CPU's top-2 gap
+  // after prompt + a[i][:k] is below 0.05 + 4e-3 max|logit| and the GPU's character is in its top 2
+  // (the tolerance of tests/parity.py)
   EXPECT(same >= static_cast<int>(a.size()) - 1, "batch_decode agreement");
+  for (size_t i = 0; i < a.size(); ++i) {
+    if (a[i] == b[i]) continue;
+    size_t k = 0;
+    while (k < a[i].size() && k < b[i].size() && a[i][k] == b[i][k]) ++k;
+    std::vector<int> seq = {iolm::Tokenizer::kBos};
+    for (char ch : prompts[i]) seq.push_back(ch);
+    for (size_t j = 0; j < k; ++j) seq.push_back(a[i][j]);
+    iolm::FlopCounter fc;
+    const auto lg = cpu.forward(seq, {}, fc);
+    const int last = static_cast<int>(seq.size()) - 1;
+    int t1 = 0, t2 = -1;
+    double amax = 0;
+    for (int v = 0; v < 131; ++v) {
+      amax = std::max(amax, std::fabs(static_cast<double>(lg.at(last, v))));
+      if (v == 0) continue;
+      if (lg.at(last, v) > lg.at(last, t1)) {
+        t2 = t1;
+        t1 = v;
+      } else if (t2 < 0 || lg.at(last, v) > lg.at(last, t2)) {
+        t2 = v;
+      }
+    }
+    const double gap = lg.at(last, t1) - lg.at(last, t2);
+    const int gtok = k < b[i].size() ? static_cast<unsigned char>(b[i][k]) : iolm::Tokenizer::kEos;
+    std::printf("row %zu diverges at char %zu: CPU top-2 gap %.4g, GPU token %d, CPU top-2 {%d, %d}\n", i, k, gap,
+                gtok, t1, t2);
+    EXPECT(gap < 0.05 + 4e-3 * amax, "divergence is an fp tie");
+    EXPECT(gtok == t1 || gtok == t2, "GPU token in the CPU top 2");
+  }
   EXPECT(c1.total() == c2.total(), "FlopCounter madds");
   std::printf("batch_decode: %d/%zu identical, madds %llu vs %llu\n", same, a.size(),
               static_cast<unsigned long long>(c1.total()), static_cast<unsigned long long>(c2.total()));

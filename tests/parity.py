@@ -46,3 +46,36 @@ def check_agreement(om, ids, offs, gi, gl, oi, ol, min_frac: float = 0.99, label
     for i, k, gap, tol in traced:
         assert gap < tol, f"{label}: row {i} diverges at step {k} with CPU top-2 gap {gap:.4g} >= {tol:.4g}"
     return traced
+
+
+def check_string_agreement(ref, prompt_ids, got_ids, got_lens, want, max_new: int, min_frac: float = 0.99,
+                           label: str = "", eos: int = 130):
+    """Rendered-string form of check_agreement, for references that only return batch_decode strings
+    (oracle.RefRuntime, the reference compiled unmodified). `got_ids` / `got_lens` are the GPU's token
+    rows for the same prompts (decode_token_rows); a row whose render differs from the reference's
+    string is traced at its first GPU token k whose render leaves the reference string: the reference's
+    logits after prompt + got_ids[:k] must put that token in their top 2 with a top-2 gap below the
+    tie tolerance (the two paths agree up to k, so that is the step where the argmax flipped). A GPU row
+    that stops short of `max_new` without matching stopped on EOS at step k."""
+    from oracle.oracle import render
+
+    n = len(want)
+    bad = [i for i in range(n) if render(got_ids[i], got_lens[i]) != want[i]]
+    traced = []
+    for i in bad:
+        k = 0
+        while k < got_lens[i] and want[i].startswith(render(got_ids[i], k + 1)):
+            k += 1
+        seq = np.array(list(prompt_ids[i]) + list(got_ids[i, :k]), np.int32)
+        logits = ref.forward(seq)[0][-1]
+        order = np.argsort(logits)
+        gap = float(logits[order[-1]] - logits[order[-2]])
+        tol = TIE_ABS + TIE_REL * float(np.abs(logits).max())
+        # the GPU's token at step k: its emitted id, or EOS when it stopped early (EOS is not emitted)
+        tok = int(got_ids[i, k]) if k < got_lens[i] else (eos if got_lens[i] < max_new else -1)
+        top2 = tok in (int(order[-1]), int(order[-2]))
+        traced.append((i, k, gap, tol, top2))
+    assert n - len(bad) >= min_frac * n or len(bad) <= 1, f"{label}: {n - len(bad)}/{n} rows agree; divergences {traced}"
+    for i, k, gap, tol, top2 in traced:
+        assert top2 and gap < tol, f"{label}: row {i} diverges at step {k} (GPU token in CPU top-2: {top2}), gap {gap:.4g} >= {tol:.4g}"
+    return traced

@@ -10,6 +10,7 @@ import pytest
 from oracle import oracle as O
 from paper_2507_04967_b200 import runtime as R
 from paper_2507_04967_b200 import synth
+from parity import check_agreement, check_string_agreement
 
 pytestmark = pytest.mark.gpu
 
@@ -176,8 +177,7 @@ def test_parity_production_head_dims(cfg, row_chars, n_rows):
     gi, gl, gm = rt.decode_token_rows(ids, offs, 8)
     oi, ol, omm = om.decode_ids(ids, offs, 8, threads=8)
     assert gm == omm
-    same = sum(gl[i] == ol[i] and np.array_equal(gi[i, :gl[i]], oi[i, :ol[i]]) for i in range(n_rows))
-    assert same >= n_rows - 1, (same, n_rows)
+    check_agreement(om, ids, offs, gi, gl, oi, ol, label=f"{cfg}")
 
 
 @pytest.mark.parametrize("cfg,row_chars", [((1280, 2, 20, 5120, 128), 64), ((256, 2, 2, 1024, 576), 512)],
@@ -196,8 +196,10 @@ def test_prefill_tc_matches_mma_sync(cfg, row_chars):
         assert rel.max() <= 5e-3, rel.max()
     gi, gl, _ = tc.decode_token_rows(ids, offs, 8)
     mi, ml, _ = mm.decode_token_rows(ids, offs, 8)
-    same = sum(gl[i] == ml[i] and np.array_equal(gi[i, :gl[i]], mi[i, :ml[i]]) for i in range(6))
-    assert same >= 5
+    om = O.OracleModel(b)
+    oi, ol, _ = om.decode_ids(ids, offs, 8, threads=8)
+    check_agreement(om, ids, offs, gi, gl, oi, ol, label="prefill tcgen05")
+    check_agreement(om, ids, offs, mi, ml, oi, ol, label="prefill mma.sync")
     one, ol, _ = tc.decode_token_rows(ids[offs[3]:offs[4]], np.array([0, offs[4] - offs[3]]), 8)
     assert ol[0] == gl[3] and np.array_equal(one[0, :ol[0]], gi[3, :gl[3]])
 
@@ -218,8 +220,7 @@ def test_ragged_rows_and_budgets(model, max_new):
     gi, gl, gm = rt.decode_token_rows(ids, offs, max_new)
     oi, ol, omm = om.decode_ids(ids, offs, max_new, threads=8)
     assert gm == omm
-    bad = [i for i in range(len(rows)) if gl[i] != ol[i] or not np.array_equal(gi[i, :gl[i]], oi[i, :ol[i]])]
-    assert len(bad) <= 1, bad
+    check_agreement(om, ids, offs, gi, gl, oi, ol, label=f"ragged max_new={max_new}")
     for i in [0, 1, 12, 20]:
         one, l1, _ = rt.decode_token_rows(ids[offs[i]:offs[i + 1]], np.array([0, offs[i + 1] - offs[i]]), max_new)
         assert l1[0] == gl[i] and np.array_equal(one[0, :l1[0]], gi[i, :gl[i]])
@@ -237,7 +238,13 @@ def test_c1_full_model_against_compiled_reference():
     c = R.FlopCounter()
     got = rt.batch_decode(prompts, 8, c)
     assert c.total() == rm
-    assert sum(a == b2 for a, b2 in zip(got, want)) >= 7, (got, want)
+    # >= 99% of rows (at 8 rows: at most one), every divergence an fp tie of the reference's logits
+    pids = [[R.BOS] + R.encode(p) for p in prompts]
+    ids = np.concatenate([np.array(x, np.int32) for x in pids])
+    offs = np.concatenate([[0], np.cumsum([len(x) for x in pids])]).astype(np.int64)
+    gi, gl, _ = rt.decode_token_rows(ids, offs, 8)
+    assert [O.render(gi[i], gl[i]) for i in range(len(prompts))] == got
+    check_string_agreement(ref, pids, gi, gl, want, 8, label="C1 full model", eos=R.EOS)
     ids, offs = synth.rows(0, 1, 64)
     row = ids[offs[0]:offs[1]]
     g, r = rt.forward(row)[-1], ref.forward(row)[0][-1]
