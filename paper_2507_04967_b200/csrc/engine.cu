@@ -58,6 +58,8 @@ int decode_heads_per_cta(int heads, int hd);
 void launch_head(const float* x, int d, const int* rows, int n_rows, const float* g, const float* b,
                  const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
                  float* logits_out, cudaStream_t st);
+void launch_gather_head_rows(const float* x, int d, const h16* z, int ldz, int kh, const int* rows, int n_rows,
+                             float* xc, h16* zc, int ldzc, cudaStream_t st);
 void launch_lcp(const int32_t* ids, const int64_t* offsets, int64_t n_rows, int limit, int* out, cudaStream_t st);
 void launch_check_ids(const int32_t* ids, int64_t n, int V, int* bad, cudaStream_t st);
 void launch_decode_weight(const void* payload, int enc, int rows, int cols, h16* dst, int ld,
@@ -222,6 +224,7 @@ struct StepBuffers {
   // device views into d_meta for the current step
   const int64_t* tok_src = nullptr;
   const int *tok_slot = nullptr, *tok_pos = nullptr, *head_rows = nullptr, *head_slot = nullptr;
+  const int* head_iota = nullptr;  // 0 .. R-1: the head rows of the compacted last layer
   const AttnGroup *pre = nullptr, *dec = nullptr;
   Step step;
   ~StepBuffers() {
@@ -474,6 +477,7 @@ class Engine {
   };
   std::vector<KPending> kpend_;
 
+  std::vector<int> iota_;  // host 0, 1, 2, ... (head_iota staging)
   std::vector<std::unique_ptr<Layer>> layers_;
   DevArray<float> tok_embed_, tok_embed_t_, pos_embed_, lnf_g_, lnf_b_;
   DevArray<float> x_;
@@ -486,6 +490,16 @@ class Engine {
   CUtensorMap tm_h8_, tm_h8s_;
   CUtensorMap tm_hs_;  // fp16 h in the sparse kernel's 112-row boxes (W_SP24F)
   CUtensorMap tm_x_resid_;  // x as the 2:4 GEMM's TMA reduce-add target (32 x 8 boxes)
+  // Last-layer head-row compaction: after the last layer's QKV GEMM (which still writes K/V for every
+  // token) and attention, only the tokens whose logits are read (the step's head rows) go through
+  // Wo / LN2 / W_in / W_out: their x and z rows are gathered into xc_ / zc_ (rows 0 .. R-1) and the
+  // head reads xc_. Every op after the gather is row-wise, so outputs are bitwise those of the
+  // uncompacted path. Off for forward() (all positions' logits) and the calibration capture, and
+  // with IOLM_LAST_COMPACT=0 (A/B measurements).
+  bool last_compact_ = std::getenv("IOLM_LAST_COMPACT") == nullptr || std::string(std::getenv("IOLM_LAST_COMPACT")) != "0";
+  DevArray<float> xc_;
+  DevArray<h16> zc_;
+  CUtensorMap tm_zc_, tm_zcs_, tm_xc_resid_;
   bool any_int8_ = false;
   DevArray<int> page_table_;
   StepBuffers sbuf_[2];
@@ -909,6 +923,11 @@ void Engine::alloc_runtime() {
   z_.alloc(T * kh_max_);
   g_.alloc(T * f_ld_max_);
   CUDA_OK(cudaMemset(z_.p, 0, T * kh_max_ * sizeof(h16)));
+  if (last_compact_ && L_ > 0) {
+    xc_.alloc(T * d_);
+    zc_.alloc(T * kh_max_);
+    CUDA_OK(cudaMemset(zc_.p, 0, T * kh_max_ * sizeof(h16)));
+  }
   const auto BF = H16_TMA;
   tm_h_ = make_kmajor_map(h_.p, BF, 2, d_, T, 2ull * d_, 128);
   tm_q_ = make_rows_map_h16(q_.p, kh_max_, T, 2ull * kh_max_, std::min(hd_, 64), 64);
@@ -921,6 +940,12 @@ void Engine::alloc_runtime() {
   }
   tm_hs_ = sp24_act_map_h16(h_.p, d_, static_cast<int>(T), d_);
   tm_x_resid_ = make_resid_map(x_.p, d_, T, 4ull * d_);
+  if (last_compact_ && L_ > 0) {
+    const int khl = layers_.back()->kh;
+    tm_zc_ = make_kmajor_map(zc_.p, BF, 2, khl, T, 2ull * kh_max_, 128);
+    tm_zcs_ = sp24_act_map_h16(zc_.p, khl, static_cast<int>(T), kh_max_);
+    tm_xc_resid_ = make_resid_map(xc_.p, d_, T, 4ull * d_);
+  }
   if (any_int8_) {
     const auto U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
     h8_.alloc(T * d_);
@@ -940,7 +965,7 @@ void Engine::alloc_runtime() {
   }
   // packed step metadata: tok_src i64[T], tok_slot/pos i32[T], groups 2 x [T], head rows/slots i32[T]
   const size_t meta_bytes = align16(T * 8) + 2 * align16(T * 4) + 2 * align16(T * sizeof(AttnGroup)) +
-                            2 * align16(T * 4) + 64;
+                            3 * align16(T * 4) + 64;
   for (auto& sb : sbuf_) {
     sb.h_meta.ensure(meta_bytes);
     sb.d_meta.alloc(meta_bytes);
@@ -1020,7 +1045,10 @@ void Engine::gemm_w(int epi, const GemmW& w, const CUtensorMap& act, const CUten
                     const GemmEpi& ep, const CUtensorMap* out_map) {
   if (w.mode == W_SP24 || w.mode == W_SP24F) {
     launch_gemm_sp(epi, w.tm, act_sp, w.tm_e, K, w.sl.katoms_pad, ep, stream_, sms_, w.mode == W_SP24F,
-                   epi == iolmk::EPI_RESID_F32 && ep.out == x_.p ? &tm_x_resid_ : nullptr);
+                   epi != iolmk::EPI_RESID_F32 ? nullptr
+                   : ep.out == x_.p     ? &tm_x_resid_
+                   : ep.out == xc_.p    ? &tm_xc_resid_
+                                        : nullptr);
     ++stats_.kernel_launches;
   } else if (w.mode == W_INT4) {
     launch_gemm_w4(use_pair(M, N), epi, act, w.tm, M, N, K, ep, stream_, sms_, out_map);
@@ -1102,6 +1130,17 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
   sb.dec = reinterpret_cast<const AttnGroup*>(put(s.dec.data(), s.dec.size() * sizeof(AttnGroup)));
   sb.head_rows = reinterpret_cast<const int*>(put(s.head_rows.data(), R * sizeof(int)));
   sb.head_slot = reinterpret_cast<const int*>(put(s.head_slot.data(), R * sizeof(int)));
+  // last-layer compaction (see last_compact_): only when the step computes fewer head rows than
+  // tokens, and never for forward() logits or a calibration capture (they read every position)
+  const bool compact = last_compact_ && d_logits == nullptr && cap_ == nullptr && cap8_ == nullptr && R < T;
+  if (compact) {
+    if (iota_.size() < static_cast<size_t>(R)) {
+      const size_t n0 = iota_.size();
+      iota_.resize(R);
+      for (size_t i = n0; i < iota_.size(); ++i) iota_[i] = static_cast<int>(i);
+    }
+    sb.head_iota = reinterpret_cast<const int*>(put(iota_.data(), R * sizeof(int)));
+  }
   CUDA_OK(cudaMemcpyAsync(d, h, off, cudaMemcpyHostToDevice, stream_));
 
   const double dT = static_cast<double>(T);
@@ -1152,6 +1191,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       gemm_w(iolmk::EPI_QKV, ly.qkv, i8_qkv ? tm_h8_ : tm_h_, ly.qkv.mode == W_SP24F ? tm_hs_ : tm_h8s_, T, 3 * ly.kh,
              d_, ep);
     });
+    if (compact && R == 0 && l + 1 == L_) break;  // K/V-only step (shared prefix): nothing reads the rest
     AttnParams ap{};
     ap.q_map = tm_q_;
     ap.kv_map = ly.tm_kv;
@@ -1184,50 +1224,62 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
       timed(3, 4.0 * hd_ * ly.heads * dec_keys, [&] { launch_attention(none, dec, hd_, stream_); });
       ++stats_.kernel_launches;
     }
-    // x += z * Wo^T
-    if (i8_o) {
-      timed(9, dT * ly.kh * 3.0, [&] { launch_quant_rows(z_.p, kh_max_, T, ly.kh, z8_.p, kh_max_, zs_.p, stream_); });
+    // last layer, compacted: only the R head rows continue (x / z rows gathered into xc_ / zc_)
+    const bool cl = compact && l + 1 == L_;
+    const int Tl = cl ? R : T;
+    const double dTl = static_cast<double>(Tl);
+    float* const xl = cl ? xc_.p : x_.p;
+    const h16* const zl = cl ? zc_.p : z_.p;
+    if (cl) {
+      timed(8, static_cast<double>(R) * (8.0 * d_ + 4.0 * ly.kh), [&] {
+        launch_gather_head_rows(x_.p, d_, z_.p, kh_max_, ly.kh, sb.head_rows, R, xc_.p, zc_.p, kh_max_, stream_);
+      });
       ++stats_.kernel_launches;
     }
-    capture_point(1, T, ly.kh);  // layers.l.attn_out_in
+    // x += z * Wo^T
+    if (i8_o) {
+      timed(9, dTl * ly.kh * 3.0, [&] { launch_quant_rows(zl, kh_max_, Tl, ly.kh, z8_.p, kh_max_, zs_.p, stream_); });
+      ++stats_.kernel_launches;
+    }
+    capture_point(1, Tl, ly.kh);  // layers.l.attn_out_in
     GemmEpi eo;
-    eo.M = T;
+    eo.M = Tl;
     eo.N = d_;
-    eo.out = x_.p;
+    eo.out = xl;
     eo.ldo = d_;
     scales(eo, ly.o, zs_.p);
-    timed(4, 2.0 * dT * d_ * ly.kh, [&] {
-      gemm_w(iolmk::EPI_RESID_F32, ly.o, i8_o ? ly.tm_z8 : ly.tm_z, ly.o.mode == W_SP24F ? ly.tm_zs : ly.tm_z8s, T, d_,
+    timed(4, 2.0 * dTl * d_ * ly.kh, [&] {
+      gemm_w(iolmk::EPI_RESID_F32, ly.o, i8_o ? ly.tm_z8 : cl ? tm_zc_ : ly.tm_z, ly.o.mode == W_SP24F ? (cl ? tm_zcs_ : ly.tm_zs) : ly.tm_z8s, Tl, d_,
              ly.kh, eo);
     });
     // h = LN2(x)
-    timed(5, dT * d_ * 6.0, [&] {
-      launch_ln(x_.p, T, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_, i8_in ? h8_.p : nullptr, hs_.p);
+    timed(5, dTl * d_ * 6.0, [&] {
+      launch_ln(xl, Tl, d_, ly.ln2_g.p, ly.ln2_b.p, h_.p, d_, stream_, i8_in ? h8_.p : nullptr, hs_.p);
     });
     ++stats_.kernel_launches;
-    capture_point(2, T, d_);  // layers.l.ffn_in
+    capture_point(2, Tl, d_);  // layers.l.ffn_in
     // g = gelu(h * Win^T)
     GemmEpi ei;
-    ei.M = T;
+    ei.M = Tl;
     ei.N = ly.f;
     ei.out = g_.p;
     ei.ldo = f_ld_max_;
     scales(ei, ly.in, hs_.p);
-    timed(6, 2.0 * dT * ly.f * d_, [&] {
-      gemm_w(iolmk::EPI_GELU_H16, ly.in, i8_in ? tm_h8_ : tm_h_, ly.in.mode == W_SP24F ? tm_hs_ : tm_h8s_, T, ly.f, d_,
+    timed(6, 2.0 * dTl * ly.f * d_, [&] {
+      gemm_w(iolmk::EPI_GELU_H16, ly.in, i8_in ? tm_h8_ : tm_h_, ly.in.mode == W_SP24F ? tm_hs_ : tm_h8s_, Tl, ly.f, d_,
              ei,
              tma_epi_ ? &ly.tm_g_out : nullptr);
     });
     // x += g * Wout^T
     if (i8_out) {
-      timed(9, dT * ly.f * 3.0, [&] { launch_quant_rows(g_.p, f_ld_max_, T, ly.f, g8_.p, f_ld_max_, gs_.p, stream_); });
+      timed(9, dTl * ly.f * 3.0, [&] { launch_quant_rows(g_.p, f_ld_max_, Tl, ly.f, g8_.p, f_ld_max_, gs_.p, stream_); });
       ++stats_.kernel_launches;
     }
-    capture_point(3, T, ly.f);  // layers.l.ffn_mid (post-GELU)
+    capture_point(3, Tl, ly.f);  // layers.l.ffn_mid (post-GELU)
     GemmEpi eo2 = eo;
     scales(eo2, ly.out, gs_.p);
-    timed(7, 2.0 * dT * d_ * ly.f, [&] {
-      gemm_w(iolmk::EPI_RESID_F32, ly.out, i8_out ? ly.tm_g8 : ly.tm_g, ly.out.mode == W_SP24F ? ly.tm_gs : ly.tm_g8s, T,
+    timed(7, 2.0 * dTl * d_ * ly.f, [&] {
+      gemm_w(iolmk::EPI_RESID_F32, ly.out, i8_out ? ly.tm_g8 : ly.tm_g, ly.out.mode == W_SP24F ? ly.tm_gs : ly.tm_g8s, Tl,
              d_, ly.f, eo2);
     });
     if (l + 1 < L_) {
@@ -1242,7 +1294,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
   }
   if (R > 0) {
     timed(8, static_cast<double>(R) * d_ * 4.0 + static_cast<double>(V_) * d_ * 4.0, [&] {
-      launch_head(x_.p, d_, sb.head_rows, R, lnf_g_.p, lnf_b_.p, tok_embed_t_.p, V_, sb.head_slot, sb.d_next.p,
+      launch_head(compact ? xc_.p : x_.p, d_, compact ? sb.head_iota : sb.head_rows, R, lnf_g_.p, lnf_b_.p, tok_embed_t_.p, V_, sb.head_slot, sb.d_next.p,
                   d_last_tok_.p, d_logits, stream_);
     });
     ++stats_.kernel_launches;

@@ -1439,6 +1439,31 @@ void launch_attention(const AttnParams& prefill, const AttnParams& decode, int h
   CUDA_OK(cudaGetLastError());
 }
 
+// Head-row compaction of the last layer (engine.cu, Engine::launch_step): row c of xc / zc <- row
+// rows[c] of x (fp32 residual stream, d) and z (fp16 attention output, kh). One CTA per row.
+__global__ void __launch_bounds__(128) gather_head_rows_kernel(const float* __restrict__ x, int d,
+                                                               const h16* __restrict__ z, int ldz, int kh,
+                                                               const int* __restrict__ rows, float* __restrict__ xc,
+                                                               h16* __restrict__ zc, int ldzc) {
+  pdl_sync();
+  const int c = blockIdx.x, r = rows[c];
+  const float4* xs = reinterpret_cast<const float4*>(x + static_cast<size_t>(r) * d);
+  float4* xd = reinterpret_cast<float4*>(xc + static_cast<size_t>(c) * d);
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) xd[i] = xs[i];
+  const uint4* zs = reinterpret_cast<const uint4*>(z + static_cast<size_t>(r) * ldz);
+  uint4* zd = reinterpret_cast<uint4*>(zc + static_cast<size_t>(c) * ldzc);
+  for (int i = threadIdx.x; i < kh / 8; i += blockDim.x) zd[i] = zs[i];
+}
+
+void launch_gather_head_rows(const float* x, int d, const h16* z, int ldz, int kh, const int* rows, int n_rows,
+                             float* xc, h16* zc, int ldzc, cudaStream_t st) {
+  if (n_rows <= 0) return;
+  if (d % 4 != 0 || kh % 8 != 0 || ldz % 8 != 0 || ldzc % 8 != 0)
+    throw Unsupported("gather_head_rows: d must be a multiple of 4, kh / ld a multiple of 8");
+  launch_k(gather_head_rows_kernel, n_rows, 128, 0, st, x, d, z, ldz, kh, rows, xc, zc, ldzc);
+  CUDA_OK(cudaGetLastError());
+}
+
 void launch_head(const float* x, int d, const int* rows, int n_rows, const float* g, const float* b,
                  const float* embed_t, int V, const int* row_slot, int32_t* next_tok, int32_t* last_tok,
                  float* logits_out, cudaStream_t st) {
