@@ -483,8 +483,6 @@ class Engine {
   DevArray<float> x_;
   DevArray<h16> h_, q_, z_, g_;
   CUtensorMap tm_h_, tm_q_;
-  // (the TMA reduce-add epilogue for the residual GEMMs exists - GemmEpi::tma_out with an fp32 map -
-  // but measured 2% slower than the coalesced read-modify-write at the C1 shapes, so it is unused)
   DevArray<int8_t> h8_, z8_, g8_;  // W8A8 operands + per-token scales
   DevArray<float> hs_, zs_, gs_;
   CUtensorMap tm_h8_, tm_h8s_;
@@ -500,6 +498,11 @@ class Engine {
   DevArray<float> xc_;
   DevArray<h16> zc_;
   CUtensorMap tm_zc_, tm_zcs_, tm_xc_resid_;
+  // dense residual GEMMs: x += acc through TMA reduce-add (32 x 32 fp32 boxes, fp32 RN add in L2:
+  // bitwise equal) instead of the warps' coalesced read-modify-write: C2-W8A8 Wo 182 -> 148 ms,
+  // C1 +0.6% (profiles/r02_experiments.md). IOLM_RESID_TMA=0 restores the RMW (A/B).
+  bool resid_tma_ = std::getenv("IOLM_RESID_TMA") == nullptr || std::string(std::getenv("IOLM_RESID_TMA")) != "0";
+  CUtensorMap tm_x_out_, tm_xc_out_;
   bool any_int8_ = false;
   DevArray<int> page_table_;
   StepBuffers sbuf_[2];
@@ -940,11 +943,13 @@ void Engine::alloc_runtime() {
   }
   tm_hs_ = sp24_act_map_h16(h_.p, d_, static_cast<int>(T), d_);
   tm_x_resid_ = make_resid_map(x_.p, d_, T, 4ull * d_);
+  if (resid_tma_) tm_x_out_ = make_out_map(x_.p, true, d_, T, 4ull * d_);
   if (last_compact_ && L_ > 0) {
     const int khl = layers_.back()->kh;
     tm_zc_ = make_kmajor_map(zc_.p, BF, 2, khl, T, 2ull * kh_max_, 128);
     tm_zcs_ = sp24_act_map_h16(zc_.p, khl, static_cast<int>(T), kh_max_);
     tm_xc_resid_ = make_resid_map(xc_.p, d_, T, 4ull * d_);
+    if (resid_tma_) tm_xc_out_ = make_out_map(xc_.p, true, d_, T, 4ull * d_);
   }
   if (any_int8_) {
     const auto U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
@@ -1250,7 +1255,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     scales(eo, ly.o, zs_.p);
     timed(4, 2.0 * dTl * d_ * ly.kh, [&] {
       gemm_w(iolmk::EPI_RESID_F32, ly.o, i8_o ? ly.tm_z8 : cl ? tm_zc_ : ly.tm_z, ly.o.mode == W_SP24F ? (cl ? tm_zcs_ : ly.tm_zs) : ly.tm_z8s, Tl, d_,
-             ly.kh, eo);
+             ly.kh, eo, resid_tma_ && d_ % 8 == 0 ? (cl ? &tm_xc_out_ : &tm_x_out_) : nullptr);
     });
     // h = LN2(x)
     timed(5, dTl * d_ * 6.0, [&] {
@@ -1280,7 +1285,7 @@ void Engine::launch_step(StepBuffers& sb, const int32_t* d_ids, const uint8_t* d
     scales(eo2, ly.out, gs_.p);
     timed(7, 2.0 * dTl * d_ * ly.f, [&] {
       gemm_w(iolmk::EPI_RESID_F32, ly.out, i8_out ? ly.tm_g8 : ly.tm_g, ly.out.mode == W_SP24F ? ly.tm_gs : ly.tm_g8s, Tl,
-             d_, ly.f, eo2);
+             d_, ly.f, eo2, resid_tma_ && d_ % 8 == 0 ? (cl ? &tm_xc_out_ : &tm_x_out_) : nullptr);
     });
     if (l + 1 < L_) {
       const bool q8_next = layers_[l + 1]->qkv.int8();

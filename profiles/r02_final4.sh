@@ -1,4 +1,4 @@
-# Round-2 final validation after the last-layer head-row compaction: full GPU suite, smoke, every bench
+# Round-2 final validation after the last-layer head-row compaction and the TMA reduce-add residual epilogue: full GPU suite, smoke, every bench
 # config, the reference arm, launch lists (C1 / C3) and a full ncu capture of the C1 GEMMs. Outputs: gpurun_out/f4_*.
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/f4_gpu.txt
